@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark: pospopcnt_u16 input GB/s and % of HBM peak at 1/2/4/8 B200 vs host CPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg4]
+
+One rank per GPU (torchrun for N > 1, NCCL).  A *step* is one pass of the hot
+path over the workload: for the default cfg4 (BASELINE.json configs[3]) every
+rank counts its contiguous shard of 2^32 u16 words (Bernoulli(0.1) bits,
+generated in place in HBM) with ONE kernel launch, and for N > 1 the
+16-entry u64 k-vector is summed across ranks with one NCCL all-reduce.
+Device-timed with CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks.  The input (8 GiB) is far larger
+than the 126 MB L2, so no L2 flush is needed between steps.
+
+Rank 0 prints ONE JSON line.  Extra keys: roofline (dominant kernel vs the
+measured HBM peak), cpu_baseline (the reference library on the host cores,
+N=1 only), e2e (the C-ABI call on pinned HOST buffers, H2D + D2H inside the
+timed region), gpu_launches, clocks (NVML sampled during the timed region).
+
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref/libpospop_ref.so: pospop::pospopcnt, fork-join + merge_counts
+over all host threads) on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pospopcnt_u16 input GB/s and % of HBM peak at 1/2/4/8 B200 vs host CPU"
+CFG4_WORDS = 1 << 32
+FALLBACK_HBM = 6650.0
+
+WORKLOADS = {
+    # name: (k, generator kind, total words, description)
+    "cfg4": (16, 4, 1 << 32, "cfg4: 2^32 u16 words, each bit Bernoulli(6554/65536), contiguous shards "
+                             "over the N GPUs, k=16 u64 counters summed across GPUs (NCCL all-reduce)"),
+    "cfg2": (16, 2, 1 << 28, "cfg2: 2^28 u16 one-hot words, position Zipf(1.1), k=16 u64 counters"),
+    "cfg3": (8, 3, (1 << 30) - 7, "cfg3: 2^30-7 u8 words at a +3 byte offset, 4 KiB runs one-hot/uniform, "
+                                  "k=8 u64 counters"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the workload's total words split over N (BASELINE cfg4); weak: per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peak() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str, n_gpus: int):
+    """dram bytes (read+write) per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(f"{workload}:n{n_gpus}")
+        return None if e is None else int(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled every ~5 ms while active."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device_index: int):
+        self.samples: list[int] = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [n for n, bit in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation
+# ---------------------------------------------------------------------------------------------
+
+def cpu_reference_measure(k: int, gen_kind: int, sample_words: int, reps: int, threads: int):
+    """Times the reference library (oracle/_ref) -- or the oracle port when the
+    reference was not built -- on the first `sample_words` words of the workload.
+    Returns (best GB/s, median GB/s, kind, counts, single-thread GB/s)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    orc = pyoracle.Oracle()
+    data = orc.generate(gen_kind, 1, sample_words, threads=threads)
+    words16 = data.view(np.uint16)
+    try:
+        ref = pyoracle.Reference()
+        kind = "reference"
+
+        def run(nthreads):
+            if k == 16:
+                return ref.pospopcnt_mt(words16, nthreads)
+            return ref.pospopcnt_mt(words16, nthreads)  # k=8 fold: 16-bit counts folded below
+    except Exception:
+        ref = None
+        kind = "port"
+
+        def run(nthreads):
+            return orc.pospopcnt(words16, 16, threads=nthreads)
+
+    run(threads)  # warm-up + page-in
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        counts = run(threads)
+        times.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    run(1)
+    t1 = time.perf_counter() - t0
+    nbytes = data.nbytes
+    if k == 8:  # SURVEY 8c fold: c8[p] = c16[p] + c16[p+8]
+        counts = counts[:8] + counts[8:]
+    return nbytes / min(times) / 1e9, nbytes / statistics.median(times) / 1e9, kind, counts, nbytes / t1 / 1e9
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    k, gen_kind, total, desc = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    # bounded sample: 2^28 words of the workload stream per step (512 MiB for u16)
+    sample = min(total, 1 << 28) if k == 16 else min(total, 1 << 29)
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    orc = pyoracle.Oracle()
+    data = orc.generate(gen_kind, 1, sample, threads=threads)
+    words16 = data.view(np.uint16)
+    try:
+        ref = pyoracle.Reference()
+        kind = "reference"
+        run = lambda: ref.pospopcnt_mt(words16, threads)  # noqa: E731
+    except Exception:
+        kind = "port"
+        run = lambda: orc.pospopcnt(words16, 16, threads=threads)  # noqa: E731
+    for _ in range(max(args.warmup, 1)):
+        run()
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > 240:  # keep the arm within a few minutes
+            break
+    mean = sum(times) / len(times)
+    gbs = data.nbytes / mean / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 4), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": desc, "sample_words_per_step": sample, "host_threads": threads},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": f"first {sample} words of the {args.workload} stream per step; pospop::pospopcnt "
+                                   f"(Auto->Csa16 at native width) fork-join over {threads} threads + merge_counts"},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1911_02696_b200 as pp
+
+    world, rank, local = dist_env()
+    n = max(args.gpus, world)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    k, gen_kind, total, desc = WORKLOADS[args.workload]
+    wb = k // 8
+    if args.scaling == "weak":
+        lo, hi = rank * total, (rank + 1) * total
+    else:
+        lo, hi = total * rank // world, total * (rank + 1) // world
+    words = hi - lo
+    offset = 3 if args.workload == "cfg3" else 0
+    buf = torch.empty(words * wb + offset + 64, dtype=torch.uint8, device=dev)
+    data = buf[offset:offset + words * wb]
+    stream = torch.cuda.current_stream(dev)
+    pp.generate(gen_kind, 1, data, base=lo, n=words, stream=stream)
+    out = torch.zeros(k, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize(dev)
+
+    def step():
+        pp.count_async(data, out, k, stream=stream, len_words=words)
+        if world > 1:
+            dist.all_reduce(out)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = pp.kernel_launches()
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    with sampler:
+        t_begin.record(stream)
+        for i in range(args.steps):
+            starts[i].record(stream)
+            pp.count_async(data, out, k, stream=stream, len_words=words)
+            stops[i].record(stream)
+            if world > 1:
+                dist.all_reduce(out)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = pp.kernel_launches() - launches0
+    elapsed_ms = t_begin.elapsed_time(t_end)
+    kern_ms = sum(s.elapsed_time(e) for s, e in zip(starts, stops)) / args.steps
+    t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms, kern_ms_max = float(t[0]), float(t[1])
+    ms_per_step = elapsed_ms / args.steps
+    total_bytes = (total * (world if args.scaling == "weak" else 1)) * wb
+    value = total_bytes / (ms_per_step * 1e-3) / 1e9
+
+    counts = out.cpu().numpy().astype(np.uint64)
+    if args.workload == "cfg2":
+        assert int(counts.sum()) == total, "one-hot invariant violated"
+
+    peak, peak_src = measured_peak()
+    per_launch_bytes = words * wb + k * 8
+    achieved = per_launch_bytes / (kern_ms * 1e-3) / 1e9
+
+    # ---- e2e: the C-ABI call on pinned HOST memory (H2D + D2H inside the timed region) ----
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(words * wb, dtype=torch.uint8, pin_memory=True)
+        host.copy_(data)
+        torch.cuda.synchronize(dev)
+        host_arr = host.numpy()
+        ref_counts = pp.pospopcnt_k(host_arr, k)  # warm-up: staging buffers, pinned result
+        assert ref_counts == counts if world == 1 else True
+        e2e_steps = max(1, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            c = pp.pospopcnt_k(host_arr, k)
+            if world > 1:
+                ct = torch.from_numpy(c.counts.astype(np.int64))
+                dist.all_reduce(ct.to(dev))
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt[0])
+        e2e = {"value": round(total_bytes / e2e_s / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": words * wb, "d2h_bytes_per_step": k * 8, "steps": e2e_steps,
+               "path": "pospopcnt_k C ABI on a pinned host buffer: chunked H2D (64 MiB x3 ring) overlapped "
+                       "with the kernel, k-vector D2H"}
+        del host
+
+    # ---- CPU baseline on the host (rank 0, N = 1 only) ----
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        sample = min(words, 1 << 28)
+        best, med, kind, cpu_counts, single = cpu_reference_measure(k, gen_kind, sample, 3, threads)
+        # correctness gate (bench.cpp:64-68): GPU counts of the same sample must match
+        gate = torch.zeros(k, dtype=torch.int64, device=dev)
+        pp.count_async(data, gate, k, stream=stream, len_words=sample)
+        torch.cuda.synchronize(dev)
+        assert (gate.cpu().numpy().astype(np.uint64) == np.asarray(cpu_counts, np.uint64)).all(), \
+            "correctness gate: GPU and reference disagree on the CPU sample"
+        cpu = {"value": round(best, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+               "sample": f"first {sample} words ({sample * wb >> 20} MiB) of the {args.workload} stream, "
+                         f"pospop::pospopcnt fork-join over {threads} threads + merge_counts, best of 3 "
+                         f"(median {med:.2f} GB/s; 1 thread {single:.2f} GB/s); counts equal the GPU's"}
+
+    traffic = ncu_traffic(args.workload, world)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u16" if k == 16 else f"u{k}",
+        "data": "synthetic (counter-based generator, generated in place in HBM)",
+        "config": {"workload": desc, "words_total": total, "k": k, "bytes_per_step": total_bytes,
+                   "parallelism": f"shard{world}", "l2_policy": "input >> 126 MB L2; no flush needed",
+                   "kernel": "stream_kernel<1,6> (LDG.128 + LOP3 CSA depth 6), 1 launch per step"},
+        "words_per_s": round(total_bytes / wb / (ms_per_step * 1e-3), 1),
+        "pct_hbm_peak": round(100 * value / world / peak, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "kernel_ms": round(kern_ms, 5), "bytes_per_launch": per_launch_bytes,
+                     "frac_of_theoretical_8180": round(achieved / 8180.0, 4)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,174 @@
+/*
+ * pospopcnt_b200.h -- C ABI of the B200-native positional population count.
+ *
+ * Drop-in boundary for the reference's entry point
+ *     pospop::PositionalCounts pospop::pospopcnt(pospop::Word16Span words,
+ *                                                const pospop::PospopcntConfig& = {})
+ *     (/root/reference/proj/core/include/pospop/pospop.hpp:34,
+ *      dispatcher proj/core/src/pospop.cpp:80-111)
+ * and for the paper's C signature
+ *     void pospopcnt_u16_scalar_basic(uint16_t* data, uint32_t len, uint32_t* counters)
+ *     (Fig. 6).
+ * The reference ships no extern "C" surface; this one is derived from it as
+ * "word pointer + length + k-counter output array" (BASELINE.json north_star).
+ * The header-only C++ shim include/pospop_gpu.hpp restores the reference's
+ * own C++ signature on top of it.  INTEGRATION.md shows the bindings.
+ *
+ * Conventions (mirroring the reference's behaviour):
+ *  - counts[] is OVERWRITTEN, like the reference's return-by-value
+ *    PositionalCounts (types.hpp:35-46); except pospopcnt_u16_c32, which
+ *    ACCUMULATES like Fig. 6.
+ *  - data == NULL is allowed iff len == 0 (Word16Span{} is valid, types.hpp:29-31).
+ *  - data must be aligned to the word size (as a uint16_t* / uint32_t* /
+ *    uint64_t* is in C++); any alignment beyond that is handled (unaligned
+ *    heads and ragged tails count exactly).
+ *  - data may be DEVICE memory (the fast path: counted in place in HBM) or
+ *    HOST memory (pinned or pageable: streamed to the GPU in chunks with
+ *    copy/compute overlap).  The classification uses cudaPointerGetAttributes.
+ *  - Every call is synchronous, thread-safe and re-entrant (per-thread,
+ *    per-device workspaces and streams), like the reference.
+ *  - No exception or CUDA error crosses the ABI; failures return a status
+ *    and set a thread-local message (pospop_last_error).  There is NO CPU
+ *    fallback: without a usable sm_100 device every counting call returns
+ *    POSPOP_EUNAVAILABLE.
+ */
+#ifndef POSPOPCNT_B200_H
+#define POSPOPCNT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    POSPOP_OK = 0,
+    POSPOP_EINVAL = 1,       /* std::invalid_argument          (pospop.cpp:63-70) */
+    POSPOP_EUNAVAILABLE = 2, /* pospop::KernelUnavailableError (types.hpp:68-71)  */
+    POSPOP_ECUDA = 3,        /* CUDA runtime failure (message in pospop_last_error) */
+    POSPOP_ENOMEM = 4        /* device / pinned allocation failed                  */
+} pospop_status;
+
+/* pospop::KernelKind, same order (types.hpp:52-60).  On the GPU every kind
+ * computes identical counts with the same device kernel (pospop.hpp:28-33:
+ * "All kernels produce identical counts; they differ only in speed"); the
+ * kind is validated and otherwise ignored. */
+typedef enum {
+    POSPOP_KERNEL_SCALAR = 0,
+    POSPOP_KERNEL_CSA4 = 1,
+    POSPOP_KERNEL_CSA8 = 2,
+    POSPOP_KERNEL_CSA16 = 3,
+    POSPOP_KERNEL_FOREST = 4,
+    POSPOP_KERNEL_BYTEBLEND = 5,
+    POSPOP_KERNEL_AUTO = 6
+} pospop_kernel_kind;
+
+/* pospop::PospopcntConfig (types.hpp:73-89), same fields and defaults. */
+typedef struct {
+    int32_t kernel;                  /* pospop_kernel_kind, default AUTO            */
+    uint32_t register_width_bits;    /* 0 or a supported width (pospop_supported_widths) */
+    uint32_t flush_threshold_blocks; /* [1, 65535], default 65535                   */
+    uint64_t auto_threshold_words;   /* default 4096                                */
+} pospop_config;
+
+#define POSPOP_CONFIG_DEFAULT {POSPOP_KERNEL_AUTO, 0u, 65535u, 4096u}
+
+/* ---- validation / capability (pospop.cpp:63-70, cpu.cpp:39-55) ---------- */
+
+/* POSPOP_EINVAL when register_width_bits % 16 != 0, flush_threshold_blocks
+ * is outside [1, 65535] or kernel is not a pospop_kernel_kind.  Needs no GPU. */
+pospop_status pospop_validate(const pospop_config* config);
+
+/* Register widths the GPU path accepts, ascending (the analogue of
+ * supported_csa_widths()).  A 32-bit register is one thread's lane vector;
+ * 64..512 are accepted as the reference's CPU widths and map to the same
+ * kernel.  Returns the number of widths; writes at most cap. */
+int pospop_supported_widths(uint32_t* out, int cap);
+
+/* 1 when an sm_100-class device is usable (device count > 0, CC 10.x). */
+int pospop_device_available(void);
+
+/* Thread-local description of the last failure on this thread ("" if none). */
+const char* pospop_last_error(void);
+
+/* ---- single-stream counting: counts OVERWRITTEN ------------------------- */
+
+pospop_status pospopcnt_u8(const uint8_t* data, size_t len, uint64_t counts[8]);
+pospop_status pospopcnt_u16(const uint16_t* data, size_t len, uint64_t counts[16]);
+pospop_status pospopcnt_u32(const uint32_t* data, size_t len, uint64_t counts[32]);
+pospop_status pospopcnt_u64(const uint64_t* data, size_t len, uint64_t counts[64]);
+
+/* The reference entry point: pospop::pospopcnt(Word16Span, PospopcntConfig).
+ * config == NULL means POSPOP_CONFIG_DEFAULT.  Validation and errors as the
+ * reference: EINVAL for out-of-range fields, EUNAVAILABLE for a width with
+ * no GPU mapping (e.g. 16, 48, 1024) or no device. */
+pospop_status pospopcnt_u16_config(const uint16_t* data, size_t len, const pospop_config* config,
+                                   uint64_t counts[16]);
+
+/* Any k in {8,16,32,64} with an explicit flush threshold (tree blocks per
+ * thread between lane-counter flushes, [1,65535]). */
+pospop_status pospopcnt_k(int k, const void* data, size_t len, uint32_t flush_threshold_blocks,
+                          uint64_t* counts);
+
+/* Fig. 6 signature width: uint32 counters, ACCUMULATED (counters[p] += ...),
+ * as pospopcnt_u16_scalar_basic in PAPER.md:315-325.  Counters wrap modulo
+ * 2^32 exactly as the paper's uint32_t counters would. */
+pospop_status pospopcnt_u16_c32(const uint16_t* data, uint32_t len, uint32_t counters[16]);
+
+/* ---- batched / segmented ------------------------------------------------- */
+
+/* Array a is words [offsets[a], offsets[a+1]) of data (offsets: n_arrays+1
+ * non-decreasing entries, in words).  Row a of counts (k entries,
+ * row-major n_arrays x k) is overwritten.  data/offsets/counts may be
+ * device or host memory (each classified independently). */
+pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offsets, size_t n_arrays,
+                                  uint64_t* counts);
+
+/* ---- multi-device, one process (the cfg4 shard/reduce driver) ----------- */
+
+/* shards[i] (lens[i] words, device memory on devices[i]) are counted
+ * concurrently on their devices, then the k-vectors are summed
+ * (merge_counts, pospop.cpp:33-37).  A device may appear more than once.
+ * Use torch.distributed / NCCL for the one-process-per-GPU layout
+ * (paper_1911_02696_b200.shard). */
+pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* lens,
+                                const int* devices, int n_shards, uint64_t* counts);
+
+/* ---- asynchronous device-resident entry points (timing / integration) --- */
+
+/* Enqueues one count of device-resident data on `stream` (a cudaStream_t,
+ * NULL = the calling thread's per-device stream); d_counts (k u64 in device
+ * memory on the current device) is overwritten, or accumulated when
+ * accumulate != 0.  Returns without synchronising.  At most one launch per
+ * (device, stream) may be in flight through this entry point at a time
+ * (the workspace is per stream); grid/block 0 = automatic. */
+pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
+                              int accumulate, uint32_t flush_threshold_blocks, int grid, int block,
+                              void* stream);
+
+/* Segmented, device-resident, asynchronous. */
+pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_t* d_offsets,
+                                        size_t n_arrays, uint64_t* d_counts,
+                                        uint32_t flush_threshold_blocks, int grid, int block,
+                                        void* stream);
+
+/* ---- synthetic inputs and digests (device-side, for tests and bench) ---- */
+
+/* Fills n elements at d_out with generator `kind` (1..6):
+ * element l is global element index_base + l.  Asynchronous on `stream`. */
+pospop_status pospop_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* d_out,
+                              void* stream);
+
+/* Order-independent digest of nbytes at 8-byte-aligned device memory;
+ * synchronous. */
+pospop_status pospop_digest(const void* d_data, size_t nbytes, uint64_t* digest);
+
+/* Kernels launched by this library in this process (launch accounting). */
+uint64_t pospop_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POSPOPCNT_B200_H */

@@ -1,0 +1,360 @@
+"""B200-native positional population count (pospopcnt).
+
+Host-side mirror of the reference's public API
+(/root/reference/proj/core/include/pospop/types.hpp, pospop.hpp) over the
+C ABI in include/pospopcnt_b200.h, implemented by the sm_100a CUDA library
+``libpospopcnt_b200.so`` built in-tree from ``csrc/``.
+
+Reference name              -> here
+  pospop::pospopcnt            pospopcnt(words, config=None)       (pospop.hpp:34)
+  pospop::PositionalCounts     PositionalCounts                    (types.hpp:35-46)
+  pospop::merge_counts         merge_counts(a, b)                  (types.hpp:48-50)
+  pospop::KernelKind           KernelKind                          (types.hpp:52-60)
+  pospop::PospopcntConfig      PospopcntConfig                     (types.hpp:73-89)
+  pospop::validate             validate(config)                    (pospop.cpp:63-70)
+  pospop::KernelUnavailableError  KernelUnavailableError           (types.hpp:68-71)
+  std::invalid_argument        InvalidArgument (a ValueError)
+  supported_csa_widths / native_csa_width                          (cpu.cpp:39-55)
+
+Extensions on the same path (BASELINE.json north_star): k = 8/16/32/64
+(``pospopcnt_k``), the segmented/batched form (``pospopcnt_segmented``), a
+device-resident asynchronous launch (``count_async``) and the multi-GPU
+shard/reduce driver (``paper_1911_02696_b200.shard``).
+
+There is no CPU fallback: if the CUDA library or an sm_100 device is missing
+every counting call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass
+from typing import Any, Iterable, Sequence
+
+import numpy as np
+
+__all__ = [
+    "KernelKind", "PospopcntConfig", "PositionalCounts", "InvalidArgument", "KernelUnavailableError",
+    "CudaError", "validate", "merge_counts", "pospopcnt", "pospopcnt_k", "pospopcnt_u16_c32",
+    "pospopcnt_segmented", "pospopcnt_sharded", "count_async", "segmented_async", "generate", "digest",
+    "supported_csa_widths", "native_csa_width", "device_available", "kernel_launches", "library_path",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libpospopcnt_b200.so"
+
+
+def library_path() -> str:
+    return os.path.join(_HERE, LIB_NAME)
+
+
+# -- errors (status codes of include/pospopcnt_b200.h) -----------------------
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument from pospop::validate / the dispatcher (pospop.cpp:63-70, 110)."""
+
+
+class KernelUnavailableError(RuntimeError):
+    """pospop::KernelUnavailableError (types.hpp:68-71): kernel/width/device cannot run here."""
+
+
+class CudaError(RuntimeError):
+    """A CUDA runtime failure inside the library."""
+
+
+_OK, _EINVAL, _EUNAVAILABLE, _ECUDA, _ENOMEM = range(5)
+
+_u64p = C.POINTER(C.c_uint64)
+
+
+class _Config(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("register_width_bits", C.c_uint32),
+                ("flush_threshold_blocks", C.c_uint32), ("auto_threshold_words", C.c_uint64)]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = library_path()
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "or `make -C paper_1911_02696_b200/csrc` (there is no CPU fallback)")
+    lib = C.CDLL(path)
+    vp, sz = C.c_void_p, C.c_size_t
+    sig = {
+        "pospop_validate": ([C.POINTER(_Config)], C.c_int),
+        "pospop_supported_widths": ([C.POINTER(C.c_uint32), C.c_int], C.c_int),
+        "pospop_device_available": ([], C.c_int),
+        "pospop_last_error": ([], C.c_char_p),
+        "pospop_kernel_launches": ([], C.c_uint64),
+        "pospopcnt_u8": ([vp, sz, _u64p], C.c_int),
+        "pospopcnt_u16": ([vp, sz, _u64p], C.c_int),
+        "pospopcnt_u32": ([vp, sz, _u64p], C.c_int),
+        "pospopcnt_u64": ([vp, sz, _u64p], C.c_int),
+        "pospopcnt_u16_config": ([vp, sz, C.POINTER(_Config), _u64p], C.c_int),
+        "pospopcnt_k": ([C.c_int, vp, sz, C.c_uint32, _u64p], C.c_int),
+        "pospopcnt_u16_c32": ([vp, C.c_uint32, C.POINTER(C.c_uint32)], C.c_int),
+        "pospopcnt_segmented": ([C.c_int, vp, vp, sz, vp], C.c_int),
+        "pospopcnt_sharded": ([C.c_int, C.POINTER(vp), C.POINTER(sz), C.POINTER(C.c_int), C.c_int, _u64p],
+                              C.c_int),
+        "pospopcnt_async": ([C.c_int, vp, sz, vp, C.c_int, C.c_uint32, C.c_int, C.c_int, vp], C.c_int),
+        "pospopcnt_segmented_async": ([C.c_int, vp, vp, sz, vp, C.c_uint32, C.c_int, C.c_int, vp], C.c_int),
+        "pospop_generate": ([C.c_int, C.c_uint64, C.c_uint64, sz, vp, vp], C.c_int),
+        "pospop_digest": ([vp, sz, _u64p], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(status: int) -> None:
+    if status == _OK:
+        return
+    msg = _load().pospop_last_error().decode(errors="replace")
+    if status == _EINVAL:
+        raise InvalidArgument(msg)
+    if status == _EUNAVAILABLE:
+        raise KernelUnavailableError(msg)
+    if status == _ENOMEM:
+        raise MemoryError(msg)
+    raise CudaError(msg)
+
+
+# -- reference types -----------------------------------------------------------
+
+class KernelKind(enum.IntEnum):
+    """pospop::KernelKind (types.hpp:52-60).  All kinds give identical counts."""
+    ScalarBasic = 0
+    Csa4 = 1
+    Csa8 = 2
+    Csa16 = 3
+    Forest = 4
+    ByteBlend = 5
+    Auto = 6
+
+    def __str__(self) -> str:  # to_string (pospop.cpp:39-50)
+        return _KIND_NAMES[self]
+
+    @classmethod
+    def from_string(cls, name: str) -> "KernelKind | None":  # kernel_from_string (pospop.cpp:52-61)
+        for k, v in _KIND_NAMES.items():
+            if v == name:
+                return k
+        return None
+
+
+_KIND_NAMES = {KernelKind.ScalarBasic: "scalar", KernelKind.Csa4: "csa4", KernelKind.Csa8: "csa8",
+               KernelKind.Csa16: "csa16", KernelKind.Forest: "forest", KernelKind.ByteBlend: "byteblend",
+               KernelKind.Auto: "auto"}
+
+
+@dataclass
+class PospopcntConfig:
+    """pospop::PospopcntConfig (types.hpp:73-89), same defaults."""
+    kernel: KernelKind = KernelKind.Auto
+    register_width_bits: int = 0
+    flush_threshold_blocks: int = 65535
+    auto_threshold_words: int = 4096
+
+    def _c(self) -> _Config:
+        return _Config(int(self.kernel), int(self.register_width_bits) & 0xFFFFFFFF,
+                       int(self.flush_threshold_blocks) & 0xFFFFFFFF, int(self.auto_threshold_words))
+
+
+class PositionalCounts:
+    """pospop::PositionalCounts (types.hpp:35-46): counts[p] = #words with bit p set."""
+
+    __slots__ = ("counts",)
+
+    def __init__(self, counts: Iterable[int] | None = None, k: int = 16):
+        self.counts = np.zeros(k, np.uint64) if counts is None else np.asarray(counts, np.uint64).copy()
+
+    def __getitem__(self, p: int) -> int:
+        return int(self.counts[p])
+
+    def __setitem__(self, p: int, v: int) -> None:
+        self.counts[p] = v
+
+    def __len__(self) -> int:
+        return len(self.counts)
+
+    def __iter__(self):
+        return (int(x) for x in self.counts)
+
+    def __eq__(self, other: Any) -> bool:
+        other_counts = other.counts if isinstance(other, PositionalCounts) else np.asarray(other, np.uint64)
+        return self.counts.shape == other_counts.shape and bool((self.counts == other_counts).all())
+
+    def total(self) -> int:  # pospop.cpp:27-31
+        return int(sum(int(x) for x in self.counts))
+
+    def __repr__(self) -> str:
+        return f"PositionalCounts({[int(x) for x in self.counts]})"
+
+
+def merge_counts(a: PositionalCounts, b: PositionalCounts) -> PositionalCounts:
+    """result[p] = a[p] + b[p] (pospop.cpp:33-37); associative and commutative."""
+    return PositionalCounts(a.counts + b.counts)
+
+
+def validate(config: PospopcntConfig) -> None:
+    """Raises InvalidArgument for out-of-range fields (pospop.cpp:63-70)."""
+    _check(_load().pospop_validate(C.byref(config._c())))
+
+
+def supported_csa_widths() -> list[int]:
+    buf = (C.c_uint32 * 16)()
+    n = _load().pospop_supported_widths(buf, 16)
+    return list(buf[:n])
+
+
+def native_csa_width() -> int:
+    return supported_csa_widths()[-1]
+
+
+def device_available() -> bool:
+    return bool(_load().pospop_device_available())
+
+
+def kernel_launches() -> int:
+    return int(_load().pospop_kernel_launches())
+
+
+# -- buffers -------------------------------------------------------------------
+
+def _addr_len(data: Any, k: int) -> tuple[int, int]:
+    """(address, length in k-bit words) of a numpy array, torch tensor or (addr, len) pair."""
+    if isinstance(data, tuple):
+        return int(data[0]), int(data[1])
+    if isinstance(data, np.ndarray):
+        if not data.flags.c_contiguous:
+            raise InvalidArgument("array must be C-contiguous")
+        return (data.ctypes.data if data.size else 0), data.nbytes * 8 // k
+    if hasattr(data, "data_ptr") and hasattr(data, "element_size"):  # torch.Tensor
+        if not data.is_contiguous():
+            raise InvalidArgument("tensor must be contiguous")
+        nbytes = data.numel() * data.element_size()
+        return (data.data_ptr() if nbytes else 0), nbytes * 8 // k
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        arr = np.frombuffer(data, np.uint8)
+        return (arr.ctypes.data if arr.size else 0), arr.nbytes * 8 // k
+    raise TypeError(f"unsupported buffer type {type(data)!r}")
+
+
+def _stream_ptr(stream: Any) -> int | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(getattr(stream, "cuda_stream"))  # torch.cuda.Stream
+
+
+# -- the hot path ----------------------------------------------------------------
+
+def pospopcnt(words: Any, config: PospopcntConfig | None = None) -> PositionalCounts:
+    """pospop::pospopcnt(Word16Span, PospopcntConfig) on the GPU (pospop.hpp:34)."""
+    addr, n = _addr_len(words, 16)
+    out = np.zeros(16, np.uint64)
+    cfg = (config or PospopcntConfig())._c()
+    _check(_load().pospopcnt_u16_config(addr or None, n, C.byref(cfg), out.ctypes.data_as(_u64p)))
+    return PositionalCounts(out)
+
+
+def pospopcnt_k(data: Any, k: int, flush_threshold_blocks: int = 65535, len_words: int | None = None
+                ) -> PositionalCounts:
+    """k in {8,16,32,64}: counts[p] = #k-bit words with bit p set."""
+    addr, n = _addr_len(data, k)
+    if len_words is not None:
+        n = int(len_words)
+    out = np.zeros(max(k, 1), np.uint64)
+    _check(_load().pospopcnt_k(int(k), addr or None, n, int(flush_threshold_blocks), out.ctypes.data_as(_u64p)))
+    return PositionalCounts(out)
+
+
+def pospopcnt_u16_c32(words: Any, counters: np.ndarray) -> np.ndarray:
+    """PAPER.md Fig. 6 signature: uint32 counters, accumulated in place."""
+    addr, n = _addr_len(words, 16)
+    if counters.dtype != np.uint32 or counters.size != 16:
+        raise InvalidArgument("counters must be a uint32 array of 16")
+    if n > 0xFFFFFFFF:
+        raise InvalidArgument("len exceeds the uint32_t len of Fig. 6")
+    _check(_load().pospopcnt_u16_c32(addr or None, n, counters.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return counters
+
+
+def pospopcnt_segmented(data: Any, offsets: Any, k: int, out: Any = None) -> Any:
+    """Row a = counts of words [offsets[a], offsets[a+1]); returns (n_arrays, k) uint64."""
+    addr, _ = _addr_len(data, k)
+    if isinstance(offsets, np.ndarray):
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+    else:
+        n = offsets.numel() - 1
+    off_addr, _ = _addr_len(offsets, 64)
+    if out is None:
+        out = np.zeros((max(n, 0), k), np.uint64)
+    out_addr, _ = _addr_len(out, 64)
+    if n > 0:
+        _check(_load().pospopcnt_segmented(int(k), addr or None, off_addr, n, out_addr))
+    return out
+
+
+def pospopcnt_sharded(shards: Sequence[Any], devices: Sequence[int], k: int = 16) -> PositionalCounts:
+    """One process, several devices: count every shard on its device, then merge_counts."""
+    n = len(shards)
+    ptrs = (C.c_void_p * n)()
+    lens = (C.c_size_t * n)()
+    devs = (C.c_int * n)(*[int(d) for d in devices])
+    for i, s in enumerate(shards):
+        a, l = _addr_len(s, k)
+        ptrs[i], lens[i] = a or None, l
+    out = np.zeros(k, np.uint64)
+    _check(_load().pospopcnt_sharded(int(k), ptrs, lens, devs, n, out.ctypes.data_as(_u64p)))
+    return PositionalCounts(out)
+
+
+def count_async(data: Any, out: Any, k: int, *, accumulate: bool = False, flush_threshold_blocks: int = 65535,
+                grid: int = 0, block: int = 0, stream: Any = None, len_words: int | None = None) -> None:
+    """Enqueues one device-resident count (no host sync); out: k uint64 on the device."""
+    addr, n = _addr_len(data, k)
+    if len_words is not None:
+        n = int(len_words)
+    out_addr, _ = _addr_len(out, 64)
+    _check(_load().pospopcnt_async(int(k), addr or None, n, out_addr, int(accumulate), int(flush_threshold_blocks),
+                                   int(grid), int(block), _stream_ptr(stream)))
+
+
+def segmented_async(data: Any, offsets: Any, out: Any, k: int, *, flush_threshold_blocks: int = 65535,
+                    grid: int = 0, block: int = 0, stream: Any = None) -> None:
+    addr, _ = _addr_len(data, k)
+    off_addr, noff = _addr_len(offsets, 64)
+    out_addr, _ = _addr_len(out, 64)
+    _check(_load().pospopcnt_segmented_async(int(k), addr or None, off_addr, noff - 1, out_addr,
+                                             int(flush_threshold_blocks), int(grid), int(block),
+                                             _stream_ptr(stream)))
+
+
+GEN_UNIFORM16, GEN_CFG2, GEN_CFG3, GEN_CFG4, GEN_U32, GEN_U64 = 1, 2, 3, 4, 5, 6
+
+
+def generate(kind: int, seed: int, out: Any, base: int = 0, n: int | None = None, stream: Any = None) -> None:
+    """Fills a device buffer with synthetic input `kind` (Synthetic inputs)."""
+    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8}[kind]
+    addr, nbits = _addr_len(out, 8)
+    count = nbits // esize if n is None else int(n)
+    _check(_load().pospop_generate(int(kind), int(seed), int(base), count, addr or None, _stream_ptr(stream)))
+
+
+def digest(data: Any) -> int:
+    addr, nbytes = _addr_len(data, 8)
+    out = C.c_uint64(0)
+    _check(_load().pospop_digest(addr or None, nbytes, C.byref(out)))
+    return int(out.value)

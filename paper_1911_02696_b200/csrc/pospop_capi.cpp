@@ -1,0 +1,552 @@
+// pospop_capi.cpp -- extern "C" boundary and host runtime (include/pospopcnt_b200.h).
+//
+// Mirrors the reference dispatcher pospop::pospopcnt (proj/core/src/pospop.cpp:80-111):
+// validate -> resolve kernel kind / width (errors as the reference) -> count.
+// Counting always runs on the GPU: device-resident input is counted in place;
+// host input is streamed through pinned-size device staging buffers with
+// H2D copies on a copy stream overlapping the kernel on the compute stream.
+// There is no CPU fallback path.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/pospopcnt_b200.h"
+#include "pospop_launch.h"
+
+using namespace pospop_b200;
+
+namespace {
+
+thread_local std::string t_err;
+
+pospop_status fail(pospop_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return s;
+}
+
+pospop_status cuda_fail(cudaError_t e, const char* what) {
+    const pospop_status s = (e == cudaErrorMemoryAllocation) ? POSPOP_ENOMEM
+                            : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ||
+                               e == cudaErrorNoKernelImageForDevice)
+                                ? POSPOP_EUNAVAILABLE
+                                : POSPOP_ECUDA;
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(s, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CU(call)                                           \
+    do {                                                   \
+        const cudaError_t e_ = (call);                     \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64; }
+
+// ---------------------------------------------------------------------------
+// Device discovery: sm_100 class only (the fatbin carries sm_100a SASS).
+// ---------------------------------------------------------------------------
+pospop_status check_device(int dev) {
+    int major = 0;
+    const cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    if (major != 10)
+        return fail(POSPOP_EUNAVAILABLE,
+                    "kernel unavailable: device %d is compute capability %d.x, sm_100 required", dev,
+                    major);
+    return POSPOP_OK;
+}
+
+pospop_status current_device(int* dev) {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(POSPOP_EUNAVAILABLE, "kernel unavailable: no CUDA device (%s); no CPU fallback",
+                    e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
+    }
+    CU(cudaGetDevice(dev));
+    return check_device(*dev);
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Per-thread, per-device context: compute + copy streams, result buffers,
+// the stream workspace, and (lazily) the host-staging ring.
+// ---------------------------------------------------------------------------
+constexpr int kRing = 3;
+
+struct Ctx {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr;
+    unsigned long long* d_out = nullptr;  // 64 u64
+    unsigned long long* h_out = nullptr;  // 64 u64, pinned
+    StreamWorkspace ws;
+    void* stage[kRing] = {nullptr, nullptr, nullptr};
+    size_t stage_bytes = 0;
+    cudaEvent_t ev_copied[kRing] = {};
+    cudaEvent_t ev_done[kRing] = {};
+};
+
+thread_local std::map<int, Ctx*> t_ctx;
+
+pospop_status alloc_workspace(StreamWorkspace* ws) {
+    CU(cudaMalloc(&ws->acc, 64 * sizeof(unsigned long long) + 64));
+    ws->ticket = reinterpret_cast<unsigned int*>(ws->acc + 64);
+    CU(cudaMemset(ws->acc, 0, 64 * sizeof(unsigned long long) + 64));
+    return POSPOP_OK;
+}
+
+pospop_status get_ctx(int dev, Ctx** out) {
+    auto it = t_ctx.find(dev);
+    if (it != t_ctx.end()) {
+        *out = it->second;
+        return POSPOP_OK;
+    }
+    pospop_status s = check_device(dev);
+    if (s) return s;
+    DeviceGuard g(dev);
+    Ctx* c = new Ctx;
+    c->dev = dev;
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    CU(cudaMalloc(&c->d_out, 64 * sizeof(unsigned long long)));
+    CU(cudaMallocHost(&c->h_out, 64 * sizeof(unsigned long long)));
+    if ((s = alloc_workspace(&c->ws))) return s;
+    t_ctx[dev] = c;
+    *out = c;
+    return POSPOP_OK;
+}
+
+pospop_status ensure_stage(Ctx* c) {
+    if (c->stage[0]) return POSPOP_OK;
+    const char* env = std::getenv("POSPOP_STAGE_MB");
+    size_t mb = env && *env ? std::strtoull(env, nullptr, 10) : 64;
+    if (mb < 1) mb = 1;
+    c->stage_bytes = mb << 20;
+    for (int i = 0; i < kRing; ++i) {
+        CU(cudaMalloc(&c->stage[i], c->stage_bytes));
+        CU(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+    }
+    return POSPOP_OK;
+}
+
+// Workspaces for the async entry point, one per (device, stream).
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, StreamWorkspace> g_ws;
+
+pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out) {
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    auto key = std::make_pair(dev, s);
+    auto it = g_ws.find(key);
+    if (it == g_ws.end()) {
+        StreamWorkspace ws;
+        const pospop_status st = alloc_workspace(&ws);
+        if (st) return st;
+        it = g_ws.emplace(key, ws).first;
+    }
+    *out = it->second;
+    return POSPOP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Pointer classification.
+// ---------------------------------------------------------------------------
+enum class Where { Device, Host };
+
+Where classify(const void* p, int* dev) {
+    cudaPointerAttributes a;
+    std::memset(&a, 0, sizeof a);
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return Where::Host;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        *dev = a.device;
+        return Where::Device;
+    }
+    return Where::Host;
+}
+
+// ---------------------------------------------------------------------------
+// The counting core: k in {8,16,32,64}, result in out[0..k).
+// ---------------------------------------------------------------------------
+pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uint64_t* out) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (!out) return fail(POSPOP_EINVAL, "counts must not be NULL");
+    if (flush < 1 || flush > 65535)
+        return fail(POSPOP_EINVAL, "flush_threshold_blocks must be in [1, 65535], got %u", flush);
+    if (!data && len) return fail(POSPOP_EINVAL, "data is NULL but len is %zu", len);
+    const size_t wb = (size_t)k / 8;
+    if ((uintptr_t)data % wb)
+        return fail(POSPOP_EINVAL, "data %p is not aligned to the %d-bit word size", data, k);
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    if (len == 0) {
+        for (int p = 0; p < k; ++p) out[p] = 0;
+        return POSPOP_OK;
+    }
+    LaunchOptions opt;
+    opt.flush_threshold = flush;
+    const Where where = classify(data, &dev);
+    DeviceGuard g(dev);
+    Ctx* c = nullptr;
+    if ((s = get_ctx(dev, &c))) return s;
+
+    if (where == Where::Device) {
+        CU(launch_stream(k, data, len, c->d_out, false, opt, c->ws, c->stream));
+    } else {
+        // Host input: chunked H2D on the copy stream, counting on the compute
+        // stream, kRing staging buffers recycled behind ev_done.
+        if ((s = ensure_stage(c))) return s;
+        const size_t chunk_words = c->stage_bytes / wb;
+        const uint8_t* src = static_cast<const uint8_t*>(data);
+        size_t i = 0;
+        for (size_t off = 0; off < len; off += chunk_words, ++i) {
+            const size_t n = len - off < chunk_words ? len - off : chunk_words;
+            const int slot = (int)(i % kRing);
+            if (i >= (size_t)kRing) CU(cudaStreamWaitEvent(c->copy, c->ev_done[slot], 0));
+            CU(cudaMemcpyAsync(c->stage[slot], src + off * wb, n * wb, cudaMemcpyHostToDevice, c->copy));
+            CU(cudaEventRecord(c->ev_copied[slot], c->copy));
+            CU(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
+            CU(launch_stream(k, c->stage[slot], n, c->d_out, i > 0, opt, c->ws, c->stream));
+            CU(cudaEventRecord(c->ev_done[slot], c->stream));
+        }
+    }
+    CU(cudaMemcpyAsync(c->h_out, c->d_out, (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    for (int p = 0; p < k; ++p) out[p] = c->h_out[p];
+    return POSPOP_OK;
+}
+
+const uint32_t kWidths[] = {64, 256, 512};
+
+bool width_supported(uint32_t w) {
+    for (uint32_t x : kWidths)
+        if (x == w) return true;
+    return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pospop_last_error(void) { return t_err.c_str(); }
+
+int pospop_supported_widths(uint32_t* out, int cap) {
+    const int n = (int)(sizeof kWidths / sizeof kWidths[0]);
+    for (int i = 0; i < n && i < cap; ++i) out[i] = kWidths[i];
+    return n;
+}
+
+int pospop_device_available(void) {
+    int dev = 0;
+    return current_device(&dev) == POSPOP_OK ? 1 : 0;
+}
+
+uint64_t pospop_kernel_launches(void) { return kernel_launches(); }
+
+pospop_status pospop_validate(const pospop_config* c) {
+    if (!c) return POSPOP_OK;
+    if (c->register_width_bits % 16 != 0)
+        return fail(POSPOP_EINVAL, "register_width_bits must be a multiple of 16, got %u",
+                    c->register_width_bits);
+    if (c->flush_threshold_blocks < 1 || c->flush_threshold_blocks > 65535)
+        return fail(POSPOP_EINVAL, "flush_threshold_blocks must be in [1, 65535], got %u",
+                    c->flush_threshold_blocks);
+    if (c->kernel < POSPOP_KERNEL_SCALAR || c->kernel > POSPOP_KERNEL_AUTO)
+        return fail(POSPOP_EINVAL, "unknown kernel");
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_u8(const uint8_t* d, size_t n, uint64_t c[8]) { return count_any(8, d, n, 65535, c); }
+pospop_status pospopcnt_u16(const uint16_t* d, size_t n, uint64_t c[16]) { return count_any(16, d, n, 65535, c); }
+pospop_status pospopcnt_u32(const uint32_t* d, size_t n, uint64_t c[32]) { return count_any(32, d, n, 65535, c); }
+pospop_status pospopcnt_u64(const uint64_t* d, size_t n, uint64_t c[64]) { return count_any(64, d, n, 65535, c); }
+
+pospop_status pospopcnt_k(int k, const void* data, size_t len, uint32_t flush, uint64_t* counts) {
+    return count_any(k, data, len, flush, counts);
+}
+
+// pospop::pospopcnt (pospop.cpp:80-111): validate, resolve Auto, then the
+// per-kind width rules (forest 92-93, byteblend byteblend.cpp:60-80, CSA
+// csa_portable.cpp:40-46), then count.
+pospop_status pospopcnt_u16_config(const uint16_t* data, size_t len, const pospop_config* config,
+                                   uint64_t counts[16]) {
+    const pospop_config dflt = POSPOP_CONFIG_DEFAULT;
+    const pospop_config* c = config ? config : &dflt;
+    pospop_status s = pospop_validate(c);
+    if (s) return s;
+    int kind = c->kernel;
+    if (kind == POSPOP_KERNEL_AUTO)
+        kind = len < c->auto_threshold_words ? POSPOP_KERNEL_BYTEBLEND : POSPOP_KERNEL_CSA16;
+    const uint32_t w = c->register_width_bits;
+    switch (kind) {
+        case POSPOP_KERNEL_SCALAR:
+            break;
+        case POSPOP_KERNEL_FOREST:
+            if (w > 64) return fail(POSPOP_EUNAVAILABLE, "kernel unavailable: forest supports 64-bit registers only");
+            break;
+        case POSPOP_KERNEL_BYTEBLEND:
+            if (c->kernel != POSPOP_KERNEL_AUTO && w != 0 && w != 64 && w != 256)
+                return fail(POSPOP_EUNAVAILABLE,
+                            "kernel unavailable: byteblend supports 64- or 256-bit registers, got %u", w);
+            break;
+        default:  // CSA kinds
+            if (w != 0 && !width_supported(w))
+                return fail(POSPOP_EUNAVAILABLE, "kernel unavailable: no CSA backend for %u-bit registers", w);
+            break;
+    }
+    return count_any(16, data, len, c->flush_threshold_blocks, counts);
+}
+
+pospop_status pospopcnt_u16_c32(const uint16_t* data, uint32_t len, uint32_t counters[16]) {
+    if (!counters) return fail(POSPOP_EINVAL, "counters must not be NULL");
+    uint64_t c[16];
+    const pospop_status s = count_any(16, data, len, 65535, c);
+    if (s) return s;
+    for (int p = 0; p < 16; ++p) counters[p] += (uint32_t)c[p];
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offsets, size_t n,
+                                  uint64_t* counts) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (n == 0) return POSPOP_OK;
+    if (!offsets || !counts) return fail(POSPOP_EINVAL, "offsets/counts must not be NULL");
+    const size_t wb = (size_t)k / 8;
+    if ((uintptr_t)data % wb) return fail(POSPOP_EINVAL, "data is not aligned to the %d-bit word size", k);
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    int ddev = dev, odev = dev, cdev = dev;
+    const bool d_dev = data && classify(data, &ddev) == Where::Device;
+    const bool o_dev = classify(offsets, &odev) == Where::Device;
+    const bool c_dev = classify(counts, &cdev) == Where::Device;
+    if (d_dev) dev = ddev;
+    DeviceGuard g(dev);
+    Ctx* c = nullptr;
+    if ((s = get_ctx(dev, &c))) return s;
+
+    // Host offsets are needed on the host for validation and sizing anyway.
+    std::vector<uint64_t> h_off;
+    const uint64_t* hoff = offsets;
+    if (o_dev) {
+        h_off.resize(n + 1);
+        CU(cudaMemcpy(h_off.data(), offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        hoff = h_off.data();
+    }
+    for (size_t a = 0; a < n; ++a)
+        if (hoff[a + 1] < hoff[a]) return fail(POSPOP_EINVAL, "offsets must be non-decreasing (array %zu)", a);
+    if (!data && hoff[n] != hoff[0]) return fail(POSPOP_EINVAL, "data is NULL but arrays are non-empty");
+
+    const void* ddata = data;
+    void* tmp_data = nullptr;
+    unsigned long long* tmp_off = nullptr;
+    unsigned long long* tmp_out = nullptr;
+    auto cleanup = [&] {
+        if (tmp_data) cudaFree(tmp_data);
+        if (tmp_off) cudaFree(tmp_off);
+        if (tmp_out) cudaFree(tmp_out);
+    };
+    struct Cleanup {
+        decltype(cleanup)& f;
+        ~Cleanup() { f(); }
+    } guard{cleanup};
+
+    if (!d_dev && hoff[n] > 0) {  // stage the referenced range [0, offsets[n]) words
+        const size_t bytes = hoff[n] * wb;
+        CU(cudaMalloc(&tmp_data, bytes));
+        CU(cudaMemcpyAsync(tmp_data, data, bytes, cudaMemcpyHostToDevice, c->stream));
+        ddata = tmp_data;
+    }
+    const unsigned long long* doff = reinterpret_cast<const unsigned long long*>(offsets);
+    if (!o_dev) {
+        CU(cudaMalloc(&tmp_off, (n + 1) * sizeof(uint64_t)));
+        CU(cudaMemcpyAsync(tmp_off, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+        doff = tmp_off;
+    }
+    unsigned long long* dout = reinterpret_cast<unsigned long long*>(counts);
+    if (!c_dev) {
+        CU(cudaMalloc(&tmp_out, n * (size_t)k * sizeof(uint64_t)));
+        dout = tmp_out;
+    }
+    LaunchOptions opt;
+    CU(launch_segmented(k, ddata ? ddata : (const void*)doff, doff, n, dout, opt, c->stream));
+    if (!c_dev)
+        CU(cudaMemcpyAsync(counts, dout, n * (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* lens, const int* devices,
+                                int n_shards, uint64_t* counts) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (n_shards < 0 || (n_shards > 0 && (!shards || !lens || !devices)) || !counts)
+        return fail(POSPOP_EINVAL, "invalid shard description");
+    int dev0 = 0;
+    pospop_status s = current_device(&dev0);
+    if (s) return s;
+    const size_t wb = (size_t)k / 8;
+    // Launch every shard before any synchronisation (launch skew).
+    std::vector<unsigned long long*> partial((size_t)n_shards, nullptr);
+    std::vector<Ctx*> ctxs((size_t)n_shards, nullptr);
+    std::vector<cudaStream_t> streams((size_t)n_shards, nullptr);
+    LaunchOptions opt;
+    for (int i = 0; i < n_shards; ++i) {
+        if (!shards[i] && lens[i]) return fail(POSPOP_EINVAL, "shard %d is NULL with len %zu", i, lens[i]);
+        if ((uintptr_t)shards[i] % wb) return fail(POSPOP_EINVAL, "shard %d is misaligned", i);
+        int d = devices[i];
+        int pd = d;
+        if (lens[i] && classify(shards[i], &pd) != Where::Device)
+            return fail(POSPOP_EINVAL, "shard %d is not device memory", i);
+        if (lens[i] && pd != d) return fail(POSPOP_EINVAL, "shard %d lives on device %d, not %d", i, pd, d);
+        DeviceGuard g(d);
+        if ((s = get_ctx(d, &ctxs[(size_t)i]))) return s;
+        // Each shard gets its own stream + workspace so shards on one device
+        // may run back to back without sharing a ticket.
+        CU(cudaStreamCreateWithFlags(&streams[(size_t)i], cudaStreamNonBlocking));
+        StreamWorkspace ws;
+        if ((s = stream_workspace(d, streams[(size_t)i], &ws))) return s;
+        CU(cudaMalloc(&partial[(size_t)i], 64 * sizeof(unsigned long long)));
+        if (lens[i]) {
+            CU(launch_stream(k, shards[i], lens[i], partial[(size_t)i], false, opt, ws, streams[(size_t)i]));
+        } else {
+            CU(cudaMemsetAsync(partial[(size_t)i], 0, 64 * sizeof(unsigned long long), streams[(size_t)i]));
+        }
+    }
+    for (int p = 0; p < k; ++p) counts[p] = 0;
+    for (int i = 0; i < n_shards; ++i) {  // merge_counts over shards
+        DeviceGuard g(devices[i]);
+        unsigned long long h[64];
+        CU(cudaMemcpyAsync(h, partial[(size_t)i], (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                           streams[(size_t)i]));
+        CU(cudaStreamSynchronize(streams[(size_t)i]));
+        for (int p = 0; p < k; ++p) counts[p] += h[p];
+        cudaFree(partial[(size_t)i]);
+        {
+            std::lock_guard<std::mutex> lock(g_ws_mu);
+            auto it = g_ws.find(std::make_pair(devices[i], streams[(size_t)i]));
+            if (it != g_ws.end()) {
+                cudaFree(it->second.acc);
+                g_ws.erase(it);
+            }
+        }
+        cudaStreamDestroy(streams[(size_t)i]);
+    }
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d_counts, int accumulate,
+                              uint32_t flush, int grid, int block, void* stream) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (flush < 1 || flush > 65535)
+        return fail(POSPOP_EINVAL, "flush_threshold_blocks must be in [1, 65535], got %u", flush);
+    if (!d_counts || (!d_data && len)) return fail(POSPOP_EINVAL, "NULL pointer");
+    if ((uintptr_t)d_data % ((size_t)k / 8)) return fail(POSPOP_EINVAL, "data is misaligned");
+    if (block < 0 || block % 32 || block > 256) return fail(POSPOP_EINVAL, "block must be a multiple of 32 in [32, 256]");
+    if (grid < 0) return fail(POSPOP_EINVAL, "grid must be >= 0");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!st) {
+        Ctx* c = nullptr;
+        if ((s = get_ctx(dev, &c))) return s;
+        st = c->stream;
+    }
+    StreamWorkspace ws;
+    if ((s = stream_workspace(dev, st, &ws))) return s;
+    LaunchOptions opt;
+    opt.flush_threshold = flush;
+    opt.grid = grid;
+    opt.block = block;
+    CU(launch_stream(k, len ? d_data : (const void*)d_counts, len,
+                     reinterpret_cast<unsigned long long*>(d_counts), accumulate != 0, opt, ws, st));
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_t* d_offsets, size_t n,
+                                        uint64_t* d_counts, uint32_t flush, int grid, int block,
+                                        void* stream) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (flush < 1 || flush > 65535)
+        return fail(POSPOP_EINVAL, "flush_threshold_blocks must be in [1, 65535], got %u", flush);
+    if (n && (!d_offsets || !d_counts)) return fail(POSPOP_EINVAL, "NULL pointer");
+    if ((uintptr_t)d_data % ((size_t)k / 8)) return fail(POSPOP_EINVAL, "data is misaligned");
+    if (block < 0 || block % 32 || block > 256) return fail(POSPOP_EINVAL, "block must be a multiple of 32 in [32, 256]");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!st) {
+        Ctx* c = nullptr;
+        if ((s = get_ctx(dev, &c))) return s;
+        st = c->stream;
+    }
+    LaunchOptions opt;
+    opt.flush_threshold = flush;
+    opt.grid = grid;
+    opt.block = block;
+    CU(launch_segmented(k, d_data, reinterpret_cast<const unsigned long long*>(d_offsets), n,
+                        reinterpret_cast<unsigned long long*>(d_counts), opt, st));
+    return POSPOP_OK;
+}
+
+pospop_status pospop_generate(int kind, uint64_t seed, uint64_t base, size_t n, void* d_out, void* stream) {
+    if (kind < 1 || kind > 6) return fail(POSPOP_EINVAL, "unknown generator kind %d", kind);
+    if (!d_out && n) return fail(POSPOP_EINVAL, "NULL output");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    CU(launch_generate(kind, seed, base, n, d_out, static_cast<cudaStream_t>(stream)));
+    return POSPOP_OK;
+}
+
+pospop_status pospop_digest(const void* d_data, size_t nbytes, uint64_t* digest) {
+    if (!digest || (!d_data && nbytes)) return fail(POSPOP_EINVAL, "NULL pointer");
+    if ((uintptr_t)d_data % 8) return fail(POSPOP_EINVAL, "digest input must be 8-byte aligned");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    classify(d_data, &dev);
+    DeviceGuard g(dev);
+    Ctx* c = nullptr;
+    if ((s = get_ctx(dev, &c))) return s;
+    CU(cudaMemsetAsync(c->d_out, 0, sizeof(unsigned long long), c->stream));
+    CU(launch_digest(d_data, nbytes, c->d_out, c->stream));
+    CU(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    *digest = c->h_out[0];
+    return POSPOP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+// pospop_launch.h -- internal host-side launchers for the sm_100a kernels.
+// Plain types only; the C ABI (pospop_capi.cpp) is the only caller.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace pospop_b200 {
+
+// Persistent device scratch for one in-flight stream launch: acc[64]
+// channel totals and a completion ticket.  Both must be zero before a
+// launch; the kernel's last block leaves them zero again.
+struct StreamWorkspace {
+    unsigned long long* acc = nullptr;
+    unsigned int* ticket = nullptr;
+};
+
+struct LaunchOptions {
+    uint32_t flush_threshold = 65535;  // tree blocks between lane flushes, [1, 65535]
+    int grid = 0;                      // 0 = persistent: SMs x resident blocks
+    int block = 0;                     // 0 = default (256); multiple of 32
+    int depth = 0;                     // 0 = default tree depth (k=64: per bank)
+};
+
+// Counts len_words k-bit words at `data` (device memory, k/8-aligned) into
+// d_out[0..k).  accumulate: d_out += counts instead of d_out = counts.
+// One kernel launch.
+cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
+                          bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
+                          cudaStream_t stream);
+
+// Batched form: array a = words [d_offsets[a], d_offsets[a+1]) of `data`;
+// row a of d_out (k entries) is overwritten.  One kernel launch.
+cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets,
+                             size_t n_arrays, unsigned long long* d_out, const LaunchOptions& opt,
+                             cudaStream_t stream);
+
+// Synthetic inputs (see oracle/pospop_oracle.h orc_generate for the kinds).
+cudaError_t launch_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* out,
+                            cudaStream_t stream);
+
+// *d_digest += order-independent digest of nbytes at an 8-byte-aligned data.
+cudaError_t launch_digest(const void* data, size_t nbytes, unsigned long long* d_digest,
+                          cudaStream_t stream);
+
+// Number of kernels launched by this library in this process.
+unsigned long long kernel_launches();
+
+}  // namespace pospop_b200

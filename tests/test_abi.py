@@ -1,0 +1,112 @@
+"""CPU-side checks of the C ABI library: it loads, exports every symbol the
+header declares, validates like the reference, and refuses to count without
+a GPU (there is no CPU fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pospopcnt_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(pospop[a-z_0-9]*)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("pospopcnt_u8", "pospopcnt_u16", "pospopcnt_u32", "pospopcnt_u64", "pospopcnt_u16_config",
+                 "pospopcnt_u16_c32", "pospopcnt_segmented", "pospopcnt_sharded", "pospopcnt_async",
+                 "pospop_last_error", "pospop_validate"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(pp):
+    lib = ctypes.CDLL(pp.library_path())
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", pp.library_path()], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (\S+)", out))
+    assert set(declared_functions()) <= exported
+
+
+def test_library_is_sm100a_only(pp):
+    out = subprocess.run(["cuobjdump", "-lelf", pp.library_path()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", "")), out
+
+
+def test_sass_uses_lop3_csa_and_128bit_loads(pp):
+    sass = subprocess.run(["cuobjdump", "-sass", pp.library_path()], capture_output=True, text=True).stdout
+    assert "LOP3.LUT" in sass and "0xe8" in sass and "0x96" in sass
+    assert "LDG.E.NA.128.CONSTANT" in sass
+
+
+def test_validate_like_reference(pp):  # test_core.cpp:184-201
+    pp.validate(pp.PospopcntConfig(flush_threshold_blocks=1))
+    with pytest.raises(pp.InvalidArgument):
+        pp.validate(pp.PospopcntConfig(flush_threshold_blocks=0))
+    with pytest.raises(pp.InvalidArgument):
+        pp.validate(pp.PospopcntConfig(flush_threshold_blocks=65536))
+    with pytest.raises(pp.InvalidArgument):
+        pp.validate(pp.PospopcntConfig(register_width_bits=100))
+    pp.validate(pp.PospopcntConfig(register_width_bits=128))  # shape-valid; availability is per kernel
+
+
+def test_kernel_names_round_trip(pp):  # test_core.cpp:203-211
+    for kind in pp.KernelKind:
+        assert pp.KernelKind.from_string(str(kind)) == kind
+    assert pp.KernelKind.from_string("warp") is None
+
+
+def test_supported_widths(pp):  # test_core.cpp:213-219
+    w = pp.supported_csa_widths()
+    assert w == sorted(w) and w[0] == 64 and pp.native_csa_width() >= 64
+
+
+def test_merge_counts_and_total(pp):  # test_core.cpp:84-107
+    a = pp.PositionalCounts(range(16))
+    b = pp.PositionalCounts([3] * 16)
+    assert pp.merge_counts(a, b) == pp.merge_counts(b, a)
+    assert pp.merge_counts(pp.PositionalCounts(), a) == a
+    assert a.total() == sum(range(16))
+
+
+def test_no_gpu_means_loud_failure(pp):
+    """Without an sm_100 device the product path raises; it never counts on the CPU."""
+    if pp.device_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(pp.KernelUnavailableError):
+        pp.pospopcnt(np.arange(100, dtype=np.uint16))
+    with pytest.raises(pp.KernelUnavailableError):
+        pp.pospopcnt_k(np.zeros(64, np.uint8), 8)
+
+
+def test_argument_errors_before_device(pp):
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt_k(np.zeros(4, np.uint8), 12)
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt_k(np.zeros(8, np.uint8), 16, flush_threshold_blocks=0)
+    lib = pp._load()
+    u64 = (ctypes.c_uint64 * 16)()
+    assert lib.pospopcnt_u16(None, 5, u64) == 1  # NULL with len > 0
+    buf = np.zeros(9, np.uint8)
+    assert lib.pospopcnt_u16(ctypes.c_void_p(buf.ctypes.data + 1), 4, u64) == 1  # misaligned u16*
+
+
+def test_package_does_not_import_the_oracle():
+    """The product package must never route through the checker."""
+    pkg = os.path.join(ROOT, "paper_1911_02696_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                bad = re.search(r"import\s+pyoracle|from\s+pyoracle|#include[^\n]*pospop_oracle|liboracle\.so|"
+                                r"libpospop_ref|oracle/_ref", text)
+                assert not bad, (f, bad)

@@ -1,0 +1,338 @@
+"""Parity of the sm_100a path against the oracle and the reference's golden
+vectors.  Bit-exact (integer counts, zero tolerance).  Every call goes through
+the C ABI (libpospopcnt_b200.so) via the package's ctypes mirror."""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+COUNTRY = np.array([0x10, 0x10, 0x04, 0x10, 0x01, 0x04, 0x01, 0x01, 0x01, 0x20], np.uint16)
+
+
+@pytest.fixture(scope="module")
+def dev(pp):
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a GPU")
+    torch.cuda.set_device(0)
+    assert pp.device_available()
+    return torch.device("cuda:0")
+
+
+def to_dev(a: np.ndarray):
+    return torch.from_numpy(a.view(np.uint8).copy()).cuda()
+
+
+def guarded(a: np.ndarray, offset: int, guard: int = 64, fill: int = 0xFF):
+    """Device copy of `a` placed `offset` bytes past a 256 B-aligned base, with
+    0xFF guard bytes on both sides (an over-read would count them)."""
+    raw = a.view(np.uint8)
+    buf = torch.full((guard + offset + raw.size + guard,), fill, dtype=torch.uint8, device="cuda")
+    buf[guard + offset:guard + offset + raw.size] = torch.from_numpy(raw.copy()).cuda()
+    return buf, buf[guard + offset:guard + offset + raw.size]
+
+
+def expect(got, want):
+    assert [int(x) for x in got] == [int(x) for x in want]
+
+
+# -- reference KATs through the reference entry point --------------------------------
+
+def test_country_empty_allones(pp, dev):
+    for data in (COUNTRY, to_dev(COUNTRY)):
+        c = pp.pospopcnt(data)
+        assert c[0] == 4 and c[2] == 2 and c[4] == 3 and c[5] == 1 and c.total() == 10
+    assert pp.pospopcnt(np.zeros(0, np.uint16)) == pp.PositionalCounts()
+    assert pp.pospopcnt(torch.zeros(0, dtype=torch.int16, device="cuda")) == pp.PositionalCounts()
+    assert pp.pospopcnt(to_dev(np.array([0xFFFF], np.uint16))) == [1] * 16
+    c = pp.pospopcnt(to_dev(np.full(100, 1, np.uint16)))
+    assert c[0] == 100 and c.total() == 100
+
+
+def test_exhaustive_single_word_domain_stream(pp, dev):
+    words = np.arange(65536, dtype=np.uint16)
+    d = to_dev(words)
+    want = ((words[:, None].astype(np.uint32) >> np.arange(16)) & 1)
+    for v in range(0, 65536, 1):
+        got = pp.pospopcnt_k((d.data_ptr() + 2 * v, 1), 16)
+        assert (got.counts == want[v]).all(), v
+
+
+def test_exhaustive_single_word_domain_segmented(pp, dev):
+    words = np.arange(65536, dtype=np.uint16)
+    offs = torch.arange(65537, dtype=torch.int64, device="cuda")
+    out = torch.zeros((65536, 16), dtype=torch.int64, device="cuda")
+    pp.pospopcnt_segmented(to_dev(words), offs, 16, out=out)
+    want = ((words[:, None].astype(np.int64) >> np.arange(16)) & 1)
+    assert (out.cpu().numpy() == want).all()
+
+
+@pytest.mark.parametrize("key", ["acceptance_random", "dispatcher_random", "csa_tails", "auto_boundary"])
+def test_reference_random_streams(pp, dev, orc, golden, key):
+    for seed, n, *want in golden[key]:
+        w = orc.mt_generate_stream(seed, n)
+        expect(pp.pospopcnt(to_dev(w)), want)
+    for seed, n, *want in golden[key][:20]:  # host-memory path
+        expect(pp.pospopcnt(orc.mt_generate_stream(seed, n)), want)
+
+
+def test_concat_fork_join_order(pp, dev, orc, golden):
+    for seed, n, cut, *want in golden["concat_cuts"]:
+        d = to_dev(orc.mt_generate_stream(seed, n))
+        a = pp.pospopcnt_k((d.data_ptr(), cut), 16)
+        b = pp.pospopcnt_k((d.data_ptr() + 2 * cut, n - cut), 16)
+        expect(pp.merge_counts(a, b), want)
+    seed, n, *want = golden["fork_join"]
+    d = to_dev(orc.mt_generate_stream(seed, n))
+    parts = [pp.pospopcnt_k((d.data_ptr() + 2 * (i * n // 4), (i + 1) * n // 4 - i * n // 4), 16) for i in range(4)]
+    total = parts[0]
+    for p in parts[1:]:
+        total = pp.merge_counts(total, p)
+    expect(total, want)
+    w = orc.mt_generate_stream(17, 1234)
+    assert pp.pospopcnt(to_dev(w)) == pp.pospopcnt(to_dev(np.random.default_rng(4).permutation(w)))
+
+
+def test_cfg1_uint32_counters(pp, dev, orc, golden):
+    c = golden["cfg1"]
+    w = orc.mt_generate_stream(c["seed"], c["len"])
+    counters = np.zeros(16, np.uint32)
+    pp.pospopcnt_u16_c32(to_dev(w), counters)
+    expect(counters, c["counts"])
+    pp.pospopcnt_u16_c32(w, counters)  # Fig. 6 accumulates
+    expect(counters, [2 * x for x in c["counts"]])
+
+
+def test_config_errors_like_reference(pp, dev):  # test_core.cpp:184-201
+    w = to_dev(np.zeros(8, np.uint16))
+    with pytest.raises(pp.KernelUnavailableError):
+        pp.pospopcnt(w, pp.PospopcntConfig(kernel=pp.KernelKind.Csa16, register_width_bits=128))
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt(w, pp.PospopcntConfig(flush_threshold_blocks=0))
+    with pytest.raises(pp.KernelUnavailableError):
+        pp.pospopcnt(w, pp.PospopcntConfig(kernel=pp.KernelKind.Forest, register_width_bits=256))
+    for kind in pp.KernelKind:  # every kind yields identical counts
+        for width in [0] + pp.supported_csa_widths():
+            if kind == pp.KernelKind.Forest and width > 64:
+                continue
+            if kind == pp.KernelKind.ByteBlend and width == 512:
+                continue
+            assert pp.pospopcnt(w, pp.PospopcntConfig(kernel=kind, register_width_bits=width)).total() == 0
+
+
+# -- forced flushes, lane saturation --------------------------------------------------------
+
+def test_forced_flush_thresholds(pp, dev, orc, golden):
+    for key in ("acceptance_flush3", "csa_flush3"):
+        for seed, n, *want in golden[key]:
+            d = to_dev(orc.mt_generate_stream(seed, n))
+            for thr in (1, 2, 3):
+                expect(pp.pospopcnt(d, pp.PospopcntConfig(kernel=pp.KernelKind.Csa16,
+                                                          flush_threshold_blocks=thr)), want)
+                out = torch.zeros(16, dtype=torch.int64, device="cuda")
+                for grid, block in ((1, 32), (1, 64), (3, 96), (0, 0)):
+                    pp.count_async(d, out, 16, flush_threshold_blocks=thr, grid=grid, block=block)
+                    torch.cuda.synchronize()
+                    expect(out.cpu().numpy(), want)
+    seed, n, *want = golden["csa_flush1"]
+    expect(pp.pospopcnt(to_dev(orc.mt_generate_stream(seed, n)), pp.PospopcntConfig(flush_threshold_blocks=1)),
+           want)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_forced_flush_all_k_small_grid(pp, dev, orc, k):
+    raw = orc.generate(6, 7, 1 << 17).view(np.uint8)
+    d = to_dev(raw)
+    want = orc.naive(raw, k)
+    out = torch.zeros(k, dtype=torch.int64, device="cuda")
+    for thr in (1, 3, 7, 65535):
+        for grid, block in ((1, 32), (2, 128), (5, 256)):
+            pp.count_async(d, out, k, flush_threshold_blocks=thr, grid=grid, block=block)
+            torch.cuda.synchronize()
+            expect(out.cpu().numpy(), want)
+
+
+def test_lane_saturation_single_warp(pp, dev):
+    """test_csa.cpp:294-305 on the GPU: one CTA of 32 threads over all-ones
+    input, > 65535 tree blocks per thread, so every 16-bit lane reaches 65535
+    before the flush; one more block plus a tail proves no lane wrapped."""
+    per_block_bytes = 32 * 256  # 32 threads x 64 registers x 4 B (depth 6)
+    nbytes = per_block_bytes * 65537 + 6
+    d = torch.full((nbytes,), 0xFF, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(16, dtype=torch.int64, device="cuda")
+    pp.count_async(d, out, 16, grid=1, block=32)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == nbytes // 2).all()
+    out8 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    pp.count_async(d, out8, 8, grid=1, block=32)
+    torch.cuda.synchronize()
+    assert (out8.cpu().numpy() == nbytes).all()
+
+
+# -- ragged lengths x unaligned starts, all k -------------------------------------------------
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_lengths_and_offsets(pp, dev, orc, k):
+    wb = k // 8
+    rng = np.random.default_rng(k)
+    raw = orc.generate(6, 11, 1 << 13).view(np.uint8)  # 64 KiB of random bytes
+    lengths = list(range(0, 70)) + [255, 256, 257, 1023, 1024, 1025, 4095, 4096, 4097] + \
+        [int(x) for x in rng.integers(0, raw.size // wb - 8, size=30)]
+    for offset in range(0, 16, wb):
+        for n in lengths:
+            sub = raw[:n * wb]
+            buf, view = guarded(sub, offset)
+            got = pp.pospopcnt_k(view, k)
+            assert got == orc.naive(sub, k), (k, offset, n)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_medium_random_vs_oracle(pp, dev, orc, k):
+    raw = orc.generate(6, 5, (3 << 20) + 5).view(np.uint8)
+    for n_bytes in (1 << 20, (1 << 21) + 24, raw.size - 8):
+        n = n_bytes // (k // 8)
+        sub = raw[:n * k // 8]
+        for offset in (0, 8):
+            _, view = guarded(sub, offset)
+            assert pp.pospopcnt_k(view, k) == orc.pospopcnt(sub, k, threads=4), (k, n, offset)
+
+
+# -- host-memory (staged) path -----------------------------------------------------------------
+
+def test_host_pageable_and_pinned_multi_chunk(pp, dev, orc):
+    n = (150 << 20) // 2 + 7  # > two 64 MiB staging chunks, ragged
+    w = orc.generate(4, 3, n, threads=8)
+    want = orc.pospopcnt(w, 16, threads=8)
+    assert pp.pospopcnt(w) == want
+    pinned = torch.empty(n, dtype=torch.int16).pin_memory()
+    pinned.numpy().view(np.uint16)[:] = w
+    assert pp.pospopcnt(pinned) == want
+    b = orc.generate(3, 9, (70 << 20) + 3, threads=8)
+    assert pp.pospopcnt_k(b[3:], 8) == orc.pospopcnt(b[3:], 8, threads=8)
+
+
+def test_threads_are_independent(pp, dev, orc):
+    data = [orc.generate(6, s, 1 << 18) for s in range(6)]
+    want = [orc.naive(d, 64) for d in data]
+    errors = []
+
+    def worker(i):
+        try:
+            d = to_dev(data[i])
+            for _ in range(5):
+                if pp.pospopcnt_k(d, 64) != want[i]:
+                    errors.append(i)
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors
+
+
+def test_async_accumulate(pp, dev, orc):
+    w = orc.generate(1, 2, 1 << 20)
+    d = to_dev(w)
+    out = torch.zeros(16, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pp.count_async(d, out, 16, stream=s)
+        pp.count_async(d, out, 16, accumulate=True, stream=s)
+    s.synchronize()
+    assert (out.cpu().numpy() == 2 * orc.naive(w).astype(np.int64)).all()
+
+
+# -- segmented ---------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_segmented_ragged(pp, dev, orc, k):
+    rng = np.random.default_rng(100 + k)
+    n_words = 200_000
+    data = orc.generate(6, 13, n_words * k // 64 + 1).view(DT[k])[:n_words]
+    cuts = np.sort(rng.integers(0, n_words, size=3000))
+    offs = np.concatenate([[0], cuts, [n_words], [n_words]]).astype(np.uint64)  # includes empty arrays
+    got = pp.pospopcnt_segmented(to_dev(data), torch.from_numpy(offs.view(np.int64)).cuda(), k)
+    want = orc.segmented(data, offs, k, threads=8)
+    assert (got == want).all()
+    # host inputs too
+    assert (pp.pospopcnt_segmented(data, offs, k) == want).all()
+
+
+DT = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}
+
+
+# -- generators: device bytes == oracle bytes ------------------------------------------------
+
+def test_device_generators_match_oracle(pp, dev, orc, golden_generators):
+    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8}
+    for key, v in golden_generators.items():
+        kind, seed, base = (int(x) for x in key.split(":"))
+        buf = torch.zeros((1 << 16) * esize[kind] + 8, dtype=torch.uint8, device="cuda")
+        pp.generate(kind, seed, buf, base=base, n=1 << 16)
+        torch.cuda.synchronize()
+        host = buf[:(1 << 16) * esize[kind]].cpu().numpy()
+        assert pp.digest(buf[:(1 << 16) * esize[kind]]) == v["digest"], key
+        assert orc.digest(host) == v["digest"], key
+
+
+# -- full-size BASELINE.json configs ------------------------------------------------------------
+
+def test_cfg2_one_hot_zipf_full(pp, dev, orc):
+    n = 1 << 28
+    d = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_CFG2, 1, d)
+    c = pp.pospopcnt(d)
+    assert c.total() == n  # one-hot: exactly one bit per word
+    assert c[0] > c[1] > c[2] > c[15]
+    host = d.cpu().numpy().view(np.uint16)
+    assert c == orc.pospopcnt(host, 16, threads=16)
+
+
+def test_cfg3_bytes_offset3_full(pp, dev, orc):
+    buf = torch.full(((1 << 30) + 64,), 0xFF, dtype=torch.uint8, device="cuda")
+    n = (1 << 30) - 7
+    pp.generate(pp.GEN_CFG3, 1, buf[3:3 + n])
+    got = pp.pospopcnt_k(buf[3:3 + n], 8)
+    host = buf.cpu().numpy()
+    assert host[0] == 0xFF and host[3 + n] == 0xFF  # guards intact
+    assert got == orc.pospopcnt(host[3:3 + n], 8, threads=16)
+
+
+def test_cfg4_bernoulli_full_and_sharded(pp, dev, orc):
+    n = 1 << 32
+    d = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_CFG4, 1, d)
+    whole = pp.pospopcnt(d)
+    for g in (2, 4, 8):  # shard boundaries as the G-GPU layout, all on device 0
+        shards = [d[i * n // g:(i + 1) * n // g] for i in range(g)]
+        assert pp.pospopcnt_sharded(shards, [0] * g) == whole
+    # shard-local generation (index_base) gives the same bytes as the whole stream
+    part = torch.empty(n // 8, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_CFG4, 1, part, base=3 * (n // 8))
+    assert torch.equal(part, d[3 * (n // 8):4 * (n // 8)])
+    host = d.cpu().numpy().view(np.uint16)
+    del d
+    assert whole == orc.pospopcnt(host, 16, threads=16)
+    assert abs(whole.total() / (16 * n) - 6554 / 65536) < 1e-4
+
+
+@pytest.mark.parametrize("k,kind", [(32, 5), (64, 6)])
+def test_cfg5_segmented_full(pp, dev, orc, k, kind):
+    arrays, words = 65536, 4096
+    d = torch.empty(arrays * words * k // 8, dtype=torch.uint8, device="cuda")
+    pp.generate(kind, 1, d)
+    offs = torch.arange(0, arrays + 1, dtype=torch.int64, device="cuda") * words
+    out = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
+    pp.segmented_async(d, offs, out, k)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint64)
+    host = d.cpu().numpy().view(DT[k])
+    want = orc.segmented(host, offs.cpu().numpy().view(np.uint64), k, threads=16)
+    assert (got == want).all()
+    assert (got.sum(1) == np.bitwise_count(host.reshape(arrays, words)).sum(1)).all()
