@@ -161,12 +161,9 @@ def cpu_reference_measure(k: int, gen_kind: int, sample_words: int, reps: int, t
         ref = pyoracle.Reference()
         kind = "reference"
 
-        def run(nthreads):
-            if k == 16:
-                return ref.pospopcnt_mt(words16, nthreads)
-            return ref.pospopcnt_mt(words16, nthreads)  # k=8 fold: 16-bit counts folded below
+        def run(nthreads):  # k=8 runs the 16-bit API and folds below
+            return ref.pospopcnt_mt(words16, nthreads)
     except Exception:
-        ref = None
         kind = "port"
 
         def run(nthreads):

@@ -27,6 +27,10 @@
  *    copy/compute overlap).  The classification uses cudaPointerGetAttributes.
  *  - Every call is synchronous, thread-safe and re-entrant (per-thread,
  *    per-device workspaces and streams), like the reference.
+ *    Synchronous calls on device memory are ordered after prior work on the
+ *    legacy default stream; data produced on another (non-blocking) stream
+ *    must be synchronised by the caller, or counted with pospopcnt_async on
+ *    the producing stream.
  *  - No exception or CUDA error crosses the ABI; failures return a status
  *    and set a thread-local message (pospop_last_error).  There is NO CPU
  *    fallback: without a usable sm_100 device every counting call returns
@@ -138,11 +142,12 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
 /* ---- asynchronous device-resident entry points (timing / integration) --- */
 
 /* Enqueues one count of device-resident data on `stream` (a cudaStream_t,
- * NULL = the calling thread's per-device stream); d_counts (k u64 in device
+ * used verbatim: NULL = the legacy default stream); d_counts (k u64 in device
  * memory on the current device) is overwritten, or accumulated when
- * accumulate != 0.  Returns without synchronising.  At most one launch per
- * (device, stream) may be in flight through this entry point at a time
- * (the workspace is per stream); grid/block 0 = automatic. */
+ * accumulate != 0.  Returns without synchronising.  Each (device, stream)
+ * pair owns one small workspace, so launches on one stream are serialised by
+ * stream order and launches on different streams never share state;
+ * grid/block 0 = automatic. */
 pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
                               int accumulate, uint32_t flush_threshold_blocks, int grid, int block,
                               void* stream);

@@ -133,8 +133,10 @@ pospop_status get_ctx(int dev, Ctx** out) {
     DeviceGuard g(dev);
     Ctx* c = new Ctx;
     c->dev = dev;
-    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    CU(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    // Blocking streams: synchronous entry points are ordered after prior work
+    // on the legacy default stream (where callers typically produced the data).
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault));
+    CU(cudaStreamCreateWithFlags(&c->copy, cudaStreamDefault));
     CU(cudaMalloc(&c->d_out, 64 * sizeof(unsigned long long)));
     CU(cudaMallocHost(&c->h_out, 64 * sizeof(unsigned long long)));
     if ((s = alloc_workspace(&c->ws))) return s;
@@ -433,7 +435,7 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
         if ((s = get_ctx(d, &ctxs[(size_t)i]))) return s;
         // Each shard gets its own stream + workspace so shards on one device
         // may run back to back without sharing a ticket.
-        CU(cudaStreamCreateWithFlags(&streams[(size_t)i], cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&streams[(size_t)i], cudaStreamDefault));
         StreamWorkspace ws;
         if ((s = stream_workspace(d, streams[(size_t)i], &ws))) return s;
         CU(cudaMalloc(&partial[(size_t)i], 64 * sizeof(unsigned long long)));
@@ -477,12 +479,8 @@ pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d
     int dev = 0;
     pospop_status s = current_device(&dev);
     if (s) return s;
+    // The stream is used verbatim: NULL is the legacy default stream.
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (!st) {
-        Ctx* c = nullptr;
-        if ((s = get_ctx(dev, &c))) return s;
-        st = c->stream;
-    }
     StreamWorkspace ws;
     if ((s = stream_workspace(dev, st, &ws))) return s;
     LaunchOptions opt;
@@ -506,12 +504,7 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
     int dev = 0;
     pospop_status s = current_device(&dev);
     if (s) return s;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (!st) {
-        Ctx* c = nullptr;
-        if ((s = get_ctx(dev, &c))) return s;
-        st = c->stream;
-    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     LaunchOptions opt;
     opt.flush_threshold = flush;
     opt.grid = grid;
