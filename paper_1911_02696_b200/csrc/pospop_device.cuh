@@ -107,15 +107,51 @@ __device__ __forceinline__ uint32_t bank_warp_total(const uint32_t (&counter)[16
 }
 
 // ---------------------------------------------------------------------------
-// Streaming 128-bit load: read-only path, no L1 allocation (each byte is
-// touched exactly once).
+// Streaming vector loads: read-only path, no L1 allocation (each byte is
+// touched exactly once).  VB = 16 -> LDG.E.NA.128 (512 B per warp),
+// VB = 32 -> LDG.E.NA.256 (1 KiB per warp; Blackwell's 256-bit load).
+// HINT 0: default L2 policy; 1: L2 evict_first (256-bit form only);
+// 2: L2 256 B prefetch hint (128-bit form only).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-    uint4 v;
-    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
+template <int VB, int HINT>
+__device__ __forceinline__ void ldg_stream(const uint8_t* p, uint32_t (&r)[VB / 4]) {
+    static_assert(VB == 16 || VB == 32, "vector width");
+    if constexpr (VB == 16) {
+        if constexpr (HINT == 2) {
+            asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p));
+        } else {
+            asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p));
+        }
+    } else {
+        if constexpr (HINT == 1) {
+            asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                  "=r"(r[7])
+                : "l"(p));
+        } else {
+            asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                  "=r"(r[7])
+                : "l"(p));
+        }
+    }
+}
+
+// Keeps only bytes [lo, hi) of a VB-byte vector (0 <= lo <= hi <= VB).
+// Zeroed bytes contribute nothing to any positional count, so masked
+// vectors replace scalar head/tail loops for unaligned starts and ragged ends.
+template <int VB>
+__device__ __forceinline__ void mask_bytes(uint32_t (&r)[VB / 4], int lo, int hi) {
+#pragma unroll
+    for (int j = 0; j < VB / 4; ++j) {
+        const int a = min(max(lo - 4 * j, 0), 4);
+        const int b = min(max(hi - 4 * j, 0), 4);
+        const uint32_t below_b = b >= 4 ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u);
+        const uint32_t below_a = a >= 4 ? 0xFFFFFFFFu : ((1u << (8 * a)) - 1u);
+        r[j] &= below_b & ~below_a;
+    }
 }
 
 // ---------------------------------------------------------------------------

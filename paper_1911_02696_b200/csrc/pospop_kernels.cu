@@ -25,6 +25,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "pospop_device.cuh"
@@ -36,13 +37,17 @@ namespace {
 
 std::atomic<unsigned long long> g_launches{0};
 
+// The stream is addressed in VB-byte vectors from `base`, the largest
+// 32*VB-aligned address <= data.  Vectors [v0, v1) hold the data; the first
+// and last are byte-masked to [lo_byte, VB) and [0, hi_byte), so unaligned
+// starts and ragged ends need no scalar code, and every warp load (32
+// consecutive vectors) stays 32*VB-aligned.  Vector indices below v0 are
+// never dereferenced.  Work is split over CTAs in whole groups of 32 vectors.
 struct StreamArgs {
-    const uint4* body;        // 16 B aligned
-    unsigned long long nvec;  // 16 B vectors in the body
-    const uint8_t* head;      // words before the body
-    const uint8_t* tail;      // words after the body
-    uint32_t head_bytes;
-    uint32_t tail_bytes;
+    const uint8_t* base;
+    unsigned long long v0, v1;  // valid vectors
+    unsigned long long g0, ng;  // first group, number of groups
+    int lo_byte, hi_byte;       // valid bytes of vector v0 / vector v1-1
     int k;
     uint32_t flush_threshold;
     unsigned long long* acc;
@@ -50,14 +55,6 @@ struct StreamArgs {
     unsigned long long* out;
     int accumulate;
 };
-
-// Bit `pos` of every little-endian wb-byte word in [p, p + nbytes).
-__device__ __forceinline__ unsigned long long count_pos_words(const uint8_t* p, uint32_t nbytes,
-                                                             int wb, int pos) {
-    unsigned long long c = 0;
-    for (uint32_t i = 0; i + wb <= nbytes; i += wb) c += (p[i + (pos >> 3)] >> (pos & 7)) & 1u;
-    return c;
-}
 
 // Channel -> position fold: the channels (of 32 * NBANK) that count position
 // p are p + m * k for m = 0 .. 32/k - 1 (k <= 32), or channel p (k = 64).
@@ -82,20 +79,26 @@ __device__ __forceinline__ void zero_bank(uint32_t (&counter)[NBANK][16]) {
         for (int p = 0; p < 16; ++p) counter[b][p] = 0;
 }
 
-template <int NBANK, int L>
-__global__ void __launch_bounds__(256) stream_kernel(const StreamArgs a) {
+// BLOCK > 0: compile-time block size (immediate load offsets); BLOCK == 0:
+// runtime blockDim.x (used for small test launches).
+template <int NBANK, int L, int VB, int HINT, int BLOCK>
+__global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const StreamArgs a) {
     constexpr int REGS = NBANK << L;  // 32-bit input registers per tree block
-    constexpr int V = REGS / 4;       // 128-bit vectors per tree block
-    static_assert(V >= 1, "tree must consume at least one 128-bit vector");
+    constexpr int RPV = VB / 4;       // registers per vector
+    constexpr int VPT = REGS / RPV;   // vectors per thread per tree block
+    static_assert(VPT >= 1, "tree must consume at least one vector");
+    const unsigned block = BLOCK > 0 ? (unsigned)BLOCK : blockDim.x;
 
     __shared__ unsigned long long s_acc[32 * NBANK];
     __shared__ int s_last;
-    for (int i = threadIdx.x; i < 32 * NBANK; i += blockDim.x) s_acc[i] = 0;
+    for (int i = threadIdx.x; i < 32 * NBANK; i += block) s_acc[i] = 0;
     __syncthreads();
 
-    const unsigned long long tile = (unsigned long long)V * blockDim.x;
-    const unsigned long long begin = a.nvec * blockIdx.x / gridDim.x;
-    const unsigned long long end = a.nvec * (blockIdx.x + 1) / gridDim.x;
+    const unsigned long long tile = (unsigned long long)VPT * block;
+    const unsigned long long gb = a.g0 + a.ng * blockIdx.x / gridDim.x;
+    const unsigned long long ge = a.g0 + a.ng * (blockIdx.x + 1) / gridDim.x;
+    const unsigned long long S = gb * 32;
+    const unsigned long long E = ge * 32 < a.v1 ? ge * 32 : a.v1;
     const uint32_t lane = threadIdx.x & 31u;
 
     uint32_t carries[NBANK][L];
@@ -107,47 +110,46 @@ __global__ void __launch_bounds__(256) stream_kernel(const StreamArgs a) {
     zero_bank<NBANK>(counter);
     uint32_t nb = 0;
 
-    auto flush = [&](int shift) {
-        uint32_t d[16];
-#pragma unroll
-        for (int p = 0; p < 16; ++p) d[p] = 0;
-#pragma unroll
-        for (int b = 0; b < NBANK; ++b) {
-            const uint32_t t = bank_warp_total(counter[b], shift, d);
-            if (t) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)t);
-        }
-        zero_bank<NBANK>(counter);
-        nb = 0;
-    };
-
-    unsigned long long base = begin;
-    const uint4* p = a.body + threadIdx.x;
-    for (; base + tile <= end; base += tile) {
+    for (unsigned long long t = S; t < E; t += tile) {
         uint32_t r[REGS];
+        if (t >= a.v0 && t + tile <= E) {  // interior tile: unpredicated, immediate offsets
+            const uint8_t* p = a.base + (t + threadIdx.x) * VB;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const uint4 x = ldg_stream(p + base + (unsigned long long)v * blockDim.x);
-            r[4 * v + 0] = x.x;
-            r[4 * v + 1] = x.y;
-            r[4 * v + 2] = x.z;
-            r[4 * v + 3] = x.w;
+            for (int v = 0; v < VPT; ++v) {
+                uint32_t x[RPV];
+                ldg_stream<VB, HINT>(p + (unsigned long long)v * block * VB, x);
+#pragma unroll
+                for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+            }
+        } else {  // edge tile: predicated loads, byte masks on the first/last vector
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) {
+                const unsigned long long idx = t + (unsigned long long)v * block + threadIdx.x;
+                uint32_t x[RPV];
+#pragma unroll
+                for (int j = 0; j < RPV; ++j) x[j] = 0;
+                if (idx >= a.v0 && idx < E) {
+                    ldg_stream<VB, HINT>(a.base + idx * VB, x);
+                    if (idx == a.v0 || idx + 1 == a.v1)
+                        mask_bytes<VB>(x, idx == a.v0 ? a.lo_byte : 0, idx + 1 == a.v1 ? a.hi_byte : VB);
+                }
+#pragma unroll
+                for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+            }
         }
         tree_block<NBANK, L>(r, carries, counter);
-        if (++nb == a.flush_threshold) flush(L);
-    }
-    if (base < end) {  // partial tile: zero inputs leave every count unchanged
-        uint32_t r[REGS];
+        if (++nb == a.flush_threshold) {  // block-uniform: every thread runs the same tiles
+            uint32_t d[16];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const unsigned long long idx = base + (unsigned long long)v * blockDim.x + threadIdx.x;
-            const uint4 x = idx < end ? ldg_stream(a.body + idx) : make_uint4(0u, 0u, 0u, 0u);
-            r[4 * v + 0] = x.x;
-            r[4 * v + 1] = x.y;
-            r[4 * v + 2] = x.z;
-            r[4 * v + 3] = x.w;
+            for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) {
+                const uint32_t tot = bank_warp_total(counter[b], L, d);
+                if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
+            }
+            zero_bank<NBANK>(counter);
+            nb = 0;
         }
-        tree_block<NBANK, L>(r, carries, counter);
-        if (++nb == a.flush_threshold) flush(L);
     }
 
     // Final flush of the lane bank (weight 2^L) fused with the carry drain.
@@ -155,12 +157,12 @@ __global__ void __launch_bounds__(256) stream_kernel(const StreamArgs a) {
     for (int b = 0; b < NBANK; ++b) {
         uint32_t d[16];
         drain<L>(d, carries[b]);
-        const uint32_t t = bank_warp_total(counter[b], L, d);
-        if (t) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)t);
+        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
     }
     __syncthreads();
 
-    for (int c = threadIdx.x; c < 32 * NBANK; c += blockDim.x)
+    for (int c = threadIdx.x; c < 32 * NBANK; c += block)
         if (s_acc[c]) atomicAdd(&a.acc[c], s_acc[c]);
     __threadfence();
     __syncthreads();
@@ -168,11 +170,11 @@ __global__ void __launch_bounds__(256) stream_kernel(const StreamArgs a) {
     __syncthreads();
     if (!s_last) return;
 
-    // Last CTA: every other CTA has fenced its channel atomics.
+    // Last CTA: every other CTA has fenced its channel atomics.  Fold the
+    // channels to positions, reading and re-zeroing the accumulator.
     __threadfence();
     const int k = a.k;
-    const int wb = k >> 3;
-    for (int pos = threadIdx.x; pos < k; pos += blockDim.x) {
+    for (int pos = threadIdx.x; pos < k; pos += block) {
         unsigned long long sum = 0;
         if (k == 64) {
             sum = atomicExch(&a.acc[pos], 0ull);
@@ -180,34 +182,37 @@ __global__ void __launch_bounds__(256) stream_kernel(const StreamArgs a) {
             const int m = channels_per_position(k);
             for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
         }
-        sum += count_pos_words(a.head, a.head_bytes, wb, pos);
-        sum += count_pos_words(a.tail, a.tail_bytes, wb, pos);
         a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
     }
     if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
-template <int NBANK, int L>
+// One warp per array.  Array a spans bytes [data + off[a]*wb, data + off[a+1]*wb);
+// it is read as VB-byte vectors from the VB-aligned address at or below its
+// start, the first/last vector byte-masked, 32 lanes x VPT vectors per step.
+template <int NBANK, int L, int VB>
 __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
                                                         const unsigned long long* offsets,
                                                         unsigned long long n_arrays, int k,
                                                         uint32_t flush_threshold,
                                                         unsigned long long* out) {
     constexpr int REGS = NBANK << L;
-    constexpr int V = REGS / 4;
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr unsigned long long STEP = 32ull * VPT;
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     const int wb = k >> 3;
 
     for (unsigned long long arr = warp; arr < n_arrays; arr += nwarps) {
-        const uint8_t* start = data + offsets[arr] * wb;
-        const uint8_t* stop = data + offsets[arr + 1] * wb;
-        const uint8_t* bstart = (const uint8_t*)(((uintptr_t)start + 15) & ~(uintptr_t)15);
-        const uint8_t* bstop = (const uint8_t*)((uintptr_t)stop & ~(uintptr_t)15);
-        if (bstart > bstop) bstart = bstop = stop;  // shorter than one aligned vector: all head
-        const uint4* body = (const uint4*)bstart;
-        const unsigned long long nvec = (unsigned long long)(bstop - bstart) >> 4;
+        const uintptr_t P = (uintptr_t)(data + offsets[arr] * wb);
+        const uintptr_t Q = (uintptr_t)(data + offsets[arr + 1] * wb);
+        const uintptr_t B = P & ~(uintptr_t)(VB - 1);
+        const unsigned long long nv = Q > P ? (Q - B + VB - 1) / VB : 0;
+        const int lo = (int)(P - B);
+        const int hi = nv ? (int)(Q - (B + (nv - 1) * VB)) : VB;
+        const uint8_t* base = (const uint8_t*)B;
 
         uint32_t carries[NBANK][L];
         uint32_t counter[NBANK][16];
@@ -221,19 +226,33 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
 #pragma unroll
         for (int b = 0; b < NBANK; ++b) tot[b] = 0;
 
-        for (unsigned long long base = 0; base < nvec; base += 32ull * V) {
+        for (unsigned long long t = 0; t < nv; t += STEP) {
             uint32_t r[REGS];
+            if (t > 0 && t + STEP < nv) {  // interior: neither the first nor the last vector
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const unsigned long long idx = base + 32ull * v + lane;
-                const uint4 x = idx < nvec ? ldg_stream(body + idx) : make_uint4(0u, 0u, 0u, 0u);
-                r[4 * v + 0] = x.x;
-                r[4 * v + 1] = x.y;
-                r[4 * v + 2] = x.z;
-                r[4 * v + 3] = x.w;
+                for (int v = 0; v < VPT; ++v) {
+                    uint32_t x[RPV];
+                    ldg_stream<VB, 0>(base + (t + 32ull * v + lane) * VB, x);
+#pragma unroll
+                    for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) {
+                    const unsigned long long idx = t + 32ull * v + lane;
+                    uint32_t x[RPV];
+#pragma unroll
+                    for (int j = 0; j < RPV; ++j) x[j] = 0;
+                    if (idx < nv) {
+                        ldg_stream<VB, 0>(base + idx * VB, x);
+                        if (idx == 0 || idx + 1 == nv) mask_bytes<VB>(x, idx == 0 ? lo : 0, idx + 1 == nv ? hi : VB);
+                    }
+#pragma unroll
+                    for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+                }
             }
             tree_block<NBANK, L>(r, carries, counter);
-            if (++nb == flush_threshold) {
+            if (++nb == flush_threshold) {  // warp-uniform: nv is per array
                 uint32_t d[16];
 #pragma unroll
                 for (int p = 0; p < 16; ++p) d[p] = 0;
@@ -252,19 +271,13 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
 
         // lane c holds channel c (bank b: channel 32b + c).  Fold to positions.
         unsigned long long* row = out + arr * (unsigned long long)k;
-        if (NBANK == 2) {  // k == 64
-#pragma unroll
-            for (int b = 0; b < NBANK; ++b) {
-                const int pos = 32 * b + lane;
-                row[pos] = tot[b] + count_pos_words(start, (uint32_t)(bstart - start), wb, pos) +
-                           count_pos_words(bstop, (uint32_t)(stop - bstop), wb, pos);
-            }
+        if (NBANK == 2) {  // k == 64: lane c -> positions c and 32 + c
+            row[lane] = tot[0];
+            row[32 + lane] = tot[NBANK - 1];
         } else {
             unsigned long long t = tot[0];
             for (int w = 16; w >= k; w >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, w);
-            if ((int)lane < k)
-                row[lane] = t + count_pos_words(start, (uint32_t)(bstart - start), wb, lane) +
-                            count_pos_words(bstop, (uint32_t)(stop - bstop), wb, lane);
+            if ((int)lane < k) row[lane] = t;
         }
     }
 }
@@ -375,43 +388,51 @@ int resident_blocks(Kernel kernel, int block) {
 
 using StreamKernel = void (*)(const StreamArgs);
 
-StreamKernel pick_stream(int nbank, int depth) {
-    if (nbank == 1) {
-        switch (depth) {
-            case 3: return stream_kernel<1, 3>;
-            case 4: return stream_kernel<1, 4>;
-            case 5: return stream_kernel<1, 5>;
-            case 7: return stream_kernel<1, 7>;
-            default: return stream_kernel<1, 6>;
-        }
-    }
-    switch (depth) {
-        case 2: return stream_kernel<2, 2>;
-        case 3: return stream_kernel<2, 3>;
-        case 4: return stream_kernel<2, 4>;
-        case 6: return stream_kernel<2, 6>;
-        default: return stream_kernel<2, 5>;
-    }
+struct StreamVariant {
+    int nbank, depth, vb, hint, block;
+    StreamKernel fn;
+};
+
+#define SV(NB, L, VB, H, B) {NB, L, VB, H, B, stream_kernel<NB, L, VB, H, B>}
+// Production variants first (the defaults), then tuning variants selectable
+// through POSPOP_STREAM_VARIANT="depth,vb,hint,block".
+const StreamVariant kStreamVariants[] = {
+    SV(1, 6, 16, 0, 256), SV(2, 5, 16, 0, 256),  // defaults (k <= 32 / k = 64)
+    SV(1, 6, 16, 0, 0), SV(2, 5, 16, 0, 0),      // runtime block size
+    SV(1, 6, 32, 0, 0), SV(2, 5, 32, 0, 0),
+    SV(1, 6, 16, 2, 256), SV(1, 6, 32, 0, 256), SV(1, 6, 32, 1, 256),
+    SV(1, 5, 32, 0, 256), SV(1, 7, 32, 0, 256), SV(1, 5, 16, 0, 256),
+    SV(1, 6, 32, 0, 128), SV(1, 6, 32, 0, 512), SV(1, 6, 16, 0, 512), SV(1, 6, 16, 0, 128),
+    SV(2, 5, 32, 0, 256), SV(2, 4, 32, 0, 256), SV(2, 4, 16, 0, 256),
+};
+#undef SV
+
+const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block) {
+    for (const StreamVariant& v : kStreamVariants)
+        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.hint == hint && v.block == block) return &v;
+    return nullptr;
 }
 
 using SegKernel = void (*)(const uint8_t*, const unsigned long long*, unsigned long long, int, uint32_t,
                            unsigned long long*);
 
-SegKernel pick_segmented(int nbank, int depth) {
-    if (nbank == 1) {
-        switch (depth) {
-            case 3: return segmented_kernel<1, 3>;
-            case 4: return segmented_kernel<1, 4>;
-            case 6: return segmented_kernel<1, 6>;
-            default: return segmented_kernel<1, 5>;
-        }
-    }
-    switch (depth) {
-        case 2: return segmented_kernel<2, 2>;
-        case 3: return segmented_kernel<2, 3>;
-        case 5: return segmented_kernel<2, 5>;
-        default: return segmented_kernel<2, 4>;
-    }
+struct SegVariant {
+    int nbank, depth, vb;
+    SegKernel fn;
+};
+
+#define SG(NB, L, VB) {NB, L, VB, segmented_kernel<NB, L, VB>}
+const SegVariant kSegVariants[] = {
+    SG(1, 5, 16), SG(2, 4, 16),  // defaults
+    SG(1, 4, 16), SG(1, 6, 16), SG(1, 5, 32), SG(1, 6, 32), SG(2, 3, 16), SG(2, 5, 16), SG(2, 4, 32),
+    SG(2, 5, 32),
+};
+#undef SG
+
+const SegVariant* pick_segmented(int nbank, int depth, int vb) {
+    for (const SegVariant& v : kSegVariants)
+        if (v.nbank == nbank && v.depth == depth && v.vb == vb) return &v;
+    return nullptr;
 }
 
 }  // namespace
@@ -422,24 +443,35 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
                           bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
                           cudaStream_t stream) {
     const int nbank = k == 64 ? 2 : 1;
-    const int depth = opt.depth ? opt.depth
-                                : env_int("POSPOP_TREE_DEPTH", nbank == 1 ? kDefaultDepth1 : kDefaultDepth2);
-    const int block = opt.block ? opt.block : env_int("POSPOP_BLOCK", kDefaultBlock);
-    StreamKernel kernel = pick_stream(nbank, depth);
+    // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block".
+    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 16, hint = 0, block = kDefaultBlock;
+    if (const char* v = std::getenv("POSPOP_STREAM_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &hint, &block);
+    if (opt.depth) depth = opt.depth;
+    if (opt.block) block = 0;  // explicit (test) block size: the runtime-block instantiation
+    const StreamVariant* var = pick_stream(nbank, depth, vb, hint, block);
+    if (!var) var = pick_stream(nbank, depth, vb, 0, 0);
+    if (!var) return cudaErrorInvalidConfiguration;
+    const int threads = var->block ? var->block : (opt.block ? opt.block : kDefaultBlock);
 
-    const uint8_t* p = static_cast<const uint8_t*>(data);
+    const uintptr_t P = reinterpret_cast<uintptr_t>(data);
     const size_t nbytes = len_words * (size_t)(k / 8);
-    const uint8_t* bstart = (const uint8_t*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    const uint8_t* bstop = (const uint8_t*)((uintptr_t)(p + nbytes) & ~(uintptr_t)15);
-    if (bstart > bstop || nbytes == 0) bstart = bstop = p + nbytes;
-
+    const uintptr_t VBu = (uintptr_t)var->vb;
+    const uintptr_t group = 32 * VBu;
     StreamArgs a;
-    a.body = reinterpret_cast<const uint4*>(bstart);
-    a.nvec = (unsigned long long)(bstop - bstart) >> 4;
-    a.head = p;
-    a.head_bytes = (uint32_t)(bstart - p);
-    a.tail = bstop;
-    a.tail_bytes = (uint32_t)(p + nbytes - bstop);
+    a.base = reinterpret_cast<const uint8_t*>(P & ~(group - 1));
+    if (nbytes == 0) {
+        a.v0 = a.v1 = a.g0 = a.ng = 0;
+        a.lo_byte = 0;
+        a.hi_byte = (int)VBu;
+    } else {
+        const uintptr_t B = reinterpret_cast<uintptr_t>(a.base);
+        a.v0 = (P - B) / VBu;
+        a.v1 = (P + nbytes - B + VBu - 1) / VBu;
+        a.lo_byte = (int)(P - (B + a.v0 * VBu));
+        a.hi_byte = (int)(P + nbytes - (B + (a.v1 - 1) * VBu));
+        a.g0 = a.v0 / 32;
+        a.ng = (a.v1 + 31) / 32 - a.g0;
+    }
     a.k = k;
     a.flush_threshold = opt.flush_threshold;
     a.acc = ws.acc;
@@ -449,14 +481,13 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
 
     int grid = opt.grid;
     if (grid <= 0) {
-        const int depth_regs = nbank << (depth < 2 ? 2 : depth);
-        const unsigned long long tile = (unsigned long long)(depth_regs / 4) * block;
-        const unsigned long long want = (a.nvec + tile - 1) / tile;
-        const int per_sm = env_int("POSPOP_BLOCKS_PER_SM", resident_blocks(kernel, block));
+        const unsigned long long tile = (unsigned long long)((nbank << var->depth) / (var->vb / 4)) * threads;
+        const unsigned long long want = (a.ng * 32 + tile - 1) / tile;
+        const int per_sm = env_int("POSPOP_BLOCKS_PER_SM", resident_blocks(var->fn, threads));
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
     }
-    kernel<<<grid, block, 0, stream>>>(a);
+    var->fn<<<grid, threads, 0, stream>>>(a);
     ++g_launches;
     return cudaGetLastError();
 }
@@ -465,19 +496,23 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
                              unsigned long long* d_out, const LaunchOptions& opt, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     const int nbank = k == 64 ? 2 : 1;
-    const int depth = opt.depth ? opt.depth : env_int("POSPOP_SEG_DEPTH", nbank == 1 ? 5 : 4);
+    // Tuning override: POSPOP_SEG_VARIANT="depth,vb".
+    int depth = nbank == 1 ? 5 : 4, vb = 16;
+    if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d", &depth, &vb);
+    if (opt.depth) depth = opt.depth;
+    const SegVariant* var = pick_segmented(nbank, depth, vb);
+    if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
-    SegKernel kernel = pick_segmented(nbank, depth);
     int grid = opt.grid;
     if (grid <= 0) {
         const unsigned long long warps_per_block = block / 32;
         const unsigned long long want = (n + warps_per_block - 1) / warps_per_block;
-        const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", resident_blocks(kernel, block));
+        const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", resident_blocks(var->fn, block));
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < cap ? want : cap);
     }
-    kernel<<<grid, block, 0, stream>>>(static_cast<const uint8_t*>(data), d_offsets, n, k,
-                                       opt.flush_threshold, d_out);
+    var->fn<<<grid, block, 0, stream>>>(static_cast<const uint8_t*>(data), d_offsets, n, k,
+                                        opt.flush_threshold, d_out);
     ++g_launches;
     return cudaGetLastError();
 }

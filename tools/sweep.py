@@ -1,0 +1,147 @@
+#!/usr/bin/env python
+"""Tuning sweep (measurement tool, not product): kernel variants on the BASELINE
+configs, device-timed with CUDA events (median of reps), plus the pure-read
+probe (tools/probe) for the achievable read-only HBM bandwidth.
+
+    python tools/sweep.py [--what probe,stream,seg] [--reps 20] > gpurun_out/sweep.jsonl
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1911_02696_b200 as pp  # noqa: E402
+
+
+def timed(fn, reps, stream):
+    for _ in range(3):
+        fn()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    return statistics.median(ms), min(ms)
+
+
+def emit(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--what", default="probe,stream,seg")
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    what = set(args.what.split(","))
+    torch.cuda.set_device(0)
+    s = torch.cuda.current_stream()
+    sp = s.cuda_stream
+    n = 1 << 32
+    buf = torch.empty(2 * n + 4096, dtype=torch.uint8, device="cuda")
+    data = buf[:2 * n]
+    pp.generate(pp.GEN_CFG4, 1, data, n=n, stream=s)
+    torch.cuda.synchronize()
+    nbytes = 2 * n
+
+    if "probe" in what:
+        lib = C.CDLL(os.path.join(ROOT, "tools", "probe", "libpospop_probe.so"))
+        lib.probe_read.argtypes = [C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_void_p, C.c_void_p]
+        sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for vb, hint, vpt in [(16, 0, 4), (16, 0, 8), (16, 0, 16), (16, 2, 8), (16, 2, 16), (32, 0, 2), (32, 0, 4),
+                              (32, 0, 8), (32, 1, 4), (32, 1, 8)]:
+            for block, per_sm in [(256, 0), (256, 2), (256, 4), (512, 2), (1024, 1), (128, 8)]:
+                def fn():
+                    rc = lib.probe_read(data.data_ptr(), nbytes, vb, hint, vpt, block, per_sm, sp, sink.data_ptr())
+                    assert rc == 0, rc
+                try:
+                    med, best = timed(fn, args.reps, s)
+                except AssertionError as e:
+                    emit(kind="probe", vb=vb, hint=hint, vpt=vpt, block=block, per_sm=per_sm, error=str(e))
+                    continue
+                emit(kind="probe", vb=vb, hint=hint, vpt=vpt, block=block, per_sm=per_sm,
+                     gbs_med=round(nbytes / med / 1e6, 1), gbs_best=round(nbytes / best / 1e6, 1))
+
+    if "stream" in what:
+        out = torch.zeros(16, dtype=torch.int64, device="cuda")
+        os.environ.pop("POSPOP_STREAM_VARIANT", None)
+        pp.count_async(data, out, 16, stream=s)
+        torch.cuda.synchronize()
+        want = out.clone()
+        variants = ["6,16,0,256", "6,16,2,256", "6,32,0,256", "6,32,1,256", "5,32,0,256", "7,32,0,256",
+                    "5,16,0,256", "6,32,0,128", "6,32,0,512", "6,16,0,512", "6,16,0,128"]
+        for var in variants:
+            for per_sm in ["", "1", "2", "3", "4", "6", "8"]:
+                os.environ["POSPOP_STREAM_VARIANT"] = var
+                if per_sm:
+                    os.environ["POSPOP_BLOCKS_PER_SM"] = per_sm
+                else:
+                    os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
+                try:
+                    med, best = timed(lambda: pp.count_async(data, out, 16, stream=s), args.reps, s)
+                    ok = bool(torch.equal(out, want))
+                    emit(kind="stream16", variant=var, per_sm=per_sm or "occ", gbs_med=round(nbytes / med / 1e6, 1),
+                         gbs_best=round(nbytes / best / 1e6, 1), ok=ok)
+                except Exception as e:  # noqa: BLE001
+                    emit(kind="stream16", variant=var, per_sm=per_sm, error=repr(e))
+        os.environ.pop("POSPOP_STREAM_VARIANT", None)
+        os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
+        # other k on the same bytes
+        for k, var in [(8, "6,16,0,256"), (32, "6,16,0,256"), (64, "5,16,0,256"), (64, "5,32,0,256"),
+                       (64, "4,32,0,256"), (64, "4,16,0,256")]:
+            os.environ["POSPOP_STREAM_VARIANT"] = var
+            o = torch.zeros(k, dtype=torch.int64, device="cuda")
+            med, best = timed(lambda: pp.count_async(data, o, k, stream=s), args.reps, s)
+            emit(kind=f"stream{k}", variant=var, gbs_med=round(nbytes / med / 1e6, 1), gbs_best=round(nbytes / best / 1e6, 1))
+        os.environ.pop("POSPOP_STREAM_VARIANT", None)
+        # cfg3 (u8 at +3, 2^30-7) and cfg2 (2^28 one-hot)
+        b3 = torch.empty((1 << 30) + 64, dtype=torch.uint8, device="cuda")
+        n3 = (1 << 30) - 7
+        pp.generate(pp.GEN_CFG3, 1, b3[3:3 + n3], stream=s)
+        o8 = torch.zeros(8, dtype=torch.int64, device="cuda")
+        med, best = timed(lambda: pp.count_async(b3[3:3 + n3], o8, 8, stream=s), args.reps, s)
+        emit(kind="cfg3", gbs_med=round(n3 / med / 1e6, 1), gbs_best=round(n3 / best / 1e6, 1))
+        del b3
+        b2 = torch.empty(1 << 29, dtype=torch.uint8, device="cuda")
+        pp.generate(pp.GEN_CFG2, 1, b2, stream=s)
+        med, best = timed(lambda: pp.count_async(b2, out, 16, stream=s), args.reps, s)
+        emit(kind="cfg2", gbs_med=round((1 << 29) / med / 1e6, 1), gbs_best=round((1 << 29) / best / 1e6, 1))
+        del b2
+
+    if "seg" in what:
+        for k, kind, variants in [(32, pp.GEN_U32, ["5,16", "4,16", "6,16", "5,32", "6,32"]),
+                                  (64, pp.GEN_U64, ["4,16", "3,16", "5,16", "4,32", "5,32"])]:
+            arrays, words = 65536, 4096
+            d = data[:arrays * words * k // 8]
+            pp.generate(kind, 1, d, stream=s)
+            offs = torch.arange(0, arrays + 1, dtype=torch.int64, device="cuda") * words
+            o = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
+            want = None
+            for var in variants:
+                for per_sm in ["", "2", "4", "8"]:
+                    os.environ["POSPOP_SEG_VARIANT"] = var
+                    if per_sm:
+                        os.environ["POSPOP_SEG_BLOCKS_PER_SM"] = per_sm
+                    else:
+                        os.environ.pop("POSPOP_SEG_BLOCKS_PER_SM", None)
+                    med, best = timed(lambda: pp.segmented_async(d, offs, o, k, stream=s), args.reps, s)
+                    if want is None:
+                        want = o.clone()
+                    emit(kind=f"seg{k}", variant=var, per_sm=per_sm or "occ", ok=bool(torch.equal(o, want)),
+                         gbs_med=round(d.numel() / med / 1e6, 1), gbs_best=round(d.numel() / best / 1e6, 1))
+            os.environ.pop("POSPOP_SEG_VARIANT", None)
+            os.environ.pop("POSPOP_SEG_BLOCKS_PER_SM", None)
+
+
+if __name__ == "__main__":
+    main()
