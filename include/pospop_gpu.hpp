@@ -65,7 +65,7 @@ inline void validate(const pospop::PospopcntConfig& config) {
 /// reference's own verify_kernels / bench harnesses.
 struct GpuRunner {
     pospop::PositionalCounts operator()(pospop::Word16Span words, const pospop::PospopcntConfig& config) const {
-        return pospopcnt(words, config);
+        return pospop_gpu::pospopcnt(words, config);  // qualified: ADL would also find pospop::pospopcnt
     }
 };
 

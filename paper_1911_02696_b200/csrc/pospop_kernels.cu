@@ -46,6 +46,7 @@ std::atomic<unsigned long long> g_launches{0};
 struct StreamArgs {
     const uint8_t* base;
     unsigned long long v0, v1;  // valid vectors
+    unsigned long long f0, f1;  // fully valid (unmasked) vectors [f0, f1)
     unsigned long long g0, ng;  // first group, number of groups
     int lo_byte, hi_byte;       // valid bytes of vector v0 / vector v1-1
     int k;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
     const unsigned long long ge = a.g0 + a.ng * (blockIdx.x + 1) / gridDim.x;
     const unsigned long long S = gb * 32;
     const unsigned long long E = ge * 32 < a.v1 ? ge * 32 : a.v1;
+    const unsigned long long F = E < a.f1 ? E : a.f1;  // interior tiles end here
     const uint32_t lane = threadIdx.x & 31u;
 
     uint32_t carries[NBANK][L];
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
 
     for (unsigned long long t = S; t < E; t += tile) {
         uint32_t r[REGS];
-        if (t >= a.v0 && t + tile <= E) {  // interior tile: unpredicated, immediate offsets
+        if (t >= a.f0 && t + tile <= F) {  // interior tile: unpredicated, unmasked, immediate offsets
             const uint8_t* p = a.base + (t + threadIdx.x) * VB;
 #pragma unroll
             for (int v = 0; v < VPT; ++v) {
@@ -355,7 +357,7 @@ __global__ void digest_kernel(const uint8_t* data, unsigned long long nbytes, un
 // ---------------------------------------------------------------------------
 
 constexpr int kDefaultBlock = 256;
-constexpr int kDefaultDepth1 = 6;  // k = 8/16/32: 64 registers = 256 B per thread per tree block
+constexpr int kDefaultDepth1 = 7;  // k = 8/16/32: 128 registers = 512 B per thread per tree block
 constexpr int kDefaultDepth2 = 5;  // k = 64: two banks of 32 registers
 
 int env_int(const char* name, int dflt) {
@@ -397,13 +399,11 @@ struct StreamVariant {
 // Production variants first (the defaults), then tuning variants selectable
 // through POSPOP_STREAM_VARIANT="depth,vb,hint,block".
 const StreamVariant kStreamVariants[] = {
-    SV(1, 6, 16, 0, 256), SV(2, 5, 16, 0, 256),  // defaults (k <= 32 / k = 64)
-    SV(1, 6, 16, 0, 0), SV(2, 5, 16, 0, 0),      // runtime block size
-    SV(1, 6, 32, 0, 0), SV(2, 5, 32, 0, 0),
-    SV(1, 6, 16, 2, 256), SV(1, 6, 32, 0, 256), SV(1, 6, 32, 1, 256),
-    SV(1, 5, 32, 0, 256), SV(1, 7, 32, 0, 256), SV(1, 5, 16, 0, 256),
-    SV(1, 6, 32, 0, 128), SV(1, 6, 32, 0, 512), SV(1, 6, 16, 0, 512), SV(1, 6, 16, 0, 128),
-    SV(2, 5, 32, 0, 256), SV(2, 4, 32, 0, 256), SV(2, 4, 16, 0, 256),
+    SV(1, 7, 32, 0, 256), SV(2, 5, 16, 0, 256),  // defaults (k <= 32 / k = 64)
+    SV(1, 7, 32, 0, 0), SV(2, 5, 16, 0, 0),      // runtime block size (test launches)
+    SV(1, 6, 16, 0, 256), SV(1, 6, 32, 0, 256), SV(1, 6, 16, 0, 512), SV(1, 7, 16, 0, 256),
+    SV(1, 7, 32, 1, 256), SV(1, 7, 32, 0, 128), SV(1, 7, 32, 0, 512), SV(1, 8, 32, 0, 256),
+    SV(2, 5, 32, 0, 256), SV(2, 6, 32, 0, 256), SV(2, 6, 16, 0, 256),
 };
 #undef SV
 
@@ -423,9 +423,8 @@ struct SegVariant {
 
 #define SG(NB, L, VB) {NB, L, VB, segmented_kernel<NB, L, VB>}
 const SegVariant kSegVariants[] = {
-    SG(1, 5, 16), SG(2, 4, 16),  // defaults
-    SG(1, 4, 16), SG(1, 6, 16), SG(1, 5, 32), SG(1, 6, 32), SG(2, 3, 16), SG(2, 5, 16), SG(2, 4, 32),
-    SG(2, 5, 32),
+    SG(1, 4, 16), SG(2, 4, 32),  // defaults (k <= 32 / k = 64)
+    SG(1, 3, 16), SG(1, 5, 16), SG(1, 4, 32), SG(1, 5, 32), SG(2, 3, 16), SG(2, 4, 16), SG(2, 3, 32),
 };
 #undef SG
 
@@ -444,7 +443,8 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
                           cudaStream_t stream) {
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block".
-    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 16, hint = 0, block = kDefaultBlock;
+    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = nbank == 1 ? 32 : 16, hint = 0,
+        block = kDefaultBlock;
     if (const char* v = std::getenv("POSPOP_STREAM_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &hint, &block);
     if (opt.depth) depth = opt.depth;
     if (opt.block) block = 0;  // explicit (test) block size: the runtime-block instantiation
@@ -460,7 +460,7 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
     StreamArgs a;
     a.base = reinterpret_cast<const uint8_t*>(P & ~(group - 1));
     if (nbytes == 0) {
-        a.v0 = a.v1 = a.g0 = a.ng = 0;
+        a.v0 = a.v1 = a.f0 = a.f1 = a.g0 = a.ng = 0;
         a.lo_byte = 0;
         a.hi_byte = (int)VBu;
     } else {
@@ -469,6 +469,8 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
         a.v1 = (P + nbytes - B + VBu - 1) / VBu;
         a.lo_byte = (int)(P - (B + a.v0 * VBu));
         a.hi_byte = (int)(P + nbytes - (B + (a.v1 - 1) * VBu));
+        a.f0 = a.v0 + (a.lo_byte != 0 ? 1 : 0);
+        a.f1 = a.v1 - (a.hi_byte != (int)VBu ? 1 : 0);
         a.g0 = a.v0 / 32;
         a.ng = (a.v1 + 31) / 32 - a.g0;
     }
@@ -497,11 +499,11 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (n == 0) return cudaSuccess;
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_SEG_VARIANT="depth,vb".
-    int depth = nbank == 1 ? 5 : 4, vb = 16;
+    int depth = 4, vb = nbank == 1 ? 16 : 32;
     if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d", &depth, &vb);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb);
-    if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16);
+    if (!var) var = pick_segmented(nbank, 4, nbank == 1 ? 16 : 32);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {

@@ -1,0 +1,72 @@
+// verify_gpu.cpp -- the reference's own verification harness driving the GPU path.
+//
+// Built by oracle/Makefile (target `verify`) against the UNMODIFIED reference
+// headers and library (oracle/_ref/libpospop_ref.so) plus libpospopcnt_b200.so.
+// It proves three things a maintainer needs before swapping the GPU in:
+//   1. include/pospop_gpu.hpp compiles against pospop/types.hpp and is a
+//      drop-in: pospop_gpu::pospopcnt has pospop::pospopcnt's signature;
+//   2. pospop::verify_kernels (proj/core/src/verify.cpp:33-75) with a GPU
+//      KernelRunner (proj/core/include/pospop/verify.hpp:47) passes: the
+//      exhaustive single-word domain + every length 0..max_len, bit-exact
+//      against pospop::oracle_pospopcnt;
+//   3. the error conventions match (std::invalid_argument,
+//      pospop::KernelUnavailableError).
+// Exit code 0 = all passed.
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <vector>
+
+#include "pospop/bench.hpp"
+#include "pospop/pospop.hpp"
+#include "pospop/verify.hpp"
+#include "pospop_gpu.hpp"
+
+int main(int argc, char** argv) {
+    const std::size_t max_len = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 3000;
+    int failures = 0;
+
+    // (2) the reference harness with the GPU runner
+    const pospop::KernelKind kinds[] = {pospop::KernelKind::Auto, pospop::KernelKind::Csa16,
+                                        pospop::KernelKind::ScalarBasic};
+    const pospop::VerifyReport report =
+        pospop::verify_kernels(0xACCE97, max_len, kinds, pospop_gpu::GpuRunner{});
+    if (report.ok()) {
+        std::printf("PASS verify_kernels(GpuRunner): %zu cases (65536 single words + lengths 0..%zu) x 3 kinds\n",
+                    report.cases_run, max_len);
+    } else {
+        std::printf("FAIL verify_kernels(GpuRunner):\n%s\n", pospop::format_failure(*report.first_failure).c_str());
+        ++failures;
+    }
+
+    // (1) drop-in on a large stream, against the reference's own kernel
+    const std::vector<std::uint16_t> big = pospop::bench::generate_stream({1, std::size_t{1} << 24});
+    if (pospop_gpu::pospopcnt(big) == pospop::pospopcnt(big)) {
+        std::printf("PASS pospop_gpu::pospopcnt == pospop::pospopcnt on 2^24 words\n");
+    } else {
+        std::printf("FAIL drop-in mismatch on 2^24 words\n");
+        ++failures;
+    }
+
+    // (3) error conventions (proj/tests/test_core.cpp:184-201)
+    pospop::PospopcntConfig bad;
+    bad.flush_threshold_blocks = 0;
+    try {
+        pospop_gpu::pospopcnt(big, bad);
+        std::printf("FAIL threshold 0 accepted\n");
+        ++failures;
+    } catch (const std::invalid_argument&) {
+        std::printf("PASS threshold 0 -> std::invalid_argument\n");
+    }
+    pospop::PospopcntConfig w128;
+    w128.kernel = pospop::KernelKind::Csa16;
+    w128.register_width_bits = 128;
+    try {
+        pospop_gpu::pospopcnt(std::vector<std::uint16_t>(8), w128);
+        std::printf("FAIL width 128 accepted\n");
+        ++failures;
+    } catch (const pospop::KernelUnavailableError&) {
+        std::printf("PASS width 128 -> pospop::KernelUnavailableError\n");
+    }
+    return failures;
+}

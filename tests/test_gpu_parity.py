@@ -159,7 +159,7 @@ def test_lane_saturation_single_warp(pp, dev):
     """test_csa.cpp:294-305 on the GPU: one CTA of 32 threads over all-ones
     input, > 65535 tree blocks per thread, so every 16-bit lane reaches 65535
     before the flush; one more block plus a tail proves no lane wrapped."""
-    per_block_bytes = 32 * 256  # 32 threads x 64 registers x 4 B (depth 6)
+    per_block_bytes = 32 * 512  # 32 threads x 128 registers x 4 B (depth 7; depth <= 7 sees more blocks)
     nbytes = per_block_bytes * 65537 + 6
     d = torch.full((nbytes,), 0xFF, dtype=torch.uint8, device="cuda")
     out = torch.zeros(16, dtype=torch.int64, device="cuda")
@@ -195,9 +195,12 @@ def test_medium_random_vs_oracle(pp, dev, orc, k):
     for n_bytes in (1 << 20, (1 << 21) + 24, raw.size - 8):
         n = n_bytes // (k // 8)
         sub = raw[:n * k // 8]
-        for offset in (0, 8):
-            _, view = guarded(sub, offset)
-            assert pp.pospopcnt_k(view, k) == orc.pospopcnt(sub, k, threads=4), (k, n, offset)
+        want = orc.pospopcnt(sub, k, threads=4)
+        for offset in sorted({0, k // 8, 3 * (k // 8), 8, 16 - k // 8}):
+            _, view = guarded(sub, offset)  # 0xFF guards: a missed head/tail mask counts them
+            assert pp.pospopcnt_k(view, k) == want, (k, n, offset)
+            _, view = guarded(sub[k // 8:], offset)  # ragged end too
+            assert pp.pospopcnt_k(view, k) == orc.pospopcnt(sub[k // 8:], k, threads=4), (k, n, offset)
 
 
 # -- host-memory (staged) path -----------------------------------------------------------------
@@ -336,3 +339,19 @@ def test_cfg5_segmented_full(pp, dev, orc, k, kind):
     want = orc.segmented(host, offs.cpu().numpy().view(np.uint64), k, threads=16)
     assert (got == want).all()
     assert (got.sum(1) == np.bitwise_count(host.reshape(arrays, words)).sum(1)).all()
+
+
+# -- the reference's own harness driving the GPU path (C++ drop-in) ----------------------------
+
+def test_reference_verify_kernels_with_gpu_runner():
+    """oracle/_ref/verify_gpu: pospop::verify_kernels (proj/core/src/verify.cpp:33-75) with
+    pospop_gpu::GpuRunner, the C++ drop-in against the reference's own types and errors."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "verify_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/verify_gpu not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, "3000"], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 4

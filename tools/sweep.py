@@ -78,10 +78,10 @@ def main():
         pp.count_async(data, out, 16, stream=s)
         torch.cuda.synchronize()
         want = out.clone()
-        variants = ["6,16,0,256", "6,16,2,256", "6,32,0,256", "6,32,1,256", "5,32,0,256", "7,32,0,256",
-                    "5,16,0,256", "6,32,0,128", "6,32,0,512", "6,16,0,512", "6,16,0,128"]
+        variants = ["7,32,0,256", "7,32,1,256", "7,16,0,256", "7,32,0,128", "7,32,0,512", "8,32,0,256",
+                    "6,16,0,256", "6,32,0,256", "6,16,0,512"]
         for var in variants:
-            for per_sm in ["", "1", "2", "3", "4", "6", "8"]:
+            for per_sm in ["", "1", "2", "3", "4", "8"]:
                 os.environ["POSPOP_STREAM_VARIANT"] = var
                 if per_sm:
                     os.environ["POSPOP_BLOCKS_PER_SM"] = per_sm
@@ -97,8 +97,8 @@ def main():
         os.environ.pop("POSPOP_STREAM_VARIANT", None)
         os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
         # other k on the same bytes
-        for k, var in [(8, "6,16,0,256"), (32, "6,16,0,256"), (64, "5,16,0,256"), (64, "5,32,0,256"),
-                       (64, "4,32,0,256"), (64, "4,16,0,256")]:
+        for k, var in [(8, "7,32,0,256"), (32, "7,32,0,256"), (64, "5,16,0,256"), (64, "5,32,0,256"),
+                       (64, "6,32,0,256"), (64, "6,16,0,256")]:
             os.environ["POSPOP_STREAM_VARIANT"] = var
             o = torch.zeros(k, dtype=torch.int64, device="cuda")
             med, best = timed(lambda: pp.count_async(data, o, k, stream=s), args.reps, s)
@@ -109,18 +109,28 @@ def main():
         n3 = (1 << 30) - 7
         pp.generate(pp.GEN_CFG3, 1, b3[3:3 + n3], stream=s)
         o8 = torch.zeros(8, dtype=torch.int64, device="cuda")
-        med, best = timed(lambda: pp.count_async(b3[3:3 + n3], o8, 8, stream=s), args.reps, s)
-        emit(kind="cfg3", gbs_med=round(n3 / med / 1e6, 1), gbs_best=round(n3 / best / 1e6, 1))
-        del b3
         b2 = torch.empty(1 << 29, dtype=torch.uint8, device="cuda")
         pp.generate(pp.GEN_CFG2, 1, b2, stream=s)
-        med, best = timed(lambda: pp.count_async(b2, out, 16, stream=s), args.reps, s)
-        emit(kind="cfg2", gbs_med=round((1 << 29) / med / 1e6, 1), gbs_best=round((1 << 29) / best / 1e6, 1))
-        del b2
+        for var in ["7,32,0,256", "6,16,0,256", "6,32,0,256", "6,16,0,512"]:
+            for per_sm in ["", "1", "2", "4", "8", "16"]:
+                os.environ["POSPOP_STREAM_VARIANT"] = var
+                if per_sm:
+                    os.environ["POSPOP_BLOCKS_PER_SM"] = per_sm
+                else:
+                    os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
+                med, best = timed(lambda: pp.count_async(b3[3:3 + n3], o8, 8, stream=s), args.reps, s)
+                emit(kind="cfg3", variant=var, per_sm=per_sm or "occ", gbs_med=round(n3 / med / 1e6, 1),
+                     gbs_best=round(n3 / best / 1e6, 1))
+                med, best = timed(lambda: pp.count_async(b2, out, 16, stream=s), args.reps, s)
+                emit(kind="cfg2", variant=var, per_sm=per_sm or "occ", gbs_med=round((1 << 29) / med / 1e6, 1),
+                     gbs_best=round((1 << 29) / best / 1e6, 1))
+        os.environ.pop("POSPOP_STREAM_VARIANT", None)
+        os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
+        del b3, b2
 
     if "seg" in what:
-        for k, kind, variants in [(32, pp.GEN_U32, ["5,16", "4,16", "6,16", "5,32", "6,32"]),
-                                  (64, pp.GEN_U64, ["4,16", "3,16", "5,16", "4,32", "5,32"])]:
+        for k, kind, variants in [(32, pp.GEN_U32, ["4,16", "3,16", "5,16", "4,32", "5,32"]),
+                                  (64, pp.GEN_U64, ["4,32", "3,16", "4,16", "3,32"])]:
             arrays, words = 65536, 4096
             d = data[:arrays * words * k // 8]
             pp.generate(kind, 1, d, stream=s)
