@@ -152,6 +152,14 @@ pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d
                               int accumulate, uint32_t flush_threshold_blocks, int grid, int block,
                               void* stream);
 
+/* Diagnostics: pospopcnt_async with per-CTA %globaltimer timestamps.
+ * d_trace (device, >= 5 * trace_ctas u64, trace_ctas >= 32 * SMs) receives,
+ * per CTA: {start, main-loop end, CTA channels flushed, exit, SM id};
+ * *grid_used is the grid size.  Used by tools/trace.py to measure the
+ * launch/ramp/tail/epilogue overheads of the persistent grid. */
+pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
+                                    uint64_t* d_trace, size_t trace_ctas, int* grid_used, void* stream);
+
 /* Segmented, device-resident, asynchronous. */
 pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_t* d_offsets,
                                         size_t n_arrays, uint64_t* d_counts,

@@ -492,6 +492,29 @@ pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d
     return POSPOP_OK;
 }
 
+pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
+                                    uint64_t* d_trace, size_t trace_ctas, int* grid_used, void* stream) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (!d_counts || !d_trace || !grid_used || (!d_data && len)) return fail(POSPOP_EINVAL, "NULL pointer");
+    if ((uintptr_t)d_data % ((size_t)k / 8)) return fail(POSPOP_EINVAL, "data is misaligned");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamWorkspace ws;
+    if ((s = stream_workspace(dev, st, &ws))) return s;
+    LaunchOptions opt;
+    opt.trace = reinterpret_cast<unsigned long long*>(d_trace);
+    // The grid is decided inside the launcher; refuse to launch if the trace
+    // buffer could be too small for the largest persistent grid.
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (trace_ctas < (size_t)sms * 32) return fail(POSPOP_EINVAL, "trace buffer needs >= %d CTAs", sms * 32);
+    CU(launch_stream(k, len ? d_data : (const void*)d_counts, len, reinterpret_cast<unsigned long long*>(d_counts),
+                     false, opt, ws, st, grid_used));
+    return POSPOP_OK;
+}
+
 pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_t* d_offsets, size_t n,
                                         uint64_t* d_counts, uint32_t flush, int grid, int block,
                                         void* stream) {

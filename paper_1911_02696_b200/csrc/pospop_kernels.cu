@@ -55,7 +55,20 @@ struct StreamArgs {
     unsigned int* ticket;
     unsigned long long* out;
     int accumulate;
+    unsigned long long* trace;  // diagnostics: per CTA {t_start, t_loop_end, t_flushed, t_done, smid} or null
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 
 // Channel -> position fold: the channels (of 32 * NBANK) that count position
 // p are p + m * k for m = 0 .. 32/k - 1 (k <= 32), or channel p (k = 64).
@@ -92,6 +105,10 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
 
     __shared__ unsigned long long s_acc[32 * NBANK];
     __shared__ int s_last;
+    if (a.trace && threadIdx.x == 0) {
+        a.trace[blockIdx.x * 5 + 0] = globaltimer();
+        a.trace[blockIdx.x * 5 + 4] = smid();
+    }
     for (int i = threadIdx.x; i < 32 * NBANK; i += block) s_acc[i] = 0;
     __syncthreads();
 
@@ -154,6 +171,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
         }
     }
 
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer();
     // Final flush of the lane bank (weight 2^L) fused with the carry drain.
 #pragma unroll
     for (int b = 0; b < NBANK; ++b) {
@@ -168,6 +186,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
         if (s_acc[c]) atomicAdd(&a.acc[c], s_acc[c]);
     __threadfence();
     __syncthreads();
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = globaltimer();
     if (threadIdx.x == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
@@ -187,6 +206,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
         a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
     }
     if (threadIdx.x == 0) *a.ticket = 0u;
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 3] = globaltimer();
 }
 
 // One warp per array.  Array a spans bytes [data + off[a]*wb, data + off[a+1]*wb);
@@ -215,6 +235,8 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
         const int lo = (int)(P - B);
         const int hi = nv ? (int)(Q - (B + (nv - 1) * VB)) : VB;
         const uint8_t* base = (const uint8_t*)B;
+        const unsigned long long f0 = lo ? 1 : 0;                    // fully valid vectors [f0, f1)
+        const unsigned long long f1 = nv - (nv && hi != VB ? 1 : 0);
 
         uint32_t carries[NBANK][L];
         uint32_t counter[NBANK][16];
@@ -230,7 +252,7 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
 
         for (unsigned long long t = 0; t < nv; t += STEP) {
             uint32_t r[REGS];
-            if (t > 0 && t + STEP < nv) {  // interior: neither the first nor the last vector
+            if (t >= f0 && t + STEP <= f1) {  // interior: unpredicated, unmasked
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
                     uint32_t x[RPV];
@@ -358,7 +380,7 @@ __global__ void digest_kernel(const uint8_t* data, unsigned long long nbytes, un
 
 constexpr int kDefaultBlock = 256;
 constexpr int kDefaultDepth1 = 7;  // k = 8/16/32: 128 registers = 512 B per thread per tree block
-constexpr int kDefaultDepth2 = 5;  // k = 64: two banks of 32 registers
+constexpr int kDefaultDepth2 = 6;  // k = 64: two banks of 64 registers
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -399,11 +421,12 @@ struct StreamVariant {
 // Production variants first (the defaults), then tuning variants selectable
 // through POSPOP_STREAM_VARIANT="depth,vb,hint,block".
 const StreamVariant kStreamVariants[] = {
-    SV(1, 7, 32, 0, 256), SV(2, 5, 16, 0, 256),  // defaults (k <= 32 / k = 64)
-    SV(1, 7, 32, 0, 0), SV(2, 5, 16, 0, 0),      // runtime block size (test launches)
+    SV(1, 7, 32, 0, 256), SV(2, 6, 32, 0, 256),  // defaults (k <= 32 / k = 64)
+    SV(1, 7, 32, 0, 0), SV(2, 6, 32, 0, 0),      // runtime block size (test launches)
+    SV(2, 5, 16, 0, 256), SV(2, 5, 16, 0, 0),
     SV(1, 6, 16, 0, 256), SV(1, 6, 32, 0, 256), SV(1, 6, 16, 0, 512), SV(1, 7, 16, 0, 256),
     SV(1, 7, 32, 1, 256), SV(1, 7, 32, 0, 128), SV(1, 7, 32, 0, 512), SV(1, 8, 32, 0, 256),
-    SV(2, 5, 32, 0, 256), SV(2, 6, 32, 0, 256), SV(2, 6, 16, 0, 256),
+    SV(2, 5, 32, 0, 256), SV(2, 6, 16, 0, 256),
 };
 #undef SV
 
@@ -440,10 +463,10 @@ unsigned long long kernel_launches() { return g_launches.load(); }
 
 cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
                           bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, int* grid_used) {
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block".
-    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = nbank == 1 ? 32 : 16, hint = 0,
+    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 32, hint = 0,
         block = kDefaultBlock;
     if (const char* v = std::getenv("POSPOP_STREAM_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &hint, &block);
     if (opt.depth) depth = opt.depth;
@@ -480,6 +503,7 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
     a.ticket = ws.ticket;
     a.out = d_out;
     a.accumulate = accumulate ? 1 : 0;
+    a.trace = opt.trace;
 
     int grid = opt.grid;
     if (grid <= 0) {
@@ -489,6 +513,7 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
     }
+    if (grid_used) *grid_used = grid;
     var->fn<<<grid, threads, 0, stream>>>(a);
     ++g_launches;
     return cudaGetLastError();

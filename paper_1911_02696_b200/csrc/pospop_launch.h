@@ -22,6 +22,7 @@ struct LaunchOptions {
     int grid = 0;                      // 0 = persistent: SMs x resident blocks
     int block = 0;                     // 0 = default (256); multiple of 32
     int depth = 0;                     // 0 = default tree depth (k=64: per bank)
+    unsigned long long* trace = nullptr;  // diagnostics: 5 u64 per CTA (see pospopcnt_trace_async)
 };
 
 // Counts len_words k-bit words at `data` (device memory, k/8-aligned) into
@@ -29,7 +30,7 @@ struct LaunchOptions {
 // One kernel launch.
 cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
                           bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
-                          cudaStream_t stream);
+                          cudaStream_t stream, int* grid_used = nullptr);
 
 // Batched form: array a = words [d_offsets[a], d_offsets[a+1]) of `data`;
 // row a of d_out (k entries) is overwritten.  One kernel launch.
