@@ -116,9 +116,10 @@ struct Ctx {
 thread_local std::map<int, Ctx*> t_ctx;
 
 pospop_status alloc_workspace(StreamWorkspace* ws) {
-    CU(cudaMalloc(&ws->acc, 64 * sizeof(unsigned long long) + 64));
+    CU(cudaMalloc(&ws->acc, kWorkspaceBytes));
     ws->ticket = reinterpret_cast<unsigned int*>(ws->acc + 64);
-    CU(cudaMemset(ws->acc, 0, 64 * sizeof(unsigned long long) + 64));
+    ws->next = ws->acc + 65;
+    CU(cudaMemset(ws->acc, 0, kWorkspaceBytes));
     return POSPOP_OK;
 }
 
@@ -402,7 +403,7 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
         dout = tmp_out;
     }
     LaunchOptions opt;
-    CU(launch_segmented(k, ddata ? ddata : (const void*)doff, doff, n, dout, opt, c->stream));
+    CU(launch_segmented(k, ddata ? ddata : (const void*)doff, doff, n, dout, opt, c->ws, c->stream));
     if (!c_dev)
         CU(cudaMemcpyAsync(counts, dout, n * (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -528,12 +529,14 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
     pospop_status s = current_device(&dev);
     if (s) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+    StreamWorkspace ws;
+    if ((s = stream_workspace(dev, st, &ws))) return s;
     LaunchOptions opt;
     opt.flush_threshold = flush;
     opt.grid = grid;
     opt.block = block;
     CU(launch_segmented(k, d_data, reinterpret_cast<const unsigned long long*>(d_offsets), n,
-                        reinterpret_cast<unsigned long long*>(d_counts), opt, st));
+                        reinterpret_cast<unsigned long long*>(d_counts), opt, ws, st));
     return POSPOP_OK;
 }
 

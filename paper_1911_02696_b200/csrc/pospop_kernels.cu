@@ -56,6 +56,9 @@ struct StreamArgs {
     unsigned long long* out;
     int accumulate;
     unsigned long long* trace;  // diagnostics: per CTA {t_start, t_loop_end, t_flushed, t_done, smid} or null
+    // dynamic schedule (SCHED 1): warp tiles, chunk counter, chunk sizes
+    unsigned long long* next;   // global chunk counter (zero on entry, re-zeroed by the last CTA)
+    unsigned long long nwt, nA, CA, CB;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -93,9 +96,111 @@ __device__ __forceinline__ void zero_bank(uint32_t (&counter)[NBANK][16]) {
         for (int p = 0; p < 16; ++p) counter[b][p] = 0;
 }
 
-// BLOCK > 0: compile-time block size (immediate load offsets); BLOCK == 0:
-// runtime blockDim.x (used for small test launches).
-template <int NBANK, int L, int VB, int HINT, int BLOCK>
+// Loads one tree block for this thread: VPT vectors at first + v * stride.
+// `fast`: the whole tile lies in the fully valid range (no predicates, no
+// masks, immediate offsets when stride is a compile-time constant).
+template <int VB, int HINT, int VPT>
+__device__ __forceinline__ void load_tree_block(const StreamArgs& a, unsigned long long first, unsigned stride,
+                                                bool fast, uint32_t (&r)[VPT * (VB / 4)]) {
+    constexpr int RPV = VB / 4;
+    if (fast) {
+        const uint8_t* p = a.base + first * VB;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            uint32_t x[RPV];
+            ldg_stream<VB, HINT>(p + (unsigned long long)v * stride * VB, x);
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            const unsigned long long idx = first + (unsigned long long)v * stride;
+            uint32_t x[RPV];
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) x[j] = 0;
+            if (idx >= a.v0 && idx < a.v1) {
+                ldg_stream<VB, HINT>(a.base + idx * VB, x);
+                if (idx == a.v0 || idx + 1 == a.v1)
+                    mask_bytes<VB>(x, idx == a.v0 ? a.lo_byte : 0, idx + 1 == a.v1 ? a.hi_byte : VB);
+            }
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+        }
+    }
+}
+
+// Lane-bank flush (weight 2^L) into the CTA's shared channel totals; must be
+// called by all 32 lanes of a warp together.
+template <int NBANK, int L>
+__device__ __forceinline__ void flush_bank_to_smem(uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
+                                                   uint32_t lane) {
+    uint32_t d[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
+    }
+    zero_bank<NBANK>(counter);
+}
+
+// CTA epilogue: final flush fused with the carry drain, CTA channel totals to
+// the global accumulator, ticket; the last CTA folds channels to positions,
+// writes/accumulates out[k] and leaves the scratch (acc, ticket, chunk
+// counter) zeroed for the next launch.
+template <int NBANK, int L>
+__device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carries)[NBANK][L],
+                                           uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
+                                           int* s_last, unsigned block, uint32_t lane) {
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer();
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        uint32_t d[16];
+        drain<L>(d, carries[b]);
+        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < 32 * NBANK; c += block)
+        if (s_acc[c]) atomicAdd(&a.acc[c], s_acc[c]);
+    __threadfence();
+    __syncthreads();
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = globaltimer();
+    if (threadIdx.x == 0) *s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!*s_last) return;
+
+    // Last CTA: every other CTA has fenced its channel atomics.
+    __threadfence();
+    const int k = a.k;
+    for (int pos = threadIdx.x; pos < k; pos += block) {
+        unsigned long long sum = 0;
+        if (k == 64) {
+            sum = atomicExch(&a.acc[pos], 0ull);
+        } else {
+            const int m = channels_per_position(k);
+            for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
+        }
+        a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+    }
+    if (threadIdx.x == 0) {
+        *a.ticket = 0u;
+        if (a.next) *a.next = 0ull;
+    }
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 3] = globaltimer();
+}
+
+// SCHED 0 (static): CTA b owns a contiguous range of whole 32-vector groups and
+// walks it in CTA tiles of BLOCK x VPT vectors.
+// SCHED 1 (dynamic): warps pull chunks of warp tiles (32 lanes x VPT vectors,
+// VPT 1 KiB-aligned warp loads) from a global counter, large chunks first
+// (nA chunks of CA warp tiles) then small ones (CB) so no warp or CTA idles
+// while another still holds a big share; the next chunk index is fetched one
+// chunk ahead so the atomic's latency hides behind the loads.
+// BLOCK > 0: compile-time block size; BLOCK == 0: runtime blockDim.x.
+template <int NBANK, int L, int VB, int HINT, int BLOCK, int SCHED>
 __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const StreamArgs a) {
     constexpr int REGS = NBANK << L;  // 32-bit input registers per tree block
     constexpr int RPV = VB / 4;       // registers per vector
@@ -111,13 +216,6 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
     }
     for (int i = threadIdx.x; i < 32 * NBANK; i += block) s_acc[i] = 0;
     __syncthreads();
-
-    const unsigned long long tile = (unsigned long long)VPT * block;
-    const unsigned long long gb = a.g0 + a.ng * blockIdx.x / gridDim.x;
-    const unsigned long long ge = a.g0 + a.ng * (blockIdx.x + 1) / gridDim.x;
-    const unsigned long long S = gb * 32;
-    const unsigned long long E = ge * 32 < a.v1 ? ge * 32 : a.v1;
-    const unsigned long long F = E < a.f1 ? E : a.f1;  // interior tiles end here
     const uint32_t lane = threadIdx.x & 31u;
 
     uint32_t carries[NBANK][L];
@@ -129,105 +227,91 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
     zero_bank<NBANK>(counter);
     uint32_t nb = 0;
 
-    for (unsigned long long t = S; t < E; t += tile) {
-        uint32_t r[REGS];
-        if (t >= a.f0 && t + tile <= F) {  // interior tile: unpredicated, unmasked, immediate offsets
-            const uint8_t* p = a.base + (t + threadIdx.x) * VB;
+    if constexpr (SCHED == 0) {
+        const unsigned long long tile = (unsigned long long)VPT * block;
+        const unsigned long long gb = a.g0 + a.ng * blockIdx.x / gridDim.x;
+        const unsigned long long ge = a.g0 + a.ng * (blockIdx.x + 1) / gridDim.x;
+        const unsigned long long E = ge * 32 < a.v1 ? ge * 32 : a.v1;
+        const unsigned long long F = E < a.f1 ? E : a.f1;
+        for (unsigned long long t = gb * 32; t < E; t += tile) {
+            uint32_t r[REGS];
+            const bool fast = t >= a.f0 && t + tile <= F;
+            if (fast) load_tree_block<VB, HINT, VPT>(a, t + threadIdx.x, block, true, r);
+            else {
+                // Edge tile of this CTA: loads past E belong to the next CTA.
+                load_tree_block<VB, HINT, VPT>(a, t + threadIdx.x, block, false, r);
 #pragma unroll
-            for (int v = 0; v < VPT; ++v) {
-                uint32_t x[RPV];
-                ldg_stream<VB, HINT>(p + (unsigned long long)v * block * VB, x);
+                for (int v = 0; v < VPT; ++v)
+                    if (t + (unsigned long long)v * block + threadIdx.x >= E)
 #pragma unroll
-                for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+                        for (int j = 0; j < RPV; ++j) r[v * RPV + j] = 0;
             }
-        } else {  // edge tile: predicated loads, byte masks on the first/last vector
-#pragma unroll
-            for (int v = 0; v < VPT; ++v) {
-                const unsigned long long idx = t + (unsigned long long)v * block + threadIdx.x;
-                uint32_t x[RPV];
-#pragma unroll
-                for (int j = 0; j < RPV; ++j) x[j] = 0;
-                if (idx >= a.v0 && idx < E) {
-                    ldg_stream<VB, HINT>(a.base + idx * VB, x);
-                    if (idx == a.v0 || idx + 1 == a.v1)
-                        mask_bytes<VB>(x, idx == a.v0 ? a.lo_byte : 0, idx + 1 == a.v1 ? a.hi_byte : VB);
+            tree_block<NBANK, L>(r, carries, counter);
+            if (++nb == a.flush_threshold) {  // block-uniform: every thread runs the same tiles
+                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                nb = 0;
+            }
+        }
+    } else {
+        constexpr unsigned long long WT = 32ull * VPT;  // vectors per warp tile
+        const unsigned long long S0 = a.g0 * 32;
+        unsigned long long mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+        unsigned long long c = __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;  // prefetch: consumed one chunk later
+        for (;;) {
+            unsigned long long w0, w1;
+            if (c < a.nA) {
+                w0 = c * a.CA;
+                w1 = w0 + a.CA;
+            } else {
+                w0 = a.nA * a.CA + (c - a.nA) * a.CB;
+                w1 = w0 + a.CB < a.nwt ? w0 + a.CB : a.nwt;
+            }
+            if (w0 >= a.nwt) break;  // warp-uniform
+            for (unsigned long long w = w0; w < w1; ++w) {
+                const unsigned long long t = S0 + w * WT;
+                uint32_t r[REGS];
+                load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
+                tree_block<NBANK, L>(r, carries, counter);
+                if (++nb == a.flush_threshold) {  // warp-uniform
+                    flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                    nb = 0;
                 }
-#pragma unroll
-                for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
             }
-        }
-        tree_block<NBANK, L>(r, carries, counter);
-        if (++nb == a.flush_threshold) {  // block-uniform: every thread runs the same tiles
-            uint32_t d[16];
-#pragma unroll
-            for (int p = 0; p < 16; ++p) d[p] = 0;
-#pragma unroll
-            for (int b = 0; b < NBANK; ++b) {
-                const uint32_t tot = bank_warp_total(counter[b], L, d);
-                if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
-            }
-            zero_bank<NBANK>(counter);
-            nb = 0;
+            c = __shfl_sync(0xFFFFFFFFu, mine, 0);
+            mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
         }
     }
-
-    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer();
-    // Final flush of the lane bank (weight 2^L) fused with the carry drain.
-#pragma unroll
-    for (int b = 0; b < NBANK; ++b) {
-        uint32_t d[16];
-        drain<L>(d, carries[b]);
-        const uint32_t tot = bank_warp_total(counter[b], L, d);
-        if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
-    }
-    __syncthreads();
-
-    for (int c = threadIdx.x; c < 32 * NBANK; c += block)
-        if (s_acc[c]) atomicAdd(&a.acc[c], s_acc[c]);
-    __threadfence();
-    __syncthreads();
-    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = globaltimer();
-    if (threadIdx.x == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-
-    // Last CTA: every other CTA has fenced its channel atomics.  Fold the
-    // channels to positions, reading and re-zeroing the accumulator.
-    __threadfence();
-    const int k = a.k;
-    for (int pos = threadIdx.x; pos < k; pos += block) {
-        unsigned long long sum = 0;
-        if (k == 64) {
-            sum = atomicExch(&a.acc[pos], 0ull);
-        } else {
-            const int m = channels_per_position(k);
-            for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
-        }
-        a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
-    }
-    if (threadIdx.x == 0) *a.ticket = 0u;
-    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 3] = globaltimer();
+    cta_finish<NBANK, L>(a, carries, counter, s_acc, &s_last, block, lane);
 }
 
 // One warp per array.  Array a spans bytes [data + off[a]*wb, data + off[a+1]*wb);
 // it is read as VB-byte vectors from the VB-aligned address at or below its
 // start, the first/last vector byte-masked, 32 lanes x VPT vectors per step.
+// Warps pull array indices from a global counter (prefetched one array
+// ahead), so arrays of any length mix balance across warps and SMs; the last
+// CTA re-zeroes the counter and ticket for the next launch.
 template <int NBANK, int L, int VB>
 __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
                                                         const unsigned long long* offsets,
                                                         unsigned long long n_arrays, int k,
                                                         uint32_t flush_threshold,
-                                                        unsigned long long* out) {
+                                                        unsigned long long* out,
+                                                        unsigned long long* next,
+                                                        unsigned int* ticket) {
     constexpr int REGS = NBANK << L;
     constexpr int RPV = VB / 4;
     constexpr int VPT = REGS / RPV;
     constexpr unsigned long long STEP = 32ull * VPT;
     const uint32_t lane = threadIdx.x & 31u;
-    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
-    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     const int wb = k >> 3;
+    __shared__ int s_last;
 
-    for (unsigned long long arr = warp; arr < n_arrays; arr += nwarps) {
+    unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    unsigned long long arr = __shfl_sync(0xFFFFFFFFu, mine, 0);
+    mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    for (; arr < n_arrays; arr = __shfl_sync(0xFFFFFFFFu, mine, 0),
+                           mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull) {
         const uintptr_t P = (uintptr_t)(data + offsets[arr] * wb);
         const uintptr_t Q = (uintptr_t)(data + offsets[arr + 1] * wb);
         const uintptr_t B = P & ~(uintptr_t)(VB - 1);
@@ -302,6 +386,17 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
             unsigned long long t = tot[0];
             for (int w = 16; w >= k; w >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, w);
             if ((int)lane < k) row[lane] = t;
+        }
+    }
+    // Every warp has drawn an index >= n_arrays; once all CTAs are past that
+    // point the counter can be reset.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (s_last) {
+            *next = 0ull;
+            *ticket = 0u;
         }
     }
 }
@@ -413,31 +508,34 @@ int resident_blocks(Kernel kernel, int block) {
 using StreamKernel = void (*)(const StreamArgs);
 
 struct StreamVariant {
-    int nbank, depth, vb, hint, block;
+    int nbank, depth, vb, hint, block, sched;
     StreamKernel fn;
 };
 
-#define SV(NB, L, VB, H, B) {NB, L, VB, H, B, stream_kernel<NB, L, VB, H, B>}
+#define SV(NB, L, VB, H, B, S) {NB, L, VB, H, B, S, stream_kernel<NB, L, VB, H, B, S>}
 // Production variants first (the defaults), then tuning variants selectable
-// through POSPOP_STREAM_VARIANT="depth,vb,hint,block".
+// through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched".
 const StreamVariant kStreamVariants[] = {
-    SV(1, 7, 32, 0, 256), SV(2, 6, 32, 0, 256),  // defaults (k <= 32 / k = 64)
-    SV(1, 7, 32, 0, 0), SV(2, 6, 32, 0, 0),      // runtime block size (test launches)
-    SV(2, 5, 16, 0, 256), SV(2, 5, 16, 0, 0),
-    SV(1, 6, 16, 0, 256), SV(1, 6, 32, 0, 256), SV(1, 6, 16, 0, 512), SV(1, 7, 16, 0, 256),
-    SV(1, 7, 32, 1, 256), SV(1, 7, 32, 0, 128), SV(1, 7, 32, 0, 512), SV(1, 8, 32, 0, 256),
-    SV(2, 5, 32, 0, 256), SV(2, 6, 16, 0, 256),
+    SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // defaults (k <= 32 / k = 64)
+    SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1),      // runtime block size (test launches)
+    SV(1, 7, 32, 0, 256, 0), SV(2, 6, 32, 0, 256, 0),  // static CTA partition
+    SV(1, 7, 32, 0, 0, 0), SV(2, 6, 32, 0, 0, 0),
+    SV(1, 6, 32, 0, 256, 1), SV(1, 6, 16, 0, 256, 1), SV(1, 7, 16, 0, 256, 1), SV(1, 7, 32, 1, 256, 1),
+    SV(1, 7, 32, 0, 128, 1), SV(1, 7, 32, 0, 512, 1), SV(1, 6, 32, 0, 512, 1), SV(1, 5, 32, 0, 256, 1),
+    SV(2, 5, 32, 0, 256, 1), SV(2, 5, 16, 0, 256, 1), SV(2, 6, 16, 0, 256, 1),
 };
 #undef SV
 
-const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block) {
+const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block, int sched) {
     for (const StreamVariant& v : kStreamVariants)
-        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.hint == hint && v.block == block) return &v;
+        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.hint == hint && v.block == block &&
+            v.sched == sched)
+            return &v;
     return nullptr;
 }
 
 using SegKernel = void (*)(const uint8_t*, const unsigned long long*, unsigned long long, int, uint32_t,
-                           unsigned long long*);
+                           unsigned long long*, unsigned long long*, unsigned int*);
 
 struct SegVariant {
     int nbank, depth, vb;
@@ -446,8 +544,8 @@ struct SegVariant {
 
 #define SG(NB, L, VB) {NB, L, VB, segmented_kernel<NB, L, VB>}
 const SegVariant kSegVariants[] = {
-    SG(1, 4, 16), SG(2, 4, 32),  // defaults (k <= 32 / k = 64)
-    SG(1, 3, 16), SG(1, 5, 16), SG(1, 4, 32), SG(1, 5, 32), SG(2, 3, 16), SG(2, 4, 16), SG(2, 3, 32),
+    SG(1, 5, 16), SG(2, 4, 16),  // defaults (k <= 32 / k = 64)
+    SG(1, 4, 16), SG(1, 6, 16), SG(1, 4, 32), SG(1, 5, 32), SG(2, 3, 16), SG(2, 4, 32), SG(2, 5, 16),
 };
 #undef SG
 
@@ -465,16 +563,17 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
                           bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
                           cudaStream_t stream, int* grid_used) {
     const int nbank = k == 64 ? 2 : 1;
-    // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block".
-    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 32, hint = 0,
-        block = kDefaultBlock;
-    if (const char* v = std::getenv("POSPOP_STREAM_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &hint, &block);
+    // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched".
+    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 32, hint = 0, block = kDefaultBlock, sched = 1;
+    if (const char* v = std::getenv("POSPOP_STREAM_VARIANT"))
+        std::sscanf(v, "%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched);
     if (opt.depth) depth = opt.depth;
     if (opt.block) block = 0;  // explicit (test) block size: the runtime-block instantiation
-    const StreamVariant* var = pick_stream(nbank, depth, vb, hint, block);
-    if (!var) var = pick_stream(nbank, depth, vb, 0, 0);
+    const StreamVariant* var = pick_stream(nbank, depth, vb, hint, block, sched);
+    if (!var) var = pick_stream(nbank, depth, vb, 0, 0, sched);
     if (!var) return cudaErrorInvalidConfiguration;
     const int threads = var->block ? var->block : (opt.block ? opt.block : kDefaultBlock);
+    const int vpt = (nbank << var->depth) / (var->vb / 4);
 
     const uintptr_t P = reinterpret_cast<uintptr_t>(data);
     const size_t nbytes = len_words * (size_t)(k / 8);
@@ -504,15 +603,29 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
     a.out = d_out;
     a.accumulate = accumulate ? 1 : 0;
     a.trace = opt.trace;
+    a.next = ws.next;
 
     int grid = opt.grid;
     if (grid <= 0) {
-        const unsigned long long tile = (unsigned long long)((nbank << var->depth) / (var->vb / 4)) * threads;
+        const unsigned long long tile = (unsigned long long)vpt * threads;
         const unsigned long long want = (a.ng * 32 + tile - 1) / tile;
         const int per_sm = env_int("POSPOP_BLOCKS_PER_SM", resident_blocks(var->fn, threads));
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
     }
+    // Dynamic schedule: nwt warp tiles; the last ~tail_per_warp warp tiles per
+    // warp go out in small chunks of CB, everything before in chunks of CA.
+    const unsigned long long wt = 32ull * vpt;
+    a.nwt = a.ng ? (a.v1 - a.g0 * 32 + wt - 1) / wt : 0;
+    a.CA = (unsigned long long)env_int("POSPOP_CHUNK_A", 16);
+    a.CB = (unsigned long long)env_int("POSPOP_CHUNK_B", 2);
+    if (a.CA < 1) a.CA = 1;
+    if (a.CB < 1) a.CB = 1;
+    const unsigned long long warps = (unsigned long long)grid * (threads / 32);
+    unsigned long long tail = warps * (unsigned long long)env_int("POSPOP_TAIL_TILES_PER_WARP", 8);
+    if (tail > a.nwt) tail = a.nwt;
+    a.nA = (a.nwt - tail) / a.CA;
+
     if (grid_used) *grid_used = grid;
     var->fn<<<grid, threads, 0, stream>>>(a);
     ++g_launches;
@@ -520,26 +633,27 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
 }
 
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets, size_t n,
-                             unsigned long long* d_out, const LaunchOptions& opt, cudaStream_t stream) {
+                             unsigned long long* d_out, const LaunchOptions& opt, const StreamWorkspace& ws,
+                             cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_SEG_VARIANT="depth,vb".
-    int depth = 4, vb = nbank == 1 ? 16 : 32;
+    int depth = nbank == 1 ? 5 : 4, vb = 16;
     if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d", &depth, &vb);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb);
-    if (!var) var = pick_segmented(nbank, 4, nbank == 1 ? 16 : 32);
+    if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {
         const unsigned long long warps_per_block = block / 32;
         const unsigned long long want = (n + warps_per_block - 1) / warps_per_block;
-        const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", resident_blocks(var->fn, block));
+        const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", resident_blocks(var->fn, block));  // one wave
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < cap ? want : cap);
     }
     var->fn<<<grid, block, 0, stream>>>(static_cast<const uint8_t*>(data), d_offsets, n, k,
-                                        opt.flush_threshold, d_out);
+                                        opt.flush_threshold, d_out, ws.next, ws.ticket);
     ++g_launches;
     return cudaGetLastError();
 }

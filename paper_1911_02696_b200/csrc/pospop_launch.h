@@ -13,9 +13,13 @@ namespace pospop_b200 {
 // channel totals and a completion ticket.  Both must be zero before a
 // launch; the kernel's last block leaves them zero again.
 struct StreamWorkspace {
-    unsigned long long* acc = nullptr;
-    unsigned int* ticket = nullptr;
+    unsigned long long* acc = nullptr;   // 64 channel accumulators
+    unsigned int* ticket = nullptr;      // CTA completion ticket
+    unsigned long long* next = nullptr;  // dynamic-schedule chunk counter
 };
+
+// Bytes of one workspace allocation: acc[64], ticket (u32 at +512), next (u64 at +520).
+constexpr size_t kWorkspaceBytes = 64 * sizeof(unsigned long long) + 64;
 
 struct LaunchOptions {
     uint32_t flush_threshold = 65535;  // tree blocks between lane flushes, [1, 65535]
@@ -36,7 +40,7 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
 // row a of d_out (k entries) is overwritten.  One kernel launch.
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets,
                              size_t n_arrays, unsigned long long* d_out, const LaunchOptions& opt,
-                             cudaStream_t stream);
+                             const StreamWorkspace& ws, cudaStream_t stream);
 
 // Synthetic inputs (see oracle/pospop_oracle.h orc_generate for the kinds).
 cudaError_t launch_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* out,

@@ -74,63 +74,69 @@ def main():
 
     if "stream" in what:
         out = torch.zeros(16, dtype=torch.int64, device="cuda")
-        os.environ.pop("POSPOP_STREAM_VARIANT", None)
+        for key in ("POSPOP_STREAM_VARIANT", "POSPOP_BLOCKS_PER_SM", "POSPOP_CHUNK_A", "POSPOP_CHUNK_B",
+                    "POSPOP_TAIL_TILES_PER_WARP"):
+            os.environ.pop(key, None)
         pp.count_async(data, out, 16, stream=s)
         torch.cuda.synchronize()
         want = out.clone()
-        variants = ["7,32,0,256", "7,32,1,256", "7,16,0,256", "7,32,0,128", "7,32,0,512", "8,32,0,256",
-                    "6,16,0,256", "6,32,0,256", "6,16,0,512"]
-        for var in variants:
-            for per_sm in ["", "1", "2", "3", "4", "8"]:
-                os.environ["POSPOP_STREAM_VARIANT"] = var
-                if per_sm:
-                    os.environ["POSPOP_BLOCKS_PER_SM"] = per_sm
+        cases = [  # (variant, per_sm, CA, CB, tail)
+            ("7,32,0,256,0", "", "", "", ""),
+            ("7,32,0,256,1", "", "", "", ""),
+            ("7,32,0,256,1", "", "4", "", ""), ("7,32,0,256,1", "", "8", "", ""),
+            ("7,32,0,256,1", "", "32", "", ""), ("7,32,0,256,1", "", "64", "", ""),
+            ("7,32,0,256,1", "", "", "1", ""), ("7,32,0,256,1", "", "", "4", ""),
+            ("7,32,0,256,1", "", "", "", "2"), ("7,32,0,256,1", "", "", "", "4"), ("7,32,0,256,1", "", "", "", "16"),
+            ("7,32,0,256,1", "2", "", "", ""),
+            ("6,32,0,256,1", "", "", "", ""), ("6,32,0,256,1", "2", "", "", ""),
+            ("6,16,0,256,1", "", "", "", ""), ("7,16,0,256,1", "", "", "", ""),
+            ("7,32,0,512,1", "", "", "", ""), ("6,32,0,512,1", "", "", "", ""), ("5,32,0,256,1", "", "", "", ""),
+        ]
+        for var, per_sm, ca, cb, tail in cases:
+            env = {"POSPOP_STREAM_VARIANT": var, "POSPOP_BLOCKS_PER_SM": per_sm, "POSPOP_CHUNK_A": ca,
+                   "POSPOP_CHUNK_B": cb, "POSPOP_TAIL_TILES_PER_WARP": tail}
+            for kk, vv in env.items():
+                if vv:
+                    os.environ[kk] = vv
                 else:
-                    os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
+                    os.environ.pop(kk, None)
+            for nb in (1 << 29, 1 << 30, 1 << 33):
                 try:
-                    med, best = timed(lambda: pp.count_async(data, out, 16, stream=s), args.reps, s)
-                    ok = bool(torch.equal(out, want))
-                    emit(kind="stream16", variant=var, per_sm=per_sm or "occ", gbs_med=round(nbytes / med / 1e6, 1),
-                         gbs_best=round(nbytes / best / 1e6, 1), ok=ok)
+                    med, best = timed(lambda: pp.count_async(data, out, 16, stream=s, len_words=nb // 2), args.reps, s)
+                    ok = nb != (1 << 33) or bool(torch.equal(out, want))
+                    emit(kind="stream16", bytes=nb, variant=var, per_sm=per_sm or "occ", CA=ca or "16", CB=cb or "2",
+                         tail=tail or "8", gbs_med=round(nb / med / 1e6, 1), gbs_best=round(nb / best / 1e6, 1), ok=ok)
                 except Exception as e:  # noqa: BLE001
-                    emit(kind="stream16", variant=var, per_sm=per_sm, error=repr(e))
-        os.environ.pop("POSPOP_STREAM_VARIANT", None)
-        os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
+                    emit(kind="stream16", variant=var, error=repr(e))
+        for key in ("POSPOP_STREAM_VARIANT", "POSPOP_BLOCKS_PER_SM", "POSPOP_CHUNK_A", "POSPOP_CHUNK_B",
+                    "POSPOP_TAIL_TILES_PER_WARP"):
+            os.environ.pop(key, None)
         # other k on the same bytes
-        for k, var in [(8, "7,32,0,256"), (32, "7,32,0,256"), (64, "5,16,0,256"), (64, "5,32,0,256"),
-                       (64, "6,32,0,256"), (64, "6,16,0,256")]:
+        for k, var in [(8, "7,32,0,256,1"), (32, "7,32,0,256,1"), (64, "6,32,0,256,1"), (64, "6,32,0,256,0"),
+                       (64, "5,32,0,256,1"), (64, "5,16,0,256,1"), (64, "6,16,0,256,1")]:
             os.environ["POSPOP_STREAM_VARIANT"] = var
             o = torch.zeros(k, dtype=torch.int64, device="cuda")
-            med, best = timed(lambda: pp.count_async(data, o, k, stream=s), args.reps, s)
-            emit(kind=f"stream{k}", variant=var, gbs_med=round(nbytes / med / 1e6, 1), gbs_best=round(nbytes / best / 1e6, 1))
+            for nb in (1 << 30, 1 << 33):
+                med, best = timed(lambda: pp.count_async(data, o, k, stream=s, len_words=nb * 8 // k), args.reps, s)
+                emit(kind=f"stream{k}", bytes=nb, variant=var, gbs_med=round(nb / med / 1e6, 1),
+                     gbs_best=round(nb / best / 1e6, 1))
         os.environ.pop("POSPOP_STREAM_VARIANT", None)
-        # cfg3 (u8 at +3, 2^30-7) and cfg2 (2^28 one-hot)
+        # cfg3 (u8 at +3, 2^30-7) and cfg2 (2^28 one-hot), default variant
         b3 = torch.empty((1 << 30) + 64, dtype=torch.uint8, device="cuda")
         n3 = (1 << 30) - 7
         pp.generate(pp.GEN_CFG3, 1, b3[3:3 + n3], stream=s)
         o8 = torch.zeros(8, dtype=torch.int64, device="cuda")
         b2 = torch.empty(1 << 29, dtype=torch.uint8, device="cuda")
         pp.generate(pp.GEN_CFG2, 1, b2, stream=s)
-        for var in ["7,32,0,256", "6,16,0,256", "6,32,0,256", "6,16,0,512"]:
-            for per_sm in ["", "1", "2", "4", "8", "16"]:
-                os.environ["POSPOP_STREAM_VARIANT"] = var
-                if per_sm:
-                    os.environ["POSPOP_BLOCKS_PER_SM"] = per_sm
-                else:
-                    os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
-                med, best = timed(lambda: pp.count_async(b3[3:3 + n3], o8, 8, stream=s), args.reps, s)
-                emit(kind="cfg3", variant=var, per_sm=per_sm or "occ", gbs_med=round(n3 / med / 1e6, 1),
-                     gbs_best=round(n3 / best / 1e6, 1))
-                med, best = timed(lambda: pp.count_async(b2, out, 16, stream=s), args.reps, s)
-                emit(kind="cfg2", variant=var, per_sm=per_sm or "occ", gbs_med=round((1 << 29) / med / 1e6, 1),
-                     gbs_best=round((1 << 29) / best / 1e6, 1))
-        os.environ.pop("POSPOP_STREAM_VARIANT", None)
-        os.environ.pop("POSPOP_BLOCKS_PER_SM", None)
+        med, best = timed(lambda: pp.count_async(b3[3:3 + n3], o8, 8, stream=s), args.reps, s)
+        emit(kind="cfg3", gbs_med=round(n3 / med / 1e6, 1), gbs_best=round(n3 / best / 1e6, 1))
+        med, best = timed(lambda: pp.count_async(b2, out, 16, stream=s), args.reps, s)
+        emit(kind="cfg2", gbs_med=round((1 << 29) / med / 1e6, 1), gbs_best=round((1 << 29) / best / 1e6, 1))
         del b3, b2
 
     if "seg" in what:
-        for k, kind, variants in [(32, pp.GEN_U32, ["4,16", "3,16", "5,16", "4,32", "5,32"]),
-                                  (64, pp.GEN_U64, ["4,32", "3,16", "4,16", "3,32"])]:
+        for k, kind, variants in [(32, pp.GEN_U32, ["5,16", "4,16", "6,16", "5,32"]),
+                                  (64, pp.GEN_U64, ["4,16", "4,32", "5,16", "3,16"])]:
             arrays, words = 65536, 4096
             d = data[:arrays * words * k // 8]
             pp.generate(kind, 1, d, stream=s)
