@@ -59,6 +59,7 @@ struct StreamArgs {
     // dynamic schedule (SCHED 1): warp tiles, chunk counter, chunk sizes
     unsigned long long* next;   // global chunk counter (zero on entry, re-zeroed by the last CTA)
     unsigned long long nwt, nA, CA, CB;
+    unsigned long long pool;    // SCHED 2: warp tiles in the global tail pool
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -252,6 +253,57 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
                 nb = 0;
             }
         }
+    } else if constexpr (SCHED == 2) {
+        // Warp tiles [0, P) are split statically into contiguous CTA ranges
+        // (DRAM locality); inside a CTA, warps claim warp tiles from a shared
+        // counter, so no warp idles while another still holds a share.  Warp
+        // tiles [P, nwt) form a global pool handed out in chunks of CB, so
+        // CTAs on faster SMs absorb the tail.
+        constexpr unsigned long long WT = 32ull * VPT;
+        const unsigned long long S0 = a.g0 * 32;
+        const unsigned long long P = a.nwt - a.pool;
+        const unsigned long long lo = P * blockIdx.x / gridDim.x;
+        const unsigned long long hi = P * (blockIdx.x + 1) / gridDim.x;
+        __shared__ unsigned s_claim;
+        if (threadIdx.x == 0) s_claim = 0u;
+        __syncthreads();
+        unsigned mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
+        unsigned long long w = lo + __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;  // prefetch
+        while (w < hi) {
+            const unsigned long long t = S0 + w * WT;
+            uint32_t r[REGS];
+            load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
+            tree_block<NBANK, L>(r, carries, counter);
+            if (++nb == a.flush_threshold) {  // warp-uniform
+                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                nb = 0;
+            }
+            w = lo + __shfl_sync(0xFFFFFFFFu, mine, 0);
+            mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
+        }
+        if (a.pool) {
+            unsigned long long m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            unsigned long long c = __shfl_sync(0xFFFFFFFFu, m, 0);
+            m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            for (;;) {
+                const unsigned long long w0 = P + c * a.CB;
+                if (w0 >= a.nwt) break;  // warp-uniform
+                const unsigned long long w1 = w0 + a.CB < a.nwt ? w0 + a.CB : a.nwt;
+                for (unsigned long long ww = w0; ww < w1; ++ww) {
+                    const unsigned long long t = S0 + ww * WT;
+                    uint32_t r[REGS];
+                    load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
+                    tree_block<NBANK, L>(r, carries, counter);
+                    if (++nb == a.flush_threshold) {
+                        flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                        nb = 0;
+                    }
+                }
+                c = __shfl_sync(0xFFFFFFFFu, m, 0);
+                m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            }
+        }
     } else {
         constexpr unsigned long long WT = 32ull * VPT;  // vectors per warp tile
         const unsigned long long S0 = a.g0 * 32;
@@ -291,14 +343,17 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
 // Warps pull array indices from a global counter (prefetched one array
 // ahead), so arrays of any length mix balance across warps and SMs; the last
 // CTA re-zeroes the counter and ticket for the next launch.
-template <int NBANK, int L, int VB>
+// SCHED 0: warp w takes arrays w, w + nwarps, ... (strided, no atomics).
+// SCHED 1: warps pull runs of `per_grab` consecutive arrays from a global
+// counter (prefetched one run ahead).
+template <int NBANK, int L, int VB, int SCHED>
 __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
                                                         const unsigned long long* offsets,
                                                         unsigned long long n_arrays, int k,
                                                         uint32_t flush_threshold,
                                                         unsigned long long* out,
                                                         unsigned long long* next,
-                                                        unsigned int* ticket) {
+                                                        unsigned int* ticket, unsigned per_grab) {
     constexpr int REGS = NBANK << L;
     constexpr int RPV = VB / 4;
     constexpr int VPT = REGS / RPV;
@@ -307,11 +362,25 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
     const int wb = k >> 3;
     __shared__ int s_last;
 
-    unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
-    unsigned long long arr = __shfl_sync(0xFFFFFFFFu, mine, 0);
-    mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
-    for (; arr < n_arrays; arr = __shfl_sync(0xFFFFFFFFu, mine, 0),
-                           mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull) {
+    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    unsigned long long mine = 0, run = 0, arr = warp, stop = n_arrays;
+    if (SCHED == 1) {
+        mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+        run = __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+        arr = run * per_grab;
+        stop = arr + per_grab < n_arrays ? arr + per_grab : n_arrays;
+    }
+    for (;;) {
+        if (arr >= stop) {
+            if (SCHED == 0) break;
+            run = __shfl_sync(0xFFFFFFFFu, mine, 0);
+            mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+            arr = run * per_grab;
+            if (arr >= n_arrays) break;
+            stop = arr + per_grab < n_arrays ? arr + per_grab : n_arrays;
+        }
         const uintptr_t P = (uintptr_t)(data + offsets[arr] * wb);
         const uintptr_t Q = (uintptr_t)(data + offsets[arr + 1] * wb);
         const uintptr_t B = P & ~(uintptr_t)(VB - 1);
@@ -387,7 +456,9 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
             for (int w = 16; w >= k; w >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, w);
             if ((int)lane < k) row[lane] = t;
         }
+        arr += SCHED == 0 ? nwarps : 1;
     }
+    if (SCHED == 0) return;
     // Every warp has drawn an index >= n_arrays; once all CTAs are past that
     // point the counter can be reset.
     __syncthreads();
@@ -516,10 +587,12 @@ struct StreamVariant {
 // Production variants first (the defaults), then tuning variants selectable
 // through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched".
 const StreamVariant kStreamVariants[] = {
-    SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // defaults (k <= 32 / k = 64)
-    SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1),      // runtime block size (test launches)
+    SV(1, 7, 32, 0, 256, 2), SV(2, 6, 32, 0, 256, 2),  // defaults (k <= 32 / k = 64)
+    SV(1, 7, 32, 0, 0, 2), SV(2, 6, 32, 0, 0, 2),      // runtime block size (test launches)
     SV(1, 7, 32, 0, 256, 0), SV(2, 6, 32, 0, 256, 0),  // static CTA partition
     SV(1, 7, 32, 0, 0, 0), SV(2, 6, 32, 0, 0, 0),
+    SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // per-warp guided chunks
+    SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1), SV(1, 6, 32, 0, 256, 2), SV(1, 7, 16, 0, 256, 2),
     SV(1, 6, 32, 0, 256, 1), SV(1, 6, 16, 0, 256, 1), SV(1, 7, 16, 0, 256, 1), SV(1, 7, 32, 1, 256, 1),
     SV(1, 7, 32, 0, 128, 1), SV(1, 7, 32, 0, 512, 1), SV(1, 6, 32, 0, 512, 1), SV(1, 5, 32, 0, 256, 1),
     SV(2, 5, 32, 0, 256, 1), SV(2, 5, 16, 0, 256, 1), SV(2, 6, 16, 0, 256, 1),
@@ -535,23 +608,24 @@ const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int blo
 }
 
 using SegKernel = void (*)(const uint8_t*, const unsigned long long*, unsigned long long, int, uint32_t,
-                           unsigned long long*, unsigned long long*, unsigned int*);
+                           unsigned long long*, unsigned long long*, unsigned int*, unsigned);
 
 struct SegVariant {
-    int nbank, depth, vb;
+    int nbank, depth, vb, sched;
     SegKernel fn;
 };
 
-#define SG(NB, L, VB) {NB, L, VB, segmented_kernel<NB, L, VB>}
+#define SG(NB, L, VB, S) {NB, L, VB, S, segmented_kernel<NB, L, VB, S>}
 const SegVariant kSegVariants[] = {
-    SG(1, 5, 16), SG(2, 4, 16),  // defaults (k <= 32 / k = 64)
-    SG(1, 4, 16), SG(1, 6, 16), SG(1, 4, 32), SG(1, 5, 32), SG(2, 3, 16), SG(2, 4, 32), SG(2, 5, 16),
+    SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
+    SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
+    SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
 };
 #undef SG
 
-const SegVariant* pick_segmented(int nbank, int depth, int vb) {
+const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched) {
     for (const SegVariant& v : kSegVariants)
-        if (v.nbank == nbank && v.depth == depth && v.vb == vb) return &v;
+        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.sched == sched) return &v;
     return nullptr;
 }
 
@@ -564,7 +638,7 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
                           cudaStream_t stream, int* grid_used) {
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched".
-    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 32, hint = 0, block = kDefaultBlock, sched = 1;
+    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 32, hint = 0, block = kDefaultBlock, sched = 2;
     if (const char* v = std::getenv("POSPOP_STREAM_VARIANT"))
         std::sscanf(v, "%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched);
     if (opt.depth) depth = opt.depth;
@@ -625,6 +699,9 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
     unsigned long long tail = warps * (unsigned long long)env_int("POSPOP_TAIL_TILES_PER_WARP", 8);
     if (tail > a.nwt) tail = a.nwt;
     a.nA = (a.nwt - tail) / a.CA;
+    // SCHED 2: the global tail pool, in warp tiles.
+    a.pool = warps * (unsigned long long)env_int("POSPOP_POOL_TILES_PER_WARP", 4);
+    if (a.pool > a.nwt) a.pool = a.nwt;
 
     if (grid_used) *grid_used = grid;
     var->fn<<<grid, threads, 0, stream>>>(a);
@@ -637,23 +714,26 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
                              cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     const int nbank = k == 64 ? 2 : 1;
-    // Tuning override: POSPOP_SEG_VARIANT="depth,vb".
-    int depth = nbank == 1 ? 5 : 4, vb = 16;
-    if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d", &depth, &vb);
+    // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched".
+    int depth = 5, vb = 16, sched = nbank == 1 ? 0 : 1;
+    if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d", &depth, &vb, &sched);
     if (opt.depth) depth = opt.depth;
-    const SegVariant* var = pick_segmented(nbank, depth, vb);
-    if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16);
+    const SegVariant* var = pick_segmented(nbank, depth, vb, sched);
+    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 0 : 1);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {
         const unsigned long long warps_per_block = block / 32;
         const unsigned long long want = (n + warps_per_block - 1) / warps_per_block;
-        const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", resident_blocks(var->fn, block));  // one wave
+        // measured (r01 sweep): 4 CTAs/SM for the strided schedule, one resident wave for the dynamic one
+        const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", var->sched == 0 ? 4 : resident_blocks(var->fn, block));
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < cap ? want : cap);
     }
+    const unsigned per_grab = (unsigned)env_int("POSPOP_SEG_PER_GRAB", 1);
     var->fn<<<grid, block, 0, stream>>>(static_cast<const uint8_t*>(data), d_offsets, n, k,
-                                        opt.flush_threshold, d_out, ws.next, ws.ticket);
+                                        opt.flush_threshold, d_out, ws.next, ws.ticket,
+                                        per_grab < 1 ? 1u : per_grab);
     ++g_launches;
     return cudaGetLastError();
 }

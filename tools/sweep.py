@@ -75,26 +75,25 @@ def main():
     if "stream" in what:
         out = torch.zeros(16, dtype=torch.int64, device="cuda")
         for key in ("POSPOP_STREAM_VARIANT", "POSPOP_BLOCKS_PER_SM", "POSPOP_CHUNK_A", "POSPOP_CHUNK_B",
-                    "POSPOP_TAIL_TILES_PER_WARP"):
+                    "POSPOP_TAIL_TILES_PER_WARP", "POSPOP_POOL_TILES_PER_WARP"):
             os.environ.pop(key, None)
         pp.count_async(data, out, 16, stream=s)
         torch.cuda.synchronize()
         want = out.clone()
-        cases = [  # (variant, per_sm, CA, CB, tail)
+        cases = [  # (variant, per_sm, CA, CB, tail or pool tiles per warp)
             ("7,32,0,256,0", "", "", "", ""),
-            ("7,32,0,256,1", "", "", "", ""),
-            ("7,32,0,256,1", "", "4", "", ""), ("7,32,0,256,1", "", "8", "", ""),
-            ("7,32,0,256,1", "", "32", "", ""), ("7,32,0,256,1", "", "64", "", ""),
-            ("7,32,0,256,1", "", "", "1", ""), ("7,32,0,256,1", "", "", "4", ""),
-            ("7,32,0,256,1", "", "", "", "2"), ("7,32,0,256,1", "", "", "", "4"), ("7,32,0,256,1", "", "", "", "16"),
-            ("7,32,0,256,1", "2", "", "", ""),
-            ("6,32,0,256,1", "", "", "", ""), ("6,32,0,256,1", "2", "", "", ""),
-            ("6,16,0,256,1", "", "", "", ""), ("7,16,0,256,1", "", "", "", ""),
-            ("7,32,0,512,1", "", "", "", ""), ("6,32,0,512,1", "", "", "", ""), ("5,32,0,256,1", "", "", "", ""),
+            ("7,32,0,256,1", "", "64", "", "32"), ("7,32,0,256,1", "", "32", "", "64"),
+            ("7,32,0,256,2", "", "", "", ""),
+            ("7,32,0,256,2", "", "", "", "0"), ("7,32,0,256,2", "", "", "", "1"), ("7,32,0,256,2", "", "", "", "2"),
+            ("7,32,0,256,2", "", "", "", "8"), ("7,32,0,256,2", "", "", "", "16"),
+            ("7,32,0,256,2", "", "", "1", ""), ("7,32,0,256,2", "", "", "4", ""), ("7,32,0,256,2", "", "", "8", "16"),
+            ("7,32,0,256,2", "2", "", "", ""),
+            ("6,32,0,256,2", "", "", "", ""), ("7,16,0,256,2", "", "", "", ""),
         ]
         for var, per_sm, ca, cb, tail in cases:
             env = {"POSPOP_STREAM_VARIANT": var, "POSPOP_BLOCKS_PER_SM": per_sm, "POSPOP_CHUNK_A": ca,
-                   "POSPOP_CHUNK_B": cb, "POSPOP_TAIL_TILES_PER_WARP": tail}
+                   "POSPOP_CHUNK_B": cb, "POSPOP_TAIL_TILES_PER_WARP": tail if var.endswith(",1") else "",
+                   "POSPOP_POOL_TILES_PER_WARP": tail if var.endswith(",2") else ""}
             for kk, vv in env.items():
                 if vv:
                     os.environ[kk] = vv
@@ -109,11 +108,10 @@ def main():
                 except Exception as e:  # noqa: BLE001
                     emit(kind="stream16", variant=var, error=repr(e))
         for key in ("POSPOP_STREAM_VARIANT", "POSPOP_BLOCKS_PER_SM", "POSPOP_CHUNK_A", "POSPOP_CHUNK_B",
-                    "POSPOP_TAIL_TILES_PER_WARP"):
+                    "POSPOP_TAIL_TILES_PER_WARP", "POSPOP_POOL_TILES_PER_WARP"):
             os.environ.pop(key, None)
         # other k on the same bytes
-        for k, var in [(8, "7,32,0,256,1"), (32, "7,32,0,256,1"), (64, "6,32,0,256,1"), (64, "6,32,0,256,0"),
-                       (64, "5,32,0,256,1"), (64, "5,16,0,256,1"), (64, "6,16,0,256,1")]:
+        for k, var in [(8, "7,32,0,256,2"), (32, "7,32,0,256,2"), (64, "6,32,0,256,2"), (64, "6,32,0,256,0")]:
             os.environ["POSPOP_STREAM_VARIANT"] = var
             o = torch.zeros(k, dtype=torch.int64, device="cuda")
             for nb in (1 << 30, 1 << 33):
@@ -135,28 +133,30 @@ def main():
         del b3, b2
 
     if "seg" in what:
-        for k, kind, variants in [(32, pp.GEN_U32, ["5,16", "4,16", "6,16", "5,32"]),
-                                  (64, pp.GEN_U64, ["4,16", "4,32", "5,16", "3,16"])]:
+        for k, kind in [(32, pp.GEN_U32), (64, pp.GEN_U64)]:
             arrays, words = 65536, 4096
             d = data[:arrays * words * k // 8]
             pp.generate(kind, 1, d, stream=s)
             offs = torch.arange(0, arrays + 1, dtype=torch.int64, device="cuda") * words
             o = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
             want = None
-            for var in variants:
-                for per_sm in ["", "2", "4", "8"]:
-                    os.environ["POSPOP_SEG_VARIANT"] = var
-                    if per_sm:
-                        os.environ["POSPOP_SEG_BLOCKS_PER_SM"] = per_sm
+            cases = [(v, ps, g) for v in ("5,16,0", "4,16,0", "5,32,0") for ps in ("", "2", "4", "8") for g in ("",)]
+            cases += [(v, ps, g) for v in ("5,16,1", "4,16,1") for ps in ("", "2") for g in ("1", "2", "4")]
+            for var, per_sm, g in cases:
+                env = {"POSPOP_SEG_VARIANT": var, "POSPOP_SEG_BLOCKS_PER_SM": per_sm, "POSPOP_SEG_PER_GRAB": g}
+                for kk, vv in env.items():
+                    if vv:
+                        os.environ[kk] = vv
                     else:
-                        os.environ.pop("POSPOP_SEG_BLOCKS_PER_SM", None)
-                    med, best = timed(lambda: pp.segmented_async(d, offs, o, k, stream=s), args.reps, s)
-                    if want is None:
-                        want = o.clone()
-                    emit(kind=f"seg{k}", variant=var, per_sm=per_sm or "occ", ok=bool(torch.equal(o, want)),
-                         gbs_med=round(d.numel() / med / 1e6, 1), gbs_best=round(d.numel() / best / 1e6, 1))
-            os.environ.pop("POSPOP_SEG_VARIANT", None)
-            os.environ.pop("POSPOP_SEG_BLOCKS_PER_SM", None)
+                        os.environ.pop(kk, None)
+                med, best = timed(lambda: pp.segmented_async(d, offs, o, k, stream=s), args.reps, s)
+                if want is None:
+                    want = o.clone()
+                emit(kind=f"seg{k}", variant=var, per_sm=per_sm or "dflt", per_grab=g or "1",
+                     ok=bool(torch.equal(o, want)), gbs_med=round(d.numel() / med / 1e6, 1),
+                     gbs_best=round(d.numel() / best / 1e6, 1))
+            for kk in ("POSPOP_SEG_VARIANT", "POSPOP_SEG_BLOCKS_PER_SM", "POSPOP_SEG_PER_GRAB"):
+                os.environ.pop(kk, None)
 
 
 if __name__ == "__main__":
