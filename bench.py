@@ -368,7 +368,7 @@ def run_ours(args):
         "data": "synthetic (counter-based generator, generated in place in HBM)",
         "config": {"workload": desc, "words_total": total, "k": k, "bytes_per_step": total_bytes,
                    "parallelism": f"shard{world}", "l2_policy": "input >> 126 MB L2; no flush needed",
-                   "kernel": "stream_kernel<NBANK=1,L=7,VB=32,BLOCK=256>: LDG.E.NA.256 + LOP3 Harley-Seal depth 7, one launch per step"},
+                   "kernel": "stream_kernel<NBANK=1,L=7,VB=32,BLOCK=256,SCHED=2>: LDG.E.NA.256 + LOP3 Harley-Seal depth 7, CTA ranges + shared-counter warp tiles + global tail pool; one launch per step"},
         "words_per_s": round(total_bytes / wb / (ms_per_step * 1e-3), 1),
         "pct_hbm_peak": round(100 * value / world / peak, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",

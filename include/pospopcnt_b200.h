@@ -51,7 +51,8 @@ typedef enum {
     POSPOP_EINVAL = 1,       /* std::invalid_argument          (pospop.cpp:63-70) */
     POSPOP_EUNAVAILABLE = 2, /* pospop::KernelUnavailableError (types.hpp:68-71)  */
     POSPOP_ECUDA = 3,        /* CUDA runtime failure (message in pospop_last_error) */
-    POSPOP_ENOMEM = 4        /* device / pinned allocation failed                  */
+    POSPOP_ENOMEM = 4,       /* device / pinned allocation failed                  */
+    POSPOP_EFLAG = 5         /* pospop::InvalidFlagWordError (flagstats.hpp:64-75)  */
 } pospop_status;
 
 /* pospop::KernelKind, same order (types.hpp:52-60).  On the GPU every kind
@@ -128,6 +129,42 @@ pospop_status pospopcnt_u16_c32(const uint16_t* data, uint32_t len, uint32_t cou
  * device or host memory (each classified independently). */
 pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offsets, size_t n_arrays,
                                   uint64_t* counts);
+
+/* ---- file / pipe ingestion (the reference CLI's input path) ------------- */
+
+/* Counts a raw little-endian stream of k-bit words read from `fd` (a regular
+ * file: parallel pread; a pipe/stdin: sequential read) through pinned double
+ * buffers, overlapping host reads with H2D copies and the kernel.  As the
+ * reference's read_word_stream/decode_words (proj/tools/pospopcnt.cpp:52-75):
+ * a byte length that is not a multiple of k/8 is POSPOP_EINVAL ("odd byte
+ * length").  *n_words (may be NULL) receives the word count. */
+pospop_status pospopcnt_fd(int fd, int k, uint64_t* counts, uint64_t* n_words);
+
+/* Same for a path; "-" reads stdin.  Unopenable path: POSPOP_EINVAL. */
+pospop_status pospopcnt_file(const char* path, int k, uint64_t* counts, uint64_t* n_words);
+
+/* ---- FLAG statistics: the reference's application of the path ----------- */
+
+/* pospop::FlagBucket / FlagSummary (proj/core/include/pospop/flagstats.hpp:39-62),
+ * same fields in the same order. */
+typedef struct {
+    uint64_t total, secondary, supplementary, n_pair_good, n_read1, n_read2, n_sgltn, pair_map, mapped, dup;
+} pospop_flag_bucket;
+
+typedef struct {
+    pospop_flag_bucket pass; /* FQCFAIL clear */
+    pospop_flag_bucket fail; /* FQCFAIL set   */
+} pospop_flag_summary;
+
+/* pospop::flagstats_pospopcnt (flagstats.hpp:100, flagstats.cpp:127-145) fused
+ * into ONE pass over the FLAG words on the GPU: branchless transform, QC-pass
+ * and QC-fail positional counts, bucket derivation.  Equals
+ * flagstats_reference on every valid input.  A word with any of bits 12-15
+ * set returns POSPOP_EFLAG with *bad_offset / *bad_word of the FIRST such
+ * word (InvalidFlagWordError, flagstats.cpp:34-36); either pointer may be
+ * NULL.  `flags` may be host or device memory, 2-byte aligned. */
+pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_summary* out,
+                               uint64_t* bad_offset, uint16_t* bad_word);
 
 /* ---- multi-device, one process (the cfg4 shard/reduce driver) ----------- */
 

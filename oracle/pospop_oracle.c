@@ -269,6 +269,97 @@ int orc_segmented(const void* data, const uint64_t* offsets, size_t n, int k, in
 }
 
 /* ------------------------------------------------------------------------ */
+/* FLAG statistics                                                           */
+/* ------------------------------------------------------------------------ */
+
+enum { FPAIRED = 0x1, FPROPER_PAIR = 0x2, FUNMAP = 0x4, FMUNMAP = 0x8, FREAD1 = 0x40, FREAD2 = 0x80,
+       FSECONDARY = 0x100, FQCFAIL = 0x200, FDUP = 0x400, FSUPPLEMENTARY = 0x800, PAIRMAP = 0x1000,
+       RESERVED = 0xF000 };
+
+/* proj/core/src/flagstats.cpp:70-92 */
+int orc_flagstats_reference(const uint16_t* flags, size_t len, uint64_t out[20], uint64_t* bad) {
+    for (int i = 0; i < 20; ++i) out[i] = 0;
+    for (size_t i = 0; i < len; ++i) {
+        const uint16_t c = flags[i];
+        if (c & RESERVED) {
+            *bad = i;
+            return 1;
+        }
+        uint64_t* b = (c & FQCFAIL) ? out + 10 : out;
+        ++b[0];
+        if (c & FSECONDARY) {
+            ++b[1];
+        } else if (c & FSUPPLEMENTARY) {
+            ++b[2];
+        } else if (c & FPAIRED) {
+            if ((c & FPROPER_PAIR) && !(c & FUNMAP)) ++b[3];
+            if (c & FREAD1) ++b[4];
+            if (c & FREAD2) ++b[5];
+            if ((c & FMUNMAP) && !(c & FUNMAP)) ++b[6];
+            if (!(c & FUNMAP) && !(c & FMUNMAP)) ++b[7];
+        }
+        if (!(c & FUNMAP)) ++b[8];
+        if (!(c & FDUP)) ++b[9];
+    }
+    return 0;
+}
+
+/* proj/core/src/flagstats.cpp:94-125 */
+void orc_flag_transform(uint16_t word, uint16_t* pass, uint16_t* fail) {
+    const uint16_t keep_secsupp = FUNMAP | FSECONDARY | FDUP | FSUPPLEMENTARY | FQCFAIL;
+    const uint16_t pairing = FPROPER_PAIR | FMUNMAP | FREAD1 | FREAD2;
+    const uint16_t is_secsupp = (word & (FSECONDARY | FSUPPLEMENTARY)) ? 0xFFFF : 0;
+    const uint16_t is_sec = (word & FSECONDARY) ? 0xFFFF : 0;
+    const uint16_t is_paired = (word & FPAIRED) ? 0xFFFF : 0;
+    const uint16_t is_unmap = (word & FUNMAP) ? 0xFFFF : 0;
+    const uint16_t is_munmap = (word & FMUNMAP) ? 0xFFFF : 0;
+    uint16_t dat = word;
+    dat &= (uint16_t)~(is_secsupp & (uint16_t)~keep_secsupp);
+    dat &= (uint16_t)~(is_sec & FSUPPLEMENTARY);
+    dat &= (uint16_t)~((uint16_t)~is_paired & pairing);
+    dat &= (uint16_t)~(is_unmap & (FPROPER_PAIR | FMUNMAP));
+    dat |= (uint16_t)(is_paired & (uint16_t)~is_secsupp & (uint16_t)~is_unmap & (uint16_t)~is_munmap & PAIRMAP);
+    const uint16_t is_fail = (word & FQCFAIL) ? 0xFFFF : 0;
+    *pass = (uint16_t)(dat & (uint16_t)~is_fail);
+    *fail = (uint16_t)(dat & is_fail);
+}
+
+/* flagstats.cpp:50-63 (bucket_from_counts) */
+static void bucket_from_counts(const uint64_t c[16], uint64_t total, uint64_t b[10]) {
+    b[0] = total;
+    b[1] = c[8];
+    b[2] = c[11];
+    b[3] = c[1];
+    b[4] = c[6];
+    b[5] = c[7];
+    b[6] = c[3];
+    b[7] = c[12];
+    b[8] = total - c[2];
+    b[9] = total - c[10];
+}
+
+/* proj/core/src/flagstats.cpp:127-145 */
+int orc_flagstats_pospopcnt(const uint16_t* flags, size_t len, uint64_t out[20], uint64_t* bad) {
+    uint64_t pc[16] = {0}, fc[16] = {0};
+    for (size_t i = 0; i < len; ++i) {
+        if (flags[i] & RESERVED) {
+            *bad = i;
+            return 1;
+        }
+        uint16_t p, f;
+        orc_flag_transform(flags[i], &p, &f);
+        for (int q = 0; q < 16; ++q) {
+            pc[q] += (p >> q) & 1u;
+            fc[q] += (f >> q) & 1u;
+        }
+    }
+    const uint64_t fail_total = fc[9];
+    bucket_from_counts(fc, fail_total, out + 10);
+    bucket_from_counts(pc, len - fail_total, out);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* generators                                                                */
 /* ------------------------------------------------------------------------ */
 
@@ -300,6 +391,12 @@ uint64_t orc_mt64_next(orc_mt64* s) {
     y ^= (y << 37) & 0xFFF7EEE000000000ull;
     y ^= y >> 43;
     return y;
+}
+
+void orc_mt64_draws(uint64_t seed, size_t n, uint64_t* out) {
+    orc_mt64 s;
+    orc_mt64_seed(&s, seed);
+    for (size_t i = 0; i < n; ++i) out[i] = orc_mt64_next(&s);
 }
 
 void orc_mt_generate_stream(uint64_t seed, size_t len, uint16_t* out) {
@@ -364,6 +461,9 @@ static void gen_range(int kind, uint64_t key, uint64_t base, size_t lo, size_t h
             case 6:
                 ((uint64_t*)out)[l] = draw(key, i);
                 break;
+            case 7:
+                ((uint16_t*)out)[l] = (uint16_t)((draw(key, i >> 2) >> (16 * (i & 3))) & 0x0FFF);
+                break;
         }
     }
 }
@@ -382,7 +482,7 @@ static void* gen_worker(void* arg) {
 }
 
 int orc_generate(int kind, uint64_t seed, uint64_t base, size_t n, void* out, int threads) {
-    if (kind < 1 || kind > 6) return 1;
+    if (kind < 1 || kind > 7) return 1;
     const uint64_t key = gen_key(seed, kind);
     if (threads < 1) threads = 1;
     if ((size_t)threads > n / 65536 + 1) threads = (int)(n / 65536 + 1);

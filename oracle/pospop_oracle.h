@@ -75,6 +75,24 @@ int orc_pospopcnt(const void* data, size_t len_words, int k, int threads, uint64
 int orc_segmented(const void* data, const uint64_t* offsets, size_t n_arrays, int k, int threads,
                   uint64_t* counts);
 
+/* ---- FLAG statistics ---------------------------------- */
+
+/* FlagBucket field order (proj/core/include/pospop/flagstats.hpp:39-50):
+ * total, secondary, supplementary, n_pair_good, n_read1, n_read2, n_sgltn,
+ * pair_map, mapped, dup.  out20[0..10) = QC-pass bucket, out20[10..20) = QC-fail. */
+
+/* Branchy SAMtools-style reference: proj/core/src/flagstats.cpp:70-92.
+ * Returns 0, or 1 with *bad_offset = index of the first word with any of
+ * bits 12-15 set (InvalidFlagWordError, flagstats.cpp:34-36). */
+int orc_flagstats_reference(const uint16_t* flags, size_t len, uint64_t out20[20], uint64_t* bad_offset);
+
+/* Mask-select transform of one word: flagstats.cpp:94-125. */
+void orc_flag_transform(uint16_t word, uint16_t* pass, uint16_t* fail);
+
+/* Transform-then-count pipeline: flagstats.cpp:127-145 (two positional
+ * counts, buckets read from positions 1,2,3,6,7,8,9,10,11,12). */
+int orc_flagstats_pospopcnt(const uint16_t* flags, size_t len, uint64_t out20[20], uint64_t* bad_offset);
+
 /* ---- input generators (host twins of the device generators) ------------ */
 
 /* std::mt19937_64(seed), one word per draw from the low 16 bits:
@@ -85,6 +103,7 @@ void orc_mt_generate_stream(uint64_t seed, size_t len, uint16_t* out);
 typedef struct { uint64_t mt[312]; int idx; } orc_mt64;
 void orc_mt64_seed(orc_mt64* s, uint64_t seed);
 uint64_t orc_mt64_next(orc_mt64* s);
+void orc_mt64_draws(uint64_t seed, size_t n, uint64_t* out);
 
 /* Counter-based synthetic inputs, identical bytes to the device generators
  * (see DESIGN.md "Synthetic inputs").  Element index i is GLOBAL
@@ -95,6 +114,7 @@ uint64_t orc_mt64_next(orc_mt64* s);
  *   kind 4: cfg4 u16, every bit Bernoulli(6554/65536)
  *   kind 5: cfg5 uniform u32     (2 u32 per draw)
  *   kind 6: cfg5 uniform u64     (Bernoulli 0.5 per bit)
+ *   kind 7: SAM FLAG words, uniform over the 12 defined bits (bits 12-15 clear)
  * Returns 0, or 1 for an unknown kind. */
 int orc_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* out, int threads);
 

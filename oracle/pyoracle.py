@@ -67,6 +67,11 @@ class Oracle:
         lib.orc_generate.restype = C.c_int
         lib.orc_digest.argtypes = [C.c_void_p, C.c_size_t]
         lib.orc_digest.restype = C.c_uint64
+        for fn in (lib.orc_flagstats_reference, lib.orc_flagstats_pospopcnt):
+            fn.argtypes = [C.c_void_p, C.c_size_t, _u64p, _u64p]
+            fn.restype = C.c_int
+        lib.orc_flag_transform.argtypes = [C.c_uint16, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16)]
+        lib.orc_mt64_draws.argtypes = [C.c_uint64, C.c_size_t, C.c_void_p]
         self.lib = lib
 
     # -- counting -----------------------------------------------------------
@@ -133,12 +138,37 @@ class Oracle:
         self.lib.orc_finalize_carries(carries.ctypes.data_as(_u64p), depth, counts.ctypes.data_as(_u64p))
 
     # -- generators -----------------------------------------------------------
+    def mt64_draws(self, seed: int, n: int) -> np.ndarray:
+        """The first n draws of std::mt19937_64(seed)."""
+        out = np.empty(n, np.uint64)
+        self.lib.orc_mt64_draws(seed, n, _ptr(out))
+        return out
+
+    def acceptance_flag_streams(self, count: int = 100, n: int = 100000):
+        """acceptance.cpp:277-285: mt19937_64(0xF1A6), word = rng() & 0x0FFF, `count` streams of n."""
+        draws = self.mt64_draws(0xF1A6, count * n)
+        return (draws & np.uint64(0x0FFF)).astype(np.uint16).reshape(count, n)
+
     def mt_generate_stream(self, seed: int, n: int) -> np.ndarray:
         out = np.empty(n, np.uint16)
         self.lib.orc_mt_generate_stream(seed, n, _ptr(out))
         return out
 
-    GEN_DTYPE = {1: np.uint16, 2: np.uint16, 3: np.uint8, 4: np.uint16, 5: np.uint32, 6: np.uint64}
+    GEN_DTYPE = {1: np.uint16, 2: np.uint16, 3: np.uint8, 4: np.uint16, 5: np.uint32, 6: np.uint64, 7: np.uint16}
+
+    # -- FLAG statistics -----------------------------------------------------
+    def flagstats(self, flags: np.ndarray, route: str = "reference"):
+        """(rc, out20, bad_offset); rc 1 = invalid FLAG word at bad_offset."""
+        out = np.zeros(20, np.uint64)
+        bad = C.c_uint64(0)
+        fn = self.lib.orc_flagstats_reference if route == "reference" else self.lib.orc_flagstats_pospopcnt
+        rc = fn(_ptr(flags), flags.size, out.ctypes.data_as(_u64p), C.byref(bad))
+        return rc, out, bad.value
+
+    def flag_transform(self, word: int) -> tuple[int, int]:
+        p, f = C.c_uint16(), C.c_uint16()
+        self.lib.orc_flag_transform(word, C.byref(p), C.byref(f))
+        return p.value, f.value
 
     def generate(self, kind: int, seed: int, n: int, base: int = 0, threads: int = 1,
                  out: np.ndarray | None = None) -> np.ndarray:

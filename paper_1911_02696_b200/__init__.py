@@ -39,6 +39,7 @@ __all__ = [
     "CudaError", "validate", "merge_counts", "pospopcnt", "pospopcnt_k", "pospopcnt_u16_c32",
     "pospopcnt_segmented", "pospopcnt_sharded", "count_async", "segmented_async", "generate", "digest",
     "supported_csa_widths", "native_csa_width", "device_available", "kernel_launches", "library_path",
+    "FlagBucket", "FlagSummary", "InvalidFlagWordError", "flagstats",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -63,9 +64,30 @@ class CudaError(RuntimeError):
     """A CUDA runtime failure inside the library."""
 
 
-_OK, _EINVAL, _EUNAVAILABLE, _ECUDA, _ENOMEM = range(5)
+class InvalidFlagWordError(RuntimeError):
+    """pospop::InvalidFlagWordError (flagstats.hpp:64-75): a FLAG word with bits 12-15 set."""
+
+    def __init__(self, offset: int, word: int, msg: str = ""):
+        super().__init__(msg or f"invalid FLAG word 0x{word:x} at offset {offset} (bits 12-15 must be clear)")
+        self.offset = offset
+        self.word = word
+
+
+_OK, _EINVAL, _EUNAVAILABLE, _ECUDA, _ENOMEM, _EFLAG = range(6)
 
 _u64p = C.POINTER(C.c_uint64)
+
+
+_BUCKET_FIELDS = ("total", "secondary", "supplementary", "n_pair_good", "n_read1", "n_read2", "n_sgltn",
+                  "pair_map", "mapped", "dup")
+
+
+class _Bucket(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in _BUCKET_FIELDS]
+
+
+class _Summary(C.Structure):
+    _fields_ = [("pass_", _Bucket), ("fail", _Bucket)]
 
 
 class _Config(C.Structure):
@@ -106,6 +128,7 @@ def _load():
         "pospopcnt_segmented_async": ([C.c_int, vp, vp, sz, vp, C.c_uint32, C.c_int, C.c_int, vp], C.c_int),
         "pospop_generate": ([C.c_int, C.c_uint64, C.c_uint64, sz, vp, vp], C.c_int),
         "pospop_digest": ([vp, sz, _u64p], C.c_int),
+        "pospop_flagstats": ([vp, sz, C.POINTER(_Summary), _u64p, C.POINTER(C.c_uint16)], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -342,12 +365,12 @@ def segmented_async(data: Any, offsets: Any, out: Any, k: int, *, flush_threshol
                                              _stream_ptr(stream)))
 
 
-GEN_UNIFORM16, GEN_CFG2, GEN_CFG3, GEN_CFG4, GEN_U32, GEN_U64 = 1, 2, 3, 4, 5, 6
+GEN_UNIFORM16, GEN_CFG2, GEN_CFG3, GEN_CFG4, GEN_U32, GEN_U64, GEN_FLAGS = 1, 2, 3, 4, 5, 6, 7
 
 
 def generate(kind: int, seed: int, out: Any, base: int = 0, n: int | None = None, stream: Any = None) -> None:
     """Fills a device buffer with synthetic input `kind` (Synthetic inputs)."""
-    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8}[kind]
+    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8, 7: 2}[kind]
     addr, nbits = _addr_len(out, 8)
     count = nbits // esize if n is None else int(n)
     _check(_load().pospop_generate(int(kind), int(seed), int(base), count, addr or None, _stream_ptr(stream)))
@@ -358,3 +381,52 @@ def digest(data: Any) -> int:
     out = C.c_uint64(0)
     _check(_load().pospop_digest(addr or None, nbytes, C.byref(out)))
     return int(out.value)
+
+
+# -- FLAG statistics (the reference's application of the path) --------------------
+
+@dataclass
+class FlagBucket:
+    """pospop::FlagBucket (flagstats.hpp:39-50)."""
+    total: int = 0
+    secondary: int = 0
+    supplementary: int = 0
+    n_pair_good: int = 0
+    n_read1: int = 0
+    n_read2: int = 0
+    n_sgltn: int = 0
+    pair_map: int = 0
+    mapped: int = 0
+    dup: int = 0
+
+    def as_list(self) -> list[int]:
+        return [getattr(self, f) for f in _BUCKET_FIELDS]
+
+
+@dataclass
+class FlagSummary:
+    """pospop::FlagSummary (flagstats.hpp:54-62)."""
+    pass_: FlagBucket
+    fail: FlagBucket
+
+    def total(self) -> int:
+        return self.pass_.total + self.fail.total
+
+    def as_list(self) -> list[int]:
+        return self.pass_.as_list() + self.fail.as_list()
+
+
+def flagstats(flags: Any) -> FlagSummary:
+    """pospop::flagstats_pospopcnt (flagstats.hpp:100) fused into one GPU pass.
+
+    Raises InvalidFlagWordError at the first word with bits 12-15 set."""
+    addr, n = _addr_len(flags, 16)
+    out = _Summary()
+    off = C.c_uint64(0)
+    word = C.c_uint16(0)
+    st = _load().pospop_flagstats(addr or None, n, C.byref(out), C.byref(off), C.byref(word))
+    if st == _EFLAG:
+        raise InvalidFlagWordError(int(off.value), int(word.value))
+    _check(st)
+    conv = lambda b: FlagBucket(*[int(getattr(b, f)) for f in _BUCKET_FIELDS])  # noqa: E731
+    return FlagSummary(conv(out.pass_), conv(out.fail))

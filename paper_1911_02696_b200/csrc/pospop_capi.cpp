@@ -8,7 +8,13 @@
 // There is no CPU fallback path.
 #include <cuda_runtime.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cerrno>
 #include <cstdarg>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -119,6 +125,7 @@ pospop_status alloc_workspace(StreamWorkspace* ws) {
     CU(cudaMalloc(&ws->acc, kWorkspaceBytes));
     ws->ticket = reinterpret_cast<unsigned int*>(ws->acc + 64);
     ws->next = ws->acc + 65;
+    ws->bad = ws->acc + 66;
     CU(cudaMemset(ws->acc, 0, kWorkspaceBytes));
     return POSPOP_OK;
 }
@@ -248,6 +255,20 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
     CU(cudaStreamSynchronize(c->stream));
     for (int p = 0; p < k; ++p) out[p] = c->h_out[p];
     return POSPOP_OK;
+}
+
+// flagstats.cpp:50-63 (bucket_from_counts): positions of the transformed word.
+void bucket_from_counts(const uint64_t* c, uint64_t total, pospop_flag_bucket* b) {
+    b->total = total;
+    b->secondary = c[8];
+    b->supplementary = c[11];
+    b->n_pair_good = c[1];
+    b->n_read1 = c[6];
+    b->n_read2 = c[7];
+    b->n_sgltn = c[3];
+    b->pair_map = c[12];
+    b->mapped = total - c[2];
+    b->dup = total - c[10];
 }
 
 const uint32_t kWidths[] = {64, 256, 512};
@@ -410,6 +431,197 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
     return POSPOP_OK;
 }
 
+pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_summary* out, uint64_t* bad_offset,
+                               uint16_t* bad_word) {
+    if (!out) return fail(POSPOP_EINVAL, "out must not be NULL");
+    if (!flags && len) return fail(POSPOP_EINVAL, "flags is NULL but len is %zu", len);
+    if ((uintptr_t)flags % 2) return fail(POSPOP_EINVAL, "flags is not 2-byte aligned");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    std::memset(out, 0, sizeof *out);
+    if (len == 0) return POSPOP_OK;
+    const Where where = classify(flags, &dev);
+    DeviceGuard g(dev);
+    Ctx* c = nullptr;
+    if ((s = get_ctx(dev, &c))) return s;
+    LaunchOptions opt;
+    if (where == Where::Device) {
+        CU(launch_flagstats(flags, len, c->d_out, false, opt, c->ws, c->stream));
+    } else {
+        if ((s = ensure_stage(c))) return s;
+        const size_t chunk_words = c->stage_bytes / 2;
+        size_t i = 0;
+        for (size_t off = 0; off < len; off += chunk_words, ++i) {
+            const size_t n = len - off < chunk_words ? len - off : chunk_words;
+            const int slot = (int)(i % kRing);
+            if (i >= (size_t)kRing) CU(cudaStreamWaitEvent(c->copy, c->ev_done[slot], 0));
+            CU(cudaMemcpyAsync(c->stage[slot], flags + off, n * 2, cudaMemcpyHostToDevice, c->copy));
+            CU(cudaEventRecord(c->ev_copied[slot], c->copy));
+            CU(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
+            opt.word_base = off;
+            CU(launch_flagstats(static_cast<const uint16_t*>(c->stage[slot]), n, c->d_out, i > 0, opt, c->ws,
+                                c->stream));
+            CU(cudaEventRecord(c->ev_done[slot], c->stream));
+        }
+    }
+    CU(cudaMemcpyAsync(c->h_out, c->d_out, 33 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (c->h_out[32]) {
+        const uint64_t idx = ~c->h_out[32];
+        uint16_t word = 0;
+        if (where == Where::Device)
+            CU(cudaMemcpy(&word, flags + idx, 2, cudaMemcpyDeviceToHost));
+        else
+            word = flags[idx];
+        if (bad_offset) *bad_offset = idx;
+        if (bad_word) *bad_word = word;
+        return fail(POSPOP_EFLAG, "invalid FLAG word 0x%x at offset %llu (bits 12-15 must be clear)", word,
+                    (unsigned long long)idx);
+    }
+    const uint64_t* pc = reinterpret_cast<const uint64_t*>(c->h_out);
+    const uint64_t* fc = pc + 16;
+    const uint64_t fail_total = fc[9];
+    bucket_from_counts(fc, fail_total, &out->fail);
+    bucket_from_counts(pc, len - fail_total, &out->pass);
+    return POSPOP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// File / pipe ingestion (reference read_word_stream +
+// decode_words, proj/tools/pospopcnt.cpp:52-75).
+// ---------------------------------------------------------------------------
+namespace {
+
+// Fills buf with up to `want` bytes from fd at `offset` (regular file:
+// parallel pread stripes) or sequentially (pipe).  Returns bytes read, or -1.
+ssize_t fill_buffer(int fd, bool seekable, uint8_t* buf, size_t want, uint64_t offset, int threads) {
+    if (!seekable) {
+        size_t got = 0;
+        while (got < want) {
+            const ssize_t r = ::read(fd, buf + got, want - got);
+            if (r < 0) {
+                if (errno == EINTR) continue;
+                return -1;
+            }
+            if (r == 0) break;
+            got += (size_t)r;
+        }
+        return (ssize_t)got;
+    }
+    const size_t stripe = (want / (size_t)threads + 4095) & ~(size_t)4095;
+    std::vector<ssize_t> got((size_t)threads, 0);
+    std::vector<std::thread> ts;
+    for (int t = 0; t < threads; ++t) {
+        const size_t lo = (size_t)t * stripe;
+        if (lo >= want) break;
+        const size_t hi = lo + stripe < want ? lo + stripe : want;
+        ts.emplace_back([&, t, lo, hi] {
+            size_t done = 0;
+            while (lo + done < hi) {
+                const ssize_t r = ::pread(fd, buf + lo + done, hi - lo - done, (off_t)(offset + lo + done));
+                if (r < 0) {
+                    if (errno == EINTR) continue;
+                    got[(size_t)t] = -1;
+                    return;
+                }
+                if (r == 0) break;
+                done += (size_t)r;
+            }
+            got[(size_t)t] = (ssize_t)done;
+        });
+    }
+    for (auto& th : ts) th.join();
+    size_t total = 0;
+    for (size_t t = 0; t < ts.size(); ++t) {
+        if (got[t] < 0) return -1;
+        total += (size_t)got[t];
+        if ((size_t)got[t] < (t + 1 == ts.size() ? want - t * stripe : stripe)) break;  // EOF inside stripe t
+    }
+    return (ssize_t)total;
+}
+
+}  // namespace
+
+pospop_status pospopcnt_fd(int fd, int k, uint64_t* counts, uint64_t* n_words) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (!counts) return fail(POSPOP_EINVAL, "counts must not be NULL");
+    if (fd < 0) return fail(POSPOP_EINVAL, "bad file descriptor %d", fd);
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    Ctx* c = nullptr;
+    if ((s = get_ctx(dev, &c))) return s;
+    if ((s = ensure_stage(c))) return s;
+    struct stat st;
+    const bool seekable = fstat(fd, &st) == 0 && S_ISREG(st.st_mode);
+    const size_t wb = (size_t)k / 8;
+    const size_t chunk = c->stage_bytes;  // a multiple of 8
+    uint8_t* pinned[2] = {nullptr, nullptr};
+    cudaEvent_t copied[2];
+    for (int i = 0; i < 2; ++i) {
+        CU(cudaMallocHost(&pinned[i], chunk));
+        CU(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+    }
+    struct Release {
+        uint8_t** p;
+        cudaEvent_t* e;
+        ~Release() {
+            for (int i = 0; i < 2; ++i) {
+                cudaEventSynchronize(e[i]);
+                cudaFreeHost(p[i]);
+                cudaEventDestroy(e[i]);
+            }
+        }
+    } release{pinned, copied};
+    const char* env = std::getenv("POSPOP_READ_THREADS");
+    const int threads = env && *env ? std::atoi(env) : 8;
+    uint64_t total = 0;
+    LaunchOptions opt;
+    for (size_t i = 0;; ++i) {
+        const int b = (int)(i % 2), slot = (int)(i % kRing);
+        CU(cudaEventSynchronize(copied[b]));  // the H2D that last read pinned[b] is done
+        const ssize_t got = fill_buffer(fd, seekable, pinned[b], chunk, total, threads < 1 ? 1 : threads);
+        if (got < 0) return fail(POSPOP_EINVAL, "read failed: %s", std::strerror(errno));
+        if (got == 0) break;
+        total += (uint64_t)got;
+        if ((size_t)got % wb != 0) {
+            // only the final chunk may be short; a ragged word means a bad length
+            uint8_t probe;
+            const ssize_t more = seekable ? ::pread(fd, &probe, 1, (off_t)total) : ::read(fd, &probe, 1);
+            return fail(POSPOP_EINVAL, "input: %s byte length (%llu%s bytes); expected raw little-endian %d-bit words",
+                        wb == 2 ? "odd" : "ragged", (unsigned long long)total, more > 0 ? "+" : "", k);
+        }
+        if (i >= (size_t)kRing) CU(cudaStreamWaitEvent(c->copy, c->ev_done[slot], 0));
+        CU(cudaMemcpyAsync(c->stage[slot], pinned[b], (size_t)got, cudaMemcpyHostToDevice, c->copy));
+        CU(cudaEventRecord(copied[b], c->copy));
+        CU(cudaEventRecord(c->ev_copied[slot], c->copy));
+        CU(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
+        CU(launch_stream(k, c->stage[slot], (size_t)got / wb, c->d_out, i > 0, opt, c->ws, c->stream));
+        CU(cudaEventRecord(c->ev_done[slot], c->stream));
+        if ((size_t)got < chunk) break;
+    }
+    if (total == 0) {
+        for (int p = 0; p < k; ++p) counts[p] = 0;
+    } else {
+        CU(cudaMemcpyAsync(c->h_out, c->d_out, (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        for (int p = 0; p < k; ++p) counts[p] = c->h_out[p];
+    }
+    if (n_words) *n_words = total / wb;
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_file(const char* path, int k, uint64_t* counts, uint64_t* n_words) {
+    if (!path) return fail(POSPOP_EINVAL, "path must not be NULL");
+    const bool is_stdin = path[0] == '-' && path[1] == 0;
+    const int fd = is_stdin ? 0 : ::open(path, O_RDONLY);
+    if (fd < 0) return fail(POSPOP_EINVAL, "cannot open input file: %s", path);
+    const pospop_status s = pospopcnt_fd(fd, k, counts, n_words);
+    if (!is_stdin) ::close(fd);
+    return s;
+}
+
 pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* lens, const int* devices,
                                 int n_shards, uint64_t* counts) {
     if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
@@ -541,7 +753,7 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
 }
 
 pospop_status pospop_generate(int kind, uint64_t seed, uint64_t base, size_t n, void* d_out, void* stream) {
-    if (kind < 1 || kind > 6) return fail(POSPOP_EINVAL, "unknown generator kind %d", kind);
+    if (kind < 1 || kind > 7) return fail(POSPOP_EINVAL, "unknown generator kind %d", kind);
     if (!d_out && n) return fail(POSPOP_EINVAL, "NULL output");
     int dev = 0;
     pospop_status s = current_device(&dev);

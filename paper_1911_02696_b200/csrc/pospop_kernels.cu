@@ -60,6 +60,10 @@ struct StreamArgs {
     unsigned long long* next;   // global chunk counter (zero on entry, re-zeroed by the last CTA)
     unsigned long long nwt, nA, CA, CB;
     unsigned long long pool;    // SCHED 2: warp tiles in the global tail pool
+    // MODE 1 (FLAG statistics)
+    unsigned long long data_off;  // data start - base, bytes
+    unsigned long long word_base; // global index of the first word (host-staged chunks)
+    unsigned long long* bad;      // max of ~(index of an invalid FLAG word); 0 = none
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -151,7 +155,7 @@ __device__ __forceinline__ void flush_bank_to_smem(uint32_t (&counter)[NBANK][16
 // the global accumulator, ticket; the last CTA folds channels to positions,
 // writes/accumulates out[k] and leaves the scratch (acc, ticket, chunk
 // counter) zeroed for the next launch.
-template <int NBANK, int L>
+template <int NBANK, int L, int MODE>
 __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carries)[NBANK][L],
                                            uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
                                            int* s_last, unsigned block, uint32_t lane) {
@@ -175,22 +179,96 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
 
     // Last CTA: every other CTA has fenced its channel atomics.
     __threadfence();
-    const int k = a.k;
-    for (int pos = threadIdx.x; pos < k; pos += block) {
-        unsigned long long sum = 0;
-        if (k == 64) {
-            sum = atomicExch(&a.acc[pos], 0ull);
-        } else {
-            const int m = channels_per_position(k);
-            for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
+    if constexpr (MODE == 1) {  // two banks of k = 16: out[16 b + p] = acc[32 b + p] + acc[32 b + p + 16]
+        for (int pos = threadIdx.x; pos < 32; pos += block) {
+            const int b = pos >> 4, p = pos & 15;
+            const unsigned long long sum =
+                atomicExch(&a.acc[32 * b + p], 0ull) + atomicExch(&a.acc[32 * b + p + 16], 0ull);
+            a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
         }
-        a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+        if (threadIdx.x == 0) {  // ~index: the larger code is the earlier word
+            const unsigned long long code = atomicExch(a.bad, 0ull);
+            a.out[32] = a.accumulate && a.out[32] > code ? a.out[32] : code;
+        }
+    } else {
+        const int k = a.k;
+        for (int pos = threadIdx.x; pos < k; pos += block) {
+            unsigned long long sum = 0;
+            if (k == 64) {
+                sum = atomicExch(&a.acc[pos], 0ull);
+            } else {
+                const int m = channels_per_position(k);
+                for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
+            }
+            a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+        }
     }
     if (threadIdx.x == 0) {
         *a.ticket = 0u;
         if (a.next) *a.next = 0ull;
     }
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 3] = globaltimer();
+}
+
+// ---------------------------------------------------------------------------
+// FLAG statistics (reference proj/core/src/flagstats.cpp).
+// SWAR form of flag_transform (flagstats.cpp:94-125) on a register holding two
+// SAM FLAG words.  Only the positions bucket_from_counts reads (1,2,3,6,7,8,
+// 9,10,11,12; flagstats.cpp:39-63) are produced; 0,4,5,13-15 are left zero.
+//   G  = paired & !secondary & !supplementary       (lane bit 0)
+//   GU = G & !unmapped
+//   bit1,3 = w & GU ; bit6,7 = w & G ; bit 2,8,9,10 = w ; bit11 = supp & !sec ;
+//   bit12 (pair_map) = GU & !mate_unmapped ; pass/fail split on QCFAIL (bit 9).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void flag_transform2(uint32_t w, uint32_t& pass, uint32_t& fail) {
+    constexpr uint32_t L1 = 0x00010001u;
+    const uint32_t g = w & ~(w >> 8) & ~(w >> 11) & L1;
+    const uint32_t gu = g & ~(w >> 2);
+    const uint32_t mg = g * 0xFFFFu;  // lane masks (IMAD: FMA pipe)
+    const uint32_t mgu = gu * 0xFFFFu;
+    const uint32_t mf = ((w >> 9) & L1) * 0xFFFFu;
+    const uint32_t out = (w & 0x07040704u) | (w & mgu & 0x000A000Au) | (w & mg & 0x00C000C0u) |
+                         (w & ~(w << 3) & 0x08000800u) | (mgu & ~(w << 9) & 0x10001000u);
+    pass = out & ~mf;
+    fail = out & mf;
+}
+
+// Tree-block consumer.  MODE 0: positional counts of the words (NBANK banks).
+// MODE 1: FLAG statistics -- transform, then bank 0 counts the QC-pass plane
+// and bank 1 the QC-fail plane; words with reserved bits 12-15 set are
+// reported through a.bad (the first such index wins, as the reference's
+// check_reserved throws at the first one, flagstats.cpp:34-36).
+template <int MODE, int NBANK, int L, int VB, int REGS>
+__device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)[REGS], unsigned long long first,
+                                        unsigned stride, uint32_t (&carries)[NBANK][L],
+                                        uint32_t (&counter)[NBANK][16]) {
+    if constexpr (MODE == 0) {
+        tree_block<NBANK, L>(r, carries, counter);
+    } else {
+        static_assert(NBANK == 2 && REGS == (1 << L), "FLAG mode: two banks of 2^L registers");
+        constexpr int RPV = VB / 4;
+        uint32_t pass[REGS], fail[REGS];
+        uint32_t bad = 0;
+#pragma unroll
+        for (int i = 0; i < REGS; ++i) {
+            bad |= r[i];
+            flag_transform2(r[i], pass[i], fail[i]);
+        }
+        extract(counter[0], Tree<L, 1>::run(carries[0], pass));
+        extract(counter[1], Tree<L, 1>::run(carries[1], fail));
+        if (bad & 0xF000F000u) {  // rare: locate this thread's first invalid word
+            unsigned long long best = ~0ull;
+            for (int i = 0; i < REGS; ++i)
+                for (int h = 0; h < 2; ++h)
+                    if ((r[i] >> (16 * h)) & 0xF000u) {
+                        const unsigned long long byte =
+                            (first + (unsigned long long)(i / RPV) * stride) * VB + 4 * (i % RPV) + 2 * h;
+                        const unsigned long long word = ((byte - a.data_off) >> 1) + a.word_base;
+                        best = word < best ? word : best;
+                    }
+            atomicMax(a.bad, ~best);
+        }
+    }
 }
 
 // SCHED 0 (static): CTA b owns a contiguous range of whole 32-vector groups and
@@ -201,9 +279,9 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
 // while another still holds a big share; the next chunk index is fetched one
 // chunk ahead so the atomic's latency hides behind the loads.
 // BLOCK > 0: compile-time block size; BLOCK == 0: runtime blockDim.x.
-template <int NBANK, int L, int VB, int HINT, int BLOCK, int SCHED>
+template <int NBANK, int L, int VB, int HINT, int BLOCK, int SCHED, int MODE>
 __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const StreamArgs a) {
-    constexpr int REGS = NBANK << L;  // 32-bit input registers per tree block
+    constexpr int REGS = MODE == 1 ? (1 << L) : (NBANK << L);  // 32-bit input registers per tree block
     constexpr int RPV = VB / 4;       // registers per vector
     constexpr int VPT = REGS / RPV;   // vectors per thread per tree block
     static_assert(VPT >= 1, "tree must consume at least one vector");
@@ -247,7 +325,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
 #pragma unroll
                         for (int j = 0; j < RPV; ++j) r[v * RPV + j] = 0;
             }
-            tree_block<NBANK, L>(r, carries, counter);
+            consume<MODE, NBANK, L, VB>(a, r, t + threadIdx.x, block, carries, counter);
             if (++nb == a.flush_threshold) {  // block-uniform: every thread runs the same tiles
                 flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
                 nb = 0;
@@ -274,7 +352,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
             const unsigned long long t = S0 + w * WT;
             uint32_t r[REGS];
             load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
-            tree_block<NBANK, L>(r, carries, counter);
+            consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
             if (++nb == a.flush_threshold) {  // warp-uniform
                 flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
                 nb = 0;
@@ -294,7 +372,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
                     const unsigned long long t = S0 + ww * WT;
                     uint32_t r[REGS];
                     load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
-                    tree_block<NBANK, L>(r, carries, counter);
+                    consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
                     if (++nb == a.flush_threshold) {
                         flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
                         nb = 0;
@@ -324,7 +402,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
                 const unsigned long long t = S0 + w * WT;
                 uint32_t r[REGS];
                 load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
-                tree_block<NBANK, L>(r, carries, counter);
+                consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
                 if (++nb == a.flush_threshold) {  // warp-uniform
                     flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
                     nb = 0;
@@ -334,7 +412,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
             mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
         }
     }
-    cta_finish<NBANK, L>(a, carries, counter, s_acc, &s_last, block, lane);
+    cta_finish<NBANK, L, MODE>(a, carries, counter, s_acc, &s_last, block, lane);
 }
 
 // One warp per array.  Array a spans bytes [data + off[a]*wb, data + off[a+1]*wb);
@@ -517,6 +595,9 @@ __global__ void generate_kernel(int kind, uint64_t key, uint64_t index_base, uns
             case 6:
                 ((uint64_t*)out)[l] = mix64(key + (i + 1) * kGamma);
                 break;
+            case 7:  // SAM FLAG words: the 12 defined bits uniform, bits 12-15 clear
+                ((uint16_t*)out)[l] = (uint16_t)((mix64(key + ((i >> 2) + 1) * kGamma) >> (16 * (i & 3))) & 0x0FFF);
+                break;
         }
     }
 }
@@ -579,13 +660,15 @@ int resident_blocks(Kernel kernel, int block) {
 using StreamKernel = void (*)(const StreamArgs);
 
 struct StreamVariant {
-    int nbank, depth, vb, hint, block, sched;
+    int nbank, depth, vb, hint, block, sched, mode;
     StreamKernel fn;
 };
 
-#define SV(NB, L, VB, H, B, S) {NB, L, VB, H, B, S, stream_kernel<NB, L, VB, H, B, S>}
+#define SV(NB, L, VB, H, B, S) {NB, L, VB, H, B, S, 0, stream_kernel<NB, L, VB, H, B, S, 0>}
+#define SVF(L, VB, B, S) {2, L, VB, 0, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1>}
 // Production variants first (the defaults), then tuning variants selectable
-// through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched".
+// through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched" (POSPOP_FLAG_VARIANT
+// for MODE 1).
 const StreamVariant kStreamVariants[] = {
     SV(1, 7, 32, 0, 256, 2), SV(2, 6, 32, 0, 256, 2),  // defaults (k <= 32 / k = 64)
     SV(1, 7, 32, 0, 0, 2), SV(2, 6, 32, 0, 0, 2),      // runtime block size (test launches)
@@ -593,16 +676,16 @@ const StreamVariant kStreamVariants[] = {
     SV(1, 7, 32, 0, 0, 0), SV(2, 6, 32, 0, 0, 0),
     SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // per-warp guided chunks
     SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1), SV(1, 6, 32, 0, 256, 2), SV(1, 7, 16, 0, 256, 2),
-    SV(1, 6, 32, 0, 256, 1), SV(1, 6, 16, 0, 256, 1), SV(1, 7, 16, 0, 256, 1), SV(1, 7, 32, 1, 256, 1),
-    SV(1, 7, 32, 0, 128, 1), SV(1, 7, 32, 0, 512, 1), SV(1, 6, 32, 0, 512, 1), SV(1, 5, 32, 0, 256, 1),
-    SV(2, 5, 32, 0, 256, 1), SV(2, 5, 16, 0, 256, 1), SV(2, 6, 16, 0, 256, 1),
+    SVF(5, 32, 256, 2), SVF(5, 32, 0, 2),               // FLAG statistics defaults
+    SVF(6, 32, 256, 2), SVF(5, 16, 256, 2), SVF(4, 32, 256, 2), SVF(6, 16, 256, 2),
 };
 #undef SV
+#undef SVF
 
-const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block, int sched) {
+const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block, int sched, int mode) {
     for (const StreamVariant& v : kStreamVariants)
         if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.hint == hint && v.block == block &&
-            v.sched == sched)
+            v.sched == sched && v.mode == mode)
             return &v;
     return nullptr;
 }
@@ -633,21 +716,22 @@ const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched) {
 
 unsigned long long kernel_launches() { return g_launches.load(); }
 
-cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
-                          bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
-                          cudaStream_t stream, int* grid_used) {
-    const int nbank = k == 64 ? 2 : 1;
-    // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched".
-    int depth = nbank == 1 ? kDefaultDepth1 : kDefaultDepth2, vb = 32, hint = 0, block = kDefaultBlock, sched = 2;
-    if (const char* v = std::getenv("POSPOP_STREAM_VARIANT"))
+static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t len_words,
+                                      unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
+                                      const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
+    const int nbank = (k == 64 || mode == 1) ? 2 : 1;
+    // Tuning override: POSPOP_STREAM_VARIANT / POSPOP_FLAG_VARIANT="depth,vb,hint,block,sched".
+    int depth = mode == 1 ? 5 : (nbank == 1 ? kDefaultDepth1 : kDefaultDepth2), vb = 32, hint = 0,
+        block = kDefaultBlock, sched = 2;
+    if (const char* v = std::getenv(mode == 1 ? "POSPOP_FLAG_VARIANT" : "POSPOP_STREAM_VARIANT"))
         std::sscanf(v, "%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched);
     if (opt.depth) depth = opt.depth;
     if (opt.block) block = 0;  // explicit (test) block size: the runtime-block instantiation
-    const StreamVariant* var = pick_stream(nbank, depth, vb, hint, block, sched);
-    if (!var) var = pick_stream(nbank, depth, vb, 0, 0, sched);
+    const StreamVariant* var = pick_stream(nbank, depth, vb, hint, block, sched, mode);
+    if (!var) var = pick_stream(nbank, depth, vb, 0, 0, sched, mode);
     if (!var) return cudaErrorInvalidConfiguration;
     const int threads = var->block ? var->block : (opt.block ? opt.block : kDefaultBlock);
-    const int vpt = (nbank << var->depth) / (var->vb / 4);
+    const int vpt = (mode == 1 ? (1 << var->depth) : (nbank << var->depth)) / (var->vb / 4);
 
     const uintptr_t P = reinterpret_cast<uintptr_t>(data);
     const size_t nbytes = len_words * (size_t)(k / 8);
@@ -678,6 +762,9 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
     a.accumulate = accumulate ? 1 : 0;
     a.trace = opt.trace;
     a.next = ws.next;
+    a.bad = ws.bad;
+    a.word_base = opt.word_base;
+    a.data_off = nbytes ? (unsigned long long)(P - reinterpret_cast<uintptr_t>(a.base)) : 0ull;
 
     int grid = opt.grid;
     if (grid <= 0) {
@@ -700,13 +787,24 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
     if (tail > a.nwt) tail = a.nwt;
     a.nA = (a.nwt - tail) / a.CA;
     // SCHED 2: the global tail pool, in warp tiles.
-    a.pool = warps * (unsigned long long)env_int("POSPOP_POOL_TILES_PER_WARP", 4);
+    a.pool = warps * (unsigned long long)env_int("POSPOP_POOL_TILES_PER_WARP", 16);
     if (a.pool > a.nwt) a.pool = a.nwt;
 
     if (grid_used) *grid_used = grid;
     var->fn<<<grid, threads, 0, stream>>>(a);
     ++g_launches;
     return cudaGetLastError();
+}
+
+cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
+                          bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
+                          cudaStream_t stream, int* grid_used) {
+    return launch_stream_mode(0, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
+}
+
+cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long long* d_out33, bool accumulate,
+                             const LaunchOptions& opt, const StreamWorkspace& ws, cudaStream_t stream) {
+    return launch_stream_mode(1, 16, flags, len, d_out33, accumulate, opt, ws, stream, nullptr);
 }
 
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets, size_t n,

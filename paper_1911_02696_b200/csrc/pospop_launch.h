@@ -16,9 +16,11 @@ struct StreamWorkspace {
     unsigned long long* acc = nullptr;   // 64 channel accumulators
     unsigned int* ticket = nullptr;      // CTA completion ticket
     unsigned long long* next = nullptr;  // dynamic-schedule chunk counter
+    unsigned long long* bad = nullptr;   // FLAG mode: ~(first invalid word index), 0 = none
 };
 
-// Bytes of one workspace allocation: acc[64], ticket (u32 at +512), next (u64 at +520).
+// Bytes of one workspace allocation: acc[64], ticket (u32 at +512), next (u64
+// at +520), bad (u64 at +528).
 constexpr size_t kWorkspaceBytes = 64 * sizeof(unsigned long long) + 64;
 
 struct LaunchOptions {
@@ -27,6 +29,7 @@ struct LaunchOptions {
     int block = 0;                     // 0 = default (256); multiple of 32
     int depth = 0;                     // 0 = default tree depth (k=64: per bank)
     unsigned long long* trace = nullptr;  // diagnostics: 5 u64 per CTA (see pospopcnt_trace_async)
+    unsigned long long word_base = 0;     // FLAG mode: global index of the first word
 };
 
 // Counts len_words k-bit words at `data` (device memory, k/8-aligned) into
@@ -35,6 +38,13 @@ struct LaunchOptions {
 cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
                           bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
                           cudaStream_t stream, int* grid_used = nullptr);
+
+// FLAG statistics (reference flagstats_pospopcnt, flagstats.cpp:127-145) in one
+// pass: d_out33[0..16) = QC-pass positional counts of the transformed words,
+// [16..32) = QC-fail counts, [32] = ~(index of the first word with reserved
+// bits 12-15 set) or 0.  One kernel launch.
+cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long long* d_out33, bool accumulate,
+                             const LaunchOptions& opt, const StreamWorkspace& ws, cudaStream_t stream);
 
 // Batched form: array a = words [d_offsets[a], d_offsets[a+1]) of `data`;
 // row a of d_out (k entries) is overwritten.  One kernel launch.

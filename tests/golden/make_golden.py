@@ -15,6 +15,8 @@ fixtures are exactly the cases those tests check:
 * test_core.cpp:143-153    -- concatenation cuts (seed 31337)
 * test_csa.cpp:252-292     -- forced flush (seed 555), threshold 1, tail lengths (seed 2)
 * bench.cpp:115-120        -- generate_stream words for several seeds; cfg1 (seed 1, 2^20)
+* acceptance.cpp:271-291   -- 100 FLAG streams of 10^5 words (seed 0xF1A6) and the 4096
+                              single-value summaries, from flagstats_reference
 
 Counts come from pospop::pospopcnt (Auto and every CSA width) and
 pospop::oracle_pospopcnt; the script asserts they agree before writing.
@@ -135,13 +137,30 @@ def main() -> None:
     w = ref.generate_stream(77, 40000)
     out["fork_join"] = [77, 40000] + [int(x) for x in ref.pospopcnt_mt(w, 4)]
 
+    # acceptance.cpp:271-291 (criterion 5): 100 FLAG streams of 10^5 words,
+    # mt19937_64(0xF1A6), word = rng() & 0x0FFF; summaries from the reference.
+    rng = MT64(orc, 0xF1A6)
+    flag_rows = []
+    for _ in range(100):
+        words = np.array([rng() & 0x0FFF for _ in range(100000)], np.uint16)
+        rc, summ, _ = ref.flagstats(words, use_pospopcnt=False)
+        rc2, summ2, _ = ref.flagstats(words, use_pospopcnt=True)
+        assert rc == 0 and rc2 == 0 and (summ == summ2).all()
+        flag_rows.append([int(x) for x in summ])
+    out["flagstats_acceptance"] = flag_rows
+    single = []
+    for v in range(4096):
+        rc, summ, _ = ref.flagstats(np.array([v], np.uint16), use_pospopcnt=False)
+        single.append([int(x) for x in summ])
+    out["flagstats_single"] = single
+
     with open(os.path.join(HERE, "reference_counts.json"), "w") as f:
         json.dump(out, f, separators=(",", ":"))
 
     # Generator fixtures (counter-based synthetic inputs).  These
     # pin the device generators; produced by the C restatement.
     gens = {}
-    for kind in range(1, 7):
+    for kind in range(1, 8):
         for seed, base in ((1, 0), (1, 123456789), (42, 2**33 + 17)):
             a = orc.generate(kind, seed, 1 << 16, base=base)
             gens[f"{kind}:{seed}:{base}"] = {"first16": [int(x) for x in a[:16]],

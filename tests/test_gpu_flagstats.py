@@ -1,0 +1,83 @@
+"""FLAG statistics on the GPU: the fused one-pass kernel
+behind pospop_flagstats() against the reference's golden summaries and the oracle.
+Bit-exact.  Restates the reference's criterion 5 (acceptance.cpp:271-291) and
+the reserved-bit error (flagstats.cpp:34-36)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev(pp):
+    assert torch.cuda.is_available() and pp.device_available()
+    torch.cuda.set_device(0)
+    return torch.device("cuda:0")
+
+
+def to_dev(a):
+    return torch.from_numpy(a.view(np.uint8).copy()).cuda()
+
+
+def test_single_values_exhaustive(pp, dev, golden):
+    words = np.arange(4096, dtype=np.uint16)
+    d = to_dev(words)
+    for v in range(4096):
+        got = pp.flagstats((d.data_ptr() + 2 * v, 1)).as_list()
+        assert got == golden["flagstats_single"][v], v
+
+
+def test_all_values_in_one_stream_and_offsets(pp, dev, orc):
+    words = np.tile(np.arange(4096, dtype=np.uint16), 37)
+    rc, want, _ = orc.flagstats(words)
+    assert rc == 0
+    for off in range(0, 34, 2):  # unaligned starts: masked head vectors
+        buf = torch.full((words.nbytes + 128,), 0xFF, dtype=torch.uint8, device="cuda")  # invalid guards
+        buf[64 + off:64 + off + words.nbytes] = torch.from_numpy(words.view(np.uint8).copy()).cuda()
+        got = pp.flagstats((buf.data_ptr() + 64 + off, words.size)).as_list()
+        assert got == list(want), off
+
+
+def test_acceptance_streams(pp, dev, orc, golden):
+    streams = orc.acceptance_flag_streams()
+    for i in range(100):
+        assert pp.flagstats(to_dev(streams[i])).as_list() == golden["flagstats_acceptance"][i], i
+    for i in range(0, 100, 10):  # host-memory path
+        assert pp.flagstats(streams[i]).as_list() == golden["flagstats_acceptance"][i], i
+
+
+def test_invalid_word_first_offset(pp, dev, orc):
+    w = orc.generate(7, 5, 1 << 20)
+    w[700001] |= 0x4000
+    w[123457] |= 0x1000
+    w[999999] |= 0x8000
+    for data in (to_dev(w), w):
+        with pytest.raises(pp.InvalidFlagWordError) as e:
+            pp.flagstats(data)
+        assert e.value.offset == 123457 and e.value.word == int(w[123457])
+
+
+def test_invalid_word_in_a_later_host_chunk(pp, dev, orc):
+    n = (70 << 20) // 2 + 5  # two 64 MiB staging chunks
+    w = orc.generate(7, 6, n, threads=8)
+    w[n - 3] |= 0x2000
+    with pytest.raises(pp.InvalidFlagWordError) as e:
+        pp.flagstats(w)
+    assert e.value.offset == n - 3
+    w[n - 3] &= 0x0FFF
+    rc, want, _ = orc.flagstats(w)
+    assert pp.flagstats(w).as_list() == list(want)
+
+
+def test_empty_and_full_size(pp, dev, orc):
+    assert pp.flagstats(np.zeros(0, np.uint16)).total() == 0
+    n = 1 << 28
+    d = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_FLAGS, 9, d)
+    got = pp.flagstats(d)
+    host = d.cpu().numpy().view(np.uint16)
+    rc, want, _ = orc.flagstats(host)
+    assert rc == 0 and got.as_list() == list(want)
+    assert got.total() == n

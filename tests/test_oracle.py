@@ -278,3 +278,37 @@ def test_reference_validation_semantics(ref):  # test_core.cpp:184-201
     assert ref.validate(width=100) == 1
     rc, _ = ref.pospopcnt(np.zeros(8, np.uint16), kernel="csa16", width=128)
     assert rc == 2
+
+
+# -- FLAG statistics (acceptance.cpp:271-291) ----------------------------
+
+def test_flagstats_oracle_vs_golden(orc, golden):
+    for v in range(4096):  # exhaustive single flag values
+        w = np.array([v], np.uint16)
+        rc, got, _ = orc.flagstats(w)
+        rc2, got2, _ = orc.flagstats(w, "pospop")
+        assert rc == rc2 == 0 and list(got) == golden["flagstats_single"][v] == list(got2), v
+    streams = orc.acceptance_flag_streams()
+    for i in range(0, 100, 9):
+        rc, got, _ = orc.flagstats(streams[i])
+        rc2, got2, _ = orc.flagstats(streams[i], "pospop")
+        assert rc == rc2 == 0 and list(got) == golden["flagstats_acceptance"][i] == list(got2), i
+
+
+def test_flagstats_invalid_word_first_offset(orc):
+    w = orc.generate(7, 3, 5000)
+    assert w.max() < 0x1000
+    w[4000] |= 0x2000
+    w[1234] |= 0x8000
+    for route in ("reference", "pospop"):
+        rc, _, bad = orc.flagstats(w, route)
+        assert rc == 1 and bad == 1234
+
+
+def test_flagstats_oracle_matches_reference_live(orc, ref):
+    w = orc.generate(7, 11, 200000)
+    rc, a, _ = orc.flagstats(w)
+    rr, b, _ = ref.flagstats(w)
+    assert rc == rr == 0 and (a == b).all()
+    w[77] |= 0x1000
+    assert orc.flagstats(w)[0::2] == ref.flagstats(w)[0::2] == (1, 77)

@@ -132,6 +132,22 @@ def main():
         emit(kind="cfg2", gbs_med=round((1 << 29) / med / 1e6, 1), gbs_best=round((1 << 29) / best / 1e6, 1))
         del b3, b2
 
+    if "flag" in what:
+        lib = pp._load()
+        nf = 1 << 32  # 8 GiB of FLAG words
+        pp.generate(pp.GEN_FLAGS, 1, data, n=nf, stream=s)
+        torch.cuda.synchronize()
+        import ctypes as CC
+        summ = pp._Summary()
+        for var in ["5,32,0,256,2", "6,32,0,256,2", "5,16,0,256,2", "4,32,0,256,2", "6,16,0,256,2"]:
+            os.environ["POSPOP_FLAG_VARIANT"] = var
+            for nb in (1 << 30, 1 << 33):
+                med, best = timed(lambda: lib.pospop_flagstats(data.data_ptr(), nb // 2, CC.byref(summ), None, None),
+                                  max(3, args.reps // 4), s)
+                emit(kind="flagstats", bytes=nb, variant=var, gbs_med=round(nb / med / 1e6, 1),
+                     gbs_best=round(nb / best / 1e6, 1), note="sync C-ABI call incl. D2H of 33 u64")
+        os.environ.pop("POSPOP_FLAG_VARIANT", None)
+
     if "seg" in what:
         for k, kind in [(32, pp.GEN_U32), (64, pp.GEN_U64)]:
             arrays, words = 65536, 4096
