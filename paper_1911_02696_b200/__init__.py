@@ -39,7 +39,7 @@ __all__ = [
     "CudaError", "validate", "merge_counts", "pospopcnt", "pospopcnt_k", "pospopcnt_u16_c32",
     "pospopcnt_segmented", "pospopcnt_sharded", "count_async", "segmented_async", "generate", "digest",
     "supported_csa_widths", "native_csa_width", "device_available", "kernel_launches", "library_path",
-    "FlagBucket", "FlagSummary", "InvalidFlagWordError", "flagstats",
+    "FlagBucket", "FlagSummary", "InvalidFlagWordError", "flagstats", "pospopcnt_file",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -129,6 +129,8 @@ def _load():
         "pospop_generate": ([C.c_int, C.c_uint64, C.c_uint64, sz, vp, vp], C.c_int),
         "pospop_digest": ([vp, sz, _u64p], C.c_int),
         "pospop_flagstats": ([vp, sz, C.POINTER(_Summary), _u64p, C.POINTER(C.c_uint16)], C.c_int),
+        "pospopcnt_fd": ([C.c_int, C.c_int, _u64p, _u64p], C.c_int),
+        "pospopcnt_file": ([C.c_char_p, C.c_int, _u64p, _u64p], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -430,3 +432,20 @@ def flagstats(flags: Any) -> FlagSummary:
     _check(st)
     conv = lambda b: FlagBucket(*[int(getattr(b, f)) for f in _BUCKET_FIELDS])  # noqa: E731
     return FlagSummary(conv(out.pass_), conv(out.fail))
+
+
+# -- file / pipe ingestion (the reference CLI's input path) ------------------------
+
+def pospopcnt_file(source: Any, k: int = 16) -> tuple[PositionalCounts, int]:
+    """Counts a raw little-endian k-bit word stream from a path ("-" = stdin) or an
+    open file descriptor; returns (counts, word count).  As the reference's
+    read_word_stream (proj/tools/pospopcnt.cpp:52-75), a byte length that is not
+    a multiple of k/8 raises InvalidArgument."""
+    out = np.zeros(k, np.uint64)
+    n = C.c_uint64(0)
+    if isinstance(source, int):
+        st = _load().pospopcnt_fd(source, int(k), out.ctypes.data_as(_u64p), C.byref(n))
+    else:
+        st = _load().pospopcnt_file(os.fsencode(source), int(k), out.ctypes.data_as(_u64p), C.byref(n))
+    _check(st)
+    return PositionalCounts(out), int(n.value)

@@ -110,3 +110,14 @@ def test_package_does_not_import_the_oracle():
                 bad = re.search(r"import\s+pyoracle|from\s+pyoracle|#include[^\n]*pospop_oracle|liboracle\.so|"
                                 r"libpospop_ref|oracle/_ref", text)
                 assert not bad, (f, bad)
+
+
+def test_cli_usage_errors_without_gpu(tmp_path):
+    """Exit code 2 for usage/input errors (proj/tools/pospopcnt.cpp:43-45); no CPU fallback."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "-m", "paper_1911_02696_b200", "count"], cwd=ROOT, capture_output=True)
+    assert r.returncode == 2
+    r = subprocess.run([sys.executable, "-m", "paper_1911_02696_b200", "count", "--input", str(tmp_path / "nope")],
+                       cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 2 and "error" in r.stderr
