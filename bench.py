@@ -243,11 +243,17 @@ def run_ours(args):
     import paper_1911_02696_b200 as pp
 
     world, rank, local = dist_env()
-    n = max(args.gpus, world)
+    # POSPOP_BENCH_DIST_BACKEND=gloo exercises the N > 1 code path with fewer GPUs
+    # than ranks (tests only): ranks share devices, the k-vector goes through gloo.
+    backend = os.environ.get("POSPOP_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     k, gen_kind, total, desc = WORKLOADS[args.workload]
     wb = k // 8
     if args.scaling == "weak":

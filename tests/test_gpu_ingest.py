@@ -51,22 +51,20 @@ def test_file_ingestion_multi_chunk(pp, orc, tmp_path, k):
     assert counts == orc.pospopcnt(data, k, threads=8)
 
 
-def test_pipe_ingestion(pp, orc):
+def test_pipe_ingestion(pp, orc, tmp_path):
     data = orc.generate(4, 8, (3 << 20) + 5, threads=4)
-    r, w = os.pipe()
-    pid = os.fork()
-    if pid == 0:  # child: stream the bytes through the pipe in odd-sized writes
-        os.close(r)
-        raw = data.tobytes()
-        for i in range(0, len(raw), 99991):
-            os.write(w, raw[i:i + 99991])
-        os._exit(0)
-    os.close(w)
+    src = tmp_path / "src.bin"
+    data.tofile(src)
+    # a separate writer process streams the bytes through a pipe in odd-sized writes
+    writer = subprocess.Popen([sys.executable, "-c",
+                               "import sys\nraw = open(sys.argv[1], 'rb').read()\n"
+                               "for i in range(0, len(raw), 99991):\n    sys.stdout.buffer.write(raw[i:i + 99991])\n"
+                               "    sys.stdout.buffer.flush()\n", str(src)], stdout=subprocess.PIPE)
     try:
-        counts, n = pp.pospopcnt_file(r, 16)
+        counts, n = pp.pospopcnt_file(writer.stdout.fileno(), 16)
     finally:
-        os.close(r)
-        os.waitpid(pid, 0)
+        writer.stdout.close()
+        writer.wait(timeout=60)
     assert n == data.size and counts == orc.pospopcnt(data, 16, threads=4)
 
 
