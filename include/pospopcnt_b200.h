@@ -214,6 +214,12 @@ pospop_status pospop_generate(int kind, uint64_t seed, uint64_t index_base, size
  * synchronous. */
 pospop_status pospop_digest(const void* d_data, size_t nbytes, uint64_t* digest);
 
+/* Diagnostics: runs the DEVICE primitives of the counting kernels on given
+ * 32-bit registers (op 0 csa, 1 Harley-Seal tree of the given depth, 2 lane
+ * extraction, 3 carry drain, 4 warp channel totals) so tests can pin them
+ * against the reference's micro-op KATs (proj/tests/test_csa.cpp).  Synchronous. */
+pospop_status pospop_microop(int op, int depth, const uint32_t* in, size_t n_in, uint32_t* out, size_t n_out);
+
 /* Kernels launched by this library in this process (launch accounting). */
 uint64_t pospop_kernel_launches(void);
 

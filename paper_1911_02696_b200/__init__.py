@@ -130,6 +130,7 @@ def _load():
         "pospop_digest": ([vp, sz, _u64p], C.c_int),
         "pospop_flagstats": ([vp, sz, C.POINTER(_Summary), _u64p, C.POINTER(C.c_uint16)], C.c_int),
         "pospopcnt_fd": ([C.c_int, C.c_int, _u64p, _u64p], C.c_int),
+        "pospop_microop": ([C.c_int, C.c_int, vp, sz, vp, sz], C.c_int),
         "pospopcnt_file": ([C.c_char_p, C.c_int, _u64p, _u64p], C.c_int),
     }
     for name, (args, res) in sig.items():
@@ -449,3 +450,12 @@ def pospopcnt_file(source: Any, k: int = 16) -> tuple[PositionalCounts, int]:
         st = _load().pospopcnt_file(os.fsencode(source), int(k), out.ctypes.data_as(_u64p), C.byref(n))
     _check(st)
     return PositionalCounts(out), int(n.value)
+
+
+def microop(op: int, depth: int, inputs: Sequence[int], n_out: int) -> np.ndarray:
+    """Diagnostics: runs a device primitive (0 csa, 1 tree, 2 extract, 3 drain,
+    4 warp totals) on 32-bit registers; see pospop_microop in the C ABI."""
+    a = np.ascontiguousarray(np.asarray(inputs, dtype=np.uint64).astype(np.uint32))
+    out = np.zeros(max(n_out, 1), np.uint32)
+    _check(_load().pospop_microop(int(op), int(depth), a.ctypes.data, a.size, out.ctypes.data, n_out))
+    return out[:n_out]

@@ -762,6 +762,29 @@ pospop_status pospop_generate(int kind, uint64_t seed, uint64_t base, size_t n, 
     return POSPOP_OK;
 }
 
+pospop_status pospop_microop(int op, int depth, const uint32_t* in, size_t n_in, uint32_t* out, size_t n_out) {
+    if (op < 0 || op > 4 || depth < 1 || depth > 7 || !in || !out) return fail(POSPOP_EINVAL, "bad micro-op request");
+    if (op == 1 && (n_in < (size_t)depth || (n_in - depth) % ((size_t)1 << depth)))
+        return fail(POSPOP_EINVAL, "tree input must be depth carries + whole blocks of 2^depth registers");
+    if (op == 4 && n_in != 32 * 17) return fail(POSPOP_EINVAL, "total needs 32 lanes x (16 counters + shift)");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    Ctx* c = nullptr;
+    if ((s = get_ctx(dev, &c))) return s;
+    uint32_t *d_in = nullptr, *d_out = nullptr;
+    CU(cudaMalloc(&d_in, n_in * 4 + 4));
+    CU(cudaMalloc(&d_out, n_out * 4 + 4));
+    CU(cudaMemcpyAsync(d_in, in, n_in * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemsetAsync(d_out, 0, n_out * 4, c->stream));
+    CU(launch_microop(op, depth, d_in, n_in, d_out, c->stream));
+    CU(cudaMemcpyAsync(out, d_out, n_out * 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_in);
+    cudaFree(d_out);
+    return POSPOP_OK;
+}
+
 pospop_status pospop_digest(const void* d_data, size_t nbytes, uint64_t* digest) {
     if (!digest || (!d_data && nbytes)) return fail(POSPOP_EINVAL, "NULL pointer");
     if ((uintptr_t)d_data % 8) return fail(POSPOP_EINVAL, "digest input must be 8-byte aligned");

@@ -602,6 +602,80 @@ __global__ void generate_kernel(int kind, uint64_t key, uint64_t index_base, uns
     }
 }
 
+// Device micro-op harness: runs the exact device
+// primitives the stream kernel inlines -- csa, Tree<L>, extract, drain,
+// bank_warp_total -- on caller-supplied 32-bit registers, so tests can pin
+// them against the reference's micro-op KATs (proj/tests/test_csa.cpp).
+//   op 0 csa:      in[3i..3i+2] -> out[2i] = high, out[2i+1] = low
+//   op 1 tree:     carries in[0..L), blocks of 2^L inputs follow; out = tops
+//                  per block, then the final carries
+//   op 2 extract:  tops in[0..n) into a zeroed bank; out = 16 counters
+//   op 3 drain:    carries in[0..L); out = 16 packed Horner lanes
+//   op 4 total:    32 lanes x (16 counters, shift) -> lane c's warp total of channel c
+template <int L>
+__device__ void micro_tree(const uint32_t* in, size_t nblocks, uint32_t* out) {
+    uint32_t carries[L];
+    for (int j = 0; j < L; ++j) carries[j] = in[j];
+    for (size_t b = 0; b < nblocks; ++b) {
+        uint32_t r[1 << L];
+        for (int i = 0; i < (1 << L); ++i) r[i] = in[L + b * (1 << L) + i];
+        out[b] = Tree<L, 1>::run(carries, r);
+    }
+    for (int j = 0; j < L; ++j) out[nblocks + j] = carries[j];
+}
+
+__global__ void microop_kernel(int op, int depth, const uint32_t* in, unsigned long long n, uint32_t* out) {
+    if (op == 4) {  // one full warp
+        uint32_t counter[16], d[16];
+        for (int p = 0; p < 16; ++p) {
+            counter[p] = in[threadIdx.x * 17 + p];
+            d[p] = 0;
+        }
+        out[threadIdx.x] = bank_warp_total(counter, (int)in[threadIdx.x * 17 + 16], d);
+        return;
+    }
+    if (threadIdx.x != 0) return;
+    switch (op) {
+        case 0:
+            for (unsigned long long i = 0; i < n; ++i) csa(out[2 * i], out[2 * i + 1], in[3 * i], in[3 * i + 1], in[3 * i + 2]);
+            break;
+        case 1: {
+            const unsigned long long nb = (n - depth) >> depth;
+            switch (depth) {
+                case 1: micro_tree<1>(in, nb, out); break;
+                case 2: micro_tree<2>(in, nb, out); break;
+                case 3: micro_tree<3>(in, nb, out); break;
+                case 4: micro_tree<4>(in, nb, out); break;
+                case 5: micro_tree<5>(in, nb, out); break;
+                case 6: micro_tree<6>(in, nb, out); break;
+                default: micro_tree<7>(in, nb, out); break;
+            }
+            break;
+        }
+        case 2: {
+            uint32_t counter[16];
+            for (int p = 0; p < 16; ++p) counter[p] = 0;
+            for (unsigned long long i = 0; i < n; ++i) extract(counter, in[i]);
+            for (int p = 0; p < 16; ++p) out[p] = counter[p];
+            break;
+        }
+        case 3: {
+            uint32_t d[16];
+            switch (depth) {
+                case 1: drain<1>(d, in); break;
+                case 2: drain<2>(d, in); break;
+                case 3: drain<3>(d, in); break;
+                case 4: drain<4>(d, in); break;
+                case 5: drain<5>(d, in); break;
+                case 6: drain<6>(d, in); break;
+                default: drain<7>(d, in); break;
+            }
+            for (int p = 0; p < 16; ++p) out[p] = d[p];
+            break;
+        }
+    }
+}
+
 __global__ void digest_kernel(const uint8_t* data, unsigned long long nbytes, unsigned long long* d) {
     const unsigned long long nw = (nbytes + 7) >> 3;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
@@ -844,6 +918,12 @@ cudaError_t launch_generate(int kind, uint64_t seed, uint64_t index_base, size_t
     const unsigned long long want = (n + block - 1) / block;
     const unsigned long long cap = (unsigned long long)device_info().sms * 16;
     generate_kernel<<<(int)(want < cap ? want : cap), block, 0, stream>>>(kind, key, index_base, n, out);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_microop(int op, int depth, const uint32_t* d_in, size_t n, uint32_t* d_out, cudaStream_t stream) {
+    microop_kernel<<<1, 32, 0, stream>>>(op, depth, d_in, n, d_out);
     ++g_launches;
     return cudaGetLastError();
 }
