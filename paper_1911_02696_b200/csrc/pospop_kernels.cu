@@ -550,6 +550,188 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
     }
 }
 
+// Segmented, software-pipelined (SCHED 2): warp w owns arrays w, w + nwarps,
+// ... and walks the concatenation of their steps (32 lanes x VPT vectors) with
+// a one-step register double buffer: the loads of step s+1 -- possibly the
+// first step of the warp's next array, whose offsets were fetched one array
+// ahead -- are issued before step s is consumed and before an array's
+// epilogue (drain + transpose-reduce + row store), so the memory pipe never
+// drains at array boundaries.
+struct SegView {
+    const uint8_t* base;     // VB-aligned start
+    unsigned long long nv;   // vectors
+    unsigned long long f0, f1;
+    int lo, hi;
+};
+
+template <int VB>
+__device__ __forceinline__ SegView seg_view(const uint8_t* data, unsigned long long w0, unsigned long long w1, int wb) {
+    SegView v;
+    const uintptr_t P = (uintptr_t)(data + w0 * wb);
+    const uintptr_t Q = (uintptr_t)(data + w1 * wb);
+    const uintptr_t B = P & ~(uintptr_t)(VB - 1);
+    v.base = (const uint8_t*)B;
+    v.nv = Q > P ? (Q - B + VB - 1) / VB : 0;
+    v.lo = (int)(P - B);
+    v.hi = v.nv ? (int)(Q - (B + (v.nv - 1) * VB)) : VB;
+    v.f0 = v.lo ? 1 : 0;
+    v.f1 = v.nv - (v.nv && v.hi != VB ? 1 : 0);
+    return v;
+}
+
+template <int VB, int VPT>
+__device__ __forceinline__ void seg_load(const SegView& v, unsigned long long t, uint32_t lane,
+                                         uint32_t (&r)[VPT * (VB / 4)]) {
+    constexpr int RPV = VB / 4;
+    constexpr unsigned long long STEP = 32ull * VPT;
+    if (t >= v.f0 && t + STEP <= v.f1) {
+#pragma unroll
+        for (int q = 0; q < VPT; ++q) {
+            uint32_t x[RPV];
+            ldg_stream<VB, 0>(v.base + (t + 32ull * q + lane) * VB, x);
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < VPT; ++q) {
+            const unsigned long long idx = t + 32ull * q + lane;
+            uint32_t x[RPV];
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) x[j] = 0;
+            if (idx < v.nv) {
+                ldg_stream<VB, 0>(v.base + idx * VB, x);
+                if (idx == 0 || idx + 1 == v.nv) mask_bytes<VB>(x, idx == 0 ? v.lo : 0, idx + 1 == v.nv ? v.hi : VB);
+            }
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+        }
+    }
+}
+
+template <int NBANK>
+__device__ __forceinline__ void seg_store_row(unsigned long long* out, unsigned long long arr, int k, uint32_t lane,
+                                              const unsigned long long (&tot)[NBANK]) {
+    unsigned long long* row = out + arr * (unsigned long long)k;
+    if (NBANK == 2) {
+        row[lane] = tot[0];
+        row[32 + lane] = tot[NBANK - 1];
+    } else {
+        unsigned long long t = tot[0];
+        for (int w = 16; w >= k; w >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, w);
+        if ((int)lane < k) row[lane] = t;
+    }
+}
+
+template <int NBANK, int L, int VB>
+__device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const unsigned long long* offsets,
+                                                    unsigned long long n_arrays, int k, uint32_t flush_threshold,
+                                                    unsigned long long* out) {
+    constexpr int REGS = NBANK << L;
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr unsigned long long STEP = 32ull * VPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const int wb = k >> 3;
+
+    // Current array: skip (and zero) empty arrays.
+    unsigned long long arr = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    SegView cur;
+    for (;; arr += nwarps) {
+        if (arr >= n_arrays) return;
+        cur = seg_view<VB>(data, offsets[arr], offsets[arr + 1], wb);
+        if (cur.nv) break;
+        unsigned long long z[NBANK];
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b) z[b] = 0;
+        seg_store_row<NBANK>(out, arr, k, lane, z);
+    }
+    // Offsets of the warp's next array, fetched one array ahead.
+    unsigned long long nxt_w0 = 0, nxt_w1 = 0;
+    if (arr + nwarps < n_arrays) {
+        nxt_w0 = offsets[arr + nwarps];
+        nxt_w1 = offsets[arr + nwarps + 1];
+    }
+
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    uint32_t nb = 0;
+    unsigned long long tot[NBANK];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+
+    unsigned long long t = 0;
+    uint32_t rc[REGS];
+    seg_load<VB, VPT>(cur, t, lane, rc);
+    for (;;) {
+        // Where the next step is: later in this array, or the next non-empty array.
+        unsigned long long t_n = t + STEP, arr_n = arr;
+        SegView nxt = cur;
+        bool have_next = true;
+        if (t_n >= cur.nv) {
+            t_n = 0;
+            arr_n = arr + nwarps;
+            have_next = false;
+            while (arr_n < n_arrays) {
+                nxt = seg_view<VB>(data, nxt_w0, nxt_w1, wb);
+                if (arr_n + nwarps < n_arrays) {  // prefetch the offsets after that
+                    nxt_w0 = offsets[arr_n + nwarps];
+                    nxt_w1 = offsets[arr_n + nwarps + 1];
+                }
+                if (nxt.nv) {
+                    have_next = true;
+                    break;
+                }
+                unsigned long long z[NBANK];
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b) z[b] = 0;
+                seg_store_row<NBANK>(out, arr_n, k, lane, z);
+                arr_n += nwarps;
+            }
+        }
+        uint32_t rn[REGS];
+        if (have_next) seg_load<VB, VPT>(nxt, t_n, lane, rn);
+
+        tree_block<NBANK, L>(rc, carries, counter);
+        if (++nb == flush_threshold) {
+            uint32_t d[16];
+#pragma unroll
+            for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) tot[b] += bank_warp_total(counter[b], L, d);
+            zero_bank<NBANK>(counter);
+            nb = 0;
+        }
+        if (t + STEP >= cur.nv) {  // last step of this array: epilogue while rn is in flight
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) {
+                uint32_t d[16];
+                drain<L>(d, carries[b]);
+                tot[b] += bank_warp_total(counter[b], L, d);
+#pragma unroll
+                for (int j = 0; j < L; ++j) carries[b][j] = 0;
+            }
+            zero_bank<NBANK>(counter);
+            nb = 0;
+            seg_store_row<NBANK>(out, arr, k, lane, tot);
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+        }
+        if (!have_next) break;
+#pragma unroll
+        for (int i = 0; i < REGS; ++i) rc[i] = rn[i];
+        cur = nxt;
+        arr = arr_n;
+        t = t_n;
+    }
+}
+
 __global__ void generate_kernel(int kind, uint64_t key, uint64_t index_base, unsigned long long n,
                                 void* out) {
     constexpr uint32_t kZipf[15] = {1417819056u, 2079255034u, 2502690694u, 2811261488u,
@@ -772,13 +954,24 @@ struct SegVariant {
     SegKernel fn;
 };
 
+template <int NBANK, int L, int VB>
+__global__ void __launch_bounds__(256) segmented_pipe_entry(const uint8_t* data, const unsigned long long* offsets,
+                                                            unsigned long long n, int k, uint32_t thr,
+                                                            unsigned long long* out, unsigned long long*,
+                                                            unsigned int*, unsigned) {
+    segmented_pipe_body<NBANK, L, VB>(data, offsets, n, k, thr, out);
+}
+
 #define SG(NB, L, VB, S) {NB, L, VB, S, segmented_kernel<NB, L, VB, S>}
+#define SGP(NB, L, VB) {NB, L, VB, 2, segmented_pipe_entry<NB, L, VB>}
 const SegVariant kSegVariants[] = {
     SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
     SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
     SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
+    SGP(1, 4, 16), SGP(1, 5, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
 };
 #undef SG
+#undef SGP
 
 const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched) {
     for (const SegVariant& v : kSegVariants)
@@ -897,7 +1090,7 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (grid <= 0) {
         const unsigned long long warps_per_block = block / 32;
         const unsigned long long want = (n + warps_per_block - 1) / warps_per_block;
-        // measured (r01 sweep): 4 CTAs/SM for the strided schedule, one resident wave for the dynamic one
+        // measured (r01 sweep): 4 CTAs/SM for the strided schedule, one resident wave otherwise
         const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", var->sched == 0 ? 4 : resident_blocks(var->fn, block));
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < cap ? want : cap);

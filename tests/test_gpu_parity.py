@@ -355,3 +355,36 @@ def test_reference_verify_kernels_with_gpu_runner():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") == 4
+
+
+SEG_VARIANTS = {
+    8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2"],
+    16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2"],
+    32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2"],
+    64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2"],
+}
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_segmented_every_variant(pp, dev, orc, k, monkeypatch):
+    """All segmented schedules (strided, dynamic, software-pipelined) on a ragged
+    batch with empty arrays, tiny arrays and misaligned starts."""
+    rng = np.random.default_rng(500 + k)
+    n_words = 300_000
+    data = orc.generate(6, 31, n_words * k // 64 + 1).view(DT[k])[:n_words]
+    cuts = np.sort(np.concatenate([rng.integers(0, n_words, size=2000), np.arange(1000, 1100)]))
+    offs = np.concatenate([[0, 0], cuts, [n_words, n_words]]).astype(np.uint64)
+    want = orc.segmented(data, offs, k, threads=8)
+    d = to_dev(data)
+    o = torch.from_numpy(offs.view(np.int64)).cuda()
+    for var in SEG_VARIANTS[k]:
+        monkeypatch.setenv("POSPOP_SEG_VARIANT", var)
+        for per_sm in ("", "1"):
+            if per_sm:
+                monkeypatch.setenv("POSPOP_SEG_BLOCKS_PER_SM", per_sm)
+            else:
+                monkeypatch.delenv("POSPOP_SEG_BLOCKS_PER_SM", raising=False)
+            out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
+            pp.segmented_async(d, o, out, k)
+            torch.cuda.synchronize()
+            assert (out.cpu().numpy().view(np.uint64) == want).all(), (var, per_sm)
