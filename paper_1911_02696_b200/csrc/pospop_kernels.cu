@@ -78,6 +78,14 @@ __device__ __forceinline__ unsigned smid() {
     return r;
 }
 
+// Programmatic dependent launch (sm_90+): `pdl_allow_next` lets the next
+// kernel in the stream start launching (its CTAs take SMs as ours retire);
+// `pdl_wait_prev` blocks until the previous kernel in the stream has completed
+// and its writes are visible.  Both are no-ops for launches without the
+// programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_allow_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_prev() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Channel -> position fold: the channels (of 32 * NBANK) that count position
 // p are p + m * k for m = 0 .. 32/k - 1 (k <= 32), or channel p (k = 64).
 __device__ __forceinline__ int channels_per_position(int k) { return k >= 32 ? 1 : 32 / k; }
@@ -160,6 +168,7 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
                                            uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
                                            int* s_last, unsigned block, uint32_t lane) {
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer();
+    pdl_wait_prev();  // the previous launch on this stream owns acc/ticket/next until it completes
 #pragma unroll
     for (int b = 0; b < NBANK; ++b) {
         uint32_t d[16];
@@ -294,6 +303,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
         a.trace[blockIdx.x * 5 + 4] = smid();
     }
     for (int i = threadIdx.x; i < 32 * NBANK; i += block) s_acc[i] = 0;
+    pdl_allow_next();
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
 
@@ -361,6 +371,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
             mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
         }
         if (a.pool) {
+            pdl_wait_prev();  // the pool counter is shared with the previous launch
             unsigned long long m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
             unsigned long long c = __shfl_sync(0xFFFFFFFFu, m, 0);
             m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
@@ -385,6 +396,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const S
     } else {
         constexpr unsigned long long WT = 32ull * VPT;  // vectors per warp tile
         const unsigned long long S0 = a.g0 * 32;
+        pdl_wait_prev();
         unsigned long long mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
         unsigned long long c = __shfl_sync(0xFFFFFFFFu, mine, 0);
         mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;  // prefetch: consumed one chunk later
@@ -968,7 +980,7 @@ const SegVariant kSegVariants[] = {
     SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
     SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
     SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
-    SGP(1, 4, 16), SGP(1, 5, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
+    SGP(1, 5, 16), SGP(1, 4, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
 };
 #undef SG
 #undef SGP
@@ -1058,9 +1070,19 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     if (a.pool > a.nwt) a.pool = a.nwt;
 
     if (grid_used) *grid_used = grid;
-    var->fn<<<grid, threads, 0, stream>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = env_int("POSPOP_PDL", 1) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, var->fn, a);
     ++g_launches;
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
@@ -1080,11 +1102,11 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (n == 0) return cudaSuccess;
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched".
-    int depth = 5, vb = 16, sched = nbank == 1 ? 0 : 1;
+    int depth = 5, vb = 16, sched = nbank == 1 ? 2 : 1;  // measured: pipelined (k <= 32), dynamic (k = 64)
     if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d", &depth, &vb, &sched);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb, sched);
-    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 0 : 1);
+    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 2 : 1);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {
