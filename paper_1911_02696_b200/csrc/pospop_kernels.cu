@@ -229,15 +229,22 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
 //   bit1,3 = w & GU ; bit6,7 = w & G ; bit 2,8,9,10 = w ; bit11 = supp & !sec ;
 //   bit12 (pair_map) = GU & !mate_unmapped ; pass/fail split on QCFAIL (bit 9).
 // ---------------------------------------------------------------------------
+// Shifts by a constant on the FMA pipe (IMAD.HI / IMAD.SHL) instead of the ALU
+// pipe's SHF: the transform is ALU-bound, and the two pipes issue independently.
+template <int S>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x) { return __umulhi(x, 1u << (32 - S)); }
+template <int S>
+__device__ __forceinline__ uint32_t shl_fma(uint32_t x) { return x * (1u << S); }
+
 __device__ __forceinline__ void flag_transform2(uint32_t w, uint32_t& pass, uint32_t& fail) {
     constexpr uint32_t L1 = 0x00010001u;
-    const uint32_t g = w & ~(w >> 8) & ~(w >> 11) & L1;
-    const uint32_t gu = g & ~(w >> 2);
+    const uint32_t g = w & ~shr_fma<8>(w) & ~shr_fma<11>(w) & L1;
+    const uint32_t gu = g & ~shr_fma<2>(w);
     const uint32_t mg = g * 0xFFFFu;  // lane masks (IMAD: FMA pipe)
     const uint32_t mgu = gu * 0xFFFFu;
-    const uint32_t mf = ((w >> 9) & L1) * 0xFFFFu;
+    const uint32_t mf = (shr_fma<9>(w) & L1) * 0xFFFFu;
     const uint32_t out = (w & 0x07040704u) | (w & mgu & 0x000A000Au) | (w & mg & 0x00C000C0u) |
-                         (w & ~(w << 3) & 0x08000800u) | (mgu & ~(w << 9) & 0x10001000u);
+                         (w & ~shl_fma<3>(w) & 0x08000800u) | (mgu & ~shl_fma<9>(w) & 0x10001000u);
     pass = out & ~mf;
     fail = out & mf;
 }
