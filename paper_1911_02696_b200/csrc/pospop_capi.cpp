@@ -65,6 +65,8 @@ bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64; }
 // Device discovery: sm_100 class only (the fatbin carries sm_100a SASS).
 // ---------------------------------------------------------------------------
 pospop_status check_device(int dev) {
+    static thread_local int checked = -1;  // last device that passed (cheap fast path per call)
+    if (dev == checked) return POSPOP_OK;
     int major = 0;
     const cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
@@ -72,6 +74,7 @@ pospop_status check_device(int dev) {
         return fail(POSPOP_EUNAVAILABLE,
                     "kernel unavailable: device %d is compute capability %d.x, sm_100 required", dev,
                     major);
+    checked = dev;
     return POSPOP_OK;
 }
 
@@ -105,6 +108,7 @@ struct DeviceGuard {
 // the stream workspace, and (lazily) the host-staging ring.
 // ---------------------------------------------------------------------------
 constexpr int kRing = 3;
+constexpr size_t kBounceBytes = 1 << 20;  // host inputs up to this size take the single-stream path
 
 struct Ctx {
     int dev = -1;
@@ -114,6 +118,7 @@ struct Ctx {
     unsigned long long* h_out = nullptr;  // 64 u64, pinned
     StreamWorkspace ws;
     void* stage[kRing] = {nullptr, nullptr, nullptr};
+    void* bounce = nullptr;  // pinned host buffer for small host inputs (kBounceBytes)
     size_t stage_bytes = 0;
     cudaEvent_t ev_copied[kRing] = {};
     cudaEvent_t ev_done[kRing] = {};
@@ -232,6 +237,14 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
 
     if (where == Where::Device) {
         CU(launch_stream(k, data, len, c->d_out, false, opt, c->ws, c->stream));
+    } else if (len * wb <= kBounceBytes) {
+        // Small host input (the latency path): copy into a
+        // pinned bounce buffer, one DMA + one launch + one D2H on one stream.
+        if ((s = ensure_stage(c))) return s;
+        if (!c->bounce) CU(cudaMallocHost(&c->bounce, kBounceBytes));
+        std::memcpy(c->bounce, data, len * wb);
+        CU(cudaMemcpyAsync(c->stage[0], c->bounce, len * wb, cudaMemcpyHostToDevice, c->stream));
+        CU(launch_stream(k, c->stage[0], len, c->d_out, false, opt, c->ws, c->stream));
     } else {
         // Host input: chunked H2D on the copy stream, counting on the compute
         // stream, kRing staging buffers recycled behind ev_done.
@@ -479,8 +492,12 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
         return fail(POSPOP_EFLAG, "invalid FLAG word 0x%x at offset %llu (bits 12-15 must be clear)", word,
                     (unsigned long long)idx);
     }
-    const uint64_t* pc = reinterpret_cast<const uint64_t*>(c->h_out);
-    const uint64_t* fc = pc + 16;
+    // Kernel output: [0,16) counts over all reads, [16,32) over QC-fail reads;
+    // QC-pass = all - fail (flagstats.cpp:137-143 counts the two streams).
+    const uint64_t* ac = reinterpret_cast<const uint64_t*>(c->h_out);
+    const uint64_t* fc = ac + 16;
+    uint64_t pc[16];
+    for (int p = 0; p < 16; ++p) pc[p] = ac[p] - fc[p];
     const uint64_t fail_total = fc[9];
     bucket_from_counts(fc, fail_total, &out->fail);
     bucket_from_counts(pc, len - fail_total, &out->pass);

@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 
 #include "pospop_device.cuh"
 #include "pospop_launch.h"
@@ -223,35 +224,36 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
 // FLAG statistics (reference proj/core/src/flagstats.cpp).
 // SWAR form of flag_transform (flagstats.cpp:94-125) on a register holding two
 // SAM FLAG words.  Only the positions bucket_from_counts reads (1,2,3,6,7,8,
-// 9,10,11,12; flagstats.cpp:39-63) are produced; 0,4,5,13-15 are left zero.
-//   G  = paired & !secondary & !supplementary       (lane bit 0)
-//   GU = G & !unmapped
-//   bit1,3 = w & GU ; bit6,7 = w & G ; bit 2,8,9,10 = w ; bit11 = supp & !sec ;
-//   bit12 (pair_map) = GU & !mate_unmapped ; pass/fail split on QCFAIL (bit 9).
+// 9,10,11,12; flagstats.cpp:39-63) are produced.  Per 16-bit lane:
+//   G  = paired & !secondary & !supplementary ;  GU = G & !unmapped
+//   bits 1,3 = w & GU ; bits 6,7 = w & G ; bits 2,8,9,10 = w ;
+//   bit 11 = supplementary & !secondary ; bit 12 (pair_map) = GU & !mate_unmapped
+// `all` is that word for every read; `fail` keeps it only for QC-fail reads.
+// The QC-pass plane is never formed: pass counts = all counts - fail counts
+// (exact integers, derived on the host).  The kernel is ALU-bound, so the
+// shifts run on the FMA pipe (IMAD.HI / IMAD.SHL) and the G/GU selections are
+// built by multiplying the lane predicate into the target bit positions
+// (g * 0x00C0 + gu * 0x100A) instead of full lane masks.
 // ---------------------------------------------------------------------------
-// Shifts by a constant on the FMA pipe (IMAD.HI / IMAD.SHL) instead of the ALU
-// pipe's SHF: the transform is ALU-bound, and the two pipes issue independently.
 template <int S>
 __device__ __forceinline__ uint32_t shr_fma(uint32_t x) { return __umulhi(x, 1u << (32 - S)); }
 template <int S>
 __device__ __forceinline__ uint32_t shl_fma(uint32_t x) { return x * (1u << S); }
 
-__device__ __forceinline__ void flag_transform2(uint32_t w, uint32_t& pass, uint32_t& fail) {
+__device__ __forceinline__ void flag_transform2(uint32_t w, uint32_t& all, uint32_t& fail) {
     constexpr uint32_t L1 = 0x00010001u;
-    const uint32_t g = w & ~shr_fma<8>(w) & ~shr_fma<11>(w) & L1;
-    const uint32_t gu = g & ~shr_fma<2>(w);
-    const uint32_t mg = g * 0xFFFFu;  // lane masks (IMAD: FMA pipe)
-    const uint32_t mgu = gu * 0xFFFFu;
-    const uint32_t mf = (shr_fma<9>(w) & L1) * 0xFFFFu;
-    const uint32_t out = (w & 0x07040704u) | (w & mgu & 0x000A000Au) | (w & mg & 0x00C000C0u) |
-                         (w & ~shl_fma<3>(w) & 0x08000800u) | (mgu & ~shl_fma<9>(w) & 0x10001000u);
-    pass = out & ~mf;
-    fail = out & mf;
+    const uint32_t g0 = w & ~shr_fma<8>(w) & ~shr_fma<11>(w);  // bit 0 / 16: paired & primary
+    const uint32_t g = g0 & L1;
+    const uint32_t gu = g0 & ~shr_fma<2>(w) & L1;
+    const uint32_t t = g * 0x00C0u + gu * 0x100Au;              // bits 6,7 <- G ; bits 1,3,12 <- GU
+    const uint32_t mf = (shr_fma<9>(w) & L1) * 0xFFFFu;           // QC-fail lane mask
+    all = (w & (t | 0x07040704u)) | (t & ~shl_fma<9>(w) & 0x10001000u) | (w & ~shl_fma<3>(w) & 0x08000800u);
+    fail = all & mf;
 }
 
 // Tree-block consumer.  MODE 0: positional counts of the words (NBANK banks).
-// MODE 1: FLAG statistics -- transform, then bank 0 counts the QC-pass plane
-// and bank 1 the QC-fail plane; words with reserved bits 12-15 set are
+// MODE 1: FLAG statistics -- transform, then bank 0 counts the transformed
+// words of all reads and bank 1 those of QC-fail reads; words with reserved bits 12-15 set are
 // reported through a.bad (the first such index wins, as the reference's
 // check_reserved throws at the first one, flagstats.cpp:34-36).
 template <int MODE, int NBANK, int L, int VB, int REGS>
@@ -263,14 +265,14 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
     } else {
         static_assert(NBANK == 2 && REGS == (1 << L), "FLAG mode: two banks of 2^L registers");
         constexpr int RPV = VB / 4;
-        uint32_t pass[REGS], fail[REGS];
+        uint32_t all[REGS], fail[REGS];
         uint32_t bad = 0;
 #pragma unroll
         for (int i = 0; i < REGS; ++i) {
             bad |= r[i];
-            flag_transform2(r[i], pass[i], fail[i]);
+            flag_transform2(r[i], all[i], fail[i]);
         }
-        extract(counter[0], Tree<L, 1>::run(carries[0], pass));
+        extract(counter[0], Tree<L, 1>::run(carries[0], all));
         extract(counter[1], Tree<L, 1>::run(carries[1], fail));
         if (bad & 0xF000F000u) {  // rare: locate this thread's first invalid word
             unsigned long long best = ~0ull;
@@ -927,8 +929,24 @@ DeviceInfo device_info() {
 
 template <class Kernel>
 int resident_blocks(Kernel kernel, int block) {
+    // The occupancy query costs microseconds; cache it per (device, kernel, block).
+    struct Key {
+        int dev;
+        const void* fn;
+        int block;
+        bool operator<(const Key& o) const {
+            return dev != o.dev ? dev < o.dev : fn != o.fn ? fn < o.fn : block < o.block;
+        }
+    };
+    static thread_local std::map<Key, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const Key key{dev, reinterpret_cast<const void*>(kernel), block};
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, 0) != cudaSuccess || n < 1) n = 1;
+    cache[key] = n;
     return n;
 }
 

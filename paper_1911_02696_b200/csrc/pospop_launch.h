@@ -40,9 +40,9 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
                           cudaStream_t stream, int* grid_used = nullptr);
 
 // FLAG statistics (reference flagstats_pospopcnt, flagstats.cpp:127-145) in one
-// pass: d_out33[0..16) = QC-pass positional counts of the transformed words,
-// [16..32) = QC-fail counts, [32] = ~(index of the first word with reserved
-// bits 12-15 set) or 0.  One kernel launch.
+// pass: d_out33[0..16) = positional counts of the transformed words of all
+// reads, [16..32) = of QC-fail reads (QC-pass = all - fail), [32] = ~(index of
+// the first word with reserved bits 12-15 set) or 0.  One kernel launch.
 cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long long* d_out33, bool accumulate,
                              const LaunchOptions& opt, const StreamWorkspace& ws, cudaStream_t stream);
 
