@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the workload's total words split over N (BASELINE cfg4); weak: per GPU")
+    ap.add_argument("--clock-interval-ms", type=float, default=20.0,
+                    help="NVML clock/throttle sampling period during the timed region (0 = off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -84,7 +86,10 @@ def ncu_traffic(workload: str, n_gpus: int):
 
 
 class ClockSampler:
-    """NVML clocks + throttle reasons sampled every ~5 ms while active."""
+    """NVML clocks + throttle reasons sampled periodically while active.  The
+    samples are taken from a side thread; at a 5 ms period the polling cost
+    the launch thread ~2% of throughput, so the default period is 20 ms (a
+    cfg4 timed region of 200 steps lasts ~230 ms, >= 10 samples)."""
 
     REASONS = {
         "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
@@ -92,12 +97,15 @@ class ClockSampler:
         "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
     }
 
-    def __init__(self, device_index: int):
+    def __init__(self, device_index: int, interval_s: float = 0.02):
+        self.interval_s = interval_s
         self.samples: list[int] = []
         self.reasons = 0
         self.max_mhz = None
         self._stop = threading.Event()
         self._ok = False
+        if interval_s <= 0:
+            return
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -116,7 +124,7 @@ class ClockSampler:
                 self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(self.interval_s)
 
     def __enter__(self):
         if self._ok:
@@ -311,7 +319,7 @@ def run_ours(args):
     t_begin = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     launches0 = pp.kernel_launches()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, args.clock_interval_ms / 1e3)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
