@@ -195,9 +195,10 @@ pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out) {
 // ---------------------------------------------------------------------------
 enum class Where { Device, Host };
 
-Where classify(const void* p, int* dev) {
+Where classify(const void* p, int* dev, bool* pinned = nullptr) {
     cudaPointerAttributes a;
     std::memset(&a, 0, sizeof a);
+    if (pinned) *pinned = false;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
         return Where::Host;
@@ -206,6 +207,7 @@ Where classify(const void* p, int* dev) {
         *dev = a.device;
         return Where::Device;
     }
+    if (pinned) *pinned = a.type == cudaMemoryTypeHost;
     return Where::Host;
 }
 
@@ -230,7 +232,8 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
     }
     LaunchOptions opt;
     opt.flush_threshold = flush;
-    const Where where = classify(data, &dev);
+    bool pinned = false;
+    const Where where = classify(data, &dev, &pinned);
     DeviceGuard g(dev);
     Ctx* c = nullptr;
     if ((s = get_ctx(dev, &c))) return s;
@@ -238,12 +241,17 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
     if (where == Where::Device) {
         CU(launch_stream(k, data, len, c->d_out, false, opt, c->ws, c->stream));
     } else if (len * wb <= kBounceBytes) {
-        // Small host input (the latency path): copy into a
-        // pinned bounce buffer, one DMA + one launch + one D2H on one stream.
+        // Small host input (the latency path): one DMA (from
+        // the caller's pinned memory, or via a pinned bounce buffer for
+        // pageable memory) + one launch + one D2H, all on one stream.
         if ((s = ensure_stage(c))) return s;
-        if (!c->bounce) CU(cudaMallocHost(&c->bounce, kBounceBytes));
-        std::memcpy(c->bounce, data, len * wb);
-        CU(cudaMemcpyAsync(c->stage[0], c->bounce, len * wb, cudaMemcpyHostToDevice, c->stream));
+        const void* src = data;
+        if (!pinned) {
+            if (!c->bounce) CU(cudaMallocHost(&c->bounce, kBounceBytes));
+            std::memcpy(c->bounce, data, len * wb);
+            src = c->bounce;
+        }
+        CU(cudaMemcpyAsync(c->stage[0], src, len * wb, cudaMemcpyHostToDevice, c->stream));
         CU(launch_stream(k, c->stage[0], len, c->d_out, false, opt, c->ws, c->stream));
     } else {
         // Host input: chunked H2D on the copy stream, counting on the compute

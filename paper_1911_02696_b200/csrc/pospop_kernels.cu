@@ -275,8 +275,12 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
         extract(counter[0], Tree<L, 1>::run(carries[0], all));
         extract(counter[1], Tree<L, 1>::run(carries[1], fail));
         if (bad & 0xF000F000u) {  // rare: locate this thread's first invalid word
+            // Fully unrolled: a runtime index into r[] would force the whole
+            // tile through local memory on the hot path.
             unsigned long long best = ~0ull;
+#pragma unroll
             for (int i = 0; i < REGS; ++i)
+#pragma unroll
                 for (int h = 0; h < 2; ++h)
                     if ((r[i] >> (16 * h)) & 0xF000u) {
                         const unsigned long long byte =
