@@ -301,8 +301,8 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
 // while another still holds a big share; the next chunk index is fetched one
 // chunk ahead so the atomic's latency hides behind the loads.
 // BLOCK > 0: compile-time block size; BLOCK == 0: runtime blockDim.x.
-template <int NBANK, int L, int VB, int HINT, int BLOCK, int SCHED, int MODE>
-__global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256) stream_kernel(const StreamArgs a) {
+template <int NBANK, int L, int VB, int HINT, int BLOCK, int SCHED, int MODE, int MINB = 1>
+__global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(const StreamArgs a) {
     constexpr int REGS = MODE == 1 ? (1 << L) : (NBANK << L);  // 32-bit input registers per tree block
     constexpr int RPV = VB / 4;       // registers per vector
     constexpr int VPT = REGS / RPV;   // vectors per thread per tree block
@@ -963,6 +963,8 @@ struct StreamVariant {
 
 #define SV(NB, L, VB, H, B, S) {NB, L, VB, H, B, S, 0, stream_kernel<NB, L, VB, H, B, S, 0>}
 #define SVF(L, VB, B, S) {2, L, VB, 0, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1>}
+// FLAG variants that must fit 2 CTAs/SM (<= 128 registers); hint slot = 2 marks them.
+#define SVF2(L, VB, B, S) {2, L, VB, 2, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1, 2>}
 // Production variants first (the defaults), then tuning variants selectable
 // through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched" (POSPOP_FLAG_VARIANT
 // for MODE 1).
@@ -975,9 +977,11 @@ const StreamVariant kStreamVariants[] = {
     SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1), SV(1, 6, 32, 0, 256, 2), SV(1, 7, 16, 0, 256, 2),
     SVF(6, 32, 256, 2), SVF(6, 32, 0, 2),               // FLAG statistics defaults
     SVF(5, 32, 256, 2), SVF(6, 16, 256, 2), SVF(7, 32, 256, 2),
+    SVF2(5, 32, 256, 2), SVF2(5, 16, 256, 2), SVF2(4, 32, 256, 2), SVF2(6, 32, 256, 2), SVF(5, 32, 512, 2),
 };
 #undef SV
 #undef SVF
+#undef SVF2
 
 const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block, int sched, int mode) {
     for (const StreamVariant& v : kStreamVariants)
