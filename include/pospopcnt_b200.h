@@ -197,6 +197,18 @@ pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d
 pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
                                     uint64_t* d_trace, size_t trace_ctas, int* grid_used, void* stream);
 
+/* CUDA-graph replay for repeated counts of one device buffer, where launch
+ * latency dominates (small inputs).  The graph is bound to (d_data, len,
+ * d_counts) and reads the buffer's current contents at every replay; d_counts
+ * is overwritten.  Each graph owns its workspace: different graphs may run
+ * concurrently, one graph must not overlap itself.  NULL stream = legacy
+ * default stream. */
+typedef struct pospop_graph_s* pospop_graph;
+pospop_status pospopcnt_graph_create(int k, const void* d_data, size_t len, uint64_t* d_counts,
+                                     pospop_graph* out);
+pospop_status pospopcnt_graph_launch(pospop_graph graph, void* stream);
+void pospopcnt_graph_destroy(pospop_graph graph);
+
 /* Segmented, device-resident, asynchronous. */
 pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_t* d_offsets,
                                         size_t n_arrays, uint64_t* d_counts,

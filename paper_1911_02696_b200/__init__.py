@@ -131,6 +131,9 @@ def _load():
         "pospop_flagstats": ([vp, sz, C.POINTER(_Summary), _u64p, C.POINTER(C.c_uint16)], C.c_int),
         "pospopcnt_fd": ([C.c_int, C.c_int, _u64p, _u64p], C.c_int),
         "pospop_microop": ([C.c_int, C.c_int, vp, sz, vp, sz], C.c_int),
+        "pospopcnt_graph_create": ([C.c_int, vp, sz, vp, C.POINTER(vp)], C.c_int),
+        "pospopcnt_graph_launch": ([vp, vp], C.c_int),
+        "pospopcnt_graph_destroy": ([vp], None),
         "pospopcnt_file": ([C.c_char_p, C.c_int, _u64p, _u64p], C.c_int),
     }
     for name, (args, res) in sig.items():
@@ -459,3 +462,34 @@ def microop(op: int, depth: int, inputs: Sequence[int], n_out: int) -> np.ndarra
     out = np.zeros(max(n_out, 1), np.uint32)
     _check(_load().pospop_microop(int(op), int(depth), a.ctypes.data, a.size, out.ctypes.data, n_out))
     return out[:n_out]
+
+
+class CountGraph:
+    """CUDA-graph replay of one device-resident count (launch-latency path).
+
+    Bound to (data, out); every replay() recounts the buffer's current
+    contents into `out` (k uint64 on the device)."""
+
+    def __init__(self, data: Any, out: Any, k: int, len_words: int | None = None):
+        addr, n = _addr_len(data, k)
+        if len_words is not None:
+            n = int(len_words)
+        out_addr, _ = _addr_len(out, 64)
+        h = C.c_void_p()
+        _check(_load().pospopcnt_graph_create(int(k), addr or None, n, out_addr, C.byref(h)))
+        self._h = h
+        self._keep = (data, out)  # the graph holds raw pointers to these buffers
+
+    def replay(self, stream: Any = None) -> None:
+        _check(_load().pospopcnt_graph_launch(self._h, _stream_ptr(stream)))
+
+    def close(self) -> None:
+        if self._h:
+            _load().pospopcnt_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass

@@ -753,6 +753,81 @@ pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint6
     return POSPOP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// CUDA-graph replay of one count (calls where launch
+// latency dominates).  The graph holds one kernel node bound to the data
+// pointer, length and output; it reads the buffer's CURRENT contents at every
+// replay.  Each graph owns its workspace, so different graphs may run
+// concurrently; one graph must not be replayed concurrently with itself.
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct pospop_graph_s {
+    int dev = -1;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    StreamWorkspace ws;
+};
+
+extern "C" {
+
+pospop_status pospopcnt_graph_create(int k, const void* d_data, size_t len, uint64_t* d_counts,
+                                     pospop_graph* out) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (!out || !d_counts || (!d_data && len)) return fail(POSPOP_EINVAL, "NULL pointer");
+    if ((uintptr_t)d_data % ((size_t)k / 8)) return fail(POSPOP_EINVAL, "data is misaligned");
+    *out = nullptr;
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    if (len && classify(d_data, &dev) != Where::Device) return fail(POSPOP_EINVAL, "graph data must be device memory");
+    DeviceGuard g(dev);
+    auto* gr = new pospop_graph_s;
+    gr->dev = dev;
+    if ((s = alloc_workspace(&gr->ws))) {
+        delete gr;
+        return s;
+    }
+    cudaStream_t cap = nullptr;
+    CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    CU(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    LaunchOptions opt;
+    const cudaError_t le = launch_stream(k, len ? d_data : (const void*)d_counts, len,
+                                         reinterpret_cast<unsigned long long*>(d_counts), false, opt, gr->ws, cap);
+    const cudaError_t ce = cudaStreamEndCapture(cap, &gr->graph);
+    cudaStreamDestroy(cap);
+    if (le != cudaSuccess || ce != cudaSuccess) {
+        cudaFree(gr->ws.acc);
+        delete gr;
+        return cuda_fail(le != cudaSuccess ? le : ce, "graph capture");
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&gr->exec, gr->graph, 0);
+    if (ie != cudaSuccess) {
+        cudaGraphDestroy(gr->graph);
+        cudaFree(gr->ws.acc);
+        delete gr;
+        return cuda_fail(ie, "cudaGraphInstantiate");
+    }
+    *out = gr;
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_graph_launch(pospop_graph gr, void* stream) {
+    if (!gr) return fail(POSPOP_EINVAL, "NULL graph");
+    DeviceGuard g(gr->dev);
+    CU(cudaGraphLaunch(gr->exec, static_cast<cudaStream_t>(stream)));
+    return POSPOP_OK;
+}
+
+void pospopcnt_graph_destroy(pospop_graph gr) {
+    if (!gr) return;
+    DeviceGuard g(gr->dev);
+    cudaGraphExecDestroy(gr->exec);
+    cudaGraphDestroy(gr->graph);
+    cudaFree(gr->ws.acc);
+    delete gr;
+}
+
 pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_t* d_offsets, size_t n,
                                         uint64_t* d_counts, uint32_t flush, int grid, int block,
                                         void* stream) {

@@ -388,3 +388,23 @@ def test_segmented_every_variant(pp, dev, orc, k, monkeypatch):
             pp.segmented_async(d, o, out, k)
             torch.cuda.synchronize()
             assert (out.cpu().numpy().view(np.uint64) == want).all(), (var, per_sm)
+
+
+def test_graph_replay_counts_current_contents(pp, dev, orc):
+    """CUDA-graph replay (latency path): bit-exact, and it recounts the buffer's
+    current contents at every replay."""
+    for k, n_bytes in ((16, 8192), (8, 12345), (64, 1 << 20)):
+        a = orc.generate(6, 40 + k, (n_bytes + 7) // 8).view(np.uint8)[:n_bytes]
+        b = orc.generate(6, 80 + k, (n_bytes + 7) // 8).view(np.uint8)[:n_bytes]
+        buf = to_dev(a)
+        out = torch.zeros(k, dtype=torch.int64, device="cuda")
+        g = pp.CountGraph(buf, out, k)
+        for _ in range(3):
+            g.replay()
+            torch.cuda.synchronize()
+            assert (out.cpu().numpy().astype(np.uint64) == orc.naive(a, k)).all()
+        buf.copy_(torch.from_numpy(b.copy()).cuda())
+        g.replay()
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy().astype(np.uint64) == orc.naive(b, k)).all()
+        g.close()

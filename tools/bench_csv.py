@@ -5,7 +5,8 @@ The reference's bench::sweep / write_csv (proj/core/src/bench.cpp:132-173,
 header proj/core/include/pospop/bench.hpp:74-75) emit
     kernel,len_words,reps,wall_ns,gbps,cycles_per_word,instructions_per_word,stderr_pct
 This tool emits the same columns for the GPU path -- `gpu_device` (device-
-resident, CUDA-event time of the kernel) and `gpu_host` (the synchronous
+resident, CUDA-event time of one async launch), `gpu_graph` (the same count
+replayed from a CUDA graph) and `gpu_host` (the synchronous
 C-ABI call on a pinned host buffer, wall time incl. H2D + D2H) -- extended
 with gpus,dev_ns,bytes,pct_hbm_peak,words_per_s.  Like the reference, every
 cell is gated on correctness first (bench.cpp:64-68: a mismatch produces an
@@ -74,7 +75,8 @@ def main():
         pinned.numpy().view(np.uint16)[:] = host
         dev = pinned.cuda()
         out = torch.zeros(16, dtype=torch.int64, device="cuda")
-        for kernel in ("gpu_device", "gpu_host"):
+        graph = pp.CountGraph(dev, out, 16)
+        for kernel in ("gpu_device", "gpu_graph", "gpu_host"):
             try:
                 if kernel == "gpu_device":
                     pp.count_async(dev, out, 16, stream=s)
@@ -86,6 +88,19 @@ def main():
                         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         a.record(s)
                         pp.count_async(dev, out, 16, stream=s)
+                        b.record(s)
+                        b.synchronize()
+                        times.append(a.elapsed_time(b) * 1e6)
+                elif kernel == "gpu_graph":  # CUDA-graph replay (latency path)
+                    graph.replay(s)
+                    torch.cuda.synchronize()
+                    if not (out.cpu().numpy().astype(np.uint64) == expected).all():
+                        raise RuntimeError("correctness gate: gpu_graph disagrees with the oracle")
+                    times = []
+                    for _ in range(args.reps):
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record(s)
+                        graph.replay(s)
                         b.record(s)
                         b.synchronize()
                         times.append(a.elapsed_time(b) * 1e6)
