@@ -1000,8 +1000,8 @@ struct SegVariant {
     SegKernel fn;
 };
 
-template <int NBANK, int L, int VB>
-__global__ void __launch_bounds__(256) segmented_pipe_entry(const uint8_t* data, const unsigned long long* offsets,
+template <int NBANK, int L, int VB, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) segmented_pipe_entry(const uint8_t* data, const unsigned long long* offsets,
                                                             unsigned long long n, int k, uint32_t thr,
                                                             unsigned long long* out, unsigned long long*,
                                                             unsigned int*, unsigned) {
@@ -1010,12 +1010,15 @@ __global__ void __launch_bounds__(256) segmented_pipe_entry(const uint8_t* data,
 
 #define SG(NB, L, VB, S) {NB, L, VB, S, segmented_kernel<NB, L, VB, S>}
 #define SGP(NB, L, VB) {NB, L, VB, 2, segmented_pipe_entry<NB, L, VB>}
+#define SGP2(NB, L, VB) {NB, L, VB, 3, segmented_pipe_entry<NB, L, VB, 2>}  // sched 3: pipelined, 2 CTAs/SM
 const SegVariant kSegVariants[] = {
     SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
     SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
     SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
     SGP(1, 5, 16), SGP(1, 4, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
+    SGP2(2, 4, 16), SGP2(2, 3, 32), SGP2(2, 3, 16), SGP2(1, 5, 16), SGP2(1, 5, 32),
 };
+#undef SGP2
 #undef SG
 #undef SGP
 
