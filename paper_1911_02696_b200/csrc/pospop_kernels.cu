@@ -449,6 +449,8 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
 // SCHED 0: warp w takes arrays w, w + nwarps, ... (strided, no atomics).
 // SCHED 1: warps pull runs of `per_grab` consecutive arrays from a global
 // counter (prefetched one run ahead).
+// (SCHED 2 / 3: segmented_pipe_entry below, software-pipelined; 3 = bounded
+// to 2 CTAs/SM, which keeps it at <= 128 registers.)
 template <int NBANK, int L, int VB, int SCHED>
 __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
                                                         const unsigned long long* offsets,
@@ -1139,11 +1141,12 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (n == 0) return cudaSuccess;
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched".
-    int depth = 5, vb = 16, sched = nbank == 1 ? 2 : 1;  // measured: pipelined (k <= 32), dynamic (k = 64)
+    // measured: pipelined with 2 CTAs/SM (k <= 32), dynamic claiming (k = 64)
+    int depth = 5, vb = 16, sched = nbank == 1 ? 3 : 1;
     if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d", &depth, &vb, &sched);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb, sched);
-    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 2 : 1);
+    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 3 : 1);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {

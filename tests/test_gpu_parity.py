@@ -358,10 +358,10 @@ def test_reference_verify_kernels_with_gpu_runner():
 
 
 SEG_VARIANTS = {
-    8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2"],
-    16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2"],
-    32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2"],
-    64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2"],
+    8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"],
+    16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"],
+    32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"],
+    64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3"],
 }
 
 
