@@ -121,3 +121,23 @@ def test_cli_usage_errors_without_gpu(tmp_path):
     r = subprocess.run([sys.executable, "-m", "paper_1911_02696_b200", "count", "--input", str(tmp_path / "nope")],
                        cwd=ROOT, capture_output=True, text=True)
     assert r.returncode == 2 and "error" in r.stderr
+
+
+def build_c_smoke(pp, tmp_path):
+    exe = tmp_path / "abi_c_smoke"
+    libdir = os.path.dirname(pp.library_path())
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-pedantic",
+                           "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "c", "abi_c_smoke.c"),
+                           "-L", libdir, "-lpospopcnt_b200", f"-Wl,-rpath,{libdir}", "-o", str(exe)])
+    return exe
+
+
+def test_header_is_plain_c_and_fails_loudly_without_gpu(pp, tmp_path):
+    """include/pospopcnt_b200.h compiles as strict C11; without a GPU the library
+    answers POSPOP_EUNAVAILABLE (exit 2) instead of counting on the CPU."""
+    exe = build_c_smoke(pp, tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    if pp.device_available():
+        assert r.returncode == 0, r.stdout
+    else:
+        assert r.returncode == 2, (r.returncode, r.stdout)

@@ -91,3 +91,11 @@ def test_flagstats_cli(orc, tmp_path, golden):
     fields = ["total", "secondary", "supplementary", "n_pair_good", "n_read1", "n_read2", "n_sgltn", "pair_map",
               "mapped", "dup"]
     assert [out["pass"][f] for f in fields] + [out["fail"][f] for f in fields] == golden["flagstats_acceptance"][0]
+
+
+def test_plain_c_caller_counts_on_gpu(pp, tmp_path):
+    """A strict-C11 caller of include/pospopcnt_b200.h (tests/c/abi_c_smoke.c)."""
+    from test_abi import build_c_smoke
+    exe = build_c_smoke(pp, tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, (r.returncode, r.stdout)
