@@ -60,7 +60,7 @@ cudaError_t launch_generate(int kind, uint64_t seed, uint64_t index_base, size_t
 cudaError_t launch_digest(const void* data, size_t nbytes, unsigned long long* d_digest,
                           cudaStream_t stream);
 
-// Device micro-op harness (see microop_kernel in pospop_kernels.cu).
+// Device micro-op harness (see microop_kernel in pospop_aux.cuh).
 cudaError_t launch_microop(int op, int depth, const uint32_t* d_in, size_t n, uint32_t* d_out, cudaStream_t stream);
 
 // Number of kernels launched by this library in this process.

@@ -1,0 +1,345 @@
+// pospop_segmented.cuh -- the segmented / batched kernels (one k-row per array): strided,
+// dynamically claimed and software-pipelined schedules.
+// Device code only; included by pospop_kernels.cu (the single CUDA translation
+// unit, which instantiates the kernels and owns the host-side launchers).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pospop_device.cuh"
+#include "pospop_stream.cuh"
+
+namespace pospop_b200 {
+namespace dev {
+
+// One warp per array.  Array a spans bytes [data + off[a]*wb, data + off[a+1]*wb);
+// it is read as VB-byte vectors from the VB-aligned address at or below its
+// start, the first/last vector byte-masked, 32 lanes x VPT vectors per step.
+// Warps pull array indices from a global counter (prefetched one array
+// ahead), so arrays of any length mix balance across warps and SMs; the last
+// CTA re-zeroes the counter and ticket for the next launch.
+// SCHED 0: warp w takes arrays w, w + nwarps, ... (strided, no atomics).
+// SCHED 1: warps pull runs of `per_grab` consecutive arrays from a global
+// counter (prefetched one run ahead).
+// (SCHED 2 / 3: segmented_pipe_entry below, software-pipelined; 3 = bounded
+// to 2 CTAs/SM, which keeps it at <= 128 registers.)
+template <int NBANK, int L, int VB, int SCHED>
+__global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
+                                                        const unsigned long long* offsets,
+                                                        unsigned long long n_arrays, int k,
+                                                        uint32_t flush_threshold,
+                                                        unsigned long long* out,
+                                                        unsigned long long* next,
+                                                        unsigned int* ticket, unsigned per_grab) {
+    constexpr int REGS = NBANK << L;
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr unsigned long long STEP = 32ull * VPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const int wb = k >> 3;
+    __shared__ int s_last;
+
+    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    unsigned long long mine = 0, run = 0, arr = warp, stop = n_arrays;
+    if (SCHED == 1) {
+        mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+        run = __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+        arr = run * per_grab;
+        stop = arr + per_grab < n_arrays ? arr + per_grab : n_arrays;
+    }
+    for (;;) {
+        if (arr >= stop) {
+            if (SCHED == 0) break;
+            run = __shfl_sync(0xFFFFFFFFu, mine, 0);
+            mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+            arr = run * per_grab;
+            if (arr >= n_arrays) break;
+            stop = arr + per_grab < n_arrays ? arr + per_grab : n_arrays;
+        }
+        const uintptr_t P = (uintptr_t)(data + offsets[arr] * wb);
+        const uintptr_t Q = (uintptr_t)(data + offsets[arr + 1] * wb);
+        const uintptr_t B = P & ~(uintptr_t)(VB - 1);
+        const unsigned long long nv = Q > P ? (Q - B + VB - 1) / VB : 0;
+        const int lo = (int)(P - B);
+        const int hi = nv ? (int)(Q - (B + (nv - 1) * VB)) : VB;
+        const uint8_t* base = (const uint8_t*)B;
+        const unsigned long long f0 = lo ? 1 : 0;                    // fully valid vectors [f0, f1)
+        const unsigned long long f1 = nv - (nv && hi != VB ? 1 : 0);
+
+        uint32_t carries[NBANK][L];
+        uint32_t counter[NBANK][16];
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+            for (int j = 0; j < L; ++j) carries[b][j] = 0;
+        zero_bank<NBANK>(counter);
+        uint32_t nb = 0;
+        unsigned long long tot[NBANK];
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+
+        for (unsigned long long t = 0; t < nv; t += STEP) {
+            uint32_t r[REGS];
+            if (t >= f0 && t + STEP <= f1) {  // interior: unpredicated, unmasked
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) {
+                    uint32_t x[RPV];
+                    ldg_stream<VB, 0>(base + (t + 32ull * v + lane) * VB, x);
+#pragma unroll
+                    for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) {
+                    const unsigned long long idx = t + 32ull * v + lane;
+                    uint32_t x[RPV];
+#pragma unroll
+                    for (int j = 0; j < RPV; ++j) x[j] = 0;
+                    if (idx < nv) {
+                        ldg_stream<VB, 0>(base + idx * VB, x);
+                        if (idx == 0 || idx + 1 == nv) mask_bytes<VB>(x, idx == 0 ? lo : 0, idx + 1 == nv ? hi : VB);
+                    }
+#pragma unroll
+                    for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+                }
+            }
+            tree_block<NBANK, L>(r, carries, counter);
+            if (++nb == flush_threshold) {  // warp-uniform: nv is per array
+                uint32_t d[16];
+#pragma unroll
+                for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b) tot[b] += bank_warp_total(counter[b], L, d);
+                zero_bank<NBANK>(counter);
+                nb = 0;
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b) {
+            uint32_t d[16];
+            drain<L>(d, carries[b]);
+            tot[b] += bank_warp_total(counter[b], L, d);
+        }
+
+        // lane c holds channel c (bank b: channel 32b + c).  Fold to positions.
+        unsigned long long* row = out + arr * (unsigned long long)k;
+        if (NBANK == 2) {  // k == 64: lane c -> positions c and 32 + c
+            row[lane] = tot[0];
+            row[32 + lane] = tot[NBANK - 1];
+        } else {
+            unsigned long long t = tot[0];
+            for (int w = 16; w >= k; w >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, w);
+            if ((int)lane < k) row[lane] = t;
+        }
+        arr += SCHED == 0 ? nwarps : 1;
+    }
+    if (SCHED == 0) return;
+    // Every warp has drawn an index >= n_arrays; once all CTAs are past that
+    // point the counter can be reset.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (s_last) {
+            *next = 0ull;
+            *ticket = 0u;
+        }
+    }
+}
+
+// Segmented, software-pipelined (SCHED 2): warp w owns arrays w, w + nwarps,
+// ... and walks the concatenation of their steps (32 lanes x VPT vectors) with
+// a one-step register double buffer: the loads of step s+1 -- possibly the
+// first step of the warp's next array, whose offsets were fetched one array
+// ahead -- are issued before step s is consumed and before an array's
+// epilogue (drain + transpose-reduce + row store), so the memory pipe never
+// drains at array boundaries.
+struct SegView {
+    const uint8_t* base;     // VB-aligned start
+    unsigned long long nv;   // vectors
+    unsigned long long f0, f1;
+    int lo, hi;
+};
+
+template <int VB>
+__device__ __forceinline__ SegView seg_view(const uint8_t* data, unsigned long long w0, unsigned long long w1, int wb) {
+    SegView v;
+    const uintptr_t P = (uintptr_t)(data + w0 * wb);
+    const uintptr_t Q = (uintptr_t)(data + w1 * wb);
+    const uintptr_t B = P & ~(uintptr_t)(VB - 1);
+    v.base = (const uint8_t*)B;
+    v.nv = Q > P ? (Q - B + VB - 1) / VB : 0;
+    v.lo = (int)(P - B);
+    v.hi = v.nv ? (int)(Q - (B + (v.nv - 1) * VB)) : VB;
+    v.f0 = v.lo ? 1 : 0;
+    v.f1 = v.nv - (v.nv && v.hi != VB ? 1 : 0);
+    return v;
+}
+
+template <int VB, int VPT>
+__device__ __forceinline__ void seg_load(const SegView& v, unsigned long long t, uint32_t lane,
+                                         uint32_t (&r)[VPT * (VB / 4)]) {
+    constexpr int RPV = VB / 4;
+    constexpr unsigned long long STEP = 32ull * VPT;
+    if (t >= v.f0 && t + STEP <= v.f1) {
+#pragma unroll
+        for (int q = 0; q < VPT; ++q) {
+            uint32_t x[RPV];
+            ldg_stream<VB, 0>(v.base + (t + 32ull * q + lane) * VB, x);
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < VPT; ++q) {
+            const unsigned long long idx = t + 32ull * q + lane;
+            uint32_t x[RPV];
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) x[j] = 0;
+            if (idx < v.nv) {
+                ldg_stream<VB, 0>(v.base + idx * VB, x);
+                if (idx == 0 || idx + 1 == v.nv) mask_bytes<VB>(x, idx == 0 ? v.lo : 0, idx + 1 == v.nv ? v.hi : VB);
+            }
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+        }
+    }
+}
+
+template <int NBANK>
+__device__ __forceinline__ void seg_store_row(unsigned long long* out, unsigned long long arr, int k, uint32_t lane,
+                                              const unsigned long long (&tot)[NBANK]) {
+    unsigned long long* row = out + arr * (unsigned long long)k;
+    if (NBANK == 2) {
+        row[lane] = tot[0];
+        row[32 + lane] = tot[NBANK - 1];
+    } else {
+        unsigned long long t = tot[0];
+        for (int w = 16; w >= k; w >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, w);
+        if ((int)lane < k) row[lane] = t;
+    }
+}
+
+template <int NBANK, int L, int VB>
+__device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const unsigned long long* offsets,
+                                                    unsigned long long n_arrays, int k, uint32_t flush_threshold,
+                                                    unsigned long long* out) {
+    constexpr int REGS = NBANK << L;
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr unsigned long long STEP = 32ull * VPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const int wb = k >> 3;
+
+    // Current array: skip (and zero) empty arrays.
+    unsigned long long arr = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    SegView cur;
+    for (;; arr += nwarps) {
+        if (arr >= n_arrays) return;
+        cur = seg_view<VB>(data, offsets[arr], offsets[arr + 1], wb);
+        if (cur.nv) break;
+        unsigned long long z[NBANK];
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b) z[b] = 0;
+        seg_store_row<NBANK>(out, arr, k, lane, z);
+    }
+    // Offsets of the warp's next array, fetched one array ahead.
+    unsigned long long nxt_w0 = 0, nxt_w1 = 0;
+    if (arr + nwarps < n_arrays) {
+        nxt_w0 = offsets[arr + nwarps];
+        nxt_w1 = offsets[arr + nwarps + 1];
+    }
+
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    uint32_t nb = 0;
+    unsigned long long tot[NBANK];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+
+    unsigned long long t = 0;
+    uint32_t rc[REGS];
+    seg_load<VB, VPT>(cur, t, lane, rc);
+    for (;;) {
+        // Where the next step is: later in this array, or the next non-empty array.
+        unsigned long long t_n = t + STEP, arr_n = arr;
+        SegView nxt = cur;
+        bool have_next = true;
+        if (t_n >= cur.nv) {
+            t_n = 0;
+            arr_n = arr + nwarps;
+            have_next = false;
+            while (arr_n < n_arrays) {
+                nxt = seg_view<VB>(data, nxt_w0, nxt_w1, wb);
+                if (arr_n + nwarps < n_arrays) {  // prefetch the offsets after that
+                    nxt_w0 = offsets[arr_n + nwarps];
+                    nxt_w1 = offsets[arr_n + nwarps + 1];
+                }
+                if (nxt.nv) {
+                    have_next = true;
+                    break;
+                }
+                unsigned long long z[NBANK];
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b) z[b] = 0;
+                seg_store_row<NBANK>(out, arr_n, k, lane, z);
+                arr_n += nwarps;
+            }
+        }
+        uint32_t rn[REGS];
+        if (have_next) seg_load<VB, VPT>(nxt, t_n, lane, rn);
+
+        tree_block<NBANK, L>(rc, carries, counter);
+        if (++nb == flush_threshold) {
+            uint32_t d[16];
+#pragma unroll
+            for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) tot[b] += bank_warp_total(counter[b], L, d);
+            zero_bank<NBANK>(counter);
+            nb = 0;
+        }
+        if (t + STEP >= cur.nv) {  // last step of this array: epilogue while rn is in flight
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) {
+                uint32_t d[16];
+                drain<L>(d, carries[b]);
+                tot[b] += bank_warp_total(counter[b], L, d);
+#pragma unroll
+                for (int j = 0; j < L; ++j) carries[b][j] = 0;
+            }
+            zero_bank<NBANK>(counter);
+            nb = 0;
+            seg_store_row<NBANK>(out, arr, k, lane, tot);
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+        }
+        if (!have_next) break;
+#pragma unroll
+        for (int i = 0; i < REGS; ++i) rc[i] = rn[i];
+        cur = nxt;
+        arr = arr_n;
+        t = t_n;
+    }
+}
+
+template <int NBANK, int L, int VB, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) segmented_pipe_entry(const uint8_t* data, const unsigned long long* offsets,
+                                                            unsigned long long n, int k, uint32_t thr,
+                                                            unsigned long long* out, unsigned long long*,
+                                                            unsigned int*, unsigned) {
+    segmented_pipe_body<NBANK, L, VB>(data, offsets, n, k, thr, out);
+}
+
+}  // namespace dev
+}  // namespace pospop_b200

@@ -1,0 +1,419 @@
+// pospop_stream.cuh -- the stream kernel family (k = 8/16/32/64 counts and the fused FLAG-statistics
+// mode): vector addressing, tree blocks, work distribution, CTA epilogue.
+// Device code only; included by pospop_kernels.cu (the single CUDA translation
+// unit, which instantiates the kernels and owns the host-side launchers).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pospop_device.cuh"
+
+namespace pospop_b200 {
+namespace dev {
+
+// The stream is addressed in VB-byte vectors from `base`, the largest
+// 32*VB-aligned address <= data.  Vectors [v0, v1) hold the data; the first
+// and last are byte-masked to [lo_byte, VB) and [0, hi_byte), so unaligned
+// starts and ragged ends need no scalar code, and every warp load (32
+// consecutive vectors) stays 32*VB-aligned.  Vector indices below v0 are
+// never dereferenced.  Work is split over CTAs in whole groups of 32 vectors.
+struct StreamArgs {
+    const uint8_t* base;
+    unsigned long long v0, v1;  // valid vectors
+    unsigned long long f0, f1;  // fully valid (unmasked) vectors [f0, f1)
+    unsigned long long g0, ng;  // first group, number of groups
+    int lo_byte, hi_byte;       // valid bytes of vector v0 / vector v1-1
+    int k;
+    uint32_t flush_threshold;
+    unsigned long long* acc;
+    unsigned int* ticket;
+    unsigned long long* out;
+    int accumulate;
+    unsigned long long* trace;  // diagnostics: per CTA {t_start, t_loop_end, t_flushed, t_done, smid} or null
+    // dynamic schedule (SCHED 1): warp tiles, chunk counter, chunk sizes
+    unsigned long long* next;   // global chunk counter (zero on entry, re-zeroed by the last CTA)
+    unsigned long long nwt, nA, CA, CB;
+    unsigned long long pool;    // SCHED 2: warp tiles in the global tail pool
+    // MODE 1 (FLAG statistics)
+    unsigned long long data_off;  // data start - base, bytes
+    unsigned long long word_base; // global index of the first word (host-staged chunks)
+    unsigned long long* bad;      // max of ~(index of an invalid FLAG word); 0 = none
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+// Programmatic dependent launch (sm_90+): `pdl_allow_next` lets the next
+// kernel in the stream start launching (its CTAs take SMs as ours retire);
+// `pdl_wait_prev` blocks until the previous kernel in the stream has completed
+// and its writes are visible.  Both are no-ops for launches without the
+// programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_allow_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_prev() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Channel -> position fold: the channels (of 32 * NBANK) that count position
+// p are p + m * k for m = 0 .. 32/k - 1 (k <= 32), or channel p (k = 64).
+__device__ __forceinline__ int channels_per_position(int k) { return k >= 32 ? 1 : 32 / k; }
+
+template <int NBANK, int L>
+__device__ __forceinline__ void tree_block(const uint32_t (&r)[NBANK << L], uint32_t (&carries)[NBANK][L],
+                                           uint32_t (&counter)[NBANK][16]) {
+    if constexpr (NBANK == 1) {
+        extract(counter[0], Tree<L, 1>::run(carries[0], r));
+    } else {
+        extract(counter[0], Tree<L, 2>::run(carries[0], r));
+        extract(counter[1], Tree<L, 2>::run(carries[1], r + 1));
+    }
+}
+
+template <int NBANK>
+__device__ __forceinline__ void zero_bank(uint32_t (&counter)[NBANK][16]) {
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int p = 0; p < 16; ++p) counter[b][p] = 0;
+}
+
+// Loads one tree block for this thread: VPT vectors at first + v * stride.
+// `fast`: the whole tile lies in the fully valid range (no predicates, no
+// masks, immediate offsets when stride is a compile-time constant).
+template <int VB, int HINT, int VPT>
+__device__ __forceinline__ void load_tree_block(const StreamArgs& a, unsigned long long first, unsigned stride,
+                                                bool fast, uint32_t (&r)[VPT * (VB / 4)]) {
+    constexpr int RPV = VB / 4;
+    if (fast) {
+        const uint8_t* p = a.base + first * VB;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            uint32_t x[RPV];
+            ldg_stream<VB, HINT>(p + (unsigned long long)v * stride * VB, x);
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            const unsigned long long idx = first + (unsigned long long)v * stride;
+            uint32_t x[RPV];
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) x[j] = 0;
+            if (idx >= a.v0 && idx < a.v1) {
+                ldg_stream<VB, HINT>(a.base + idx * VB, x);
+                if (idx == a.v0 || idx + 1 == a.v1)
+                    mask_bytes<VB>(x, idx == a.v0 ? a.lo_byte : 0, idx + 1 == a.v1 ? a.hi_byte : VB);
+            }
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
+        }
+    }
+}
+
+// Lane-bank flush (weight 2^L) into the CTA's shared channel totals; must be
+// called by all 32 lanes of a warp together.
+template <int NBANK, int L>
+__device__ __forceinline__ void flush_bank_to_smem(uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
+                                                   uint32_t lane) {
+    uint32_t d[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
+    }
+    zero_bank<NBANK>(counter);
+}
+
+// CTA epilogue: final flush fused with the carry drain, CTA channel totals to
+// the global accumulator, ticket; the last CTA folds channels to positions,
+// writes/accumulates out[k] and leaves the scratch (acc, ticket, chunk
+// counter) zeroed for the next launch.
+template <int NBANK, int L, int MODE>
+__device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carries)[NBANK][L],
+                                           uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
+                                           int* s_last, unsigned block, uint32_t lane) {
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer();
+    pdl_wait_prev();  // the previous launch on this stream owns acc/ticket/next until it completes
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        uint32_t d[16];
+        drain<L>(d, carries[b]);
+        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < 32 * NBANK; c += block)
+        if (s_acc[c]) atomicAdd(&a.acc[c], s_acc[c]);
+    __threadfence();
+    __syncthreads();
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = globaltimer();
+    if (threadIdx.x == 0) *s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!*s_last) return;
+
+    // Last CTA: every other CTA has fenced its channel atomics.
+    __threadfence();
+    if constexpr (MODE == 1) {  // two banks of k = 16: out[16 b + p] = acc[32 b + p] + acc[32 b + p + 16]
+        for (int pos = threadIdx.x; pos < 32; pos += block) {
+            const int b = pos >> 4, p = pos & 15;
+            const unsigned long long sum =
+                atomicExch(&a.acc[32 * b + p], 0ull) + atomicExch(&a.acc[32 * b + p + 16], 0ull);
+            a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+        }
+        if (threadIdx.x == 0) {  // ~index: the larger code is the earlier word
+            const unsigned long long code = atomicExch(a.bad, 0ull);
+            a.out[32] = a.accumulate && a.out[32] > code ? a.out[32] : code;
+        }
+    } else {
+        const int k = a.k;
+        for (int pos = threadIdx.x; pos < k; pos += block) {
+            unsigned long long sum = 0;
+            if (k == 64) {
+                sum = atomicExch(&a.acc[pos], 0ull);
+            } else {
+                const int m = channels_per_position(k);
+                for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
+            }
+            a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+        }
+    }
+    if (threadIdx.x == 0) {
+        *a.ticket = 0u;
+        if (a.next) *a.next = 0ull;
+    }
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 3] = globaltimer();
+}
+
+// ---------------------------------------------------------------------------
+// FLAG statistics (reference proj/core/src/flagstats.cpp).
+// SWAR form of flag_transform (flagstats.cpp:94-125) on a register holding two
+// SAM FLAG words.  Only the positions bucket_from_counts reads (1,2,3,6,7,8,
+// 9,10,11,12; flagstats.cpp:39-63) are produced.  Per 16-bit lane:
+//   G  = paired & !secondary & !supplementary ;  GU = G & !unmapped
+//   bits 1,3 = w & GU ; bits 6,7 = w & G ; bits 2,8,9,10 = w ;
+//   bit 11 = supplementary & !secondary ; bit 12 (pair_map) = GU & !mate_unmapped
+// `all` is that word for every read; `fail` keeps it only for QC-fail reads.
+// The QC-pass plane is never formed: pass counts = all counts - fail counts
+// (exact integers, derived on the host).  The kernel is ALU-bound, so the
+// shifts run on the FMA pipe (IMAD.HI / IMAD.SHL) and the G/GU selections are
+// built by multiplying the lane predicate into the target bit positions
+// (g * 0x00C0 + gu * 0x100A) instead of full lane masks.
+// ---------------------------------------------------------------------------
+template <int S>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x) { return __umulhi(x, 1u << (32 - S)); }
+template <int S>
+__device__ __forceinline__ uint32_t shl_fma(uint32_t x) { return x * (1u << S); }
+
+__device__ __forceinline__ void flag_transform2(uint32_t w, uint32_t& all, uint32_t& fail) {
+    constexpr uint32_t L1 = 0x00010001u;
+    const uint32_t g0 = w & ~shr_fma<8>(w) & ~shr_fma<11>(w);  // bit 0 / 16: paired & primary
+    const uint32_t g = g0 & L1;
+    const uint32_t gu = g0 & ~shr_fma<2>(w) & L1;
+    const uint32_t t = g * 0x00C0u + gu * 0x100Au;              // bits 6,7 <- G ; bits 1,3,12 <- GU
+    const uint32_t mf = (shr_fma<9>(w) & L1) * 0xFFFFu;           // QC-fail lane mask
+    all = (w & (t | 0x07040704u)) | (t & ~shl_fma<9>(w) & 0x10001000u) | (w & ~shl_fma<3>(w) & 0x08000800u);
+    fail = all & mf;
+}
+
+// Tree-block consumer.  MODE 0: positional counts of the words (NBANK banks).
+// MODE 1: FLAG statistics -- transform, then bank 0 counts the transformed
+// words of all reads and bank 1 those of QC-fail reads; words with reserved bits 12-15 set are
+// reported through a.bad (the first such index wins, as the reference's
+// check_reserved throws at the first one, flagstats.cpp:34-36).
+template <int MODE, int NBANK, int L, int VB, int REGS>
+__device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)[REGS], unsigned long long first,
+                                        unsigned stride, uint32_t (&carries)[NBANK][L],
+                                        uint32_t (&counter)[NBANK][16]) {
+    if constexpr (MODE == 0) {
+        tree_block<NBANK, L>(r, carries, counter);
+    } else {
+        static_assert(NBANK == 2 && REGS == (1 << L), "FLAG mode: two banks of 2^L registers");
+        constexpr int RPV = VB / 4;
+        uint32_t all[REGS], fail[REGS];
+        uint32_t bad = 0;
+#pragma unroll
+        for (int i = 0; i < REGS; ++i) {
+            bad |= r[i];
+            flag_transform2(r[i], all[i], fail[i]);
+        }
+        extract(counter[0], Tree<L, 1>::run(carries[0], all));
+        extract(counter[1], Tree<L, 1>::run(carries[1], fail));
+        if (bad & 0xF000F000u) {  // rare: locate this thread's first invalid word
+            // Fully unrolled: a runtime index into r[] would force the whole
+            // tile through local memory on the hot path.
+            unsigned long long best = ~0ull;
+#pragma unroll
+            for (int i = 0; i < REGS; ++i)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if ((r[i] >> (16 * h)) & 0xF000u) {
+                        const unsigned long long byte =
+                            (first + (unsigned long long)(i / RPV) * stride) * VB + 4 * (i % RPV) + 2 * h;
+                        const unsigned long long word = ((byte - a.data_off) >> 1) + a.word_base;
+                        best = word < best ? word : best;
+                    }
+            atomicMax(a.bad, ~best);
+        }
+    }
+}
+
+// SCHED 0 (static): CTA b owns a contiguous range of whole 32-vector groups and
+// walks it in CTA tiles of BLOCK x VPT vectors.
+// SCHED 1 (dynamic): warps pull chunks of warp tiles (32 lanes x VPT vectors,
+// VPT 1 KiB-aligned warp loads) from a global counter, large chunks first
+// (nA chunks of CA warp tiles) then small ones (CB) so no warp or CTA idles
+// while another still holds a big share; the next chunk index is fetched one
+// chunk ahead so the atomic's latency hides behind the loads.
+// BLOCK > 0: compile-time block size; BLOCK == 0: runtime blockDim.x.
+template <int NBANK, int L, int VB, int HINT, int BLOCK, int SCHED, int MODE, int MINB = 1>
+__global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(const StreamArgs a) {
+    constexpr int REGS = MODE == 1 ? (1 << L) : (NBANK << L);  // 32-bit input registers per tree block
+    constexpr int RPV = VB / 4;       // registers per vector
+    constexpr int VPT = REGS / RPV;   // vectors per thread per tree block
+    static_assert(VPT >= 1, "tree must consume at least one vector");
+    const unsigned block = BLOCK > 0 ? (unsigned)BLOCK : blockDim.x;
+
+    __shared__ unsigned long long s_acc[32 * NBANK];
+    __shared__ int s_last;
+    if (a.trace && threadIdx.x == 0) {
+        a.trace[blockIdx.x * 5 + 0] = globaltimer();
+        a.trace[blockIdx.x * 5 + 4] = smid();
+    }
+    for (int i = threadIdx.x; i < 32 * NBANK; i += block) s_acc[i] = 0;
+    pdl_allow_next();
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    uint32_t nb = 0;
+
+    if constexpr (SCHED == 0) {
+        const unsigned long long tile = (unsigned long long)VPT * block;
+        const unsigned long long gb = a.g0 + a.ng * blockIdx.x / gridDim.x;
+        const unsigned long long ge = a.g0 + a.ng * (blockIdx.x + 1) / gridDim.x;
+        const unsigned long long E = ge * 32 < a.v1 ? ge * 32 : a.v1;
+        const unsigned long long F = E < a.f1 ? E : a.f1;
+        for (unsigned long long t = gb * 32; t < E; t += tile) {
+            uint32_t r[REGS];
+            const bool fast = t >= a.f0 && t + tile <= F;
+            if (fast) load_tree_block<VB, HINT, VPT>(a, t + threadIdx.x, block, true, r);
+            else {
+                // Edge tile of this CTA: loads past E belong to the next CTA.
+                load_tree_block<VB, HINT, VPT>(a, t + threadIdx.x, block, false, r);
+#pragma unroll
+                for (int v = 0; v < VPT; ++v)
+                    if (t + (unsigned long long)v * block + threadIdx.x >= E)
+#pragma unroll
+                        for (int j = 0; j < RPV; ++j) r[v * RPV + j] = 0;
+            }
+            consume<MODE, NBANK, L, VB>(a, r, t + threadIdx.x, block, carries, counter);
+            if (++nb == a.flush_threshold) {  // block-uniform: every thread runs the same tiles
+                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                nb = 0;
+            }
+        }
+    } else if constexpr (SCHED == 2) {
+        // Warp tiles [0, P) are split statically into contiguous CTA ranges
+        // (DRAM locality); inside a CTA, warps claim warp tiles from a shared
+        // counter, so no warp idles while another still holds a share.  Warp
+        // tiles [P, nwt) form a global pool handed out in chunks of CB, so
+        // CTAs on faster SMs absorb the tail.
+        constexpr unsigned long long WT = 32ull * VPT;
+        const unsigned long long S0 = a.g0 * 32;
+        const unsigned long long P = a.nwt - a.pool;
+        const unsigned long long lo = P * blockIdx.x / gridDim.x;
+        const unsigned long long hi = P * (blockIdx.x + 1) / gridDim.x;
+        __shared__ unsigned s_claim;
+        if (threadIdx.x == 0) s_claim = 0u;
+        __syncthreads();
+        unsigned mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
+        unsigned long long w = lo + __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;  // prefetch
+        while (w < hi) {
+            const unsigned long long t = S0 + w * WT;
+            uint32_t r[REGS];
+            load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
+            consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
+            if (++nb == a.flush_threshold) {  // warp-uniform
+                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                nb = 0;
+            }
+            w = lo + __shfl_sync(0xFFFFFFFFu, mine, 0);
+            mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
+        }
+        if (a.pool) {
+            pdl_wait_prev();  // the pool counter is shared with the previous launch
+            unsigned long long m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            unsigned long long c = __shfl_sync(0xFFFFFFFFu, m, 0);
+            m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            for (;;) {
+                const unsigned long long w0 = P + c * a.CB;
+                if (w0 >= a.nwt) break;  // warp-uniform
+                const unsigned long long w1 = w0 + a.CB < a.nwt ? w0 + a.CB : a.nwt;
+                for (unsigned long long ww = w0; ww < w1; ++ww) {
+                    const unsigned long long t = S0 + ww * WT;
+                    uint32_t r[REGS];
+                    load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
+                    consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
+                    if (++nb == a.flush_threshold) {
+                        flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                        nb = 0;
+                    }
+                }
+                c = __shfl_sync(0xFFFFFFFFu, m, 0);
+                m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            }
+        }
+    } else {
+        constexpr unsigned long long WT = 32ull * VPT;  // vectors per warp tile
+        const unsigned long long S0 = a.g0 * 32;
+        pdl_wait_prev();
+        unsigned long long mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+        unsigned long long c = __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;  // prefetch: consumed one chunk later
+        for (;;) {
+            unsigned long long w0, w1;
+            if (c < a.nA) {
+                w0 = c * a.CA;
+                w1 = w0 + a.CA;
+            } else {
+                w0 = a.nA * a.CA + (c - a.nA) * a.CB;
+                w1 = w0 + a.CB < a.nwt ? w0 + a.CB : a.nwt;
+            }
+            if (w0 >= a.nwt) break;  // warp-uniform
+            for (unsigned long long w = w0; w < w1; ++w) {
+                const unsigned long long t = S0 + w * WT;
+                uint32_t r[REGS];
+                load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
+                consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
+                if (++nb == a.flush_threshold) {  // warp-uniform
+                    flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                    nb = 0;
+                }
+            }
+            c = __shfl_sync(0xFFFFFFFFu, mine, 0);
+            mine = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+        }
+    }
+    cta_finish<NBANK, L, MODE>(a, carries, counter, s_acc, &s_last, block, lane);
+}
+
+}  // namespace dev
+}  // namespace pospop_b200

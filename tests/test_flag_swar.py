@@ -1,5 +1,5 @@
 """The SWAR FLAG transform used by the fused FLAG-statistics kernel
-(flag_transform2 in paper_1911_02696_b200/csrc/pospop_kernels.cu), emulated
+(flag_transform2 in paper_1911_02696_b200/csrc/pospop_stream.cuh), emulated
 op for op in numpy and checked against the oracle's restatement of the
 reference's flag_transform (proj/core/src/flagstats.cpp:94-125) on ALL
 4096 x 4096 pairs of valid FLAG words packed in one 32-bit register.
