@@ -112,6 +112,7 @@ const StreamVariant kStreamVariants[] = {
     SVF(6, 32, 256, 2),
     SVF(5, 32, 256, 2), SVF(6, 16, 256, 2), SVF(7, 32, 256, 2),
     SVF2(5, 32, 256, 2), SVF2(5, 16, 256, 2), SVF2(4, 32, 256, 2), SVF(4, 32, 512, 2), SVF(5, 16, 512, 2),
+    SVF(6, 32, 512, 2), SVF2(6, 32, 256, 2), SVF(4, 32, 1024, 2), SVF(5, 32, 1024, 2),
 };
 #undef SV
 #undef SVF

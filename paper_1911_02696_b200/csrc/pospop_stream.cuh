@@ -226,6 +226,40 @@ __device__ __forceinline__ void flag_transform2(uint32_t w, uint32_t& all, uint3
     fail = all & mf;
 }
 
+// Two Harley-Seal trees fed from one register tile through flag_transform2:
+// each leaf transforms its two inputs and immediately feeds both trees, so
+// the transformed planes never exist as whole arrays (fewer live registers,
+// more warps per SM for this latency-bound kernel).  Same CSA sequence per
+// tree as Tree<L> over the transformed arrays.
+template <int L>
+struct FlagDualTree {
+    static __device__ __forceinline__ void run(uint32_t* ca, uint32_t* cf, const uint32_t* in, uint32_t& top_a,
+                                               uint32_t& top_f) {
+        uint32_t h, l;
+        if constexpr (L == 1) {
+            uint32_t a0, f0, a1, f1;
+            flag_transform2(in[0], a0, f0);
+            flag_transform2(in[1], a1, f1);
+            csa(h, l, ca[0], a0, a1);
+            ca[0] = l;
+            top_a = h;
+            csa(h, l, cf[0], f0, f1);
+            cf[0] = l;
+            top_f = h;
+        } else {
+            uint32_t a0, f0, a1, f1;
+            FlagDualTree<L - 1>::run(ca, cf, in, a0, f0);
+            FlagDualTree<L - 1>::run(ca, cf, in + (1 << (L - 1)), a1, f1);
+            csa(h, l, ca[L - 1], a0, a1);
+            ca[L - 1] = l;
+            top_a = h;
+            csa(h, l, cf[L - 1], f0, f1);
+            cf[L - 1] = l;
+            top_f = h;
+        }
+    }
+};
+
 // Tree-block consumer.  MODE 0: positional counts of the words (NBANK banks).
 // MODE 1: FLAG statistics -- transform, then bank 0 counts the transformed
 // words of all reads and bank 1 those of QC-fail reads; words with reserved bits 12-15 set are
@@ -240,15 +274,13 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
     } else {
         static_assert(NBANK == 2 && REGS == (1 << L), "FLAG mode: two banks of 2^L registers");
         constexpr int RPV = VB / 4;
-        uint32_t all[REGS], fail[REGS];
         uint32_t bad = 0;
 #pragma unroll
-        for (int i = 0; i < REGS; ++i) {
-            bad |= r[i];
-            flag_transform2(r[i], all[i], fail[i]);
-        }
-        extract(counter[0], Tree<L, 1>::run(carries[0], all));
-        extract(counter[1], Tree<L, 1>::run(carries[1], fail));
+        for (int i = 0; i < REGS; ++i) bad |= r[i];
+        uint32_t top_all, top_fail;
+        FlagDualTree<L>::run(carries[0], carries[1], r, top_all, top_fail);
+        extract(counter[0], top_all);
+        extract(counter[1], top_fail);
         if (bad & 0xF000F000u) {  // rare: locate this thread's first invalid word
             // Fully unrolled: a runtime index into r[] would force the whole
             // tile through local memory on the hot path.

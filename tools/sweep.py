@@ -139,7 +139,7 @@ def main():
         torch.cuda.synchronize()
         import ctypes as CC
         summ = pp._Summary()
-        for var in ["5,32,0,512,2", "4,32,0,512,2", "5,16,0,512,2", "6,32,0,256,2"]:
+        for var in ["5,32,0,512,2", "6,32,0,512,2", "4,32,0,512,2", "5,32,2,256,2", "4,32,0,1024,2"]:
             os.environ["POSPOP_FLAG_VARIANT"] = var
             for nb in (1 << 30, 1 << 33):
                 med, best = timed(lambda: lib.pospop_flagstats(data.data_ptr(), nb // 2, CC.byref(summ), None, None),
