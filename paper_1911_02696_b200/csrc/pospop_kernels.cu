@@ -108,11 +108,11 @@ const StreamVariant kStreamVariants[] = {
     SV(1, 7, 32, 0, 0, 0), SV(2, 6, 32, 0, 0, 0),
     SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // per-warp guided chunks
     SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1), SV(1, 6, 32, 0, 256, 2), SV(1, 7, 16, 0, 256, 2),
-    SVF(5, 32, 512, 2), SVF(5, 32, 0, 2),               // FLAG statistics defaults (16 warps/SM)
-    SVF(6, 32, 256, 2),
+    SVF(6, 32, 512, 2), SVF(6, 32, 0, 2),               // FLAG statistics defaults (16 warps/SM)
+    SVF(6, 32, 256, 2), SVF(5, 32, 512, 2),
     SVF(5, 32, 256, 2), SVF(6, 16, 256, 2), SVF(7, 32, 256, 2),
     SVF2(5, 32, 256, 2), SVF2(5, 16, 256, 2), SVF2(4, 32, 256, 2), SVF(4, 32, 512, 2), SVF(5, 16, 512, 2),
-    SVF(6, 32, 512, 2), SVF2(6, 32, 256, 2), SVF(4, 32, 1024, 2), SVF(5, 32, 1024, 2),
+    SVF2(6, 32, 256, 2), SVF(4, 32, 1024, 2),
 };
 #undef SV
 #undef SVF
@@ -163,7 +163,7 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
                                       const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
     const int nbank = (k == 64 || mode == 1) ? 2 : 1;
     // Tuning override: POSPOP_STREAM_VARIANT / POSPOP_FLAG_VARIANT="depth,vb,hint,block,sched".
-    int depth = mode == 1 ? 5 : (nbank == 1 ? kDefaultDepth1 : kDefaultDepth2), vb = 32, hint = 0,
+    int depth = mode == 1 ? 6 : (nbank == 1 ? kDefaultDepth1 : kDefaultDepth2), vb = 32, hint = 0,
         block = mode == 1 ? 512 : kDefaultBlock, sched = 2;
     if (const char* v = std::getenv(mode == 1 ? "POSPOP_FLAG_VARIANT" : "POSPOP_STREAM_VARIANT"))
         std::sscanf(v, "%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched);
