@@ -137,14 +137,17 @@ struct SegVariant {
 #define SG(NB, L, VB, S) {NB, L, VB, S, segmented_kernel<NB, L, VB, S>}
 #define SGP(NB, L, VB) {NB, L, VB, 2, segmented_pipe_entry<NB, L, VB>}
 #define SGP2(NB, L, VB) {NB, L, VB, 3, segmented_pipe_entry<NB, L, VB, 2>}  // sched 3: pipelined, 2 CTAs/SM
+#define SGP3(NB, L, VB) {NB, L, VB, 4, segmented_pipe_entry<NB, L, VB, 3>}  // sched 4: pipelined, 3 CTAs/SM
 const SegVariant kSegVariants[] = {
     SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
     SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
     SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
     SGP(1, 5, 16), SGP(1, 4, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
     SGP2(2, 4, 16), SGP2(2, 3, 32), SGP2(2, 3, 16), SGP2(1, 5, 16), SGP2(1, 5, 32),
+    SGP3(1, 4, 16), SGP3(1, 4, 32), SGP3(1, 5, 16), SGP3(2, 3, 16), SGP3(2, 3, 32),
 };
 #undef SGP2
+#undef SGP3
 #undef SG
 #undef SGP
 

@@ -156,8 +156,8 @@ def main():
             offs = torch.arange(0, arrays + 1, dtype=torch.int64, device="cuda") * words
             o = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
             want = None
-            cases = [(v, "", "") for v in ("5,16,0", "5,16,1", "5,16,2", "4,16,2", "3,32,2", "4,16,3", "3,32,3",
-                                           "3,16,3", "5,16,3", "5,32,3")]
+            cases = [(v, "", "") for v in ("5,16,1", "5,16,3", "5,32,3", "4,16,4", "4,32,4", "5,16,4", "3,16,4",
+                                           "3,32,4")]
             for var, per_sm, g in cases:
                 env = {"POSPOP_SEG_VARIANT": var, "POSPOP_SEG_BLOCKS_PER_SM": per_sm, "POSPOP_SEG_PER_GRAB": g}
                 for kk, vv in env.items():
