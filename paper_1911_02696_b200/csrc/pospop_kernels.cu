@@ -20,6 +20,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
+#include <utility>
 
 #include "pospop_aux.cuh"
 #include "pospop_device.cuh"
@@ -126,6 +128,30 @@ const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int blo
     return nullptr;
 }
 
+// TMA-staged variants (SCHED 3): (nbank, depth, mode, consumer warps, ring stages).
+struct TmaVariant {
+    int nbank, depth, mode, nc, stages;
+    StreamKernel fn;
+    size_t smem;  // dynamic shared memory: stages x stage bytes
+};
+
+#define TV(NB, L, M, NC, ST)                                                                \
+    {NB, L, M, NC, ST, stream_tma_kernel<NB, L, M, NC, ST>,                               \
+     (size_t)(ST) * (NC) * 32 * (((M) == 1 ? (1 << (L)) : ((NB) << (L))) / 4) * 16}
+const TmaVariant kTmaVariants[] = {
+    TV(1, 5, 0, 8, 6), TV(1, 6, 0, 8, 3), TV(1, 5, 0, 8, 4), TV(1, 4, 0, 8, 6), TV(1, 5, 0, 4, 6),
+    TV(2, 4, 0, 8, 6), TV(2, 5, 0, 8, 3),
+    TV(2, 5, 1, 8, 6), TV(2, 4, 1, 8, 6), TV(2, 6, 1, 8, 3), TV(2, 5, 1, 16, 3), TV(2, 4, 1, 16, 6),
+    TV(2, 5, 1, 12, 4),
+};
+#undef TV
+
+const TmaVariant* pick_tma(int nbank, int depth, int mode, int nc, int stages) {
+    for (const TmaVariant& v : kTmaVariants)
+        if (v.nbank == nbank && v.depth == depth && v.mode == mode && v.nc == nc && v.stages == stages) return &v;
+    return nullptr;
+}
+
 using SegKernel = void (*)(const uint8_t*, const unsigned long long*, unsigned long long, int, uint32_t,
                            unsigned long long*, unsigned long long*, unsigned int*, unsigned);
 
@@ -161,6 +187,91 @@ const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched) {
 
 unsigned long long kernel_launches() { return g_launches.load(); }
 
+// Vector addressing shared by every stream launch (see StreamArgs).
+static void fill_stream_args(StreamArgs& a, int k, const void* data, size_t len_words, uintptr_t vb,
+                             unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
+                             const StreamWorkspace& ws) {
+    const uintptr_t P = reinterpret_cast<uintptr_t>(data);
+    const size_t nbytes = len_words * (size_t)(k / 8);
+    const uintptr_t group = 32 * vb;
+    a.base = reinterpret_cast<const uint8_t*>(P & ~(group - 1));
+    if (nbytes == 0) {
+        a.v0 = a.v1 = a.f0 = a.f1 = a.g0 = a.ng = 0;
+        a.lo_byte = 0;
+        a.hi_byte = (int)vb;
+    } else {
+        const uintptr_t B = reinterpret_cast<uintptr_t>(a.base);
+        a.v0 = (P - B) / vb;
+        a.v1 = (P + nbytes - B + vb - 1) / vb;
+        a.lo_byte = (int)(P - (B + a.v0 * vb));
+        a.hi_byte = (int)(P + nbytes - (B + (a.v1 - 1) * vb));
+        a.f0 = a.v0 + (a.lo_byte != 0 ? 1 : 0);
+        a.f1 = a.v1 - (a.hi_byte != (int)vb ? 1 : 0);
+        a.g0 = a.v0 / 32;
+        a.ng = (a.v1 + 31) / 32 - a.g0;
+    }
+    a.k = k;
+    a.flush_threshold = opt.flush_threshold;
+    a.acc = ws.acc;
+    a.ticket = ws.ticket;
+    a.out = d_out;
+    a.accumulate = accumulate ? 1 : 0;
+    a.trace = opt.trace;
+    a.next = ws.next;
+    a.bad = ws.bad;
+    a.word_base = opt.word_base;
+    a.data_off = nbytes ? (unsigned long long)(P - reinterpret_cast<uintptr_t>(a.base)) : 0ull;
+    a.nwt = a.nA = a.pool = 0;
+    a.CA = a.CB = 1;
+}
+
+static cudaError_t launch_with_pdl(StreamKernel fn, int grid, int threads, size_t smem, cudaStream_t stream,
+                                   const StreamArgs& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = env_int("POSPOP_PDL", 1) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+    ++g_launches;
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// TMA-staged launch (SCHED 3): one CTA per SM, a producer warp + nc consumer
+// warps, `stages` x stage-bytes of dynamic shared memory.
+static cudaError_t launch_stream_tma(int mode, int nbank, int depth, int k, const void* data, size_t len_words,
+                                     unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
+                                     const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
+    int nc = 8, stages = mode == 1 ? 6 : 6;
+    if (const char* v = std::getenv("POSPOP_TMA")) std::sscanf(v, "%d,%d", &nc, &stages);
+    const TmaVariant* var = pick_tma(nbank, depth, mode, nc, stages);
+    if (!var) return cudaErrorInvalidConfiguration;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, bool> configured;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto key = std::make_pair(dev, reinterpret_cast<const void*>(var->fn));
+        if (!configured[key]) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)var->smem);
+            if (e != cudaSuccess) return e;
+            configured[key] = true;
+        }
+    }
+    StreamArgs a;
+    fill_stream_args(a, k, data, len_words, 16, d_out, accumulate, opt, ws);
+    const int grid = device_info().sms;
+    if (grid_used) *grid_used = grid;
+    return launch_with_pdl(var->fn, grid, 32 * (var->nc + 1), var->smem, stream, a);
+}
+
 static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t len_words,
                                       unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
                                       const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
@@ -171,6 +282,9 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     if (const char* v = std::getenv(mode == 1 ? "POSPOP_FLAG_VARIANT" : "POSPOP_STREAM_VARIANT"))
         std::sscanf(v, "%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched);
     if (opt.depth) depth = opt.depth;
+    if (sched == 3 && !opt.block && !opt.grid)
+        return launch_stream_tma(mode, nbank, depth, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
+    if (sched == 3) sched = 2;  // explicit test geometry: the LDG kernel
     if (opt.block) block = 0;  // explicit (test) block size: the runtime-block instantiation
     const StreamVariant* var = pick_stream(nbank, depth, vb, hint, block, sched, mode);
     if (!var) var = pick_stream(nbank, depth, vb, 0, 0, sched, mode);

@@ -447,5 +447,151 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
     cta_finish<NBANK, L, MODE>(a, carries, counter, s_acc, &s_last, block, lane);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged variant (SCHED 3).  One producer warp per CTA pulls stage indices
+// from the global counter and moves each 32 KiB (NC warp tiles) stage of the
+// stream into a shared-memory ring with one cp.async.bulk (UBLKCP), tracked by
+// a full/empty mbarrier pair per slot; NC consumer warps wait on `full`, read
+// their warp tile with LDS.128 (vectors outside the valid range read as zero,
+// the first/last vector byte-masked), release the slot on `empty` and run the
+// same tree/flush/epilogue as the LDG kernel.  Memory latency is covered by
+// the ring depth instead of by registers and warps, which matters for the
+// ALU-heavy FLAG mode.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(smem_addr(bar)), "r"(parity)
+                     : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+// Stage s of the ring holds NC * 32 * VPT 16-byte vectors.
+template <int NBANK, int L, int MODE, int NC, int STAGES>
+__global__ void __launch_bounds__(32 * (NC + 1), 1) stream_tma_kernel(const StreamArgs a) {
+    constexpr int REGS = MODE == 1 ? (1 << L) : (NBANK << L);
+    constexpr int VPT = REGS / 4;                                   // 16-byte vectors per lane per tree block
+    constexpr unsigned long long WTV = 32ull * VPT;                 // vectors per warp tile
+    constexpr unsigned long long STV = NC * WTV;                    // vectors per stage
+    constexpr uint32_t STB = (uint32_t)(STV * 16);                  // bytes per stage
+    extern __shared__ __align__(128) uint8_t ring[];                // STAGES x STB
+    __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
+    __shared__ unsigned long long stage_idx[STAGES];
+    __shared__ unsigned long long s_acc[32 * NBANK];
+    __shared__ int s_last;
+
+    const unsigned block = blockDim.x;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    if (a.trace && threadIdx.x == 0) {
+        a.trace[blockIdx.x * 5 + 0] = globaltimer();
+        a.trace[blockIdx.x * 5 + 4] = smid();
+    }
+    for (int i = threadIdx.x; i < 32 * NBANK; i += block) s_acc[i] = 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_allow_next();
+    __syncthreads();
+
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+
+    const unsigned long long S0 = a.g0 * 32;
+    const unsigned long long NS = a.ng ? (a.v1 - S0 + STV - 1) / STV : 0;  // stages in the stream
+
+    if (warp == NC) {  // producer
+        if (lane == 0) {
+            pdl_wait_prev();  // the stage counter is shared with the previous launch
+            for (unsigned it = 0;; ++it) {
+                const unsigned s = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1u);
+                const unsigned long long idx = atomicAdd(a.next, 1ull);
+                stage_idx[s] = idx;
+                if (idx >= NS) {  // end marker: wake the consumers without data
+                    mbar_arrive(&full[s]);
+                    break;
+                }
+                const unsigned long long t0 = S0 + idx * STV;
+                const unsigned long long lo = t0 > a.v0 ? t0 : a.v0;
+                const unsigned long long hi = t0 + STV < a.v1 ? t0 + STV : a.v1;
+                const uint32_t bytes = (uint32_t)((hi - lo) * 16);
+                mbar_arrive_expect_tx(&full[s], bytes);
+                tma_bulk_g2s(ring + (size_t)s * STB + (lo - t0) * 16, a.base + lo * 16, bytes, &full[s]);
+            }
+        }
+    } else {  // consumers
+        uint32_t nb = 0;
+        for (unsigned it = 0;; ++it) {
+            const unsigned s = it % STAGES;
+            mbar_wait(&full[s], (it / STAGES) & 1u);
+            const unsigned long long idx = stage_idx[s];
+            if (idx >= NS) break;
+            const unsigned long long t0 = S0 + idx * STV;
+            const unsigned long long first = t0 + warp * WTV + lane;  // lane's first vector (global index)
+            const uint8_t* tile = ring + (size_t)s * STB + (warp * WTV + lane) * 16;
+            const bool fast = t0 + warp * WTV >= a.f0 && t0 + (warp + 1) * WTV <= a.f1;
+            uint32_t r[REGS];
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) {
+                uint32_t x[4];
+                const unsigned long long g = first + 32ull * v;
+                if (fast || (g >= a.v0 && g < a.v1)) {
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3])
+                                 : "r"(smem_addr(tile + 512 * v)));
+                    if (!fast && (g == a.v0 || g + 1 == a.v1))
+                        mask_bytes<16>(x, g == a.v0 ? a.lo_byte : 0, g + 1 == a.v1 ? a.hi_byte : 16);
+                } else {
+                    x[0] = x[1] = x[2] = x[3] = 0;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) r[v * 4 + j] = x[j];
+            }
+            mbar_arrive(&empty[s]);  // this lane's reads are in registers: the slot may be refilled
+            consume<MODE, NBANK, L, 16>(a, r, first, 32u, carries, counter);
+            if (++nb == a.flush_threshold) {  // warp-uniform
+                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                nb = 0;
+            }
+        }
+    }
+    cta_finish<NBANK, L, MODE>(a, carries, counter, s_acc, &s_last, block, lane);
+}
+
 }  // namespace dev
 }  // namespace pospop_b200

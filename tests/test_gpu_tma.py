@@ -1,0 +1,83 @@
+"""The TMA-staged stream kernel (SCHED 3: cp.async.bulk into a shared-memory
+ring, mbarrier full/empty slots, LDS.128 consumers) -- bit-exact against the
+oracle on the same cases as the LDG kernel: every k, unaligned starts and
+ragged ends inside 0xFF guard bytes, forced flushes, full size, and the FLAG
+mode including the first-invalid-word report."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TMA_STREAM = [("5,32,0,256,3", "8,6"), ("6,32,0,256,3", "8,3"), ("4,32,0,256,3", "8,6"), ("5,32,0,256,3", "4,6")]
+TMA_STREAM64 = [("4,32,0,256,3", "8,6"), ("5,32,0,256,3", "8,3")]
+TMA_FLAG = [("5,32,0,256,3", "8,6"), ("6,32,0,256,3", "8,3"), ("5,32,0,256,3", "16,3"), ("4,32,0,256,3", "16,6")]
+
+
+def guarded(a, offset, guard=64):
+    raw = a.view(np.uint8)
+    buf = torch.full((guard + offset + raw.size + guard,), 0xFF, dtype=torch.uint8, device="cuda")
+    buf[guard + offset:guard + offset + raw.size] = torch.from_numpy(raw.copy()).cuda()
+    return buf, buf[guard + offset:guard + offset + raw.size]
+
+
+@pytest.fixture(scope="module")
+def dev(pp):
+    assert torch.cuda.is_available() and pp.device_available()
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_tma_stream_lengths_offsets(pp, dev, orc, k, monkeypatch):
+    wb = k // 8
+    raw = orc.generate(6, 17 + k, (5 << 20) // 8).view(np.uint8)
+    lengths = [0, 1, 7, 31, 33, 1000, 4097, 65537, 300_001, raw.size // wb - 8]
+    for var, tma in (TMA_STREAM64 if k == 64 else TMA_STREAM):
+        monkeypatch.setenv("POSPOP_STREAM_VARIANT", var)
+        monkeypatch.setenv("POSPOP_TMA", tma)
+        for offset in sorted({0, wb, 3 * wb, 8, 16 - wb}):
+            for n in lengths:
+                sub = raw[:n * wb]
+                _, view = guarded(sub, offset)
+                assert pp.pospopcnt_k(view, k) == orc.pospopcnt(sub, k, threads=4), (var, tma, k, offset, n)
+
+
+def test_tma_forced_flush_and_full_size(pp, dev, orc, monkeypatch):
+    monkeypatch.setenv("POSPOP_STREAM_VARIANT", "5,32,0,256,3")
+    monkeypatch.setenv("POSPOP_TMA", "8,6")
+    raw = orc.generate(6, 5, 1 << 18).view(np.uint8)
+    d = torch.from_numpy(raw.copy()).cuda()
+    want = orc.naive(raw, 16)
+    for thr in (1, 3, 65535):
+        assert pp.pospopcnt_k(d, 16, flush_threshold_blocks=thr) == want
+    n = 1 << 31  # 4 GiB of u16
+    big = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_CFG4, 3, big)
+    got = pp.pospopcnt(big)
+    monkeypatch.setenv("POSPOP_STREAM_VARIANT", "7,32,0,256,2")  # the LDG kernel on the same bytes
+    assert pp.pospopcnt(big) == got
+    assert got == orc.pospopcnt(big.cpu().numpy().view(np.uint16), 16, threads=16)
+
+
+@pytest.mark.parametrize("var,tma", TMA_FLAG)
+def test_tma_flagstats(pp, dev, orc, golden, var, tma, monkeypatch):
+    monkeypatch.setenv("POSPOP_FLAG_VARIANT", var)
+    monkeypatch.setenv("POSPOP_TMA", tma)
+    streams = orc.acceptance_flag_streams()
+    for i in range(0, 100, 7):
+        assert pp.flagstats(torch.from_numpy(streams[i].view(np.int16).copy()).cuda()).as_list() == \
+            golden["flagstats_acceptance"][i]
+    w = orc.generate(7, 5, (1 << 22) + 3)
+    w[123457] |= 0x1000
+    w[2_000_001] |= 0x8000
+    for offset in (0, 2, 6):
+        _, view = guarded(w, offset)
+        with pytest.raises(pp.InvalidFlagWordError) as e:
+            pp.flagstats(view)
+        assert e.value.offset == 123457
+    w[123457] &= 0x0FFF
+    w[2_000_001] &= 0x0FFF
+    rc, want, _ = orc.flagstats(w)
+    _, view = guarded(w, 2)
+    assert pp.flagstats(view).as_list() == list(want)

@@ -132,6 +132,32 @@ def main():
         emit(kind="cfg2", gbs_med=round((1 << 29) / med / 1e6, 1), gbs_best=round((1 << 29) / best / 1e6, 1))
         del b3, b2
 
+    if "tma" in what:  # TMA-staged (SCHED 3) vs LDG (SCHED 2) on the same bytes
+        out = torch.zeros(16, dtype=torch.int64, device="cuda")
+        cases = [("7,32,0,256,2", ""), ("5,32,0,256,3", "8,6"), ("6,32,0,256,3", "8,3"), ("5,32,0,256,3", "8,4"),
+                 ("4,32,0,256,3", "8,6"), ("5,32,0,256,3", "4,6")]
+        for var, tma in cases:
+            os.environ["POSPOP_STREAM_VARIANT"] = var
+            if tma:
+                os.environ["POSPOP_TMA"] = tma
+            else:
+                os.environ.pop("POSPOP_TMA", None)
+            for nb in (1 << 30, 1 << 33):
+                med, best = timed(lambda: pp.count_async(data, out, 16, stream=s, len_words=nb // 2), args.reps, s)
+                emit(kind="tma16", variant=var, tma=tma, bytes=nb, gbs_med=round(nb / med / 1e6, 1),
+                     gbs_best=round(nb / best / 1e6, 1))
+        for var, tma in [("6,32,0,256,2", ""), ("4,32,0,256,3", "8,6"), ("5,32,0,256,3", "8,3")]:
+            os.environ["POSPOP_STREAM_VARIANT"] = var
+            if tma:
+                os.environ["POSPOP_TMA"] = tma
+            else:
+                os.environ.pop("POSPOP_TMA", None)
+            o = torch.zeros(64, dtype=torch.int64, device="cuda")
+            med, best = timed(lambda: pp.count_async(data, o, 64, stream=s), args.reps, s)
+            emit(kind="tma64", variant=var, tma=tma, bytes=1 << 33, gbs_med=round((1 << 33) / med / 1e6, 1))
+        os.environ.pop("POSPOP_STREAM_VARIANT", None)
+        os.environ.pop("POSPOP_TMA", None)
+
     if "flag" in what:
         lib = pp._load()
         nf = 1 << 32  # 8 GiB of FLAG words
@@ -139,14 +165,21 @@ def main():
         torch.cuda.synchronize()
         import ctypes as CC
         summ = pp._Summary()
-        for var in ["5,32,0,512,2", "6,32,0,512,2", "4,32,0,512,2", "5,32,2,256,2", "4,32,0,1024,2"]:
+        for var in ["6,32,0,512,2", "5,32,0,256,3/8,6", "4,32,0,256,3/8,6", "6,32,0,256,3/8,3",
+                    "5,32,0,256,3/16,3", "4,32,0,256,3/16,6", "5,32,0,256,3/12,4"]:
+            var, _, tma = var.partition("/")
             os.environ["POSPOP_FLAG_VARIANT"] = var
+            if tma:
+                os.environ["POSPOP_TMA"] = tma
+            else:
+                os.environ.pop("POSPOP_TMA", None)
             for nb in (1 << 30, 1 << 33):
                 med, best = timed(lambda: lib.pospop_flagstats(data.data_ptr(), nb // 2, CC.byref(summ), None, None),
                                   max(3, args.reps // 4), s)
-                emit(kind="flagstats", bytes=nb, variant=var, gbs_med=round(nb / med / 1e6, 1),
+                emit(kind="flagstats", bytes=nb, variant=var, tma=tma, gbs_med=round(nb / med / 1e6, 1),
                      gbs_best=round(nb / best / 1e6, 1), note="sync C-ABI call incl. D2H of 33 u64")
         os.environ.pop("POSPOP_FLAG_VARIANT", None)
+        os.environ.pop("POSPOP_TMA", None)
 
     if "seg" in what:
         for k, kind in [(32, pp.GEN_U32), (64, pp.GEN_U64)]:
