@@ -128,9 +128,9 @@ thread_local std::map<int, Ctx*> t_ctx;
 
 pospop_status alloc_workspace(StreamWorkspace* ws) {
     CU(cudaMalloc(&ws->acc, kWorkspaceBytes));
-    ws->ticket = reinterpret_cast<unsigned int*>(ws->acc + 64);
-    ws->next = ws->acc + 65;
-    ws->bad = ws->acc + 66;
+    ws->ticket = reinterpret_cast<unsigned int*>(ws->acc + kAccChannels);
+    ws->next = ws->acc + kAccChannels + 1;
+    ws->bad = ws->acc + kAccChannels + 2;
     CU(cudaMemset(ws->acc, 0, kWorkspaceBytes));
     return POSPOP_OK;
 }

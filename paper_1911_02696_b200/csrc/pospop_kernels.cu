@@ -100,6 +100,8 @@ struct StreamVariant {
 #define SVF(L, VB, B, S) {2, L, VB, 0, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1>}
 // FLAG variants that must fit 2 CTAs/SM (<= 128 registers); hint slot = 2 marks them.
 #define SVF2(L, VB, B, S) {2, L, VB, 2, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1, 2>}
+#define SVB(L, VB, B, S) {3, L, VB, 0, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2>}
+#define SVB2(L, VB, B, S) {3, L, VB, 2, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2, 2>}
 // Production variants first (the defaults), then tuning variants selectable
 // through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched" (POSPOP_FLAG_VARIANT
 // for MODE 1).
@@ -115,9 +117,16 @@ const StreamVariant kStreamVariants[] = {
     SVF(5, 32, 256, 2), SVF(6, 16, 256, 2), SVF(7, 32, 256, 2),
     SVF2(5, 32, 256, 2), SVF2(5, 16, 256, 2), SVF2(4, 32, 256, 2), SVF(4, 32, 512, 2), SVF(5, 16, 512, 2),
     SVF2(6, 32, 256, 2), SVF(4, 32, 1024, 2),
+    // byte-frame FLAG statistics (MODE 2): defaults first
+    SVB(5, 32, 512, 2), SVB(5, 32, 0, 2),
+    SVB(5, 32, 256, 2), SVB(4, 32, 512, 2), SVB(4, 32, 256, 2), SVB2(4, 32, 256, 2), SVB2(4, 32, 512, 2),
+    SVB(4, 16, 512, 2), SVB(6, 32, 256, 2), SVB(5, 16, 512, 2), SVB2(5, 32, 256, 2),
 };
 #undef SV
 #undef SVF
+#undef SVF2
+#undef SVB
+#undef SVB2
 #undef SVF2
 
 const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block, int sched, int mode) {
@@ -275,12 +284,22 @@ static cudaError_t launch_stream_tma(int mode, int nbank, int depth, int k, cons
 static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t len_words,
                                       unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
                                       const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
-    const int nbank = (k == 64 || mode == 1) ? 2 : 1;
-    // Tuning override: POSPOP_STREAM_VARIANT / POSPOP_FLAG_VARIANT="depth,vb,hint,block,sched".
-    int depth = mode == 1 ? 6 : (nbank == 1 ? kDefaultDepth1 : kDefaultDepth2), vb = 32, hint = 0,
-        block = mode == 1 ? 512 : kDefaultBlock, sched = 2;
-    if (const char* v = std::getenv(mode == 1 ? "POSPOP_FLAG_VARIANT" : "POSPOP_STREAM_VARIANT"))
+    // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched";
+    // FLAG statistics: POSPOP_FLAG_VARIANT="depth,vb,hint,block,sched[,mode]"
+    // (mode 2 byte-frame kernel, the default; mode 1 the 16-bit-lane kernel).
+    int depth = mode == 0 ? (k == 64 ? kDefaultDepth2 : kDefaultDepth1) : 5, vb = 32, hint = 0,
+        block = mode == 0 ? kDefaultBlock : 512, sched = 2;
+    if (mode != 0) {
+        int fmode = mode;
+        if (const char* v = std::getenv("POSPOP_FLAG_VARIANT")) {
+            const int n = std::sscanf(v, "%d,%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched, &fmode);
+            if (n < 6) fmode = 1;  // five-field strings name the 16-bit-lane kernel (r01 sweeps)
+        }
+        mode = fmode;
+    } else if (const char* v = std::getenv("POSPOP_STREAM_VARIANT")) {
         std::sscanf(v, "%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched);
+    }
+    const int nbank = mode == 2 ? 3 : (k == 64 || mode == 1) ? 2 : 1;
     if (opt.depth) depth = opt.depth;
     if (sched == 3 && !opt.block && !opt.grid)
         return launch_stream_tma(mode, nbank, depth, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
@@ -290,7 +309,8 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     if (!var) var = pick_stream(nbank, depth, vb, 0, 0, sched, mode);
     if (!var) return cudaErrorInvalidConfiguration;
     const int threads = var->block ? var->block : (opt.block ? opt.block : kDefaultBlock);
-    const int vpt = (mode == 1 ? (1 << var->depth) : (nbank << var->depth)) / (var->vb / 4);
+    const int vpt = (mode == 1 ? (1 << var->depth) : mode == 2 ? (2 << var->depth) : (nbank << var->depth)) /
+                    (var->vb / 4);
 
     const uintptr_t P = reinterpret_cast<uintptr_t>(data);
     const size_t nbytes = len_words * (size_t)(k / 8);
@@ -314,7 +334,12 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
         a.ng = (a.v1 + 31) / 32 - a.g0;
     }
     a.k = k;
-    a.flush_threshold = opt.flush_threshold;
+    // byte-lane counters (MODE 2) take at most 255 tree blocks between flushes;
+    // POSPOP_FLUSH_THRESHOLD lowers the threshold (tests: exercise the flush path)
+    uint32_t thr = opt.flush_threshold;
+    const int env_thr = env_int("POSPOP_FLUSH_THRESHOLD", 0);
+    if (env_thr > 0 && (uint32_t)env_thr < thr) thr = (uint32_t)env_thr;
+    a.flush_threshold = mode == 2 && thr > 255 ? 255 : thr;
     a.acc = ws.acc;
     a.ticket = ws.ticket;
     a.out = d_out;
@@ -373,7 +398,7 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
 
 cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long long* d_out33, bool accumulate,
                              const LaunchOptions& opt, const StreamWorkspace& ws, cudaStream_t stream) {
-    return launch_stream_mode(1, 16, flags, len, d_out33, accumulate, opt, ws, stream, nullptr);
+    return launch_stream_mode(2, 16, flags, len, d_out33, accumulate, opt, ws, stream, nullptr);
 }
 
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets, size_t n,

@@ -9,19 +9,21 @@
 
 namespace pospop_b200 {
 
-// Persistent device scratch for one in-flight stream launch: acc[64]
-// channel totals and a completion ticket.  Both must be zero before a
+// Persistent device scratch for one in-flight stream launch: acc[96]
+// channel totals (32 per counter bank; the FLAG kernel uses three banks) and a
+// completion ticket.  Both must be zero before a
 // launch; the kernel's last block leaves them zero again.
 struct StreamWorkspace {
-    unsigned long long* acc = nullptr;   // 64 channel accumulators
+    unsigned long long* acc = nullptr;   // kAccChannels channel accumulators
     unsigned int* ticket = nullptr;      // CTA completion ticket
     unsigned long long* next = nullptr;  // dynamic-schedule chunk counter
     unsigned long long* bad = nullptr;   // FLAG mode: ~(first invalid word index), 0 = none
 };
 
-// Bytes of one workspace allocation: acc[64], ticket (u32 at +512), next (u64
-// at +520), bad (u64 at +528).
-constexpr size_t kWorkspaceBytes = 64 * sizeof(unsigned long long) + 64;
+// Bytes of one workspace allocation: acc[96], ticket (u32 at +768), next (u64
+// at +776), bad (u64 at +784).
+constexpr int kAccChannels = 96;
+constexpr size_t kWorkspaceBytes = kAccChannels * sizeof(unsigned long long) + 64;
 
 struct LaunchOptions {
     uint32_t flush_threshold = 65535;  // tree blocks between lane flushes, [1, 65535]

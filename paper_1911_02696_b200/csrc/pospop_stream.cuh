@@ -77,6 +77,9 @@ __device__ __forceinline__ void tree_block(const uint32_t (&r)[NBANK << L], uint
     }
 }
 
+__device__ __forceinline__ uint32_t bank_warp_total_bytes(const uint32_t (&counter)[16], int shift,
+                                                          const uint32_t (&d)[16]);
+
 template <int NBANK>
 __device__ __forceinline__ void zero_bank(uint32_t (&counter)[NBANK][16]) {
 #pragma unroll
@@ -121,7 +124,7 @@ __device__ __forceinline__ void load_tree_block(const StreamArgs& a, unsigned lo
 
 // Lane-bank flush (weight 2^L) into the CTA's shared channel totals; must be
 // called by all 32 lanes of a warp together.
-template <int NBANK, int L>
+template <int NBANK, int L, int MODE = 0>
 __device__ __forceinline__ void flush_bank_to_smem(uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
                                                    uint32_t lane) {
     uint32_t d[16];
@@ -129,7 +132,7 @@ __device__ __forceinline__ void flush_bank_to_smem(uint32_t (&counter)[NBANK][16
     for (int p = 0; p < 16; ++p) d[p] = 0;
 #pragma unroll
     for (int b = 0; b < NBANK; ++b) {
-        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        const uint32_t tot = MODE == 2 ? bank_warp_total_bytes(counter[b], L, d) : bank_warp_total(counter[b], L, d);
         if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
     }
     zero_bank<NBANK>(counter);
@@ -149,7 +152,7 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
     for (int b = 0; b < NBANK; ++b) {
         uint32_t d[16];
         drain<L>(d, carries[b]);
-        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        const uint32_t tot = MODE == 2 ? bank_warp_total_bytes(counter[b], L, d) : bank_warp_total(counter[b], L, d);
         if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
     }
     __syncthreads();
@@ -164,7 +167,28 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
 
     // Last CTA: every other CTA has fenced its channel atomics.
     __threadfence();
-    if constexpr (MODE == 1) {  // two banks of k = 16: out[16 b + p] = acc[32 b + p] + acc[32 b + p + 16]
+    if constexpr (MODE == 2) {
+        // Byte-frame banks: stat j of bank b = sum of channels 8i + j.  Written
+        // in MODE 1's layout (flag_transform positions, flagstats.cpp:39-49):
+        // out[p] all reads, out[16 + p] QC-fail reads.
+        for (int c = threadIdx.x; c < 96; c += block) s_acc[c] = atomicExch(&a.acc[c], 0ull);
+        __syncthreads();
+        for (int pos = threadIdx.x; pos < 32; pos += block) {
+            const int f = pos >> 4, p = pos & 15;
+            auto stat = [&](int b, int j) {
+                return s_acc[32 * b + j] + s_acc[32 * b + 8 + j] + s_acc[32 * b + 16 + j] + s_acc[32 * b + 24 + j];
+            };
+            unsigned long long v = 0;
+            if (p == 1 || p == 2 || p == 3 || p == 6 || p == 7) v = stat(f, p);
+            else if (p >= 8 && p <= 11) v = stat(2, p - 8 + 4 * f);
+            else if (p == 12) v = stat(f, 0) - stat(f, 3);  // pair_map = GU - GU & mate_unmapped
+            a.out[pos] = a.accumulate ? a.out[pos] + v : v;
+        }
+        if (threadIdx.x == 0) {
+            const unsigned long long code = atomicExch(a.bad, 0ull);
+            a.out[32] = a.accumulate && a.out[32] > code ? a.out[32] : code;
+        }
+    } else if constexpr (MODE == 1) {  // two banks of k = 16: out[16 b + p] = acc[32 b + p] + acc[32 b + p + 16]
         for (int pos = threadIdx.x; pos < 32; pos += block) {
             const int b = pos >> 4, p = pos & 15;
             const unsigned long long sum =
@@ -260,7 +284,109 @@ struct FlagDualTree {
     }
 };
 
+// ---------------------------------------------------------------------------
+// FLAG statistics, byte-frame form (MODE 2, the default).  A leaf takes two
+// registers = four FLAG words and regroups them with two PRMTs into
+//   Lb = the four low bytes (bits 0-7: paired .. read2)
+//   Hb = the four high bytes (bits 8-15: secondary, qcfail, dup, supplementary, reserved)
+// so every SWAR operation below works on four words at once (8-bit lanes)
+// instead of two.  Three planes leave the leaf, each counted by its own
+// Harley-Seal tree (bank 0/1/2); per byte lane:
+//   AL  bit 0 GU, 1 GU&proper, 2 unmapped, 3 GU&mate_unmapped, 6 G&read1, 7 G&read2
+//   FL  = AL of QC-fail reads
+//   AHF bits 0-3 secondary, qcfail, dup, supplementary&!secondary; bits 4-7 the
+//       same for QC-fail reads (AH << 4 under the QC-fail mask)
+// with G = paired & !secondary & !supplementary and GU = G & !unmapped, so
+// pair_map = GU - GU&mate_unmapped (flagstats.cpp:84).  G/GU are formed at bit 0
+// of each byte and multiplied into their target bits (no carries: g, gu are
+// 0/1 per byte); the QC-fail byte mask is PRMT's sign-replicate of bit 9
+// moved to each byte's msb.  Bits 4,5 of AL are don't-care (never read).
+// Reserved bits 12-15 sit in Hb's high nibbles, so `bad |= Hb` tracks them.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+__device__ __forceinline__ void flag_leaf(uint32_t r0, uint32_t r1, uint32_t& al, uint32_t& fl, uint32_t& ahf,
+                                          uint32_t& bad) {
+    constexpr uint32_t B1 = 0x01010101u;
+    const uint32_t lb = prmt(r0, r1, 0x6420u);
+    const uint32_t hb = prmt(r0, r1, 0x7531u);
+    bad |= hb;
+    const uint32_t g = lb & ~hb & ~shr_fma<3>(hb) & B1;        // paired & !secondary & !supplementary
+    const uint32_t gu = g & ~shr_fma<2>(lb);                    // ... & !unmapped
+    const uint32_t t = g * 0xC0u + gu * 0x0Bu;                  // G -> bits 6,7 ; GU -> bits 0,1,3
+    al = lb & (t | 0x04040404u);
+    const uint32_t mf = prmt(shl_fma<6>(hb), 0u, 0xBA98u);     // 0xFF per QC-fail byte
+    fl = al & mf;
+    const uint32_t ah = hb & ~(shl_fma<3>(hb) & 0x08080808u);  // bit 3: supplementary & !secondary
+    ahf = ah | (shl_fma<4>(ah) & mf);
+}
+
+template <int LT, int L = LT>
+struct FlagByteTree {  // 2^L leaves = 2^(L+1) input registers; c[b][j] = carry of weight 2^j
+    static __device__ __forceinline__ void run(uint32_t (&c)[3][LT], const uint32_t* in, uint32_t (&top)[3],
+                                               uint32_t& bad) {
+        uint32_t x[3], y[3];
+        if constexpr (L == 1) {
+            flag_leaf(in[0], in[1], x[0], x[1], x[2], bad);
+            flag_leaf(in[2], in[3], y[0], y[1], y[2], bad);
+        } else {
+            FlagByteTree<LT, L - 1>::run(c, in, x, bad);
+            FlagByteTree<LT, L - 1>::run(c, in + (2 << (L - 1)), y, bad);
+        }
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            uint32_t h, l;
+            csa(h, l, c[b][L - 1], x[b], y[b]);
+            c[b][L - 1] = l;
+            top[b] = h;
+        }
+    }
+};
+
+// Byte-lane counters: counter[p] byte lane j counts channel 8j + p (p < 8);
+// a lane takes at most 255 extracts between flushes.
+__device__ __forceinline__ void extract_bytes(uint32_t (&counter)[16], uint32_t top) {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) counter[p] += (top >> p) & 0x01010101u;
+}
+
+__device__ __forceinline__ uint32_t bank_warp_total_bytes(const uint32_t (&counter)[16], int shift,
+                                                          const uint32_t (&d)[16]) {
+    uint32_t v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+        v[c] = (((counter[c & 7] >> (8 * (c >> 3))) & 0xFFu) << shift) +
+               (c < 16 ? (d[c] & 0xFFFFu) : (d[c - 16] >> 16));
+    return warp_transpose_reduce(v);
+}
+
+// Rare path: this thread's tile holds a FLAG word with reserved bits 12-15
+// set; report the smallest such word index through a.bad (max of ~index).
+// Fully unrolled: a runtime index into r[] would force the whole tile through
+// local memory on the hot path.
+template <int REGS, int RPV, int VB>
+__device__ __forceinline__ void flag_locate_bad(const StreamArgs& a, const uint32_t (&r)[REGS], unsigned long long first,
+                                             unsigned stride) {
+    unsigned long long best = ~0ull;
+#pragma unroll
+    for (int i = 0; i < REGS; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if ((r[i] >> (16 * h)) & 0xF000u) {
+                const unsigned long long byte =
+                    (first + (unsigned long long)(i / RPV) * stride) * VB + 4 * (i % RPV) + 2 * h;
+                const unsigned long long word = ((byte - a.data_off) >> 1) + a.word_base;
+                best = word < best ? word : best;
+            }
+    atomicMax(a.bad, ~best);
+}
+
 // Tree-block consumer.  MODE 0: positional counts of the words (NBANK banks).
+// MODE 2: byte-frame FLAG statistics (three banks, see flag_leaf).
 // MODE 1: FLAG statistics -- transform, then bank 0 counts the transformed
 // words of all reads and bank 1 those of QC-fail reads; words with reserved bits 12-15 set are
 // reported through a.bad (the first such index wins, as the reference's
@@ -271,6 +397,14 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
                                         uint32_t (&counter)[NBANK][16]) {
     if constexpr (MODE == 0) {
         tree_block<NBANK, L>(r, carries, counter);
+    } else if constexpr (MODE == 2) {
+        static_assert(NBANK == 3 && REGS == (2 << L), "byte-frame FLAG mode: three banks, 2^(L+1) registers");
+        constexpr int RPV = VB / 4;
+        uint32_t bad = 0, top[3];
+        FlagByteTree<L>::run(carries, r, top, bad);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) extract_bytes(counter[b], top[b]);
+        if (bad & 0xF0F0F0F0u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
     } else {
         static_assert(NBANK == 2 && REGS == (1 << L), "FLAG mode: two banks of 2^L registers");
         constexpr int RPV = VB / 4;
@@ -281,22 +415,7 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
         FlagDualTree<L>::run(carries[0], carries[1], r, top_all, top_fail);
         extract(counter[0], top_all);
         extract(counter[1], top_fail);
-        if (bad & 0xF000F000u) {  // rare: locate this thread's first invalid word
-            // Fully unrolled: a runtime index into r[] would force the whole
-            // tile through local memory on the hot path.
-            unsigned long long best = ~0ull;
-#pragma unroll
-            for (int i = 0; i < REGS; ++i)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-                    if ((r[i] >> (16 * h)) & 0xF000u) {
-                        const unsigned long long byte =
-                            (first + (unsigned long long)(i / RPV) * stride) * VB + 4 * (i % RPV) + 2 * h;
-                        const unsigned long long word = ((byte - a.data_off) >> 1) + a.word_base;
-                        best = word < best ? word : best;
-                    }
-            atomicMax(a.bad, ~best);
-        }
+        if (bad & 0xF000F000u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
     }
 }
 
@@ -310,7 +429,7 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
 // BLOCK > 0: compile-time block size; BLOCK == 0: runtime blockDim.x.
 template <int NBANK, int L, int VB, int HINT, int BLOCK, int SCHED, int MODE, int MINB = 1>
 __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(const StreamArgs a) {
-    constexpr int REGS = MODE == 1 ? (1 << L) : (NBANK << L);  // 32-bit input registers per tree block
+    constexpr int REGS = MODE == 1 ? (1 << L) : MODE == 2 ? (2 << L) : (NBANK << L);  // registers per tree block
     constexpr int RPV = VB / 4;       // registers per vector
     constexpr int VPT = REGS / RPV;   // vectors per thread per tree block
     static_assert(VPT >= 1, "tree must consume at least one vector");
@@ -357,7 +476,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
             }
             consume<MODE, NBANK, L, VB>(a, r, t + threadIdx.x, block, carries, counter);
             if (++nb == a.flush_threshold) {  // block-uniform: every thread runs the same tiles
-                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                 nb = 0;
             }
         }
@@ -384,7 +503,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
             load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
             consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
             if (++nb == a.flush_threshold) {  // warp-uniform
-                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                 nb = 0;
             }
             w = lo + __shfl_sync(0xFFFFFFFFu, mine, 0);
@@ -405,7 +524,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                     load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
                     consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
                     if (++nb == a.flush_threshold) {
-                        flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                        flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                         nb = 0;
                     }
                 }
@@ -436,7 +555,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                 load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
                 consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
                 if (++nb == a.flush_threshold) {  // warp-uniform
-                    flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                    flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                     nb = 0;
                 }
             }
@@ -494,7 +613,7 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 // Stage s of the ring holds NC * 32 * VPT 16-byte vectors.
 template <int NBANK, int L, int MODE, int NC, int STAGES>
 __global__ void __launch_bounds__(32 * (NC + 1), 1) stream_tma_kernel(const StreamArgs a) {
-    constexpr int REGS = MODE == 1 ? (1 << L) : (NBANK << L);
+    constexpr int REGS = MODE == 1 ? (1 << L) : MODE == 2 ? (2 << L) : (NBANK << L);
     constexpr int VPT = REGS / 4;                                   // 16-byte vectors per lane per tree block
     constexpr unsigned long long WTV = 32ull * VPT;                 // vectors per warp tile
     constexpr unsigned long long STV = NC * WTV;                    // vectors per stage
@@ -585,7 +704,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) stream_tma_kernel(const Stre
             mbar_arrive(&empty[s]);  // this lane's reads are in registers: the slot may be refilled
             consume<MODE, NBANK, L, 16>(a, r, first, 32u, carries, counter);
             if (++nb == a.flush_threshold) {  // warp-uniform
-                flush_bank_to_smem<NBANK, L>(counter, s_acc, lane);
+                flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                 nb = 0;
             }
         }

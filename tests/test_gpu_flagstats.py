@@ -81,3 +81,49 @@ def test_empty_and_full_size(pp, dev, orc):
     rc, want, _ = orc.flagstats(host)
     assert rc == 0 and got.as_list() == list(want)
     assert got.total() == n
+
+
+FLAG_VARIANTS = ["5,32,0,512,2,2", "4,32,0,512,2,2", "4,32,2,256,2,2", "4,16,0,512,2,2", "6,32,0,256,2,2",
+                 "5,32,0,256,2,2", "6,32,0,512,2"]
+
+
+@pytest.mark.parametrize("variant", FLAG_VARIANTS)
+@pytest.mark.parametrize("flush", [None, "1", "3"])
+def test_flag_kernel_variants(pp, dev, orc, golden, variant, flush, monkeypatch):
+    """Every FLAG kernel instantiation (byte-frame MODE 2 and the 16-bit-lane
+    MODE 1), with forced lane flushes, on the golden acceptance streams, all
+    4096 values at unaligned starts, and the first-invalid-word report."""
+    monkeypatch.setenv("POSPOP_FLAG_VARIANT", variant)
+    if flush:
+        monkeypatch.setenv("POSPOP_FLUSH_THRESHOLD", flush)
+    streams = orc.acceptance_flag_streams()
+    for i in range(0, 100, 9):
+        assert pp.flagstats(to_dev(streams[i])).as_list() == golden["flagstats_acceptance"][i], i
+    words = np.tile(np.arange(4096, dtype=np.uint16), 301)
+    rc, want, _ = orc.flagstats(words)
+    for off in (0, 2, 6, 30):
+        buf = torch.full((words.nbytes + 128,), 0xFF, dtype=torch.uint8, device="cuda")
+        buf[64 + off:64 + off + words.nbytes] = torch.from_numpy(words.view(np.uint8).copy()).cuda()
+        assert pp.flagstats((buf.data_ptr() + 64 + off, words.size)).as_list() == list(want), off
+    w = orc.generate(7, 11, (1 << 21) + 7)
+    w[1_500_001] |= 0x8000
+    w[77_777] |= 0x1000
+    with pytest.raises(pp.InvalidFlagWordError) as e:
+        pp.flagstats(to_dev(w))
+    assert e.value.offset == 77_777
+
+
+def test_flag_byte_frame_full_size_flushes(pp, dev, orc, monkeypatch):
+    """8 GiB-class input at the default variant: every thread crosses the
+    255-block byte-lane flush several times."""
+    n = 1 << 31
+    d = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_FLAGS, 21, d)
+    got = pp.flagstats(d).as_list()
+    monkeypatch.setenv("POSPOP_FLAG_VARIANT", "6,32,0,512,2")  # the 16-bit-lane kernel on the same words
+    assert pp.flagstats(d).as_list() == got
+    host = d.cpu().numpy().view(np.uint16)
+    del d
+    rc, want, _ = orc.flagstats(host[: 1 << 26])
+    monkeypatch.delenv("POSPOP_FLAG_VARIANT")
+    assert pp.flagstats(host[: 1 << 26]).as_list() == list(want)
