@@ -106,6 +106,24 @@ __device__ __forceinline__ uint32_t bank_warp_total(const uint32_t (&counter)[16
     return warp_transpose_reduce(v);
 }
 
+// Byte-lane counters: counter[p] byte lane j counts channel 8j + p (p < 8);
+// a lane takes at most 255 extracts between flushes.
+__device__ __forceinline__ void extract_bytes(uint32_t (&counter)[16], uint32_t top) {
+#pragma unroll
+    for (int p = 0; p < 8; ++p)  // shifts on the FMA pipe (IMAD.HI): the FLAG kernel is ALU-bound
+        counter[p] += (p ? __umulhi(top, 1u << (32 - p)) : top) & 0x01010101u;
+}
+
+__device__ __forceinline__ uint32_t bank_warp_total_bytes(const uint32_t (&counter)[16], int shift,
+                                                          const uint32_t (&d)[16]) {
+    uint32_t v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+        v[c] = (((counter[c & 7] >> (8 * (c >> 3))) & 0xFFu) << shift) +
+               (c < 16 ? (d[c] & 0xFFFFu) : (d[c - 16] >> 16));
+    return warp_transpose_reduce(v);
+}
+
 // ---------------------------------------------------------------------------
 // Streaming vector loads: read-only path, no L1 allocation (each byte is
 // touched exactly once).  VB = 16 -> LDG.E.NA.128 (512 B per warp),

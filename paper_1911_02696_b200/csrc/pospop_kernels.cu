@@ -119,8 +119,10 @@ const StreamVariant kStreamVariants[] = {
     SVF2(6, 32, 256, 2), SVF(4, 32, 1024, 2),
     // byte-frame FLAG statistics (MODE 2): defaults first
     SVB(5, 32, 512, 2), SVB(5, 32, 0, 2),
-    SVB(5, 32, 256, 2), SVB(4, 32, 512, 2), SVB(4, 32, 256, 2), SVB2(4, 32, 256, 2), SVB2(4, 32, 512, 2),
+    SVB(5, 32, 256, 2), SVB(4, 32, 512, 2), SVB(4, 32, 256, 2), SVB2(4, 32, 256, 2),
     SVB(4, 16, 512, 2), SVB(6, 32, 256, 2), SVB(5, 16, 512, 2), SVB2(5, 32, 256, 2),
+    SVB(4, 32, 512, 4), SVB(4, 16, 512, 4), SVB(3, 32, 512, 4), SVB(4, 32, 256, 4), SVB2(3, 32, 256, 4),
+    SVB(5, 32, 256, 4),
 };
 #undef SV
 #undef SVF
@@ -146,12 +148,13 @@ struct TmaVariant {
 
 #define TV(NB, L, M, NC, ST)                                                                \
     {NB, L, M, NC, ST, stream_tma_kernel<NB, L, M, NC, ST>,                               \
-     (size_t)(ST) * (NC) * 32 * (((M) == 1 ? (1 << (L)) : ((NB) << (L))) / 4) * 16}
+     (size_t)(ST) * (NC) * 32 * (((M) == 1 ? (1 << (L)) : (M) == 2 ? (2 << (L)) : ((NB) << (L))) / 4) * 16}
 const TmaVariant kTmaVariants[] = {
     TV(1, 5, 0, 8, 6), TV(1, 6, 0, 8, 3), TV(1, 5, 0, 8, 4), TV(1, 4, 0, 8, 6), TV(1, 5, 0, 4, 6),
     TV(2, 4, 0, 8, 6), TV(2, 5, 0, 8, 3),
     TV(2, 5, 1, 8, 6), TV(2, 4, 1, 8, 6), TV(2, 6, 1, 8, 3), TV(2, 5, 1, 16, 3), TV(2, 4, 1, 16, 6),
     TV(2, 5, 1, 12, 4),
+    TV(3, 5, 2, 12, 2), TV(3, 5, 2, 8, 3), TV(3, 4, 2, 15, 3), TV(3, 4, 2, 12, 4), TV(3, 4, 2, 8, 6),
 };
 #undef TV
 
@@ -276,6 +279,9 @@ static cudaError_t launch_stream_tma(int mode, int nbank, int depth, int k, cons
     }
     StreamArgs a;
     fill_stream_args(a, k, data, len_words, 16, d_out, accumulate, opt, ws);
+    const int env_thr = env_int("POSPOP_FLUSH_THRESHOLD", 0);
+    if (env_thr > 0 && (uint32_t)env_thr < a.flush_threshold) a.flush_threshold = (uint32_t)env_thr;
+    if (mode == 2 && a.flush_threshold > 255) a.flush_threshold = 255;  // byte-lane counters
     const int grid = device_info().sms;
     if (grid_used) *grid_used = grid;
     return launch_with_pdl(var->fn, grid, 32 * (var->nc + 1), var->smem, stream, a);

@@ -66,6 +66,13 @@ __device__ __forceinline__ void pdl_wait_prev() { asm volatile("griddepcontrol.w
 // p are p + m * k for m = 0 .. 32/k - 1 (k <= 32), or channel p (k = 64).
 __device__ __forceinline__ int channels_per_position(int k) { return k >= 32 ? 1 : 32 / k; }
 
+// Byte-frame FLAG mode with shallow trees (L <= 4): two consecutive tiles are
+// joined by one more CSA level, so the byte-lane extract runs once per pair.
+// (At L = 5 the two extra carry words per bank cost more in spills than the
+// halved extract saves.)
+template <int MODE, int L>
+__host__ __device__ constexpr bool pair_tiles() { return MODE == 2 && L <= 4; }
+
 template <int NBANK, int L>
 __device__ __forceinline__ void tree_block(const uint32_t (&r)[NBANK << L], uint32_t (&carries)[NBANK][L],
                                            uint32_t (&counter)[NBANK][16]) {
@@ -76,9 +83,6 @@ __device__ __forceinline__ void tree_block(const uint32_t (&r)[NBANK << L], uint
         extract(counter[1], Tree<L, 2>::run(carries[1], r + 1));
     }
 }
-
-__device__ __forceinline__ uint32_t bank_warp_total_bytes(const uint32_t (&counter)[16], int shift,
-                                                          const uint32_t (&d)[16]);
 
 template <int NBANK>
 __device__ __forceinline__ void zero_bank(uint32_t (&counter)[NBANK][16]) {
@@ -132,7 +136,9 @@ __device__ __forceinline__ void flush_bank_to_smem(uint32_t (&counter)[NBANK][16
     for (int p = 0; p < 16; ++p) d[p] = 0;
 #pragma unroll
     for (int b = 0; b < NBANK; ++b) {
-        const uint32_t tot = MODE == 2 ? bank_warp_total_bytes(counter[b], L, d) : bank_warp_total(counter[b], L, d);
+        // paired tiles extract once per pair: weight 2^(L+1)
+        constexpr int W = pair_tiles<MODE, L>() ? L + 1 : L;
+        const uint32_t tot = MODE == 2 ? bank_warp_total_bytes(counter[b], W, d) : bank_warp_total(counter[b], W, d);
         if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
     }
     zero_bank<NBANK>(counter);
@@ -142,17 +148,25 @@ __device__ __forceinline__ void flush_bank_to_smem(uint32_t (&counter)[NBANK][16
 // the global accumulator, ticket; the last CTA folds channels to positions,
 // writes/accumulates out[k] and leaves the scratch (acc, ticket, chunk
 // counter) zeroed for the next launch.
-template <int NBANK, int L, int MODE>
-__device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carries)[NBANK][L],
+template <int NBANK, int L, int MODE, int CD>
+__device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carries)[NBANK][CD],
                                            uint32_t (&counter)[NBANK][16], unsigned long long* s_acc,
                                            int* s_last, unsigned block, uint32_t lane) {
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer();
     pdl_wait_prev();  // the previous launch on this stream owns acc/ticket/next until it completes
+    if constexpr (pair_tiles<MODE, L>()) {  // fold a pending (unpaired) top into level L
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b) {
+            extract_bytes(counter[b], carries[b][L] & carries[b][L + 1]);
+            carries[b][L] ^= carries[b][L + 1];
+        }
+    }
 #pragma unroll
     for (int b = 0; b < NBANK; ++b) {
         uint32_t d[16];
-        drain<L>(d, carries[b]);
-        const uint32_t tot = MODE == 2 ? bank_warp_total_bytes(counter[b], L, d) : bank_warp_total(counter[b], L, d);
+        constexpr int W = pair_tiles<MODE, L>() ? L + 1 : L;  // carry levels / counter weight 2^W
+        drain<W>(d, carries[b]);
+        const uint32_t tot = MODE == 2 ? bank_warp_total_bytes(counter[b], W, d) : bank_warp_total(counter[b], W, d);
         if (tot) atomicAdd(&s_acc[b * 32 + lane], (unsigned long long)tot);
     }
     __syncthreads();
@@ -310,11 +324,10 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 }
 
 __device__ __forceinline__ void flag_leaf(uint32_t r0, uint32_t r1, uint32_t& al, uint32_t& fl, uint32_t& ahf,
-                                          uint32_t& bad) {
+                                          uint32_t& hb) {
     constexpr uint32_t B1 = 0x01010101u;
     const uint32_t lb = prmt(r0, r1, 0x6420u);
-    const uint32_t hb = prmt(r0, r1, 0x7531u);
-    bad |= hb;
+    hb = prmt(r0, r1, 0x7531u);
     const uint32_t g = lb & ~hb & ~shr_fma<3>(hb) & B1;        // paired & !secondary & !supplementary
     const uint32_t gu = g & ~shr_fma<2>(lb);                    // ... & !unmapped
     const uint32_t t = g * 0xC0u + gu * 0x0Bu;                  // G -> bits 6,7 ; GU -> bits 0,1,3
@@ -325,17 +338,19 @@ __device__ __forceinline__ void flag_leaf(uint32_t r0, uint32_t r1, uint32_t& al
     ahf = ah | (shl_fma<4>(ah) & mf);
 }
 
-template <int LT, int L = LT>
+template <int CD, int L>
 struct FlagByteTree {  // 2^L leaves = 2^(L+1) input registers; c[b][j] = carry of weight 2^j
-    static __device__ __forceinline__ void run(uint32_t (&c)[3][LT], const uint32_t* in, uint32_t (&top)[3],
+    static __device__ __forceinline__ void run(uint32_t (&c)[3][CD], const uint32_t* in, uint32_t (&top)[3],
                                                uint32_t& bad) {
         uint32_t x[3], y[3];
         if constexpr (L == 1) {
-            flag_leaf(in[0], in[1], x[0], x[1], x[2], bad);
-            flag_leaf(in[2], in[3], y[0], y[1], y[2], bad);
+            uint32_t hx, hy;
+            flag_leaf(in[0], in[1], x[0], x[1], x[2], hx);
+            flag_leaf(in[2], in[3], y[0], y[1], y[2], hy);
+            bad = bad | hx | hy;  // one LOP3 per two leaves
         } else {
-            FlagByteTree<LT, L - 1>::run(c, in, x, bad);
-            FlagByteTree<LT, L - 1>::run(c, in + (2 << (L - 1)), y, bad);
+            FlagByteTree<CD, L - 1>::run(c, in, x, bad);
+            FlagByteTree<CD, L - 1>::run(c, in + (2 << (L - 1)), y, bad);
         }
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
@@ -347,22 +362,6 @@ struct FlagByteTree {  // 2^L leaves = 2^(L+1) input registers; c[b][j] = carry 
     }
 };
 
-// Byte-lane counters: counter[p] byte lane j counts channel 8j + p (p < 8);
-// a lane takes at most 255 extracts between flushes.
-__device__ __forceinline__ void extract_bytes(uint32_t (&counter)[16], uint32_t top) {
-#pragma unroll
-    for (int p = 0; p < 8; ++p) counter[p] += (top >> p) & 0x01010101u;
-}
-
-__device__ __forceinline__ uint32_t bank_warp_total_bytes(const uint32_t (&counter)[16], int shift,
-                                                          const uint32_t (&d)[16]) {
-    uint32_t v[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-        v[c] = (((counter[c & 7] >> (8 * (c >> 3))) & 0xFFu) << shift) +
-               (c < 16 ? (d[c] & 0xFFFFu) : (d[c - 16] >> 16));
-    return warp_transpose_reduce(v);
-}
 
 // Rare path: this thread's tile holds a FLAG word with reserved bits 12-15
 // set; report the smallest such word index through a.bad (max of ~index).
@@ -391,19 +390,34 @@ __device__ __forceinline__ void flag_locate_bad(const StreamArgs& a, const uint3
 // words of all reads and bank 1 those of QC-fail reads; words with reserved bits 12-15 set are
 // reported through a.bad (the first such index wins, as the reference's
 // check_reserved throws at the first one, flagstats.cpp:34-36).
-template <int MODE, int NBANK, int L, int VB, int REGS>
+template <int MODE, int NBANK, int L, int VB, int REGS, int CD>
 __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)[REGS], unsigned long long first,
-                                        unsigned stride, uint32_t (&carries)[NBANK][L],
-                                        uint32_t (&counter)[NBANK][16]) {
+                                        unsigned stride, uint32_t (&carries)[NBANK][CD],
+                                        uint32_t (&counter)[NBANK][16], uint32_t& phase) {
     if constexpr (MODE == 0) {
         tree_block<NBANK, L>(r, carries, counter);
     } else if constexpr (MODE == 2) {
         static_assert(NBANK == 3 && REGS == (2 << L), "byte-frame FLAG mode: three banks, 2^(L+1) registers");
         constexpr int RPV = VB / 4;
         uint32_t bad = 0, top[3];
-        FlagByteTree<L>::run(carries, r, top, bad);
+        FlagByteTree<CD, L>::run(carries, r, top, bad);
+        if constexpr (!pair_tiles<MODE, L>()) {
 #pragma unroll
-        for (int b = 0; b < 3; ++b) extract_bytes(counter[b], top[b]);
+            for (int b = 0; b < 3; ++b) extract_bytes(counter[b], top[b]);
+        } else if (phase) {  // second tile of the pair: level-L CSA, one extract per two tiles
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                uint32_t h, l;
+                csa(h, l, carries[b][L], carries[b][L + 1], top[b]);
+                carries[b][L] = l;
+                carries[b][L + 1] = 0;
+                extract_bytes(counter[b], h);
+            }
+        } else {
+#pragma unroll
+            for (int b = 0; b < 3; ++b) carries[b][L + 1] = top[b];
+        }
+        phase ^= 1u;
         if (bad & 0xF0F0F0F0u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
     } else {
         static_assert(NBANK == 2 && REGS == (1 << L), "FLAG mode: two banks of 2^L registers");
@@ -446,12 +460,16 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
 
-    uint32_t carries[NBANK][L];
+    // MODE 2 keeps two extra words per bank: the level-L carry and the pending
+    // top of the previous tile (tiles are paired into one depth-L+1 tree).
+    constexpr int CD = pair_tiles<MODE, L>() ? L + 2 : L;
+    uint32_t carries[NBANK][CD];
     uint32_t counter[NBANK][16];
+    uint32_t phase = 0;
 #pragma unroll
     for (int b = 0; b < NBANK; ++b)
 #pragma unroll
-        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+        for (int j = 0; j < CD; ++j) carries[b][j] = 0;
     zero_bank<NBANK>(counter);
     uint32_t nb = 0;
 
@@ -474,8 +492,74 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
 #pragma unroll
                         for (int j = 0; j < RPV; ++j) r[v * RPV + j] = 0;
             }
-            consume<MODE, NBANK, L, VB>(a, r, t + threadIdx.x, block, carries, counter);
+            consume<MODE, NBANK, L, VB>(a, r, t + threadIdx.x, block, carries, counter, phase);
             if (++nb == a.flush_threshold) {  // block-uniform: every thread runs the same tiles
+                flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
+                nb = 0;
+            }
+        }
+    } else if constexpr (SCHED == 4) {
+        // SCHED 2's work split with double-buffered tile registers: the next
+        // warp tile is claimed and its loads issued before the current tile is
+        // consumed, so each warp keeps a tile in flight while it computes
+        // (for the ALU-heavy FLAG mode, whose warps would otherwise alternate
+        // between waiting and computing).
+        constexpr unsigned long long WT = 32ull * VPT;
+        const unsigned long long S0 = a.g0 * 32;
+        const unsigned long long P = a.nwt - a.pool;
+        const unsigned long long lo = P * blockIdx.x / gridDim.x;
+        const unsigned long long hi = P * (blockIdx.x + 1) / gridDim.x;
+        constexpr unsigned long long kEnd = ~0ull;
+        __shared__ unsigned s_claim;
+        if (threadIdx.x == 0) s_claim = 0u;
+        __syncthreads();
+        bool local = true;
+        unsigned long long pw = 0, pe = 0;  // current pool chunk [pw, pe)
+        unsigned long long pm = 0;          // prefetched pool chunk index (lane 0)
+        // Warp-uniform: the next warp tile of this warp, or kEnd.
+        auto claim = [&]() -> unsigned long long {
+            if (local) {
+                const unsigned m = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
+                const unsigned long long w = lo + __shfl_sync(0xFFFFFFFFu, m, 0);
+                if (w < hi) return w;
+                local = false;
+                if (!a.pool) return kEnd;
+                pdl_wait_prev();  // the pool counter is shared with the previous launch
+                pm = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            }
+            if (pw >= pe) {
+                const unsigned long long c = __shfl_sync(0xFFFFFFFFu, pm, 0);
+                pm = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+                pw = P + c * a.CB;
+                if (pw >= a.nwt) {
+                    pe = pw;
+                    return kEnd;
+                }
+                pe = pw + a.CB < a.nwt ? pw + a.CB : a.nwt;
+            }
+            return pw++;
+        };
+        auto load = [&](unsigned long long w, uint32_t (&r)[REGS]) {
+            const unsigned long long t = S0 + w * WT;
+            load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
+        };
+        uint32_t ra[REGS], rb[REGS];
+        unsigned long long w0 = claim();
+        if (w0 != kEnd) load(w0, ra);
+        for (;;) {
+            if (w0 == kEnd) break;
+            const unsigned long long w1 = claim();
+            if (w1 != kEnd) load(w1, rb);
+            consume<MODE, NBANK, L, VB>(a, ra, S0 + w0 * WT + lane, 32u, carries, counter, phase);
+            if (++nb == a.flush_threshold) {
+                flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
+                nb = 0;
+            }
+            if (w1 == kEnd) break;
+            w0 = claim();
+            if (w0 != kEnd) load(w0, ra);
+            consume<MODE, NBANK, L, VB>(a, rb, S0 + w1 * WT + lane, 32u, carries, counter, phase);
+            if (++nb == a.flush_threshold) {
                 flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                 nb = 0;
             }
@@ -501,7 +585,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
             const unsigned long long t = S0 + w * WT;
             uint32_t r[REGS];
             load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
-            consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
+            consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter, phase);
             if (++nb == a.flush_threshold) {  // warp-uniform
                 flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                 nb = 0;
@@ -522,7 +606,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                     const unsigned long long t = S0 + ww * WT;
                     uint32_t r[REGS];
                     load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
-                    consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
+                    consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter, phase);
                     if (++nb == a.flush_threshold) {
                         flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                         nb = 0;
@@ -553,7 +637,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                 const unsigned long long t = S0 + w * WT;
                 uint32_t r[REGS];
                 load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
-                consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter);
+                consume<MODE, NBANK, L, VB>(a, r, t + lane, 32u, carries, counter, phase);
                 if (++nb == a.flush_threshold) {  // warp-uniform
                     flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                     nb = 0;
@@ -642,12 +726,16 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) stream_tma_kernel(const Stre
     pdl_allow_next();
     __syncthreads();
 
-    uint32_t carries[NBANK][L];
+    // MODE 2 keeps two extra words per bank: the level-L carry and the pending
+    // top of the previous tile (tiles are paired into one depth-L+1 tree).
+    constexpr int CD = pair_tiles<MODE, L>() ? L + 2 : L;
+    uint32_t carries[NBANK][CD];
     uint32_t counter[NBANK][16];
+    uint32_t phase = 0;
 #pragma unroll
     for (int b = 0; b < NBANK; ++b)
 #pragma unroll
-        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+        for (int j = 0; j < CD; ++j) carries[b][j] = 0;
     zero_bank<NBANK>(counter);
 
     const unsigned long long S0 = a.g0 * 32;
@@ -702,7 +790,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) stream_tma_kernel(const Stre
                 for (int j = 0; j < 4; ++j) r[v * 4 + j] = x[j];
             }
             mbar_arrive(&empty[s]);  // this lane's reads are in registers: the slot may be refilled
-            consume<MODE, NBANK, L, 16>(a, r, first, 32u, carries, counter);
+            consume<MODE, NBANK, L, 16>(a, r, first, 32u, carries, counter, phase);
             if (++nb == a.flush_threshold) {  // warp-uniform
                 flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                 nb = 0;

@@ -12,7 +12,9 @@ pytestmark = pytest.mark.gpu
 
 TMA_STREAM = [("5,32,0,256,3", "8,6"), ("6,32,0,256,3", "8,3"), ("4,32,0,256,3", "8,6"), ("5,32,0,256,3", "4,6")]
 TMA_STREAM64 = [("4,32,0,256,3", "8,6"), ("5,32,0,256,3", "8,3")]
-TMA_FLAG = [("5,32,0,256,3", "8,6"), ("6,32,0,256,3", "8,3"), ("5,32,0,256,3", "16,3"), ("4,32,0,256,3", "16,6")]
+TMA_FLAG = [("5,32,0,256,3", "8,6"), ("6,32,0,256,3", "8,3"), ("5,32,0,256,3", "16,3"), ("4,32,0,256,3", "16,6"),
+            ("5,32,0,512,3,2", "12,2"), ("5,32,0,512,3,2", "8,3"), ("4,32,0,512,3,2", "15,3"),
+            ("4,32,0,512,3,2", "12,4"), ("4,32,0,512,3,2", "8,6")]
 
 
 def guarded(a, offset, guard=64):
@@ -61,9 +63,12 @@ def test_tma_forced_flush_and_full_size(pp, dev, orc, monkeypatch):
 
 
 @pytest.mark.parametrize("var,tma", TMA_FLAG)
-def test_tma_flagstats(pp, dev, orc, golden, var, tma, monkeypatch):
+@pytest.mark.parametrize("flush", [None, "1"])
+def test_tma_flagstats(pp, dev, orc, golden, var, tma, flush, monkeypatch):
     monkeypatch.setenv("POSPOP_FLAG_VARIANT", var)
     monkeypatch.setenv("POSPOP_TMA", tma)
+    if flush:
+        monkeypatch.setenv("POSPOP_FLUSH_THRESHOLD", flush)
     streams = orc.acceptance_flag_streams()
     for i in range(0, 100, 7):
         assert pp.flagstats(torch.from_numpy(streams[i].view(np.int16).copy()).cuda()).as_list() == \
