@@ -47,7 +47,12 @@ WORKLOADS = {
     "cfg2": (16, 2, 1 << 28, "cfg2: 2^28 u16 one-hot words, position Zipf(1.1), k=16 u64 counters"),
     "cfg3": (8, 3, (1 << 30) - 7, "cfg3: 2^30-7 u8 words at a +3 byte offset, 4 KiB runs one-hot/uniform, "
                                   "k=8 u64 counters"),
+    # SURVEY 8f row f1 (not the headline metric): flagstats_pospopcnt over SAM FLAG words
+    "flag": (16, 7, 1 << 32, "flag: 2^32 SAM FLAG words (12 valid bits, realistic flag mix), "
+                             "flagstats_pospopcnt pass/fail buckets in one fused pass; contiguous shards, "
+                             "20-counter summary summed across GPUs"),
 }
+FLAG_METRIC = "flagstats_pospopcnt input GB/s (SAM FLAG words) vs host CPU"
 
 
 def parse():
@@ -194,10 +199,33 @@ def cpu_reference_measure(k: int, gen_kind: int, sample_words: int, reps: int, t
     return nbytes / min(times) / 1e9, nbytes / statistics.median(times) / 1e9, kind, counts, nbytes / t1 / 1e9
 
 
+def ref_flagstats_mt(words, threads):
+    """The reference's flagstats_pospopcnt (flagstats.cpp:127-145) fork-joined
+    over `threads` contiguous chunks (ctypes releases the GIL); the 20-counter
+    summaries add.  Returns the summed out20."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    ref = pyoracle.Reference()
+    n = words.size
+    cuts = [n * i // threads for i in range(threads + 1)]
+
+    def one(i):
+        rc, out, _ = ref.flagstats(words[cuts[i]:cuts[i + 1]])
+        assert rc == 0
+        return out
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(one, range(threads)))
+    return np.sum(parts, axis=0, dtype=np.uint64)
+
+
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return 0
+    if args.workload == "flag":
+        return run_reference_flag(args)
     k, gen_kind, total, desc = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     # bounded sample: 2^28 words of the workload stream per step (512 MiB for u16)
@@ -241,9 +269,193 @@ def run_reference(args):
     return 0
 
 
+def run_reference_flag(args):
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    k, gen_kind, total, desc = WORKLOADS["flag"]
+    threads = os.cpu_count() or 1
+    sample = min(total, 1 << 27)
+    words = pyoracle.Oracle().generate(gen_kind, 1, sample, threads=threads)
+    for _ in range(max(args.warmup, 1)):
+        ref_flagstats_mt(words, threads)
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref_flagstats_mt(words, threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > 240:
+            break
+    mean = sum(times) / len(times)
+    gbs = words.nbytes / mean / 1e9
+    line = {
+        "impl": "reference", "metric": FLAG_METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 4), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": desc, "sample_words_per_step": sample, "host_threads": threads},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"first {sample} words of the flag stream per step; pospop::flagstats_pospopcnt "
+                                   f"fork-joined over {threads} chunks, summaries summed"},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
+
+def run_ours_flag(args):
+    """Row f1: one pospop_flagstats C-ABI call per step over this rank's shard of
+    device-resident FLAG words (one fused kernel launch + the 33-counter D2H);
+    N > 1 sums the 20-counter summaries with one all-reduce."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1911_02696_b200 as pp
+
+    world, rank, local = dist_env()
+    backend = os.environ.get("POSPOP_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    k, gen_kind, total, desc = WORKLOADS["flag"]
+    lo, hi = (rank * total, (rank + 1) * total) if args.scaling == "weak" else \
+        (total * rank // world, total * (rank + 1) // world)
+    words = hi - lo
+    data = torch.empty(words, dtype=torch.int16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    pp.generate(gen_kind, 1, data, base=lo, n=words, stream=stream)
+    torch.cuda.synchronize(dev)
+    lib = pp._load()
+    summ = pp._Summary()
+    fields = pp._BUCKET_FIELDS
+    red = torch.zeros(2 * len(fields), dtype=torch.int64, device=dev)
+
+    def step():
+        assert lib.pospop_flagstats(data.data_ptr(), words, C.byref(summ), None, None) == 0
+        if world > 1:
+            vals = [getattr(summ.pass_, f) for f in fields] + [getattr(summ.fail, f) for f in fields]
+            red.copy_(torch.tensor(vals, dtype=torch.int64))
+            dist.all_reduce(red)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = pp.kernel_launches()
+    sampler = ClockSampler(local, args.clock_interval_ms / 1e3)
+    with sampler:
+        t_begin.record(stream)
+        for _ in range(args.steps):
+            step()
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = pp.kernel_launches() - launches0
+    elapsed_ms = t_begin.elapsed_time(t_end)
+    # kernel alone: events around single launches of the same call
+    iso = []
+    for _ in range(5):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        assert lib.pospop_flagstats(data.data_ptr(), words, C.byref(summ), None, None) == 0
+        a1.record(stream)
+        a1.synchronize()
+        iso.append(a0.elapsed_time(a1))
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t[0])
+    ms_per_step = elapsed_ms / args.steps
+    total_bytes = total * (world if args.scaling == "weak" else 1) * 2
+    value = total_bytes / (ms_per_step * 1e-3) / 1e9
+    kern_ms = elapsed_ms / args.steps if world == 1 else statistics.median(iso)
+    per_launch_bytes = words * 2
+    achieved = per_launch_bytes / (kern_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(words, dtype=torch.int16, pin_memory=True)
+        host.copy_(data)
+        host_arr = host.numpy().view(np.uint16)
+        want = pp.flagstats(host_arr).as_list()
+        e2e_steps = max(1, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            got = pp.flagstats(host_arr)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        assert got.as_list() == want
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(total_bytes / float(tt[0]) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": words * 2, "d2h_bytes_per_step": 33 * 8, "steps": e2e_steps,
+               "path": "pospop_flagstats C ABI on a pinned host buffer (staged H2D ring overlapped with the kernel)"}
+        del host
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        sample = min(words, 1 << 27)
+        host_sample = data[:sample].cpu().numpy().view(np.uint16)
+        ref_flagstats_mt(host_sample, threads)
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            ref_out = ref_flagstats_mt(host_sample, threads)
+            dt = time.perf_counter() - t0
+            best = dt if best is None or dt < best else best
+        gpu = pp.flagstats(data[:sample])
+        assert [int(x) for x in ref_out] == gpu.as_list(), "correctness gate: GPU and reference flagstats disagree"
+        cpu = {"value": round(host_sample.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads,
+               "kind": "reference",
+               "sample": f"first {sample} words ({sample * 2 >> 20} MiB) of the flag stream; "
+                         f"pospop::flagstats_pospopcnt fork-joined over {threads} chunks, best of 3; "
+                         f"summary equals the GPU's"}
+
+    line = {
+        "metric": FLAG_METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u16",
+        "data": "synthetic (counter-based FLAG generator, generated in place in HBM)",
+        "config": {"workload": desc, "words_total": total, "bytes_per_step": total_bytes,
+                   "parallelism": f"shard{world}", "l2_policy": "input >> 126 MB L2; no flush needed",
+                   "kernel": "stream_kernel<NBANK=3,L=5,VB=32,BLOCK=512,SCHED=2,MODE=2>: byte-frame FLAG "
+                             "transform (PRMT regroup, 4 words per SWAR op) + three Harley-Seal trees; one "
+                             "launch + 33-counter D2H per step"},
+        "words_per_s": round(total_bytes / 2 / (ms_per_step * 1e-3), 1),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic("flag", world),
+                     "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
+                     "kernel_ms_isolated": round(statistics.median(iso), 5),
+                     "timing": "CUDA events around K synchronous C-ABI calls (kernel + 264-byte D2H each)",
+                     "bytes_per_launch": per_launch_bytes,
+                     "frac_of_theoretical_8180": round(achieved / 8180.0, 4)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
 
 def run_ours(args):
     import numpy as np
@@ -453,6 +665,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "flag":
+        return run_ours_flag(args)
     return run_ours(args)
 
 
