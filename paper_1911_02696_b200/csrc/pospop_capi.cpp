@@ -116,6 +116,10 @@ struct Ctx {
     cudaStream_t copy = nullptr;
     unsigned long long* d_out = nullptr;  // 64 u64
     unsigned long long* h_out = nullptr;  // 64 u64, pinned
+    // Synchronous calls let the kernel's last CTA write the result straight
+    // into mapped pinned memory: no D2H copy on the small-call latency path.
+    unsigned long long* m_out = nullptr;      // 64 u64, pinned + mapped (host view)
+    unsigned long long* m_out_dev = nullptr;  // its device view
     StreamWorkspace ws;
     void* stage[kRing] = {nullptr, nullptr, nullptr};
     void* bounce = nullptr;  // pinned host buffer for small host inputs (kBounceBytes)
@@ -152,6 +156,8 @@ pospop_status get_ctx(int dev, Ctx** out) {
     CU(cudaStreamCreateWithFlags(&c->copy, cudaStreamDefault));
     CU(cudaMalloc(&c->d_out, 64 * sizeof(unsigned long long)));
     CU(cudaMallocHost(&c->h_out, 64 * sizeof(unsigned long long)));
+    CU(cudaHostAlloc(&c->m_out, 64 * sizeof(unsigned long long), cudaHostAllocMapped));
+    CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->m_out_dev), c->m_out, 0));
     if ((s = alloc_workspace(&c->ws))) return s;
     t_ctx[dev] = c;
     *out = c;
@@ -239,7 +245,7 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
     if ((s = get_ctx(dev, &c))) return s;
 
     if (where == Where::Device) {
-        CU(launch_stream(k, data, len, c->d_out, false, opt, c->ws, c->stream));
+        CU(launch_stream(k, data, len, c->m_out_dev, false, opt, c->ws, c->stream));
     } else if (len * wb <= kBounceBytes) {
         // Small host input (the latency path): one DMA (from
         // the caller's pinned memory, or via a pinned bounce buffer for
@@ -252,7 +258,7 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
             src = c->bounce;
         }
         CU(cudaMemcpyAsync(c->stage[0], src, len * wb, cudaMemcpyHostToDevice, c->stream));
-        CU(launch_stream(k, c->stage[0], len, c->d_out, false, opt, c->ws, c->stream));
+        CU(launch_stream(k, c->stage[0], len, c->m_out_dev, false, opt, c->ws, c->stream));
     } else {
         // Host input: chunked H2D on the copy stream, counting on the compute
         // stream, kRing staging buffers recycled behind ev_done.
@@ -267,14 +273,12 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
             CU(cudaMemcpyAsync(c->stage[slot], src + off * wb, n * wb, cudaMemcpyHostToDevice, c->copy));
             CU(cudaEventRecord(c->ev_copied[slot], c->copy));
             CU(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
-            CU(launch_stream(k, c->stage[slot], n, c->d_out, i > 0, opt, c->ws, c->stream));
+            CU(launch_stream(k, c->stage[slot], n, c->m_out_dev, i > 0, opt, c->ws, c->stream));
             CU(cudaEventRecord(c->ev_done[slot], c->stream));
         }
     }
-    CU(cudaMemcpyAsync(c->h_out, c->d_out, (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                       c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    for (int p = 0; p < k; ++p) out[p] = c->h_out[p];
+    CU(cudaStreamSynchronize(c->stream));  // the last CTA wrote c->m_out (mapped)
+    for (int p = 0; p < k; ++p) out[p] = c->m_out[p];
     return POSPOP_OK;
 }
 
@@ -468,7 +472,7 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
     if ((s = get_ctx(dev, &c))) return s;
     LaunchOptions opt;
     if (where == Where::Device) {
-        CU(launch_flagstats(flags, len, c->d_out, false, opt, c->ws, c->stream));
+        CU(launch_flagstats(flags, len, c->m_out_dev, false, opt, c->ws, c->stream));
     } else {
         if ((s = ensure_stage(c))) return s;
         const size_t chunk_words = c->stage_bytes / 2;
@@ -481,15 +485,14 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
             CU(cudaEventRecord(c->ev_copied[slot], c->copy));
             CU(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
             opt.word_base = off;
-            CU(launch_flagstats(static_cast<const uint16_t*>(c->stage[slot]), n, c->d_out, i > 0, opt, c->ws,
-                                c->stream));
+            CU(launch_flagstats(static_cast<const uint16_t*>(c->stage[slot]), n, c->m_out_dev, i > 0, opt,
+                                c->ws, c->stream));
             CU(cudaEventRecord(c->ev_done[slot], c->stream));
         }
     }
-    CU(cudaMemcpyAsync(c->h_out, c->d_out, 33 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    if (c->h_out[32]) {
-        const uint64_t idx = ~c->h_out[32];
+    CU(cudaStreamSynchronize(c->stream));  // the last CTA wrote c->m_out (mapped)
+    if (c->m_out[32]) {
+        const uint64_t idx = ~c->m_out[32];
         uint16_t word = 0;
         if (where == Where::Device)
             CU(cudaMemcpy(&word, flags + idx, 2, cudaMemcpyDeviceToHost));
@@ -502,7 +505,7 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
     }
     // Kernel output: [0,16) counts over all reads, [16,32) over QC-fail reads;
     // QC-pass = all - fail (flagstats.cpp:137-143 counts the two streams).
-    const uint64_t* ac = reinterpret_cast<const uint64_t*>(c->h_out);
+    const uint64_t* ac = reinterpret_cast<const uint64_t*>(c->m_out);
     const uint64_t* fc = ac + 16;
     uint64_t pc[16];
     for (int p = 0; p < 16; ++p) pc[p] = ac[p] - fc[p];

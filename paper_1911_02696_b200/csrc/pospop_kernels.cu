@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -28,6 +29,8 @@
 #include "pospop_launch.h"
 #include "pospop_segmented.cuh"
 #include "pospop_stream.cuh"
+
+extern char** environ;
 
 namespace pospop_b200 {
 
@@ -45,8 +48,33 @@ constexpr int kDefaultBlock = 256;
 constexpr int kDefaultDepth1 = 7;  // k = 8/16/32: 128 registers = 512 B per thread per tree block
 constexpr int kDefaultDepth2 = 6;  // k = 64: two banks of 64 registers
 
+// Tuning knobs (POSPOP_*) are read from one snapshot of the environment
+// taken at the top of each public launcher: a single pass over `environ`
+// instead of a getenv() scan per knob (~0.25 us each with ~130 variables --
+// several microseconds on the small-call latency path otherwise).
+struct EnvSnapshot {
+    static constexpr int kMax = 32;
+    const char* entry[kMax];
+    int n = 0;
+};
+thread_local EnvSnapshot t_env;
+
+void env_refresh() {
+    t_env.n = 0;
+    for (char** e = environ; e && *e; ++e)
+        if ((*e)[0] == 'P' && std::strncmp(*e, "POSPOP_", 7) == 0 && t_env.n < EnvSnapshot::kMax)
+            t_env.entry[t_env.n++] = *e;
+}
+
+const char* env_get(const char* name) {
+    const size_t len = std::strlen(name);
+    for (int i = 0; i < t_env.n; ++i)
+        if (std::strncmp(t_env.entry[i], name, len) == 0 && t_env.entry[i][len] == '=') return t_env.entry[i] + len + 1;
+    return nullptr;
+}
+
 int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
+    const char* v = env_get(name);
     return v && *v ? std::atoi(v) : dflt;
 }
 
@@ -260,7 +288,7 @@ static cudaError_t launch_stream_tma(int mode, int nbank, int depth, int k, cons
                                      unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
                                      const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
     int nc = 8, stages = mode == 1 ? 6 : 6;
-    if (const char* v = std::getenv("POSPOP_TMA")) std::sscanf(v, "%d,%d", &nc, &stages);
+    if (const char* v = env_get("POSPOP_TMA")) std::sscanf(v, "%d,%d", &nc, &stages);
     const TmaVariant* var = pick_tma(nbank, depth, mode, nc, stages);
     if (!var) return cudaErrorInvalidConfiguration;
     static std::mutex mu;
@@ -297,12 +325,12 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
         block = mode == 0 ? kDefaultBlock : 512, sched = 2;
     if (mode != 0) {
         int fmode = mode;
-        if (const char* v = std::getenv("POSPOP_FLAG_VARIANT")) {
+        if (const char* v = env_get("POSPOP_FLAG_VARIANT")) {
             const int n = std::sscanf(v, "%d,%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched, &fmode);
             if (n < 6) fmode = 1;  // five-field strings name the 16-bit-lane kernel (r01 sweeps)
         }
         mode = fmode;
-    } else if (const char* v = std::getenv("POSPOP_STREAM_VARIANT")) {
+    } else if (const char* v = env_get("POSPOP_STREAM_VARIANT")) {
         std::sscanf(v, "%d,%d,%d,%d,%d", &depth, &vb, &hint, &block, &sched);
     }
     const int nbank = mode == 2 ? 3 : (k == 64 || mode == 1) ? 2 : 1;
@@ -396,14 +424,35 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// Small inputs (<= POSPOP_SMALL_BYTES, default kSmallBytes): one CTA, no
+// workspace, no cross-CTA atomics or ticket -- the latency path (SURVEY 8f
+// row f3; the reference's Auto switches kernels below 4096 words too,
+// pospop.cpp:84-86).
+constexpr int kSmallBytes = 128 << 10;  // measured crossover (tools/latency): 128 KiB 13.7 vs 15.5 us
+
+static cudaError_t launch_small(int k, const void* data, size_t len_words, unsigned long long* d_out,
+                                bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
+                                cudaStream_t stream, int* grid_used) {
+    StreamArgs a;
+    fill_stream_args(a, k, data, len_words, 16, d_out, accumulate, opt, ws);
+    if (grid_used) *grid_used = 1;
+    return launch_with_pdl(k == 64 ? small_kernel<2> : small_kernel<1>, 1, kSmallBlock, 0, stream, a);
+}
+
 cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
                           bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
                           cudaStream_t stream, int* grid_used) {
+    env_refresh();
+    const size_t nbytes = len_words * (size_t)(k / 8);
+    if (nbytes <= (size_t)env_int("POSPOP_SMALL_BYTES", kSmallBytes) && !opt.grid && !opt.block && !opt.trace &&
+        !opt.depth && !env_get("POSPOP_STREAM_VARIANT"))
+        return launch_small(k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
     return launch_stream_mode(0, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
 }
 
 cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long long* d_out33, bool accumulate,
                              const LaunchOptions& opt, const StreamWorkspace& ws, cudaStream_t stream) {
+    env_refresh();
     return launch_stream_mode(2, 16, flags, len, d_out33, accumulate, opt, ws, stream, nullptr);
 }
 
@@ -411,11 +460,12 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
                              unsigned long long* d_out, const LaunchOptions& opt, const StreamWorkspace& ws,
                              cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
+    env_refresh();
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched".
     // measured: pipelined with 2 CTAs/SM (k <= 32), dynamic claiming (k = 64)
     int depth = 5, vb = 16, sched = nbank == 1 ? 3 : 1;
-    if (const char* v = std::getenv("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d", &depth, &vb, &sched);
+    if (const char* v = env_get("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d", &depth, &vb, &sched);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb, sched);
     if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 3 : 1);

@@ -651,6 +651,59 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
 }
 
 // ---------------------------------------------------------------------------
+// Small inputs (the latency path): ONE CTA counts 16-byte
+// vectors [v0, v1) (edges byte-masked like the stream kernel), four vectors
+// per thread per tree block (depth 4; k = 64: two depth-3 banks), then drains,
+// transpose-reduces per warp, sums channels in shared memory and writes
+// out[k] directly -- no workspace, no global atomics, no ticket, so the
+// launch is load latency + one reduction.
+// ---------------------------------------------------------------------------
+constexpr int kSmallBlock = 256;
+
+template <int NBANK>
+__global__ void __launch_bounds__(kSmallBlock, 1) small_kernel(const StreamArgs a) {
+    constexpr int VPT = 4, REGS = 16, L = NBANK == 1 ? 4 : 3;
+    static_assert((NBANK << L) == REGS, "one tree block = four 16-byte vectors");
+    constexpr unsigned long long TILE = (unsigned long long)VPT * kSmallBlock;
+    __shared__ uint32_t s_ch[32 * NBANK];
+    for (int i = threadIdx.x; i < 32 * NBANK; i += kSmallBlock) s_ch[i] = 0;
+    pdl_allow_next();
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    for (unsigned long long t = a.v0; t < a.v1; t += TILE) {
+        uint32_t r[REGS];
+        load_tree_block<16, 0, VPT>(a, t + threadIdx.x, kSmallBlock, t >= a.f0 && t + TILE <= a.f1, r);
+        tree_block<NBANK, L>(r, carries, counter);
+    }
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        uint32_t d[16];
+        drain<L>(d, carries[b]);
+        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        if (tot) atomicAdd(&s_ch[b * 32 + lane], tot);
+    }
+    __syncthreads();
+    pdl_wait_prev();  // out[] may belong to the previous launch on this stream
+    const int k = a.k;
+    for (int pos = threadIdx.x; pos < k; pos += kSmallBlock) {
+        unsigned long long sum = 0;
+        if (k == 64) {
+            sum = s_ch[pos];
+        } else {
+            for (int j = 0; j < channels_per_position(k); ++j) sum += s_ch[pos + j * k];
+        }
+        a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // TMA-staged variant (SCHED 3).  One producer warp per CTA pulls stage indices
 // from the global counter and moves each 32 KiB (NC warp tiles) stage of the
 // stream into a shared-memory ring with one cp.async.bulk (UBLKCP), tracked by
