@@ -150,6 +150,30 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
 
 
+def h2d_link_gbs(host, dev, nbytes: int = 1 << 30, reps: int = 3):
+    """The host->device link ceiling: a plain pinned cudaMemcpy of `nbytes`
+    (no counting), best of `reps`, CUDA events on a side stream."""
+    import torch
+    n = min(nbytes, host.numel())
+    if n < (64 << 20):
+        return None
+    dst = torch.empty(n, dtype=torch.uint8, device=dev)
+    src = host.view(torch.uint8)[:n]
+    s = torch.cuda.Stream(dev)
+    best = None
+    with torch.cuda.stream(s):
+        for _ in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            dst.copy_(src, non_blocking=True)
+            b.record(s)
+            b.synchronize()
+            ms = a.elapsed_time(b)
+            best = ms if best is None or ms < best else best
+    del dst
+    return round(n / (best * 1e-3) / 1e9, 2)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -405,6 +429,10 @@ def run_ours_flag(args):
         e2e = {"value": round(total_bytes / float(tt[0]) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": words * 2, "d2h_bytes_per_step": 33 * 8, "steps": e2e_steps,
                "path": "pospop_flagstats C ABI on a pinned host buffer (staged H2D ring overlapped with the kernel)"}
+        link = h2d_link_gbs(host, dev)
+        if link:
+            e2e["h2d_link_gbs"] = link
+            e2e["frac_of_h2d_link"] = round(e2e["value"] / world / link, 4)
         del host
 
     cpu = None
@@ -610,6 +638,10 @@ def run_ours(args):
                "h2d_bytes_per_step": words * wb, "d2h_bytes_per_step": k * 8, "steps": e2e_steps,
                "path": "pospopcnt_k C ABI on a pinned host buffer: chunked H2D (64 MiB x3 ring) overlapped "
                        "with the kernel, k-vector D2H"}
+        link = h2d_link_gbs(host, dev)
+        if link:
+            e2e["h2d_link_gbs"] = link
+            e2e["frac_of_h2d_link"] = round(e2e["value"] / world / link, 4)
         del host
 
     # ---- CPU baseline on the host (rank 0, N = 1 only) ----
