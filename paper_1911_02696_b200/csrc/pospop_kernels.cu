@@ -198,13 +198,19 @@ using SegKernel = void (*)(const uint8_t*, const unsigned long long*, unsigned l
 struct SegVariant {
     int nbank, depth, vb, sched;
     SegKernel fn;
+    int group = 0;  // sched 5: lanes per array
 };
 
 #define SG(NB, L, VB, S) {NB, L, VB, S, segmented_kernel<NB, L, VB, S>}
 #define SGP(NB, L, VB) {NB, L, VB, 2, segmented_pipe_entry<NB, L, VB>}
 #define SGP2(NB, L, VB) {NB, L, VB, 3, segmented_pipe_entry<NB, L, VB, 2>}  // sched 3: pipelined, 2 CTAs/SM
 #define SGP3(NB, L, VB) {NB, L, VB, 4, segmented_pipe_entry<NB, L, VB, 3>}  // sched 4: pipelined, 3 CTAs/SM
+// sched 5: grouped, G lanes per array, 2 CTAs/SM
+#define SGG(NB, L, VB, G) {NB, L, VB, 5, segmented_group_kernel<NB, L, VB, G, 2>, G}
 const SegVariant kSegVariants[] = {
+    SGG(1, 6, 16, 8), SGG(1, 6, 16, 4), SGG(1, 5, 16, 8), SGG(1, 6, 32, 8), SGG(1, 5, 32, 8), SGG(1, 5, 16, 4),
+    SGG(1, 6, 16, 16), SGG(1, 5, 32, 4),
+    SGG(2, 4, 16, 8), SGG(2, 4, 32, 8), SGG(2, 4, 16, 4),
     SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
     SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
     SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
@@ -214,12 +220,14 @@ const SegVariant kSegVariants[] = {
 };
 #undef SGP2
 #undef SGP3
+#undef SGG
 #undef SG
 #undef SGP
 
-const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched) {
+const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched, int group = 0) {
     for (const SegVariant& v : kSegVariants)
-        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.sched == sched) return &v;
+        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.sched == sched && (sched != 5 || v.group == group))
+            return &v;
     return nullptr;
 }
 
@@ -462,27 +470,33 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (n == 0) return cudaSuccess;
     env_refresh();
     const int nbank = k == 64 ? 2 : 1;
-    // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched".
+    // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched[,lanes per array]".
     // measured: pipelined with 2 CTAs/SM (k <= 32), dynamic claiming (k = 64)
-    int depth = 5, vb = 16, sched = nbank == 1 ? 3 : 1;
-    if (const char* v = env_get("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d", &depth, &vb, &sched);
+    int depth = 5, vb = 16, sched = nbank == 1 ? 3 : 1, group = 0;
+    // measured (r01): arrays of <= 8 KiB run 4.4 -> 6.0 TB/s with 4 lanes per array
+    if (nbank == 1 && opt.seg_avg_bytes && opt.seg_avg_bytes <= 8192) depth = 6, sched = 5, group = 4;
+    if (const char* v = env_get("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &sched, &group);
     if (opt.depth) depth = opt.depth;
-    const SegVariant* var = pick_segmented(nbank, depth, vb, sched);
+    const SegVariant* var = pick_segmented(nbank, depth, vb, sched, group);
     if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 3 : 1);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {
         const unsigned long long warps_per_block = block / 32;
-        const unsigned long long want = (n + warps_per_block - 1) / warps_per_block;
+        const unsigned long long per_warp = var->sched == 5 ? 32 / var->group : 1;  // arrays per warp batch
+        const unsigned long long want = (n + warps_per_block * per_warp - 1) / (warps_per_block * per_warp);
         // measured (r01 sweep): 4 CTAs/SM for the strided schedule, one resident wave otherwise
         const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", var->sched == 0 ? 4 : resident_blocks(var->fn, block));
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < cap ? want : cap);
     }
-    const unsigned per_grab = (unsigned)env_int("POSPOP_SEG_PER_GRAB", 1);
+    // Last argument: SCHED 1 arrays per grab; SCHED 5 the vector count above
+    // which a batch is counted one array at a time by the whole warp.
+    unsigned extra = (unsigned)env_int("POSPOP_SEG_PER_GRAB", 1);
+    if (extra < 1) extra = 1;
+    if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
     var->fn<<<grid, block, 0, stream>>>(static_cast<const uint8_t*>(data), d_offsets, n, k,
-                                        opt.flush_threshold, d_out, ws.next, ws.ticket,
-                                        per_grab < 1 ? 1u : per_grab);
+                                        opt.flush_threshold, d_out, ws.next, ws.ticket, extra);
     ++g_launches;
     return cudaGetLastError();
 }

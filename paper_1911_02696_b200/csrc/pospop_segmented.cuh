@@ -341,5 +341,189 @@ __global__ void __launch_bounds__(256, MINB) segmented_pipe_entry(const uint8_t*
     segmented_pipe_body<NBANK, L, VB>(data, offsets, n, k, thr, out);
 }
 
+// ---------------------------------------------------------------------------
+// Grouped segmented kernel (SCHED 4): G lanes per array, so one warp counts
+// 32/G arrays at once and the per-array epilogue (drain + reduction + row
+// store) is shared by 32/G arrays instead of paid per array by the whole
+// warp.  Warps claim batches of 32/G consecutive arrays from a global counter
+// (prefetched one batch ahead); a batch holding an array longer than
+// `big_vectors` is counted one array at a time by all 32 lanes instead, so a
+// few large arrays do not leave most lanes idle.
+// ---------------------------------------------------------------------------
+
+// Reduction over aligned groups of G lanes: each lane holds v[32] (channel c
+// in v[c]); afterwards lane gl (= lane mod G) holds the group sums of channels
+// [gl*32/G, (gl+1)*32/G) in v[0 .. 32/G).  Shuffle distances stay inside the
+// group; all 32 lanes must call it together.
+template <int G, int S = 0>
+__device__ __forceinline__ void group_transpose_reduce(uint32_t (&v)[32], uint32_t lane) {
+    if constexpr ((G >> (S + 1)) >= 1) {
+        constexpr int D = G >> (S + 1);  // shuffle distance
+        constexpr int H = 16 >> S;       // values kept: n/2
+        const bool upper = (lane & D) != 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const uint32_t send = upper ? v[i] : v[i + H];
+            const uint32_t keep = upper ? v[i + H] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, D);
+        }
+        group_transpose_reduce<G, S + 1>(v, lane);
+    }
+}
+
+// tot[m] += group sum of channel gl*32/G + m of (counter << shift) + d.
+template <int G>
+__device__ __forceinline__ void group_bank_total(const uint32_t (&counter)[16], int shift, const uint32_t (&d)[16],
+                                                 unsigned long long (&tot)[32 / G], uint32_t lane) {
+    uint32_t v[32];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+        v[p] = ((counter[p] & 0xFFFFu) << shift) + (d[p] & 0xFFFFu);
+        v[p + 16] = ((counter[p] >> 16) << shift) + (d[p] >> 16);
+    }
+    group_transpose_reduce<G>(v, lane);
+#pragma unroll
+    for (int m = 0; m < 32 / G; ++m) tot[m] += v[m];
+}
+
+// Counts arrays a0 + lane/GX (one per group of GX lanes) and stores their rows.
+template <int NBANK, int L, int VB, int GX>
+__device__ __forceinline__ void seg_group_batch(const uint8_t* data, const unsigned long long* offsets,
+                                                unsigned long long a0, unsigned long long n_arrays, int k,
+                                                uint32_t flush_threshold, unsigned long long* out, uint32_t lane) {
+    static_assert(GX >= 4 && GX <= 32 && (GX & (GX - 1)) == 0, "4..32 lanes per array");
+    constexpr int REGS = NBANK << L;
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr int W = 32 / GX;                                    // channels per lane after the reduction
+    constexpr unsigned long long STEP = (unsigned long long)GX * VPT;  // vectors per group per tree block
+    const uint32_t gl = lane % GX;
+    const unsigned long long a = a0 + lane / GX;
+    const int wb = k >> 3;
+    SegView v;
+    if (a < n_arrays) {
+        v = seg_view<VB>(data, offsets[a], offsets[a + 1], wb);
+    } else {
+        v.base = data;
+        v.nv = v.f0 = v.f1 = 0;
+        v.lo = 0;
+        v.hi = VB;
+    }
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    unsigned long long tot[NBANK][W];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int m = 0; m < W; ++m) tot[b][m] = 0;
+    uint32_t nb = 0;
+    // Lockstep over the batch: groups whose array is done read zeros.
+    for (unsigned long long t = 0; __any_sync(0xFFFFFFFFu, t < v.nv); t += STEP) {
+        uint32_t r[REGS];
+        if (t >= v.f0 && t + STEP <= v.f1) {
+#pragma unroll
+            for (int q = 0; q < VPT; ++q) {
+                uint32_t x[RPV];
+                ldg_stream<VB, 0>(v.base + (t + (unsigned long long)GX * q + gl) * VB, x);
+#pragma unroll
+                for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < VPT; ++q) {
+                const unsigned long long idx = t + (unsigned long long)GX * q + gl;
+                uint32_t x[RPV];
+#pragma unroll
+                for (int j = 0; j < RPV; ++j) x[j] = 0;
+                if (idx < v.nv) {
+                    ldg_stream<VB, 0>(v.base + idx * VB, x);
+                    if (idx == 0 || idx + 1 == v.nv)
+                        mask_bytes<VB>(x, idx == 0 ? v.lo : 0, idx + 1 == v.nv ? v.hi : VB);
+                }
+#pragma unroll
+                for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+            }
+        }
+        tree_block<NBANK, L>(r, carries, counter);
+        if (++nb == flush_threshold) {  // warp-uniform
+            uint32_t d[16];
+#pragma unroll
+            for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) group_bank_total<GX>(counter[b], L, d, tot[b], lane);
+            zero_bank<NBANK>(counter);
+            nb = 0;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        uint32_t d[16];
+        drain<L>(d, carries[b]);
+        group_bank_total<GX>(counter[b], L, d, tot[b], lane);
+    }
+    // Fold channels to positions inside the group (k = 16: c, c+16; k = 8:
+    // c, c+8, c+16, c+24) and store: lane gl owns channels [gl*W, gl*W + W).
+    if (NBANK == 1) {
+#pragma unroll
+        for (int m = 0; m < W; ++m)
+            for (int w = 16; w >= k; w >>= 1) tot[0][m] += __shfl_xor_sync(0xFFFFFFFFu, tot[0][m], w / W);
+    }
+    if (a < n_arrays && (int)(gl * W) < (NBANK == 2 ? 32 : k)) {
+        unsigned long long* row = out + a * (unsigned long long)k + gl * W;
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+            for (int m = 0; m < W; ++m) row[32 * b + m] = tot[b][m];
+    }
+}
+
+template <int NBANK, int L, int VB, int G, int MINB>
+__global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_t* data,
+                                                                    const unsigned long long* offsets,
+                                                                    unsigned long long n_arrays, int k,
+                                                                    uint32_t flush_threshold, unsigned long long* out,
+                                                                    unsigned long long* next, unsigned int* ticket,
+                                                                    unsigned big_vectors) {
+    constexpr int NG = 32 / G;  // arrays per batch
+    const uint32_t lane = threadIdx.x & 31u;
+    const int wb = k >> 3;
+    __shared__ int s_last;
+    unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
+    mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    for (;;) {
+        const unsigned long long a0 = b * NG;
+        if (a0 >= n_arrays) break;  // warp-uniform
+        // Does the batch hold an array too long for G lanes?
+        unsigned long long nbytes = 0;
+        if (lane < (uint32_t)NG && a0 + lane < n_arrays) nbytes = (offsets[a0 + lane + 1] - offsets[a0 + lane]) * wb;
+        if (!__any_sync(0xFFFFFFFFu, nbytes > (unsigned long long)big_vectors * VB)) {
+            seg_group_batch<NBANK, L, VB, G>(data, offsets, a0, n_arrays, k, flush_threshold, out, lane);
+        } else {
+            for (int j = 0; j < NG; ++j)
+                if (a0 + j < n_arrays)
+                    seg_group_batch<NBANK, L, VB, 32>(data, offsets, a0 + j, n_arrays, k, flush_threshold, out, lane);
+        }
+        b = __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    }
+    // Every warp has drawn an index past the end; once all CTAs are past that
+    // point the counter can be reset.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (s_last) {
+            *next = 0ull;
+            *ticket = 0u;
+        }
+    }
+}
+
 }  // namespace dev
 }  // namespace pospop_b200

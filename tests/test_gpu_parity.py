@@ -357,11 +357,13 @@ def test_reference_verify_kernels_with_gpu_runner():
     assert r.stdout.count("PASS") == 4
 
 
+_GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4", "6,16,5,16", "5,32,5,4"]
 SEG_VARIANTS = {
-    8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"],
-    16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"],
-    32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"],
-    64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3"],
+    8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
+    16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
+    32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
+    64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3",
+         "4,16,5,8", "4,32,5,8", "4,16,5,4"],
 }
 
 
@@ -388,6 +390,32 @@ def test_segmented_every_variant(pp, dev, orc, k, monkeypatch):
             pp.segmented_async(d, o, out, k)
             torch.cuda.synchronize()
             assert (out.cpu().numpy().view(np.uint64) == want).all(), (var, per_sm)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_segmented_grouped_big_arrays_and_flushes(pp, dev, orc, k, monkeypatch):
+    """Grouped kernel (G lanes per array): batches holding an array above the
+    big-array bound are counted one array at a time by the whole warp; forced
+    flushes reduce inside each lane group; a few long arrays among many
+    short ones; misaligned starts."""
+    rng = np.random.default_rng(900 + k)
+    n_words = 2_000_000
+    data = orc.generate(6, 77, n_words * k // 64 + 1).view(DT[k])[:n_words]
+    lens = rng.integers(0, 3000, size=600)
+    lens[[5, 77, 300]] = [400_000, 250_001, 123_457]
+    cuts = np.minimum(np.cumsum(lens), n_words)
+    offs = np.concatenate([[0], cuts, [n_words]]).astype(np.uint64)
+    want = orc.segmented(data, offs, k, threads=8)
+    d = to_dev(data)
+    o = torch.from_numpy(offs.view(np.int64)).cuda()
+    var = "4,16,5,8" if k == 64 else "6,16,5,8"
+    monkeypatch.setenv("POSPOP_SEG_VARIANT", var)
+    for big_kib, flush in (("256", 65535), ("1", 65535), ("256", 1), ("1", 3)):
+        monkeypatch.setenv("POSPOP_SEG_BIG_KIB", big_kib)
+        out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
+        pp.segmented_async(d, o, out, k, flush_threshold_blocks=flush)
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy().view(np.uint64) == want).all(), (big_kib, flush)
 
 
 def test_graph_replay_counts_current_contents(pp, dev, orc):

@@ -182,30 +182,28 @@ def main():
         os.environ.pop("POSPOP_TMA", None)
 
     if "seg" in what:
+        seg_cases = {
+            32: ["5,16,3", "5,16,1", "6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4",
+                 "6,16,5,16", "5,32,5,4"],
+            64: ["5,16,1", "4,16,3", "4,16,5,8", "4,32,5,8", "4,16,5,4"],
+        }
         for k, kind in [(32, pp.GEN_U32), (64, pp.GEN_U64)]:
-            arrays, words = 65536, 4096
-            d = data[:arrays * words * k // 8]
-            pp.generate(kind, 1, d, stream=s)
-            offs = torch.arange(0, arrays + 1, dtype=torch.int64, device="cuda") * words
-            o = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
-            want = None
-            cases = [(v, "", "") for v in ("5,16,1", "5,16,3", "5,32,3", "4,16,4", "4,32,4", "5,16,4", "3,16,4",
-                                           "3,32,4")]
-            for var, per_sm, g in cases:
-                env = {"POSPOP_SEG_VARIANT": var, "POSPOP_SEG_BLOCKS_PER_SM": per_sm, "POSPOP_SEG_PER_GRAB": g}
-                for kk, vv in env.items():
-                    if vv:
-                        os.environ[kk] = vv
-                    else:
-                        os.environ.pop(kk, None)
-                med, best = timed(lambda: pp.segmented_async(d, offs, o, k, stream=s), args.reps, s)
-                if want is None:
-                    want = o.clone()
-                emit(kind=f"seg{k}", variant=var, per_sm=per_sm or "dflt", per_grab=g or "1",
-                     ok=bool(torch.equal(o, want)), gbs_med=round(d.numel() / med / 1e6, 1),
-                     gbs_best=round(d.numel() / best / 1e6, 1))
-            for kk in ("POSPOP_SEG_VARIANT", "POSPOP_SEG_BLOCKS_PER_SM", "POSPOP_SEG_PER_GRAB"):
-                os.environ.pop(kk, None)
+            shapes = [(65536, 4096)] + ([(262144, 1024), (4096, 65536), (1024, 262144)] if k == 32 else [])
+            for arrays, words in shapes:
+                d = data[:arrays * words * k // 8]
+                pp.generate(kind, 1, d, stream=s)
+                offs = torch.arange(0, arrays + 1, dtype=torch.int64, device="cuda") * words
+                o = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
+                want = None
+                variants = seg_cases[k] if (arrays, words) == (65536, 4096) else seg_cases[k][:1] + seg_cases[k][2:5]
+                for var in variants:
+                    os.environ["POSPOP_SEG_VARIANT"] = var
+                    med, best = timed(lambda: pp.segmented_async(d, offs, o, k, stream=s), args.reps, s)
+                    if want is None:
+                        want = o.clone()
+                    emit(kind=f"seg{k}", arrays=arrays, words=words, variant=var, ok=bool(torch.equal(o, want)),
+                         gbs_med=round(d.numel() / med / 1e6, 1), gbs_best=round(d.numel() / best / 1e6, 1))
+                os.environ.pop("POSPOP_SEG_VARIANT", None)
 
 
 if __name__ == "__main__":
