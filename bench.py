@@ -47,6 +47,11 @@ WORKLOADS = {
     "cfg2": (16, 2, 1 << 28, "cfg2: 2^28 u16 one-hot words, position Zipf(1.1), k=16 u64 counters"),
     "cfg3": (8, 3, (1 << 30) - 7, "cfg3: 2^30-7 u8 words at a +3 byte offset, 4 KiB runs one-hot/uniform, "
                                   "k=8 u64 counters"),
+    # segmented / batched (BASELINE cfg5): one row of k counts per array
+    "cfg5": (32, 5, 65536 * 4096, "cfg5: 65,536 arrays x 4096 uniform u32 words (1 GiB), one k=32 row per array "
+                                  "(16 MiB of rows); arrays split over the N GPUs, no exchange"),
+    "cfg5_u64": (64, 6, 65536 * 4096, "cfg5 (u64): 65,536 arrays x 4096 u64 words (2 GiB), one k=64 row per array "
+                                      "(32 MiB of rows); arrays split over the N GPUs, no exchange"),
     # SURVEY 8f row f1 (not the headline metric): flagstats_pospopcnt over SAM FLAG words
     "flag": (16, 7, 1 << 32, "flag: 2^32 SAM FLAG words (12 valid bits, realistic flag mix), "
                              "flagstats_pospopcnt pass/fail buckets in one fused pass; contiguous shards, "
@@ -244,12 +249,17 @@ def ref_flagstats_mt(words, threads):
     return np.sum(parts, axis=0, dtype=np.uint64)
 
 
+SEG_WORDS = 4096  # words per array in cfg5
+
+
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return 0
     if args.workload == "flag":
         return run_reference_flag(args)
+    if args.workload.startswith("cfg5"):
+        return run_reference_seg(args)
     k, gen_kind, total, desc = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     # bounded sample: 2^28 words of the workload stream per step (512 MiB for u16)
@@ -327,9 +337,210 @@ def run_reference_flag(args):
     return 0
 
 
+def run_reference_seg(args):
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    k, gen_kind, total, desc = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    arrays = 8192  # bounded sample: the first 8192 arrays per step
+    data = pyoracle.Oracle().generate(gen_kind, 1, arrays * SEG_WORDS, threads=threads)
+    offs = np.arange(arrays + 1, dtype=np.uint64) * SEG_WORDS
+    ref = pyoracle.Reference()
+    for _ in range(max(args.warmup, 1)):
+        ref.segmented(data, offs, k, threads)
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.segmented(data, offs, k, threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > 240:
+            break
+    mean = sum(times) / len(times)
+    gbs = data.nbytes / mean / 1e9
+    sample = (f"first {arrays} arrays x {SEG_WORDS} words per step; per array the reference's 16-bit "
+              f"pospop::pospopcnt after the SURVEY 8c deinterleave (k/16 streams), arrays fork-joined over "
+              f"{threads} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 4), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": f"u{k}", "data": "synthetic",
+        "config": {"workload": desc, "sample_arrays_per_step": arrays, "host_threads": threads},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
+
+def run_ours_seg(args):
+    """cfg5: one segmented launch per step over this rank's arrays (contiguous
+    array ranges; rows are per array, so there is no exchange)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1911_02696_b200 as pp
+
+    world, rank, local = dist_env()
+    backend = os.environ.get("POSPOP_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    k, gen_kind, total, desc = WORKLOADS[args.workload]
+    wb = k // 8
+    n_arrays_total = total // SEG_WORDS
+    if args.scaling == "weak":
+        a_lo, a_hi = rank * n_arrays_total, (rank + 1) * n_arrays_total
+    else:
+        a_lo, a_hi = n_arrays_total * rank // world, n_arrays_total * (rank + 1) // world
+    arrays = a_hi - a_lo
+    words = arrays * SEG_WORDS
+    data = torch.empty(words * wb, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    pp.generate(gen_kind, 1, data, base=a_lo * SEG_WORDS, n=words, stream=stream)
+    offs = torch.arange(arrays + 1, dtype=torch.int64, device=dev) * SEG_WORDS
+    rows = torch.empty((arrays, k), dtype=torch.int64, device=dev)
+    torch.cuda.synchronize(dev)
+
+    def step():
+        pp.segmented_async(data, offs, rows, k, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = pp.kernel_launches()
+    sampler = ClockSampler(local, args.clock_interval_ms / 1e3)
+    with sampler:
+        t_begin.record(stream)
+        for _ in range(args.steps):
+            step()  # no events between launches: programmatic dependent launch overlaps them
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = pp.kernel_launches() - launches0
+    elapsed_ms = t_begin.elapsed_time(t_end)
+    iso = []
+    for _ in range(5):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        step()
+        a1.record(stream)
+        a1.synchronize()
+        iso.append(a0.elapsed_time(a1))
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t[0])
+    ms_per_step = elapsed_ms / args.steps
+    total_bytes = n_arrays_total * SEG_WORDS * wb * (world if args.scaling == "weak" else 1)
+    value = total_bytes / (ms_per_step * 1e-3) / 1e9
+    kern_ms = elapsed_ms / args.steps
+    per_launch_bytes = words * wb + arrays * k * 8  # input read + rows written
+    achieved = per_launch_bytes / (kern_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+
+    # correctness gate against the oracle on the first arrays
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    sample_arrays = min(arrays, 512)
+    host_sample = data[: sample_arrays * SEG_WORDS * wb].cpu().numpy()
+    want = pyoracle.Oracle().segmented(host_sample, np.arange(sample_arrays + 1, dtype=np.uint64) * SEG_WORDS, k,
+                                       threads=4)
+    assert (rows[:sample_arrays].cpu().numpy().view(np.uint64) == want).all(), "segmented rows disagree with oracle"
+
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(words * wb, dtype=torch.uint8, pin_memory=True)
+        host.copy_(data)
+        host_offs = np.arange(arrays + 1, dtype=np.uint64) * SEG_WORDS
+        host_rows = np.empty((arrays, k), np.uint64)
+        host_arr = host.numpy()
+        pp.pospopcnt_segmented(host_arr, host_offs, k, out=host_rows)
+        e2e_steps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            pp.pospopcnt_segmented(host_arr, host_offs, k, out=host_rows)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        assert (host_rows[:sample_arrays] == want).all()
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(total_bytes / float(tt[0]) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": words * wb + (arrays + 1) * 8, "d2h_bytes_per_step": arrays * k * 8,
+               "steps": e2e_steps,
+               "path": "pospopcnt_segmented C ABI: host data + host offsets + host rows (H2D, one launch, D2H)"}
+        link = h2d_link_gbs(host, dev)
+        if link:
+            e2e["h2d_link_gbs"] = link
+            e2e["frac_of_h2d_link"] = round(e2e["value"] / world / link, 4)
+        del host
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        cpu_arrays = min(arrays, 8192)
+        hs = data[: cpu_arrays * SEG_WORDS * wb].cpu().numpy()
+        ho = np.arange(cpu_arrays + 1, dtype=np.uint64) * SEG_WORDS
+        ref = pyoracle.Reference()
+        ref_rows = ref.segmented(hs, ho, k, threads)
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            ref.segmented(hs, ho, k, threads)
+            dt = time.perf_counter() - t0
+            best = dt if best is None or dt < best else best
+        assert (ref_rows[:sample_arrays] == want[: min(sample_arrays, cpu_arrays)]).all()
+        cpu = {"value": round(hs.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+               "sample": f"first {cpu_arrays} arrays ({hs.nbytes >> 20} MiB); per array the reference's 16-bit "
+                         f"pospop::pospopcnt after the SURVEY 8c deinterleave, arrays fork-joined over {threads} "
+                         f"threads, best of 3; rows equal the GPU's"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": f"u{k}",
+        "data": "synthetic (counter-based generator, generated in place in HBM)",
+        "config": {"workload": desc, "arrays_total": n_arrays_total, "words_per_array": SEG_WORDS, "k": k,
+                   "bytes_per_step": total_bytes, "parallelism": f"shard{world}",
+                   "l2_policy": "input >> 126 MB L2; no flush needed",
+                   "kernel": "segmented (one warp per array, software-pipelined) for k=32; dynamic array claims "
+                             "for k=64; one launch per step"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, world),
+                     "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
+                     "kernel_ms_isolated": round(statistics.median(iso), 5),
+                     "timing": "back-to-back launches with programmatic dependent launch, CUDA events around the "
+                               "timed region; isolated = median of 5 single launches bracketed by events",
+                     "bytes_per_launch": per_launch_bytes,
+                     "frac_of_theoretical_8180": round(achieved / 8180.0, 4)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
 
 def run_ours_flag(args):
     """Row f1: one pospop_flagstats C-ABI call per step over this rank's shard of
@@ -699,6 +910,8 @@ def main():
         return run_reference(args)
     if args.workload == "flag":
         return run_ours_flag(args)
+    if args.workload.startswith("cfg5"):
+        return run_ours_seg(args)
     return run_ours(args)
 
 

@@ -204,6 +204,8 @@ class Reference:
         lib.ref_flush_bank.argtypes = [_u64p, C.POINTER(C.c_uint32), _u64p, C.c_uint32]
         lib.ref_finalize_carries.argtypes = [_u64p, C.c_int, _u64p]
         lib.ref_flagstats.argtypes = [C.c_void_p, C.c_size_t, C.c_int, _u64p, _u64p]
+        lib.ref_segmented.argtypes = [C.c_int, C.c_void_p, _u64p, C.c_size_t, C.c_int, _u64p]
+        lib.ref_segmented.restype = C.c_int
         self.lib = lib
 
     def pospopcnt(self, words: np.ndarray, kernel: str = "auto", width: int = 0,
@@ -220,6 +222,17 @@ class Reference:
     def oracle(self, words: np.ndarray) -> np.ndarray:
         out = np.zeros(16, np.uint64)
         self.lib.ref_oracle_u16(_ptr(words), words.size, out.ctypes.data_as(_u64p))
+        return out
+
+    def segmented(self, data: np.ndarray, offsets: np.ndarray, k: int, threads: int = 1) -> np.ndarray:
+        """cfg5 on the reference's 16-bit API (ref_segmented, SURVEY 8c restatement)."""
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        out = np.zeros((n, k), np.uint64)
+        rc = self.lib.ref_segmented(k, _ptr(data), offsets.ctypes.data_as(_u64p), n, threads,
+                                    out.ctypes.data_as(_u64p))
+        if rc:
+            raise RuntimeError(f"ref_segmented failed ({rc})")
         return out
 
     def pospopcnt_mt(self, words: np.ndarray, threads: int) -> np.ndarray:

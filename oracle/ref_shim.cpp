@@ -105,6 +105,60 @@ int ref_pospopcnt_u16_mt(const uint16_t* data, size_t len, int threads, uint64_t
     });
 }
 
+// cfg5 / k != 16 on the reference's own 16-bit API, as SURVEY.md 8c restates
+// it (the reference is 16-bit only): k = 16 direct; k = 32 / 64
+// deinterleaved into k/16 u16 streams (half h = bits 16h..16h+15), one
+// pospop::pospopcnt per stream, concatenated; k = 8 as c16[p] + c16[p+8] over
+// the 2-byte-aligned body with an odd head/tail byte counted directly.
+// Arrays a = words [offsets[a], offsets[a+1]) of `data`, row a of out (k u64);
+// fork-join over `threads` contiguous array ranges.  Returns 0 or an error code.
+int ref_segmented(int k, const void* data, const uint64_t* offsets, size_t n_arrays, int threads, uint64_t* out) {
+    return guarded([&] {
+        if (k != 8 && k != 16 && k != 32 && k != 64) throw std::invalid_argument("k");
+        if (threads < 1) threads = 1;
+        const size_t wb = static_cast<size_t>(k) / 8;
+        auto one = [&](size_t a, std::vector<uint16_t>& scratch) {
+            const uint8_t* p = static_cast<const uint8_t*>(data) + offsets[a] * wb;
+            const size_t n = offsets[a + 1] - offsets[a];
+            uint64_t* row = out + a * static_cast<size_t>(k);
+            for (int i = 0; i < k; ++i) row[i] = 0;
+            if (k == 16) {
+                put(pospopcnt(Word16Span(reinterpret_cast<const uint16_t*>(p), n)), row);
+            } else if (k == 8) {
+                size_t head = reinterpret_cast<uintptr_t>(p) & 1u ? 1 : 0;
+                if (head > n) head = n;
+                const size_t body = (n - head) / 2;
+                for (size_t i = 0; i < head; ++i)
+                    for (int b = 0; b < 8; ++b) row[b] += (p[i] >> b) & 1u;
+                const PositionalCounts c = pospopcnt(Word16Span(reinterpret_cast<const uint16_t*>(p + head), body));
+                for (int b = 0; b < 8; ++b) row[b] += c[b] + c[b + 8];
+                for (size_t i = head + 2 * body; i < n; ++i)
+                    for (int b = 0; b < 8; ++b) row[b] += (p[i] >> b) & 1u;
+            } else {
+                const int halves = k / 16;
+                scratch.resize(n);
+                for (int h = 0; h < halves; ++h) {
+                    for (size_t i = 0; i < n; ++i) {
+                        uint16_t w;
+                        std::memcpy(&w, p + i * wb + 2 * static_cast<size_t>(h), 2);
+                        scratch[i] = w;
+                    }
+                    put(pospopcnt(Word16Span(scratch.data(), n)), row + 16 * h);
+                }
+            }
+        };
+        std::vector<std::jthread> workers;
+        for (int t = 0; t < threads; ++t) {
+            const size_t lo = n_arrays * static_cast<size_t>(t) / static_cast<size_t>(threads);
+            const size_t hi = n_arrays * static_cast<size_t>(t + 1) / static_cast<size_t>(threads);
+            workers.emplace_back([&one, lo, hi] {
+                std::vector<uint16_t> scratch;
+                for (size_t a = lo; a < hi; ++a) one(a, scratch);
+            });
+        }
+    });
+}
+
 // bench::generate_stream (bench.cpp:115-120)
 void ref_generate_stream(uint64_t seed, size_t len, uint16_t* out) {
     const std::vector<uint16_t> s = bench::generate_stream({seed, len});

@@ -495,10 +495,20 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     unsigned extra = (unsigned)env_int("POSPOP_SEG_PER_GRAB", 1);
     if (extra < 1) extra = 1;
     if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
-    var->fn<<<grid, block, 0, stream>>>(static_cast<const uint8_t*>(data), d_offsets, n, k,
-                                        opt.flush_threshold, d_out, ws.next, ws.ticket, extra);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = env_int("POSPOP_PDL", 1) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, var->fn, static_cast<const uint8_t*>(data), d_offsets,
+                                             (unsigned long long)n, k, opt.flush_threshold, d_out, ws.next,
+                                             ws.ticket, extra);
     ++g_launches;
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* out,

@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
     const int wb = k >> 3;
     __shared__ int s_last;
 
+    pdl_allow_next();
+    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     unsigned long long mine = 0, run = 0, arr = warp, stop = n_arrays;
@@ -236,6 +238,8 @@ __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const u
     const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     const int wb = k >> 3;
 
+    pdl_allow_next();
+    pdl_wait_prev();  // the rows may belong to the previous launch on this stream
     // Current array: skip (and zero) empty arrays.
     unsigned long long arr = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
     SegView cur;
@@ -493,6 +497,8 @@ __global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_
     const uint32_t lane = threadIdx.x & 31u;
     const int wb = k >> 3;
     __shared__ int s_last;
+    pdl_allow_next();
+    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
     mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;

@@ -312,3 +312,16 @@ def test_flagstats_oracle_matches_reference_live(orc, ref):
     assert rc == rr == 0 and (a == b).all()
     w[77] |= 0x1000
     assert orc.flagstats(w)[0::2] == ref.flagstats(w)[0::2] == (1, 77)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_reference_segmented_restatement_matches_oracle(orc, ref, k):
+    """The reference-based cfg5 baseline (ref_segmented: the reference's 16-bit
+    pospopcnt per array after the SURVEY 8c deinterleave / fold) equals the
+    oracle's segmented count, including odd byte starts for k = 8."""
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}[k]
+    data = orc.generate(6, 8 + k, 5000).view(dt)
+    n = data.size
+    rng = np.random.default_rng(k)
+    offs = np.concatenate([[0, 0, 1], np.sort(rng.integers(1, n, 40)), [n]]).astype(np.uint64)
+    assert (ref.segmented(data, offs, k, threads=3) == orc.segmented(data, offs, k, threads=2)).all()
