@@ -205,9 +205,14 @@ struct SegVariant {
 #define SGP(NB, L, VB) {NB, L, VB, 2, segmented_pipe_entry<NB, L, VB>}
 #define SGP2(NB, L, VB) {NB, L, VB, 3, segmented_pipe_entry<NB, L, VB, 2>}  // sched 3: pipelined, 2 CTAs/SM
 #define SGP3(NB, L, VB) {NB, L, VB, 4, segmented_pipe_entry<NB, L, VB, 3>}  // sched 4: pipelined, 3 CTAs/SM
+// sched 6: pipelined, bit-plane epilogue, 2 CTAs/SM; sched 7: the same at 3 CTAs/SM
+#define SGPE(NB, L, VB) {NB, L, VB, 6, segmented_pipe_entry<NB, L, VB, 2, 1>}
+#define SGPE3(NB, L, VB) {NB, L, VB, 7, segmented_pipe_entry<NB, L, VB, 3, 1>}
 // sched 5: grouped, G lanes per array, 2 CTAs/SM
 #define SGG(NB, L, VB, G) {NB, L, VB, 5, segmented_group_kernel<NB, L, VB, G, 2>, G}
 const SegVariant kSegVariants[] = {
+    SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),
+    SGPE3(1, 4, 16), SGPE3(1, 4, 32), SGPE3(2, 3, 16),
     SGG(1, 6, 16, 8), SGG(1, 6, 16, 4), SGG(1, 5, 16, 8), SGG(1, 6, 32, 8), SGG(1, 5, 32, 8), SGG(1, 5, 16, 4),
     SGG(1, 6, 16, 16), SGG(1, 5, 32, 4),
     SGG(2, 4, 16, 8), SGG(2, 4, 32, 8), SGG(2, 4, 16, 4),
@@ -221,6 +226,8 @@ const SegVariant kSegVariants[] = {
 #undef SGP2
 #undef SGP3
 #undef SGG
+#undef SGPE
+#undef SGPE3
 #undef SG
 #undef SGP
 
@@ -471,14 +478,17 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     env_refresh();
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched[,lanes per array]".
-    // measured: pipelined with 2 CTAs/SM (k <= 32), dynamic claiming (k = 64)
-    int depth = 5, vb = 16, sched = nbank == 1 ? 3 : 1, group = 0;
-    // measured (r01): arrays of <= 8 KiB run 4.4 -> 6.0 TB/s with 4 lanes per array
-    if (nbank == 1 && opt.seg_avg_bytes && opt.seg_avg_bytes <= 8192) depth = 6, sched = 5, group = 4;
+    // measured (r01, tools/sweep.py --what seg): pipelined with the bit-plane
+    // epilogue, 2 CTAs/SM (k <= 32: cfg5 6612 -> 6877 GB/s, 1024-word arrays
+    // 4360 -> 5990); dynamic claiming (k = 64)
+    int depth = 5, vb = 16, sched = nbank == 1 ? 6 : 1, group = 0;
+    // very short arrays: 4 lanes per array (grouped schedule)
+    if (nbank == 1 && opt.seg_avg_bytes && opt.seg_avg_bytes <= (unsigned long long)env_int("POSPOP_SEG_GROUP_BYTES", 2048))
+        depth = 6, sched = 5, group = 4;
     if (const char* v = env_get("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &sched, &group);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb, sched, group);
-    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 3 : 1);
+    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 6 : 1);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {

@@ -153,6 +153,53 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bit-plane epilogue (EPI 1).  A lane's per-channel count is held as bit
+// planes: the tree carries (weight 2^j, j < L) and a bit-sliced counter of the
+// tree tops (weight 2^(L+i), i < M, incremented by a half-adder ripple, two
+// LOP3 per level per tree block, instead of the 16-lane extract).  The warp
+// sum of channel c over the 32 lanes is then, per plane P, popc of column c of
+// the 32x32 bit matrix whose row r is lane r's P -- a warp bit transpose
+// (5 x {SHFL, SHF funnel rotate, LOP3 bit-select}) followed by one POPC on lane
+// c.  16 instructions per plane replace the 16-lane drain (Horner over L
+// planes), the 32-value unpack and the 31-shuffle transpose-reduce.
+// ---------------------------------------------------------------------------
+struct PlaneXpose {
+    uint32_t sh[5], mk[5];  // per level: rotate amount and keep-mask for this lane
+    __device__ __forceinline__ explicit PlaneXpose(uint32_t lane) {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            const uint32_t j = 16u >> s;
+            const uint32_t m = s == 0 ? 0x0000FFFFu : s == 1 ? 0x00FF00FFu : s == 2 ? 0x0F0F0F0Fu
+                             : s == 3 ? 0x33333333u : 0x55555555u;  // columns c with (c & j) == 0
+            const bool bottom = (lane & j) != 0;
+            sh[s] = bottom ? 32u - j : j;
+            mk[s] = bottom ? ~m : m;
+        }
+    }
+    // Number of lanes whose plane has bit `lane` set.  All 32 lanes together.
+    __device__ __forceinline__ uint32_t column_popc(uint32_t x) const {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, 16u >> s);
+            const uint32_t r = __funnelshift_l(y, y, sh[s]);
+            x = (x & mk[s]) | (r & ~mk[s]);
+        }
+        return __popc(x);
+    }
+};
+
+// tops counter: U[i] has weight 2^(L+i); adds one plane (ripple half-adders).
+template <int M>
+__device__ __forceinline__ void plane_count_add(uint32_t (&U)[M], uint32_t top) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const uint32_t c = U[i] & top;
+        U[i] ^= top;
+        top = c;
+    }
+}
+
 // Segmented, software-pipelined (SCHED 2): warp w owns arrays w, w + nwarps,
 // ... and walks the concatenation of their steps (32 lanes x VPT vectors) with
 // a one-step register double buffer: the loads of step s+1 -- possibly the
@@ -226,10 +273,11 @@ __device__ __forceinline__ void seg_store_row(unsigned long long* out, unsigned 
     }
 }
 
-template <int NBANK, int L, int VB>
+template <int NBANK, int L, int VB, int EPI = 0>
 __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const unsigned long long* offsets,
                                                     unsigned long long n_arrays, int k, uint32_t flush_threshold,
                                                     unsigned long long* out) {
+    constexpr int M = 3;  // EPI 1: bit-sliced tops counter, flushed every 2^M - 1 tree blocks
     constexpr int REGS = NBANK << L;
     constexpr int RPV = VB / 4;
     constexpr int VPT = REGS / RPV;
@@ -260,12 +308,18 @@ __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const u
     }
 
     uint32_t carries[NBANK][L];
-    uint32_t counter[NBANK][16];
+    uint32_t counter[NBANK][EPI ? 1 : 16];  // EPI 0: 16-lane counters
+    uint32_t U[NBANK][M];                   // EPI 1: bit-sliced tops
 #pragma unroll
-    for (int b = 0; b < NBANK; ++b)
+    for (int b = 0; b < NBANK; ++b) {
 #pragma unroll
         for (int j = 0; j < L; ++j) carries[b][j] = 0;
-    zero_bank<NBANK>(counter);
+#pragma unroll
+        for (int i = 0; i < M; ++i) U[b][i] = 0;
+#pragma unroll
+        for (int p = 0; p < (EPI ? 1 : 16); ++p) counter[b][p] = 0;
+    }
+    const PlaneXpose xp(lane);
     uint32_t nb = 0;
     unsigned long long tot[NBANK];
 #pragma unroll
@@ -303,26 +357,60 @@ __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const u
         uint32_t rn[REGS];
         if (have_next) seg_load<VB, VPT>(nxt, t_n, lane, rn);
 
-        tree_block<NBANK, L>(rc, carries, counter);
-        if (++nb == flush_threshold) {
-            uint32_t d[16];
+        if constexpr (EPI == 1) {
 #pragma unroll
-            for (int p = 0; p < 16; ++p) d[p] = 0;
+            for (int b = 0; b < NBANK; ++b)
+                plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], rc)
+                                                    : Tree<L, 2>::run(carries[b], rc + b));
+            if (++nb == (1u << M) - 1u) {  // the tops counter is full: fold it into tot
 #pragma unroll
-            for (int b = 0; b < NBANK; ++b) tot[b] += bank_warp_total(counter[b], L, d);
-            zero_bank<NBANK>(counter);
-            nb = 0;
+                for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                        U[b][i] = 0;
+                    }
+                nb = 0;
+            }
+        } else {
+            tree_block<NBANK, L>(rc, carries, reinterpret_cast<uint32_t(&)[NBANK][16]>(counter));
+            if (++nb == flush_threshold) {
+                uint32_t d[16];
+#pragma unroll
+                for (int p = 0; p < 16; ++p) d[p] = 0;
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b)
+                    tot[b] += bank_warp_total(reinterpret_cast<uint32_t(&)[16]>(counter[b]), L, d);
+                zero_bank<NBANK>(reinterpret_cast<uint32_t(&)[NBANK][16]>(counter));
+                nb = 0;
+            }
         }
         if (t + STEP >= cur.nv) {  // last step of this array: epilogue while rn is in flight
+            if constexpr (EPI == 1) {
 #pragma unroll
-            for (int b = 0; b < NBANK; ++b) {
-                uint32_t d[16];
-                drain<L>(d, carries[b]);
-                tot[b] += bank_warp_total(counter[b], L, d);
+                for (int b = 0; b < NBANK; ++b) {
 #pragma unroll
-                for (int j = 0; j < L; ++j) carries[b][j] = 0;
+                    for (int j = 0; j < L; ++j) {
+                        tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
+                        carries[b][j] = 0;
+                    }
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                        U[b][i] = 0;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b) {
+                    uint32_t d[16];
+                    drain<L>(d, carries[b]);
+                    tot[b] += bank_warp_total(reinterpret_cast<uint32_t(&)[16]>(counter[b]), L, d);
+#pragma unroll
+                    for (int j = 0; j < L; ++j) carries[b][j] = 0;
+                }
+                zero_bank<NBANK>(reinterpret_cast<uint32_t(&)[NBANK][16]>(counter));
             }
-            zero_bank<NBANK>(counter);
             nb = 0;
             seg_store_row<NBANK>(out, arr, k, lane, tot);
 #pragma unroll
@@ -337,12 +425,12 @@ __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const u
     }
 }
 
-template <int NBANK, int L, int VB, int MINB = 1>
+template <int NBANK, int L, int VB, int MINB = 1, int EPI = 0>
 __global__ void __launch_bounds__(256, MINB) segmented_pipe_entry(const uint8_t* data, const unsigned long long* offsets,
                                                             unsigned long long n, int k, uint32_t thr,
                                                             unsigned long long* out, unsigned long long*,
                                                             unsigned int*, unsigned) {
-    segmented_pipe_body<NBANK, L, VB>(data, offsets, n, k, thr, out);
+    segmented_pipe_body<NBANK, L, VB, EPI>(data, offsets, n, k, thr, out);
 }
 
 // ---------------------------------------------------------------------------

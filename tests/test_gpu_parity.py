@@ -357,13 +357,14 @@ def test_reference_verify_kernels_with_gpu_runner():
     assert r.stdout.count("PASS") == 4
 
 
-_GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4", "6,16,5,16", "5,32,5,4"]
+_GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4", "6,16,5,16", "5,32,5,4",
+            "5,16,6", "5,32,6", "4,16,6", "4,32,6", "4,16,7", "4,32,7"]  # + bit-plane epilogue (sched 6/7)
 SEG_VARIANTS = {
     8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3",
-         "4,16,5,8", "4,32,5,8", "4,16,5,4"],
+         "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7"],
 }
 
 
@@ -408,14 +409,14 @@ def test_segmented_grouped_big_arrays_and_flushes(pp, dev, orc, k, monkeypatch):
     want = orc.segmented(data, offs, k, threads=8)
     d = to_dev(data)
     o = torch.from_numpy(offs.view(np.int64)).cuda()
-    var = "4,16,5,8" if k == 64 else "6,16,5,8"
-    monkeypatch.setenv("POSPOP_SEG_VARIANT", var)
-    for big_kib, flush in (("256", 65535), ("1", 65535), ("256", 1), ("1", 3)):
+    for var, big_kib, flush in [(v, b, f) for v in (("4,16,5,8", "4,16,6") if k == 64 else ("6,16,5,8", "5,16,6"))
+                                for b, f in (("256", 65535), ("1", 65535), ("256", 1), ("1", 3))]:
+        monkeypatch.setenv("POSPOP_SEG_VARIANT", var)
         monkeypatch.setenv("POSPOP_SEG_BIG_KIB", big_kib)
         out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
         pp.segmented_async(d, o, out, k, flush_threshold_blocks=flush)
         torch.cuda.synchronize()
-        assert (out.cpu().numpy().view(np.uint64) == want).all(), (big_kib, flush)
+        assert (out.cpu().numpy().view(np.uint64) == want).all(), (var, big_kib, flush)
 
 
 def test_graph_replay_counts_current_contents(pp, dev, orc):

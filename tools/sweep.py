@@ -183,19 +183,19 @@ def main():
 
     if "seg" in what:
         seg_cases = {
-            32: ["5,16,3", "5,16,1", "6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4",
-                 "6,16,5,16", "5,32,5,4"],
-            64: ["5,16,1", "4,16,3", "4,16,5,8", "4,32,5,8", "4,16,5,4"],
+            32: ["5,16,6", "5,32,6", "6,16,5,4", "6,16,5,8", "5,16,3", "4,16,7", "4,32,7", "6,16,5,16"],
+            64: ["5,16,1", "4,16,6", "4,32,6", "3,32,6", "3,16,7", "4,16,5,8"],
         }
         for k, kind in [(32, pp.GEN_U32), (64, pp.GEN_U64)]:
-            shapes = [(65536, 4096)] + ([(262144, 1024), (4096, 65536), (1024, 262144)] if k == 32 else [])
+            shapes = [(65536, 4096)] + ([(262144, 1024), (1048576, 256), (4194304, 64), (4096, 65536),
+                                         (1024, 262144)] if k == 32 else [])
             for arrays, words in shapes:
                 d = data[:arrays * words * k // 8]
                 pp.generate(kind, 1, d, stream=s)
                 offs = torch.arange(0, arrays + 1, dtype=torch.int64, device="cuda") * words
                 o = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
                 want = None
-                variants = seg_cases[k] if (arrays, words) == (65536, 4096) else seg_cases[k][:1] + seg_cases[k][2:5]
+                variants = seg_cases[k] if (arrays, words) == (65536, 4096) else seg_cases[k][:4]
                 for var in variants:
                     os.environ["POSPOP_SEG_VARIANT"] = var
                     med, best = timed(lambda: pp.segmented_async(d, offs, o, k, stream=s), args.reps, s)
