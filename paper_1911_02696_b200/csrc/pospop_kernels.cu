@@ -150,7 +150,7 @@ const StreamVariant kStreamVariants[] = {
     SVB(5, 32, 256, 2), SVB(4, 32, 512, 2), SVB(4, 32, 256, 2), SVB2(4, 32, 256, 2),
     SVB(4, 16, 512, 2), SVB(6, 32, 256, 2), SVB(5, 16, 512, 2), SVB2(5, 32, 256, 2),
     SVB(4, 32, 512, 4), SVB(4, 16, 512, 4), SVB(3, 32, 512, 4), SVB(4, 32, 256, 4), SVB2(3, 32, 256, 4),
-    SVB(5, 32, 256, 4),
+    SVB(5, 32, 256, 4), SVB(5, 32, 512, 5), SVB(5, 16, 512, 5), SVB(6, 32, 256, 5),
 };
 #undef SV
 #undef SVF

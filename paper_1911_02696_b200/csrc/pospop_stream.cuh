@@ -498,12 +498,15 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                 nb = 0;
             }
         }
-    } else if constexpr (SCHED == 4) {
+    } else if constexpr (SCHED == 4 || SCHED == 5) {
         // SCHED 2's work split with double-buffered tile registers: the next
         // warp tile is claimed and its loads issued before the current tile is
         // consumed, so each warp keeps a tile in flight while it computes
         // (for the ALU-heavy FLAG mode, whose warps would otherwise alternate
-        // between waiting and computing).
+        // between waiting and computing).  SCHED 5 (MODE 2): the tile is
+        // loaded in two halves and the pipeline runs at half-tile grain, so
+        // the same registers as SCHED 2 keep one half-tile always in flight
+        // while the depth-L tree is built from two depth-(L-1) halves.
         constexpr unsigned long long WT = 32ull * VPT;
         const unsigned long long S0 = a.g0 * 32;
         const unsigned long long P = a.nwt - a.pool;
@@ -539,6 +542,43 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
             }
             return pw++;
         };
+        if constexpr (SCHED == 5) {
+            static_assert(MODE == 2 && !pair_tiles<MODE, L>() && VPT % 2 == 0, "SCHED 5: byte-frame FLAG, L >= 5");
+            constexpr int HR = REGS / 2, HV = VPT / 2;  // registers / vectors per half tile
+            auto load_half = [&](unsigned long long w, int h, uint32_t (&r)[HR]) {
+                const unsigned long long t = S0 + w * WT;
+                load_tree_block<VB, HINT, HV>(a, t + lane + 32ull * HV * h, 32u, t >= a.f0 && t + WT <= a.f1, r);
+            };
+            auto half_tree = [&](const uint32_t (&r)[HR], unsigned long long w, int h, uint32_t (&top)[3]) {
+                uint32_t bad = 0;
+                FlagByteTree<CD, L - 1>::run(carries, r, top, bad);
+                if (bad & 0xF0F0F0F0u)
+                    flag_locate_bad<HR, RPV, VB>(a, r, S0 + w * WT + lane + 32ull * HV * h, 32u);
+            };
+            uint32_t ra[HR], rb[HR];
+            unsigned long long w = claim();
+            if (w != kEnd) load_half(w, 0, ra);
+            while (w != kEnd) {
+                load_half(w, 1, rb);
+                uint32_t x[3], y[3];
+                half_tree(ra, w, 0, x);
+                const unsigned long long wn = claim();
+                if (wn != kEnd) load_half(wn, 0, ra);
+                half_tree(rb, w, 1, y);
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    uint32_t h, l;
+                    csa(h, l, carries[b][L - 1], x[b], y[b]);
+                    carries[b][L - 1] = l;
+                    extract_bytes(counter[b], h);
+                }
+                if (++nb == a.flush_threshold) {
+                    flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
+                    nb = 0;
+                }
+                w = wn;
+            }
+        } else {
         auto load = [&](unsigned long long w, uint32_t (&r)[REGS]) {
             const unsigned long long t = S0 + w * WT;
             load_tree_block<VB, HINT, VPT>(a, t + lane, 32u, t >= a.f0 && t + WT <= a.f1, r);
@@ -563,6 +603,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                 flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
                 nb = 0;
             }
+        }
         }
     } else if constexpr (SCHED == 2) {
         // Warp tiles [0, P) are split statically into contiguous CTA ranges

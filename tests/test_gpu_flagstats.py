@@ -84,7 +84,8 @@ def test_empty_and_full_size(pp, dev, orc):
 
 
 FLAG_VARIANTS = ["5,32,0,512,2,2", "4,32,0,512,2,2", "4,32,2,256,2,2", "4,16,0,512,2,2", "6,32,0,256,2,2",
-                 "5,32,0,256,2,2", "4,32,0,512,4,2", "3,32,0,512,4,2", "4,32,0,256,4,2", "6,32,0,512,2"]
+                 "5,32,0,256,2,2", "4,32,0,512,4,2", "3,32,0,512,4,2", "4,32,0,256,4,2", "5,32,0,512,5,2",
+                 "5,16,0,512,5,2", "6,32,0,256,5,2", "6,32,0,512,2"]
 
 
 @pytest.mark.parametrize("variant", FLAG_VARIANTS)

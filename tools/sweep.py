@@ -165,8 +165,8 @@ def main():
         torch.cuda.synchronize()
         import ctypes as CC
         summ = pp._Summary()
-        for var in ["6,32,0,512,2", "5,32,0,512,2,2", "5,16,0,512,2,2", "4,32,0,512,2,2", "4,32,0,512,4,2",
-                    "4,16,0,512,4,2", "5,32,2,256,2,2", "4,32,2,256,2,2"]:
+        for var in ["5,32,0,512,2,2", "5,32,0,512,5,2", "5,16,0,512,5,2", "6,32,0,256,5,2", "5,16,0,512,2,2",
+                    "4,32,0,512,4,2"]:
             var, _, tma = var.partition("/")
             os.environ["POSPOP_FLAG_VARIANT"] = var
             if tma:
