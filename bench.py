@@ -71,6 +71,9 @@ def parse():
                     help="strong: the workload's total words split over N (BASELINE cfg4); weak: per GPU")
     ap.add_argument("--clock-interval-ms", type=float, default=20.0,
                     help="NVML clock/throttle sampling period during the timed region (0 = off)")
+    ap.add_argument("--collective", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 cfg4: p2p = the k-vector delivered to every GPU by the counting kernel itself "
+                         "(peer-memory stores, paper_1911_02696_b200.exchange); nccl = a separate all-reduce")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -734,13 +737,41 @@ def run_ours(args):
     # stream while step i+1's kernel counts into the other output buffer
     # (double-buffered; a buffer is reused only after its reduction finished).
     outs = [out, torch.zeros(k, dtype=torch.int64, device=dev)]
-    comm = torch.cuda.Stream(dev) if world > 1 else None
+    # High priority: when a count kernel's CTA retires, the (one-CTA) NCCL all-reduce
+    # kernel is scheduled before the next count's CTAs, which PDL launches early.
+    comm = torch.cuda.Stream(dev, priority=-1) if world > 1 else None
     counted = [torch.cuda.Event() for _ in range(2)]
     reduced = [torch.cuda.Event() for _ in range(2)]
     issued = [False, False]
 
+    # Fused exchange: set up the peer gather slots, prove they work on this
+    # machine (every rank's rows land on every GPU and sum to the NCCL
+    # all-reduce), else fall back to the NCCL all-reduce and say why.
+    pg, collective = None, ("nccl" if world > 1 else "none")
+    if world > 1 and args.collective == "p2p":
+        try:
+            from paper_1911_02696_b200.exchange import PeerGather
+            pg = PeerGather(k)
+            probe = torch.zeros(k, dtype=torch.int64, device=dev)
+            pg.count(data, probe, 0, stream=stream, len_words=min(words, 1 << 20))
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            ref = probe.clone()
+            dist.all_reduce(ref)
+            ok = torch.tensor([int(torch.equal(pg.result(0), ref))], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) != 1:
+                raise RuntimeError("peer gather rows disagree with the NCCL all-reduce")
+            collective = "p2p"
+        except Exception as e:  # noqa: BLE001 -- setup-time choice of collective, reported in config
+            print(f"[bench] p2p exchange unavailable ({e}); using NCCL all-reduce", file=sys.stderr)
+            pg, collective = None, f"nccl (p2p unavailable: {str(e)[:120]})"
+
     def step(i):
         o = outs[i % 2]
+        if pg is not None:  # one kernel: count + deliver the k-vector to every GPU
+            pg.count(data, o, i, stream=stream, len_words=words)
+            return
         if world > 1 and issued[i % 2]:
             stream.wait_event(reduced[i % 2])
         pp.count_async(data, o, k, stream=stream, len_words=words)
@@ -753,7 +784,7 @@ def run_ours(args):
             issued[i % 2] = True
 
     def join():
-        if world > 1:
+        if world > 1 and pg is None:
             stream.wait_stream(comm)
 
     for i in range(max(args.warmup, 3)):
@@ -815,6 +846,12 @@ def run_ours(args):
     value = total_bytes / (ms_per_step * 1e-3) / 1e9
 
     counts = outs[(args.steps - 1) % 2].cpu().numpy().astype(np.uint64)
+    if pg is not None:  # the delivered rows of the last step must sum to the NCCL all-reduce
+        local = outs[(args.steps - 1) % 2].clone()
+        ref = local.clone()
+        dist.all_reduce(ref)
+        assert torch.equal(pg.result(args.steps - 1), ref), "p2p exchange disagrees with NCCL"
+        counts = pg.result(args.steps - 1).cpu().numpy().astype(np.uint64)
     if args.workload == "cfg2":
         assert int(counts.sum()) == total, "one-hot invariant violated"
 
@@ -880,7 +917,10 @@ def run_ours(args):
         "data": "synthetic (counter-based generator, generated in place in HBM)",
         "config": {"workload": desc, "words_total": total, "k": k, "bytes_per_step": total_bytes,
                    "parallelism": f"shard{world}", "l2_policy": "input >> 126 MB L2; no flush needed",
-                   "kernel": "stream_kernel<NBANK=1,L=7,VB=32,BLOCK=256,SCHED=2>: LDG.E.NA.256 + LOP3 Harley-Seal depth 7, CTA ranges + shared-counter warp tiles + global tail pool; one launch per step"},
+                   "collective": collective,
+                   "kernel": "stream_kernel<NBANK=1,L=7,VB=32,BLOCK=256,SCHED=2>: LDG.E.NA.256 + LOP3 Harley-Seal depth 7, CTA ranges + shared-counter warp tiles + global tail pool; one launch per step"
+                             + ("; the last CTA also stores the k-vector into every GPU's gather slot (peer memory)"
+                                if collective == "p2p" else "")},
         "words_per_s": round(total_bytes / wb / (ms_per_step * 1e-3), 1),
         "pct_hbm_peak": round(100 * value / world / peak, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",

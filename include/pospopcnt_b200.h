@@ -197,6 +197,26 @@ pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d
 pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
                                     uint64_t* d_trace, size_t trace_ctas, int* grid_used, void* stream);
 
+/* Multi-GPU, one process per GPU: count fused with the exchange.
+ * The k-vector sum across GPUs (reference merge_counts, pospop.cpp:33-37, the
+ * sanctioned chunk-and-merge) is done through peer memory instead of a
+ * separate collective: every rank owns a gather buffer from pospop_ipc_alloc,
+ * exports its handle (64 bytes, exchanged by the caller, e.g. over
+ * torch.distributed), and maps the peers' buffers with pospop_ipc_open.
+ * pospopcnt_allgather_async counts d_data like pospopcnt_async (d_counts gets
+ * this rank's counts) and its last CTA also stores them into
+ * d_slots[j][rank*k .. rank*k + k) for every j < n_ranks -- plain stores over
+ * NVLink from inside the counting kernel.  d_slots is a DEVICE array of
+ * n_ranks device pointers (the peers' buffers, own buffer included).  Once
+ * every rank's launch has completed, summing a slot's n_ranks rows gives the
+ * all-reduced counts on every GPU.  No kernel waits on another rank. */
+pospop_status pospop_ipc_alloc(size_t bytes, void** d_ptr, unsigned char handle[64]);  /* zeroed */
+pospop_status pospop_ipc_open(const unsigned char handle[64], void** d_ptr);
+pospop_status pospop_ipc_close(void* d_ptr);
+pospop_status pospop_ipc_free(void* d_ptr);
+pospop_status pospopcnt_allgather_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
+                                        uint64_t* const* d_slots, int n_ranks, int rank, void* stream);
+
 /* CUDA-graph replay for repeated counts of one device buffer, where launch
  * latency dominates (small inputs).  The graph is bound to (d_data, len,
  * d_counts) and reads the buffer's current contents at every replay; d_counts

@@ -37,7 +37,8 @@ import numpy as np
 __all__ = [
     "KernelKind", "PospopcntConfig", "PositionalCounts", "InvalidArgument", "KernelUnavailableError",
     "CudaError", "validate", "merge_counts", "pospopcnt", "pospopcnt_k", "pospopcnt_u16_c32",
-    "pospopcnt_segmented", "pospopcnt_sharded", "count_async", "segmented_async", "generate", "digest",
+    "pospopcnt_segmented", "pospopcnt_sharded", "count_async", "segmented_async", "count_allgather_async",
+    "ipc_alloc", "ipc_open", "ipc_close", "ipc_free", "generate", "digest",
     "supported_csa_widths", "native_csa_width", "device_available", "kernel_launches", "library_path",
     "FlagBucket", "FlagSummary", "InvalidFlagWordError", "flagstats", "pospopcnt_file",
 ]
@@ -135,6 +136,11 @@ def _load():
         "pospopcnt_graph_launch": ([vp, vp], C.c_int),
         "pospopcnt_graph_destroy": ([vp], None),
         "pospopcnt_file": ([C.c_char_p, C.c_int, _u64p, _u64p], C.c_int),
+        "pospop_ipc_alloc": ([sz, C.POINTER(vp), C.POINTER(C.c_ubyte)], C.c_int),
+        "pospop_ipc_open": ([C.POINTER(C.c_ubyte), C.POINTER(vp)], C.c_int),
+        "pospop_ipc_close": ([vp], C.c_int),
+        "pospop_ipc_free": ([vp], C.c_int),
+        "pospopcnt_allgather_async": ([C.c_int, vp, sz, vp, vp, C.c_int, C.c_int, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -359,6 +365,45 @@ def count_async(data: Any, out: Any, k: int, *, accumulate: bool = False, flush_
     out_addr, _ = _addr_len(out, 64)
     _check(_load().pospopcnt_async(int(k), addr or None, n, out_addr, int(accumulate), int(flush_threshold_blocks),
                                    int(grid), int(block), _stream_ptr(stream)))
+
+
+def count_allgather_async(data: Any, out: Any, k: int, slots: Any, n_ranks: int, rank: int, *,
+                          stream: Any = None, len_words: int | None = None) -> None:
+    """Count fused with the cross-GPU exchange (pospopcnt_allgather_async): out
+    gets this rank's counts and the kernel's last CTA stores them into row
+    `rank` of every slot in `slots` (device array of n_ranks gather-slot
+    pointers, see paper_1911_02696_b200.exchange)."""
+    addr, n = _addr_len(data, k)
+    if len_words is not None:
+        n = int(len_words)
+    out_addr, _ = _addr_len(out, 64)
+    slots_addr, _ = _addr_len(slots, 64)
+    _check(_load().pospopcnt_allgather_async(int(k), addr or None, n, out_addr, slots_addr, int(n_ranks), int(rank),
+                                             _stream_ptr(stream)))
+
+
+def ipc_alloc(nbytes: int) -> tuple[int, bytes]:
+    """A zeroed device allocation exportable to other processes: (address, 64-byte handle)."""
+    ptr = C.c_void_p()
+    h = (C.c_ubyte * 64)()
+    _check(_load().pospop_ipc_alloc(int(nbytes), C.byref(ptr), h))
+    return int(ptr.value), bytes(h)
+
+
+def ipc_open(handle: bytes) -> int:
+    """Maps another process's pospop_ipc_alloc allocation into this one (peer access over NVLink)."""
+    ptr = C.c_void_p()
+    h = (C.c_ubyte * 64).from_buffer_copy(handle)
+    _check(_load().pospop_ipc_open(h, C.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(_load().pospop_ipc_close(C.c_void_p(ptr)))
+
+
+def ipc_free(ptr: int) -> None:
+    _check(_load().pospop_ipc_free(C.c_void_p(ptr)))
 
 
 def segmented_async(data: Any, offsets: Any, out: Any, k: int, *, flush_threshold_blocks: int = 65535,

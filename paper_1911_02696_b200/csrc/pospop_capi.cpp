@@ -734,6 +734,62 @@ pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d
     return POSPOP_OK;
 }
 
+pospop_status pospop_ipc_alloc(size_t bytes, void** d_ptr, unsigned char handle[64]) {
+    if (!d_ptr || !handle || !bytes) return fail(POSPOP_EINVAL, "NULL pointer or zero size");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    CU(cudaMalloc(d_ptr, bytes));
+    CU(cudaMemset(*d_ptr, 0, bytes));
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, *d_ptr));
+    std::memcpy(handle, &h, 64);
+    return POSPOP_OK;
+}
+
+pospop_status pospop_ipc_open(const unsigned char handle[64], void** d_ptr) {
+    if (!d_ptr || !handle) return fail(POSPOP_EINVAL, "NULL pointer");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    CU(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return POSPOP_OK;
+}
+
+pospop_status pospop_ipc_close(void* d_ptr) {
+    CU(cudaIpcCloseMemHandle(d_ptr));
+    return POSPOP_OK;
+}
+
+pospop_status pospop_ipc_free(void* d_ptr) {
+    CU(cudaFree(d_ptr));
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_allgather_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
+                                        uint64_t* const* d_slots, int n_ranks, int rank, void* stream) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (!d_counts || !d_slots || (!d_data && len)) return fail(POSPOP_EINVAL, "NULL pointer");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return fail(POSPOP_EINVAL, "rank %d of %d", rank, n_ranks);
+    if ((uintptr_t)d_data % ((size_t)k / 8)) return fail(POSPOP_EINVAL, "data is misaligned");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamWorkspace ws;
+    if ((s = stream_workspace(dev, st, &ws))) return s;
+    LaunchOptions opt;
+    opt.peers = reinterpret_cast<unsigned long long* const*>(d_slots);
+    opt.n_peers = n_ranks;
+    opt.rank = rank;
+    CU(launch_stream(k, len ? d_data : (const void*)d_counts, len, reinterpret_cast<unsigned long long*>(d_counts),
+                     false, opt, ws, st));
+    return POSPOP_OK;
+}
+
 pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
                                     uint64_t* d_trace, size_t trace_ctas, int* grid_used, void* stream) {
     if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);

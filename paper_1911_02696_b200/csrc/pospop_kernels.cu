@@ -278,6 +278,9 @@ static void fill_stream_args(StreamArgs& a, int k, const void* data, size_t len_
     a.data_off = nbytes ? (unsigned long long)(P - reinterpret_cast<uintptr_t>(a.base)) : 0ull;
     a.nwt = a.nA = a.pool = 0;
     a.CA = a.CB = 1;
+    a.peers = opt.peers;
+    a.n_peers = opt.peers ? opt.n_peers : 0;
+    a.rank = opt.rank;
 }
 
 static cudaError_t launch_with_pdl(StreamKernel fn, int grid, int threads, size_t smem, cudaStream_t stream,
@@ -398,6 +401,9 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     a.bad = ws.bad;
     a.word_base = opt.word_base;
     a.data_off = nbytes ? (unsigned long long)(P - reinterpret_cast<uintptr_t>(a.base)) : 0ull;
+    a.peers = mode == 0 ? opt.peers : nullptr;
+    a.n_peers = a.peers ? opt.n_peers : 0;
+    a.rank = opt.rank;
 
     int grid = opt.grid;
     if (grid <= 0) {
@@ -460,7 +466,7 @@ cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned lo
     env_refresh();
     const size_t nbytes = len_words * (size_t)(k / 8);
     if (nbytes <= (size_t)env_int("POSPOP_SMALL_BYTES", kSmallBytes) && !opt.grid && !opt.block && !opt.trace &&
-        !opt.depth && !env_get("POSPOP_STREAM_VARIANT"))
+        !opt.depth && !opt.peers && !env_get("POSPOP_STREAM_VARIANT"))
         return launch_small(k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
     return launch_stream_mode(0, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
 }

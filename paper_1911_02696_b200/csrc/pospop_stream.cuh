@@ -40,6 +40,11 @@ struct StreamArgs {
     unsigned long long data_off;  // data start - base, bytes
     unsigned long long word_base; // global index of the first word (host-staged chunks)
     unsigned long long* bad;      // max of ~(index of an invalid FLAG word); 0 = none
+    // Fused exchange (MODE 0): the last CTA also stores out[k] into every
+    // rank's gather slot, peers[j][rank * k + p] (peer memory mapped through
+    // CUDA IPC / peer access; plain stores over NVLink), j < n_peers.
+    unsigned long long* const* peers;
+    int n_peers, rank;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -223,8 +228,11 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
                 const int m = channels_per_position(k);
                 for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
             }
-            a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+            if (a.accumulate) sum += a.out[pos];
+            a.out[pos] = sum;
+            for (int j = 0; j < a.n_peers; ++j) a.peers[j][a.rank * k + pos] = sum;
         }
+        if (a.n_peers) __threadfence_system();
     }
     if (threadIdx.x == 0) {
         *a.ticket = 0u;
