@@ -13,7 +13,9 @@
 #include <unistd.h>
 
 #include <cerrno>
+#include <condition_variable>
 #include <cstdarg>
+#include <functional>
 #include <thread>
 #include <cstdio>
 #include <cstdlib>
@@ -109,6 +111,98 @@ struct DeviceGuard {
 // ---------------------------------------------------------------------------
 constexpr int kRing = 3;
 constexpr size_t kBounceBytes = 1 << 20;  // host inputs up to this size take the single-stream path
+constexpr int kHostRing = 4;              // pinned host slots for pageable / file input
+constexpr size_t kHostChunk = 16 << 20;   // bytes per pinned host slot
+
+// Persistent host worker threads for the CPU side of host-input pipelines
+// (parallel memcpy from pageable memory, parallel pread from files) into the
+// pinned host ring; one process-wide pool, one job at a time.
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool pool;
+        return pool;
+    }
+    int size() const { return (int)workers_.size() + 1; }
+    // Runs fn(0 .. tasks-1) on the pool and the calling thread; returns when all are done.
+    void run(int tasks, const std::function<void(int)>& fn) {
+        std::lock_guard<std::mutex> job(job_mu_);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            tasks_ = tasks;
+            next_ = 0;
+            done_ = 0;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return done_ == tasks_; });
+        fn_ = nullptr;
+    }
+
+  private:
+    HostPool() {
+        const char* env = std::getenv("POSPOP_HOST_THREADS");
+        int n = env && *env ? std::atoi(env) : (int)std::thread::hardware_concurrency();
+        if (n > 32) n = 32;
+        for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    void work() {
+        for (;;) {
+            int t;
+            const std::function<void(int)>* fn;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!fn_ || next_ >= tasks_) return;
+                t = next_++;
+                fn = fn_;
+            }
+            (*fn)(t);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (++done_ == tasks_) done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        unsigned long long seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex job_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int tasks_ = 0, next_ = 0, done_ = 0;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+};
+
+// Parallel memcpy of `n` bytes in 1 MiB pieces on the host pool.
+void parallel_copy(void* dst, const void* src, size_t n) {
+    constexpr size_t kPiece = 1 << 20;
+    const int tasks = (int)((n + kPiece - 1) / kPiece);
+    HostPool::get().run(tasks, [&](int t) {
+        const size_t lo = (size_t)t * kPiece;
+        const size_t len = n - lo < kPiece ? n - lo : kPiece;
+        std::memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo, len);
+    });
+}
 
 struct Ctx {
     int dev = -1;
@@ -126,6 +220,10 @@ struct Ctx {
     size_t stage_bytes = 0;
     cudaEvent_t ev_copied[kRing] = {};
     cudaEvent_t ev_done[kRing] = {};
+    // pinned host ring for pageable / file input (lazily allocated)
+    uint8_t* host_ring[kHostRing] = {};
+    cudaEvent_t ev_h2d[kHostRing] = {};  // the H2D that last read host_ring[i] is done
+    bool host_used[kHostRing] = {};
 };
 
 thread_local std::map<int, Ctx*> t_ctx;
@@ -174,6 +272,44 @@ pospop_status ensure_stage(Ctx* c) {
         CU(cudaMalloc(&c->stage[i], c->stage_bytes));
         CU(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+    }
+    return POSPOP_OK;
+}
+
+pospop_status ensure_host_ring(Ctx* c) {
+    if (c->host_ring[0]) return POSPOP_OK;
+    for (int i = 0; i < kHostRing; ++i) {
+        CU(cudaMallocHost(&c->host_ring[i], kHostChunk));
+        CU(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+    }
+    return POSPOP_OK;
+}
+
+// Host input through the pinned ring: `produce(slot_ptr, offset, bytes)`
+// fills a pinned slot (parallel memcpy or pread, on the host pool) while the
+// previous slots' H2D copies (copy stream) and kernels (compute stream) run.
+// `launch(dev_ptr, offset, bytes, chunk_index)` enqueues the counting kernel.
+template <class Produce, class Launch>
+pospop_status host_ring_pipeline(Ctx* c, size_t total_bytes, size_t align, Produce produce, Launch launch) {
+    pospop_status s;
+    if ((s = ensure_stage(c))) return s;
+    if ((s = ensure_host_ring(c))) return s;
+    const size_t chunk = kHostChunk < c->stage_bytes ? kHostChunk : c->stage_bytes;  // multiple of `align`
+    (void)align;
+    size_t i = 0;
+    for (size_t off = 0; off < total_bytes; off += chunk, ++i) {
+        const size_t n = total_bytes - off < chunk ? total_bytes - off : chunk;
+        const int hs = (int)(i % kHostRing), ds = (int)(i % kRing);
+        if (c->host_used[hs]) CU(cudaEventSynchronize(c->ev_h2d[hs]));
+        if ((s = produce(c->host_ring[hs], off, n))) return s;
+        if (i >= (size_t)kRing) CU(cudaStreamWaitEvent(c->copy, c->ev_done[ds], 0));
+        CU(cudaMemcpyAsync(c->stage[ds], c->host_ring[hs], n, cudaMemcpyHostToDevice, c->copy));
+        CU(cudaEventRecord(c->ev_h2d[hs], c->copy));
+        c->host_used[hs] = true;
+        CU(cudaEventRecord(c->ev_copied[ds], c->copy));
+        CU(cudaStreamWaitEvent(c->stream, c->ev_copied[ds], 0));
+        if ((s = launch(c->stage[ds], off, n, i))) return s;
+        CU(cudaEventRecord(c->ev_done[ds], c->stream));
     }
     return POSPOP_OK;
 }
@@ -259,9 +395,25 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
         }
         CU(cudaMemcpyAsync(c->stage[0], src, len * wb, cudaMemcpyHostToDevice, c->stream));
         CU(launch_stream(k, c->stage[0], len, c->m_out_dev, false, opt, c->ws, c->stream));
+    } else if (!pinned) {
+        // Pageable host input: parallel memcpy into the pinned host ring
+        // overlapping the H2D of the previous slot and the kernel before it.
+        const uint8_t* src = static_cast<const uint8_t*>(data);
+        s = host_ring_pipeline(
+            c, len * wb, wb,
+            [&](uint8_t* dst, size_t off, size_t n) {
+                parallel_copy(dst, src + off, n);
+                return POSPOP_OK;
+            },
+            [&](const void* d, size_t, size_t n, size_t i) -> pospop_status {
+                CU(launch_stream(k, d, n / wb, c->m_out_dev, i > 0, opt, c->ws, c->stream));
+                return POSPOP_OK;
+            });
+        if (s) return s;
     } else {
-        // Host input: chunked H2D on the copy stream, counting on the compute
-        // stream, kRing staging buffers recycled behind ev_done.
+        // Pinned host input: chunked H2D straight from the caller's buffer on
+        // the copy stream, counting on the compute stream, kRing staging
+        // buffers recycled behind ev_done.
         if ((s = ensure_stage(c))) return s;
         const size_t chunk_words = c->stage_bytes / wb;
         const uint8_t* src = static_cast<const uint8_t*>(data);
@@ -467,13 +619,30 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
     if (s) return s;
     std::memset(out, 0, sizeof *out);
     if (len == 0) return POSPOP_OK;
-    const Where where = classify(flags, &dev);
+    bool pinned = false;
+    const Where where = classify(flags, &dev, &pinned);
     DeviceGuard g(dev);
     Ctx* c = nullptr;
     if ((s = get_ctx(dev, &c))) return s;
     LaunchOptions opt;
     if (where == Where::Device) {
         CU(launch_flagstats(flags, len, c->m_out_dev, false, opt, c->ws, c->stream));
+    } else if (!pinned) {  // pageable: parallel copies into the pinned host ring
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(flags);
+        s = host_ring_pipeline(
+            c, len * 2, 2,
+            [&](uint8_t* dst, size_t off, size_t n) {
+                parallel_copy(dst, src + off, n);
+                return POSPOP_OK;
+            },
+            [&](const void* d, size_t off, size_t n, size_t i) -> pospop_status {
+                LaunchOptions o = opt;
+                o.word_base = off / 2;
+                CU(launch_flagstats(static_cast<const uint16_t*>(d), n / 2, c->m_out_dev, i > 0, o, c->ws,
+                                    c->stream));
+                return POSPOP_OK;
+            });
+        if (s) return s;
     } else {
         if ((s = ensure_stage(c))) return s;
         const size_t chunk_words = c->stage_bytes / 2;
@@ -524,7 +693,7 @@ namespace {
 
 // Fills buf with up to `want` bytes from fd at `offset` (regular file:
 // parallel pread stripes) or sequentially (pipe).  Returns bytes read, or -1.
-ssize_t fill_buffer(int fd, bool seekable, uint8_t* buf, size_t want, uint64_t offset, int threads) {
+ssize_t fill_buffer(int fd, bool seekable, uint8_t* buf, size_t want, uint64_t offset) {
     if (!seekable) {
         size_t got = 0;
         while (got < want) {
@@ -538,34 +707,31 @@ ssize_t fill_buffer(int fd, bool seekable, uint8_t* buf, size_t want, uint64_t o
         }
         return (ssize_t)got;
     }
-    const size_t stripe = (want / (size_t)threads + 4095) & ~(size_t)4095;
-    std::vector<ssize_t> got((size_t)threads, 0);
-    std::vector<std::thread> ts;
-    for (int t = 0; t < threads; ++t) {
-        const size_t lo = (size_t)t * stripe;
-        if (lo >= want) break;
-        const size_t hi = lo + stripe < want ? lo + stripe : want;
-        ts.emplace_back([&, t, lo, hi] {
-            size_t done = 0;
-            while (lo + done < hi) {
-                const ssize_t r = ::pread(fd, buf + lo + done, hi - lo - done, (off_t)(offset + lo + done));
-                if (r < 0) {
-                    if (errno == EINTR) continue;
-                    got[(size_t)t] = -1;
-                    return;
-                }
-                if (r == 0) break;
-                done += (size_t)r;
+    // Regular file: parallel pread of 1 MiB pieces on the host pool.
+    constexpr size_t kPiece = 1 << 20;
+    const int tasks = (int)((want + kPiece - 1) / kPiece);
+    std::vector<ssize_t> got((size_t)tasks, 0);
+    HostPool::get().run(tasks, [&](int t) {
+        const size_t lo = (size_t)t * kPiece;
+        const size_t hi = lo + kPiece < want ? lo + kPiece : want;
+        size_t done = 0;
+        while (lo + done < hi) {
+            const ssize_t r = ::pread(fd, buf + lo + done, hi - lo - done, (off_t)(offset + lo + done));
+            if (r < 0) {
+                if (errno == EINTR) continue;
+                got[(size_t)t] = -1;
+                return;
             }
-            got[(size_t)t] = (ssize_t)done;
-        });
-    }
-    for (auto& th : ts) th.join();
+            if (r == 0) break;
+            done += (size_t)r;
+        }
+        got[(size_t)t] = (ssize_t)done;
+    });
     size_t total = 0;
-    for (size_t t = 0; t < ts.size(); ++t) {
-        if (got[t] < 0) return -1;
-        total += (size_t)got[t];
-        if ((size_t)got[t] < (t + 1 == ts.size() ? want - t * stripe : stripe)) break;  // EOF inside stripe t
+    for (int t = 0; t < tasks; ++t) {
+        if (got[(size_t)t] < 0) return -1;
+        total += (size_t)got[(size_t)t];
+        if ((size_t)got[(size_t)t] < (t + 1 == tasks ? want - (size_t)t * kPiece : kPiece)) break;  // EOF in piece t
     }
     return (ssize_t)total;
 }
@@ -585,32 +751,15 @@ pospop_status pospopcnt_fd(int fd, int k, uint64_t* counts, uint64_t* n_words) {
     struct stat st;
     const bool seekable = fstat(fd, &st) == 0 && S_ISREG(st.st_mode);
     const size_t wb = (size_t)k / 8;
-    const size_t chunk = c->stage_bytes;  // a multiple of 8
-    uint8_t* pinned[2] = {nullptr, nullptr};
-    cudaEvent_t copied[2];
-    for (int i = 0; i < 2; ++i) {
-        CU(cudaMallocHost(&pinned[i], chunk));
-        CU(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
-    }
-    struct Release {
-        uint8_t** p;
-        cudaEvent_t* e;
-        ~Release() {
-            for (int i = 0; i < 2; ++i) {
-                cudaEventSynchronize(e[i]);
-                cudaFreeHost(p[i]);
-                cudaEventDestroy(e[i]);
-            }
-        }
-    } release{pinned, copied};
-    const char* env = std::getenv("POSPOP_READ_THREADS");
-    const int threads = env && *env ? std::atoi(env) : 8;
+    if ((s = ensure_host_ring(c))) return s;
+    const size_t chunk = kHostChunk < c->stage_bytes ? kHostChunk : c->stage_bytes;  // a multiple of 8
     uint64_t total = 0;
     LaunchOptions opt;
     for (size_t i = 0;; ++i) {
-        const int b = (int)(i % 2), slot = (int)(i % kRing);
-        CU(cudaEventSynchronize(copied[b]));  // the H2D that last read pinned[b] is done
-        const ssize_t got = fill_buffer(fd, seekable, pinned[b], chunk, total, threads < 1 ? 1 : threads);
+        const int hs = (int)(i % kHostRing), slot = (int)(i % kRing);
+        if (c->host_used[hs]) CU(cudaEventSynchronize(c->ev_h2d[hs]));  // the H2D that last read it is done
+        uint8_t* buf = c->host_ring[hs];
+        const ssize_t got = fill_buffer(fd, seekable, buf, chunk, total);
         if (got < 0) return fail(POSPOP_EINVAL, "read failed: %s", std::strerror(errno));
         if (got == 0) break;
         total += (uint64_t)got;
@@ -622,8 +771,9 @@ pospop_status pospopcnt_fd(int fd, int k, uint64_t* counts, uint64_t* n_words) {
                         wb == 2 ? "odd" : "ragged", (unsigned long long)total, more > 0 ? "+" : "", k);
         }
         if (i >= (size_t)kRing) CU(cudaStreamWaitEvent(c->copy, c->ev_done[slot], 0));
-        CU(cudaMemcpyAsync(c->stage[slot], pinned[b], (size_t)got, cudaMemcpyHostToDevice, c->copy));
-        CU(cudaEventRecord(copied[b], c->copy));
+        CU(cudaMemcpyAsync(c->stage[slot], buf, (size_t)got, cudaMemcpyHostToDevice, c->copy));
+        CU(cudaEventRecord(c->ev_h2d[hs], c->copy));
+        c->host_used[hs] = true;
         CU(cudaEventRecord(c->ev_copied[slot], c->copy));
         CU(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
         CU(launch_stream(k, c->stage[slot], (size_t)got / wb, c->d_out, i > 0, opt, c->ws, c->stream));
