@@ -220,6 +220,9 @@ struct Ctx {
     size_t stage_bytes = 0;
     cudaEvent_t ev_copied[kRing] = {};
     cudaEvent_t ev_done[kRing] = {};
+    // grow-only device scratch for the synchronous segmented call (data, offsets, rows)
+    void* scratch[3] = {};
+    size_t scratch_cap[3] = {};
     // pinned host ring for pageable / file input (lazily allocated)
     uint8_t* host_ring[kHostRing] = {};
     cudaEvent_t ev_h2d[kHostRing] = {};  // the H2D that last read host_ring[i] is done
@@ -310,6 +313,45 @@ pospop_status host_ring_pipeline(Ctx* c, size_t total_bytes, size_t align, Produ
         CU(cudaStreamWaitEvent(c->stream, c->ev_copied[ds], 0));
         if ((s = launch(c->stage[ds], off, n, i))) return s;
         CU(cudaEventRecord(c->ev_done[ds], c->stream));
+    }
+    return POSPOP_OK;
+}
+
+// Grow-only device scratch buffer `i` of the context (no cudaMalloc/cudaFree
+// per call: cudaFree synchronises the device).
+pospop_status ctx_scratch(Ctx* c, int i, size_t bytes, void** out) {
+    if (c->scratch_cap[i] < bytes) {
+        if (c->scratch[i]) {
+            CU(cudaStreamSynchronize(c->stream));
+            CU(cudaFree(c->scratch[i]));
+            c->scratch[i] = nullptr;
+            c->scratch_cap[i] = 0;
+        }
+        CU(cudaMalloc(&c->scratch[i], bytes));
+        c->scratch_cap[i] = bytes;
+    }
+    *out = c->scratch[i];
+    return POSPOP_OK;
+}
+
+// Host -> device copy of a contiguous range on the compute stream; pageable
+// sources go through the pinned host ring with parallel memcpy.
+pospop_status h2d_on_stream(Ctx* c, void* dst, const void* src, size_t bytes, bool pinned) {
+    if (pinned || bytes <= kBounceBytes) {
+        CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+        return POSPOP_OK;
+    }
+    pospop_status s;
+    if ((s = ensure_host_ring(c))) return s;
+    size_t i = 0;
+    for (size_t off = 0; off < bytes; off += kHostChunk, ++i) {
+        const size_t n = bytes - off < kHostChunk ? bytes - off : kHostChunk;
+        const int hs = (int)(i % kHostRing);
+        if (c->host_used[hs]) CU(cudaEventSynchronize(c->ev_h2d[hs]));
+        parallel_copy(c->host_ring[hs], static_cast<const uint8_t*>(src) + off, n);
+        CU(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, c->host_ring[hs], n, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaEventRecord(c->ev_h2d[hs], c->stream));
+        c->host_used[hs] = true;
     }
     return POSPOP_OK;
 }
@@ -570,35 +612,33 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
     if (!data && hoff[n] != hoff[0]) return fail(POSPOP_EINVAL, "data is NULL but arrays are non-empty");
 
     const void* ddata = data;
-    void* tmp_data = nullptr;
-    unsigned long long* tmp_off = nullptr;
-    unsigned long long* tmp_out = nullptr;
-    auto cleanup = [&] {
-        if (tmp_data) cudaFree(tmp_data);
-        if (tmp_off) cudaFree(tmp_off);
-        if (tmp_out) cudaFree(tmp_out);
-    };
-    struct Cleanup {
-        decltype(cleanup)& f;
-        ~Cleanup() { f(); }
-    } guard{cleanup};
-
-    if (!d_dev && hoff[n] > 0) {  // stage the referenced range [0, offsets[n]) words
-        const size_t bytes = hoff[n] * wb;
-        CU(cudaMalloc(&tmp_data, bytes));
-        CU(cudaMemcpyAsync(tmp_data, data, bytes, cudaMemcpyHostToDevice, c->stream));
-        ddata = tmp_data;
+    if (!d_dev && hoff[n] > hoff[0]) {  // stage the referenced range [offsets[0], offsets[n]) words
+        bool pinned = false;
+        int hdev = dev;
+        classify(data, &hdev, &pinned);
+        const size_t lo = hoff[0] * wb, bytes = (hoff[n] - hoff[0]) * wb;
+        // keep the start's alignment within 32 bytes so vector loads see the same offsets
+        const size_t pad = reinterpret_cast<uintptr_t>(static_cast<const uint8_t*>(data) + lo) & 31u;
+        void* buf = nullptr;
+        if ((s = ctx_scratch(c, 0, bytes + pad + 64, &buf))) return s;  // +64: whole last vector
+        if ((s = h2d_on_stream(c, static_cast<uint8_t*>(buf) + pad, static_cast<const uint8_t*>(data) + lo, bytes,
+                               pinned)))
+            return s;
+        // device pointer whose word offsets[0] is at buf + pad
+        ddata = static_cast<const uint8_t*>(buf) + pad - lo;
     }
     const unsigned long long* doff = reinterpret_cast<const unsigned long long*>(offsets);
     if (!o_dev) {
-        CU(cudaMalloc(&tmp_off, (n + 1) * sizeof(uint64_t)));
-        CU(cudaMemcpyAsync(tmp_off, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
-        doff = tmp_off;
+        void* buf = nullptr;
+        if ((s = ctx_scratch(c, 1, (n + 1) * sizeof(uint64_t), &buf))) return s;
+        CU(cudaMemcpyAsync(buf, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+        doff = static_cast<const unsigned long long*>(buf);
     }
     unsigned long long* dout = reinterpret_cast<unsigned long long*>(counts);
     if (!c_dev) {
-        CU(cudaMalloc(&tmp_out, n * (size_t)k * sizeof(uint64_t)));
-        dout = tmp_out;
+        void* buf = nullptr;
+        if ((s = ctx_scratch(c, 2, n * (size_t)k * sizeof(uint64_t), &buf))) return s;
+        dout = static_cast<unsigned long long*>(buf);
     }
     LaunchOptions opt;
     opt.seg_avg_bytes = (hoff[n] - hoff[0]) * wb / n;  // picks the schedule for short arrays
