@@ -356,21 +356,44 @@ pospop_status h2d_on_stream(Ctx* c, void* dst, const void* src, size_t bytes, bo
     return POSPOP_OK;
 }
 
-// Workspaces for the async entry point, one per (device, stream).
+// Workspaces for the async entry point, one per (device, stream), plus the
+// output ranges of the stream's recent launches: a launch whose input overlaps
+// one of them is enqueued without programmatic dependent launch (our kernels
+// let dependents start early and read their own input before waiting).
+struct StreamState {
+    StreamWorkspace ws;
+    static constexpr int kHist = 8;
+    uintptr_t out_lo[kHist] = {}, out_hi[kHist] = {};
+    int next = 0;
+};
 std::mutex g_ws_mu;
-std::map<std::pair<int, cudaStream_t>, StreamWorkspace> g_ws;
+std::map<std::pair<int, cudaStream_t>, StreamState> g_ws;
 
-pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out) {
+pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out, const void* in = nullptr,
+                               size_t in_bytes = 0, const void* dst = nullptr, size_t dst_bytes = 0,
+                               bool* no_pdl = nullptr) {
     std::lock_guard<std::mutex> lock(g_ws_mu);
     auto key = std::make_pair(dev, s);
     auto it = g_ws.find(key);
     if (it == g_ws.end()) {
-        StreamWorkspace ws;
-        const pospop_status st = alloc_workspace(&ws);
-        if (st) return st;
-        it = g_ws.emplace(key, ws).first;
+        StreamState st;
+        const pospop_status e = alloc_workspace(&st.ws);
+        if (e) return e;
+        it = g_ws.emplace(key, st).first;
     }
-    *out = it->second;
+    StreamState& st = it->second;
+    if (no_pdl) {
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(in), hi = lo + in_bytes;
+        *no_pdl = false;
+        for (int i = 0; i < StreamState::kHist; ++i)
+            if (in_bytes && st.out_hi[i] > lo && st.out_lo[i] < hi) *no_pdl = true;
+        if (dst) {
+            st.out_lo[st.next] = reinterpret_cast<uintptr_t>(dst);
+            st.out_hi[st.next] = reinterpret_cast<uintptr_t>(dst) + dst_bytes;
+            st.next = (st.next + 1) % StreamState::kHist;
+        }
+    }
+    *out = st.ws;
     return POSPOP_OK;
 }
 
@@ -890,7 +913,7 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
             std::lock_guard<std::mutex> lock(g_ws_mu);
             auto it = g_ws.find(std::make_pair(devices[i], streams[(size_t)i]));
             if (it != g_ws.end()) {
-                cudaFree(it->second.acc);
+                cudaFree(it->second.ws.acc);
                 g_ws.erase(it);
             }
         }
@@ -914,8 +937,9 @@ pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d
     // The stream is used verbatim: NULL is the legacy default stream.
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamWorkspace ws;
-    if ((s = stream_workspace(dev, st, &ws))) return s;
     LaunchOptions opt;
+    if ((s = stream_workspace(dev, st, &ws, d_data, len * ((size_t)k / 8), d_counts, (size_t)k * 8, &opt.no_pdl)))
+        return s;
     opt.flush_threshold = flush;
     opt.grid = grid;
     opt.block = block;
@@ -970,8 +994,9 @@ pospop_status pospopcnt_allgather_async(int k, const void* d_data, size_t len, u
     if (s) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamWorkspace ws;
-    if ((s = stream_workspace(dev, st, &ws))) return s;
     LaunchOptions opt;
+    if ((s = stream_workspace(dev, st, &ws, d_data, len * ((size_t)k / 8), d_counts, (size_t)k * 8, &opt.no_pdl)))
+        return s;
     opt.peers = reinterpret_cast<unsigned long long* const*>(d_slots);
     opt.n_peers = n_ranks;
     opt.rank = rank;
@@ -1092,8 +1117,9 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
     if (s) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     StreamWorkspace ws;
-    if ((s = stream_workspace(dev, st, &ws))) return s;
     LaunchOptions opt;
+    bool unused = false;  // segmented kernels wait for the previous launch before reading anything
+    if ((s = stream_workspace(dev, st, &ws, nullptr, 0, d_counts, n * (size_t)k * 8, &unused))) return s;
     opt.flush_threshold = flush;
     opt.grid = grid;
     opt.block = block;

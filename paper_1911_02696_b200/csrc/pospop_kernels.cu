@@ -284,7 +284,7 @@ static void fill_stream_args(StreamArgs& a, int k, const void* data, size_t len_
 }
 
 static cudaError_t launch_with_pdl(StreamKernel fn, int grid, int threads, size_t smem, cudaStream_t stream,
-                                   const StreamArgs& a) {
+                                   const StreamArgs& a, bool pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)threads);
@@ -292,7 +292,7 @@ static cudaError_t launch_with_pdl(StreamKernel fn, int grid, int threads, size_
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = env_int("POSPOP_PDL", 1) ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl && env_int("POSPOP_PDL", 1) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
@@ -330,7 +330,7 @@ static cudaError_t launch_stream_tma(int mode, int nbank, int depth, int k, cons
     if (mode == 2 && a.flush_threshold > 255) a.flush_threshold = 255;  // byte-lane counters
     const int grid = device_info().sms;
     if (grid_used) *grid_used = grid;
-    return launch_with_pdl(var->fn, grid, 32 * (var->nc + 1), var->smem, stream, a);
+    return launch_with_pdl(var->fn, grid, 32 * (var->nc + 1), var->smem, stream, a, !opt.no_pdl);
 }
 
 static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t len_words,
@@ -437,7 +437,7 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = env_int("POSPOP_PDL", 1) ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = !opt.no_pdl && env_int("POSPOP_PDL", 1) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, var->fn, a);
@@ -457,7 +457,7 @@ static cudaError_t launch_small(int k, const void* data, size_t len_words, unsig
     StreamArgs a;
     fill_stream_args(a, k, data, len_words, 16, d_out, accumulate, opt, ws);
     if (grid_used) *grid_used = 1;
-    return launch_with_pdl(k == 64 ? small_kernel<2> : small_kernel<1>, 1, kSmallBlock, 0, stream, a);
+    return launch_with_pdl(k == 64 ? small_kernel<2> : small_kernel<1>, 1, kSmallBlock, 0, stream, a, !opt.no_pdl);
 }
 
 cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,

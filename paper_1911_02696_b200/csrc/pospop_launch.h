@@ -36,6 +36,11 @@ struct LaunchOptions {
     unsigned long long* const* peers = nullptr;  // fused exchange: device array of n_peers gather slots
     int n_peers = 0;
     int rank = 0;
+    // Launch without programmatic dependent launch: the input may have been
+    // written by a preceding launch of this library on the same stream (which
+    // lets its dependents start before it finishes; our kernels read their
+    // input before griddepcontrol.wait).
+    bool no_pdl = false;
 };
 
 // Counts len_words k-bit words at `data` (device memory, k/8-aligned) into

@@ -437,3 +437,29 @@ def test_graph_replay_counts_current_contents(pp, dev, orc):
         torch.cuda.synchronize()
         assert (out.cpu().numpy().astype(np.uint64) == orc.naive(b, k)).all()
         g.close()
+
+
+def test_chained_async_launches_read_the_previous_output(pp, dev, orc):
+    """A count whose input is the output of the previous launch on the same
+    stream (our kernels let dependents start early) must see the finished
+    output: the launcher drops programmatic dependent launch for it."""
+    s = torch.cuda.current_stream()
+    words = orc.generate(4, 11, 1 << 24)
+    d = torch.from_numpy(words.view(np.int16).copy()).cuda()
+    want = np.asarray(orc.pospopcnt(words, 16), np.uint64)
+    for trial in range(20):
+        out = torch.zeros(16, dtype=torch.int64, device="cuda")
+        out2 = torch.zeros(64, dtype=torch.int64, device="cuda")
+        pp.count_async(d, out, 16, stream=s)        # 16 counts ...
+        pp.count_async(out, out2, 64, stream=s)     # ... counted as 16 u64 words
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy().astype(np.uint64) == want).all()
+        assert (out2.cpu().numpy().astype(np.uint64) == np.asarray(orc.pospopcnt(want, 64), np.uint64)).all(), trial
+        seg = torch.empty((2, 16), dtype=torch.int64, device="cuda")
+        offs = torch.tensor([0, 1 << 23, 1 << 24], dtype=torch.int64, device="cuda")
+        pp.segmented_async(d, offs, seg, 16, stream=s)
+        pp.count_async(seg, out2, 64, stream=s)     # rows of the segmented launch as input
+        torch.cuda.synchronize()
+        rows = seg.cpu().numpy().astype(np.uint64)
+        assert (rows.sum(axis=0) == want).all()
+        assert (out2.cpu().numpy().astype(np.uint64) == np.asarray(orc.pospopcnt(rows.ravel(), 64), np.uint64)).all()
