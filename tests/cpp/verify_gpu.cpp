@@ -10,11 +10,14 @@
 //      exhaustive single-word domain + every length 0..max_len, bit-exact
 //      against pospop::oracle_pospopcnt;
 //   3. the error conventions match (std::invalid_argument,
-//      pospop::KernelUnavailableError).
+//      pospop::KernelUnavailableError);
+//   4. the harness still catches faults with the GPU underneath (the
+//      reference's own fault-injection self-test, test_verify.cpp:42-76).
 // Exit code 0 = all passed.
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "pospop/bench.hpp"
@@ -67,6 +70,34 @@ int main(int argc, char** argv) {
         ++failures;
     } catch (const pospop::KernelUnavailableError&) {
         std::printf("PASS width 128 -> pospop::KernelUnavailableError\n");
+    }
+    // (4) the harness catches a faulty GPU runner and minimises it
+    //     (restates proj/tests/test_verify.cpp:42-76 with the GPU underneath)
+    {
+        const pospop::KernelRunner faulty = [](pospop::Word16Span words, const pospop::PospopcntConfig& config) {
+            pospop::PositionalCounts counts = pospop_gpu::pospopcnt(words, config);
+            if (words.size() == 37 && counts[3] > 0) counts[3] -= 1;
+            return counts;
+        };
+        const pospop::KernelKind csa16[] = {pospop::KernelKind::Csa16};
+        const pospop::VerifyReport r = pospop::verify_kernels(123, 50, csa16, faulty);
+        const bool ok = !r.ok() && r.first_failure->len == 37 && r.first_failure->seed == 123 &&
+                        !r.first_failure->single_word.has_value() &&
+                        r.first_failure->expected[3] == r.first_failure->actual[3] + 1 &&
+                        pospop::format_failure(*r.first_failure).find("len=37") != std::string::npos;
+        std::printf("%s injected fault (len 37, bit 3) caught and minimised through the GPU runner\n",
+                    ok ? "PASS" : "FAIL");
+        failures += ok ? 0 : 1;
+        const pospop::KernelRunner faulty1 = [](pospop::Word16Span words, const pospop::PospopcntConfig& config) {
+            pospop::PositionalCounts counts = pospop_gpu::pospopcnt(words, config);
+            if (words.size() == 1 && words[0] == 0x00FF) counts[0] += 1;
+            return counts;
+        };
+        const pospop::KernelKind scalar[] = {pospop::KernelKind::ScalarBasic};
+        const pospop::VerifyReport r1 = pospop::verify_kernels(1, 0, scalar, faulty1);
+        const bool ok1 = !r1.ok() && r1.first_failure->single_word.has_value() && *r1.first_failure->single_word == 0x00FF;
+        std::printf("%s single-word fault reports 0x00FF through the GPU runner\n", ok1 ? "PASS" : "FAIL");
+        failures += ok1 ? 0 : 1;
     }
     return failures;
 }
