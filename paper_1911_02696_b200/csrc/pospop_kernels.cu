@@ -29,6 +29,7 @@
 #include "pospop_launch.h"
 #include "pospop_segmented.cuh"
 #include "pospop_stream.cuh"
+#include "pospop_variants.h"
 
 extern char** environ;
 
@@ -117,124 +118,33 @@ int resident_blocks(Kernel kernel, int block) {
     return n;
 }
 
-using StreamKernel = void (*)(const StreamArgs);
-
-struct StreamVariant {
-    int nbank, depth, vb, hint, block, sched, mode;
-    StreamKernel fn;
-};
-
-#define SV(NB, L, VB, H, B, S) {NB, L, VB, H, B, S, 0, stream_kernel<NB, L, VB, H, B, S, 0>}
-#define SVF(L, VB, B, S) {2, L, VB, 0, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1>}
-// FLAG variants that must fit 2 CTAs/SM (<= 128 registers); hint slot = 2 marks them.
-#define SVF2(L, VB, B, S) {2, L, VB, 2, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1, 2>}
-#define SVB(L, VB, B, S) {3, L, VB, 0, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2>}
-#define SVB2(L, VB, B, S) {3, L, VB, 2, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2, 2>}
-// Production variants first (the defaults), then tuning variants selectable
-// through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched" (POSPOP_FLAG_VARIANT
-// for MODE 1).
-const StreamVariant kStreamVariants[] = {
-    SV(1, 7, 32, 0, 256, 2), SV(2, 6, 32, 0, 256, 2),  // defaults (k <= 32 / k = 64)
-    SV(1, 7, 32, 0, 0, 2), SV(2, 6, 32, 0, 0, 2),      // runtime block size (test launches)
-    SV(1, 7, 32, 0, 256, 0), SV(2, 6, 32, 0, 256, 0),  // static CTA partition
-    SV(1, 7, 32, 0, 0, 0), SV(2, 6, 32, 0, 0, 0),
-    SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // per-warp guided chunks
-    SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1), SV(1, 6, 32, 0, 256, 2), SV(1, 7, 16, 0, 256, 2),
-    SVF(6, 32, 512, 2), SVF(6, 32, 0, 2),               // FLAG statistics defaults (16 warps/SM)
-    SVF(6, 32, 256, 2), SVF(5, 32, 512, 2),
-    SVF(5, 32, 256, 2), SVF(6, 16, 256, 2), SVF(7, 32, 256, 2),
-    SVF2(5, 32, 256, 2), SVF2(5, 16, 256, 2), SVF2(4, 32, 256, 2), SVF(4, 32, 512, 2), SVF(5, 16, 512, 2),
-    SVF2(6, 32, 256, 2), SVF(4, 32, 1024, 2),
-    // byte-frame FLAG statistics (MODE 2): defaults first
-    SVB(5, 32, 512, 2), SVB(5, 32, 0, 2),
-    SVB(5, 32, 256, 2), SVB(4, 32, 512, 2), SVB(4, 32, 256, 2), SVB2(4, 32, 256, 2),
-    SVB(4, 16, 512, 2), SVB(6, 32, 256, 2), SVB(5, 16, 512, 2), SVB2(5, 32, 256, 2),
-    SVB(4, 32, 512, 4), SVB(4, 16, 512, 4), SVB(3, 32, 512, 4), SVB(4, 32, 256, 4), SVB2(3, 32, 256, 4),
-    SVB(5, 32, 256, 4), SVB(5, 32, 512, 5), SVB(5, 16, 512, 5), SVB(6, 32, 256, 5),
-};
-#undef SV
-#undef SVF
-#undef SVF2
-#undef SVB
-#undef SVB2
-#undef SVF2
-
 const StreamVariant* pick_stream(int nbank, int depth, int vb, int hint, int block, int sched, int mode) {
-    for (const StreamVariant& v : kStreamVariants)
-        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.hint == hint && v.block == block &&
-            v.sched == sched && v.mode == mode)
-            return &v;
+    size_t n = 0;
+    const StreamVariant* v = mode == 0 ? stream_variants_counts(&n) : mode == 1 ? stream_variants_flag16(&n)
+                                                                              : stream_variants_flag8(&n);
+    for (size_t i = 0; i < n; ++i)
+        if (v[i].nbank == nbank && v[i].depth == depth && v[i].vb == vb && v[i].hint == hint &&
+            v[i].block == block && v[i].sched == sched && v[i].mode == mode)
+            return &v[i];
     return nullptr;
 }
-
-// TMA-staged variants (SCHED 3): (nbank, depth, mode, consumer warps, ring stages).
-struct TmaVariant {
-    int nbank, depth, mode, nc, stages;
-    StreamKernel fn;
-    size_t smem;  // dynamic shared memory: stages x stage bytes
-};
-
-#define TV(NB, L, M, NC, ST)                                                                \
-    {NB, L, M, NC, ST, stream_tma_kernel<NB, L, M, NC, ST>,                               \
-     (size_t)(ST) * (NC) * 32 * (((M) == 1 ? (1 << (L)) : (M) == 2 ? (2 << (L)) : ((NB) << (L))) / 4) * 16}
-const TmaVariant kTmaVariants[] = {
-    TV(1, 5, 0, 8, 6), TV(1, 6, 0, 8, 3), TV(1, 5, 0, 8, 4), TV(1, 4, 0, 8, 6), TV(1, 5, 0, 4, 6),
-    TV(2, 4, 0, 8, 6), TV(2, 5, 0, 8, 3),
-    TV(2, 5, 1, 8, 6), TV(2, 4, 1, 8, 6), TV(2, 6, 1, 8, 3), TV(2, 5, 1, 16, 3), TV(2, 4, 1, 16, 6),
-    TV(2, 5, 1, 12, 4),
-    TV(3, 5, 2, 12, 2), TV(3, 5, 2, 8, 3), TV(3, 4, 2, 15, 3), TV(3, 4, 2, 12, 4), TV(3, 4, 2, 8, 6),
-};
-#undef TV
 
 const TmaVariant* pick_tma(int nbank, int depth, int mode, int nc, int stages) {
-    for (const TmaVariant& v : kTmaVariants)
-        if (v.nbank == nbank && v.depth == depth && v.mode == mode && v.nc == nc && v.stages == stages) return &v;
+    size_t n = 0;
+    const TmaVariant* v = tma_variants(&n);
+    for (size_t i = 0; i < n; ++i)
+        if (v[i].nbank == nbank && v[i].depth == depth && v[i].mode == mode && v[i].nc == nc && v[i].stages == stages)
+            return &v[i];
     return nullptr;
 }
 
-using SegKernel = void (*)(const uint8_t*, const unsigned long long*, unsigned long long, int, uint32_t,
-                           unsigned long long*, unsigned long long*, unsigned int*, unsigned);
-
-struct SegVariant {
-    int nbank, depth, vb, sched;
-    SegKernel fn;
-    int group = 0;  // sched 5: lanes per array
-};
-
-#define SG(NB, L, VB, S) {NB, L, VB, S, segmented_kernel<NB, L, VB, S>}
-#define SGP(NB, L, VB) {NB, L, VB, 2, segmented_pipe_entry<NB, L, VB>}
-#define SGP2(NB, L, VB) {NB, L, VB, 3, segmented_pipe_entry<NB, L, VB, 2>}  // sched 3: pipelined, 2 CTAs/SM
-#define SGP3(NB, L, VB) {NB, L, VB, 4, segmented_pipe_entry<NB, L, VB, 3>}  // sched 4: pipelined, 3 CTAs/SM
-// sched 6: pipelined, bit-plane epilogue, 2 CTAs/SM; sched 7: the same at 3 CTAs/SM
-#define SGPE(NB, L, VB) {NB, L, VB, 6, segmented_pipe_entry<NB, L, VB, 2, 1>}
-#define SGPE3(NB, L, VB) {NB, L, VB, 7, segmented_pipe_entry<NB, L, VB, 3, 1>}
-// sched 5: grouped, G lanes per array, 2 CTAs/SM
-#define SGG(NB, L, VB, G) {NB, L, VB, 5, segmented_group_kernel<NB, L, VB, G, 2>, G}
-const SegVariant kSegVariants[] = {
-    SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),
-    SGPE3(1, 4, 16), SGPE3(1, 4, 32), SGPE3(2, 3, 16),
-    SGG(1, 6, 16, 8), SGG(1, 6, 16, 4), SGG(1, 5, 16, 8), SGG(1, 6, 32, 8), SGG(1, 5, 32, 8), SGG(1, 5, 16, 4),
-    SGG(1, 6, 16, 16), SGG(1, 5, 32, 4),
-    SGG(2, 4, 16, 8), SGG(2, 4, 32, 8), SGG(2, 4, 16, 4),
-    SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
-    SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
-    SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
-    SGP(1, 5, 16), SGP(1, 4, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
-    SGP2(2, 4, 16), SGP2(2, 3, 32), SGP2(2, 3, 16), SGP2(1, 5, 16), SGP2(1, 5, 32),
-    SGP3(1, 4, 16), SGP3(1, 4, 32), SGP3(1, 5, 16), SGP3(2, 3, 16), SGP3(2, 3, 32),
-};
-#undef SGP2
-#undef SGP3
-#undef SGG
-#undef SGPE
-#undef SGPE3
-#undef SG
-#undef SGP
-
 const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched, int group = 0) {
-    for (const SegVariant& v : kSegVariants)
-        if (v.nbank == nbank && v.depth == depth && v.vb == vb && v.sched == sched && (sched != 5 || v.group == group))
-            return &v;
+    size_t n = 0;
+    const SegVariant* v = seg_variants(&n);
+    for (size_t i = 0; i < n; ++i)
+        if (v[i].nbank == nbank && v[i].depth == depth && v[i].vb == vb && v[i].sched == sched &&
+            (sched != 5 || v[i].group == group))
+            return &v[i];
     return nullptr;
 }
 

@@ -1,0 +1,47 @@
+// variants_seg.cu -- segmented kernel instantiations.
+// (one translation unit per registry so the instantiations compile in parallel)
+#include "pospop_segmented.cuh"
+#include "pospop_variants.h"
+
+namespace pospop_b200 {
+namespace {
+using namespace dev;
+#define SG(NB, L, VB, S) {NB, L, VB, S, segmented_kernel<NB, L, VB, S>}
+#define SGP(NB, L, VB) {NB, L, VB, 2, segmented_pipe_entry<NB, L, VB>}
+#define SGP2(NB, L, VB) {NB, L, VB, 3, segmented_pipe_entry<NB, L, VB, 2>}  // sched 3: pipelined, 2 CTAs/SM
+#define SGP3(NB, L, VB) {NB, L, VB, 4, segmented_pipe_entry<NB, L, VB, 3>}  // sched 4: pipelined, 3 CTAs/SM
+// sched 6: pipelined, bit-plane epilogue, 2 CTAs/SM; sched 7: the same at 3 CTAs/SM
+#define SGPE(NB, L, VB) {NB, L, VB, 6, segmented_pipe_entry<NB, L, VB, 2, 1>}
+#define SGPE3(NB, L, VB) {NB, L, VB, 7, segmented_pipe_entry<NB, L, VB, 3, 1>}
+// sched 5: grouped, G lanes per array, 2 CTAs/SM
+#define SGG(NB, L, VB, G) {NB, L, VB, 5, segmented_group_kernel<NB, L, VB, G, 2>, G}
+const SegVariant kVariants[] = {
+    SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),
+    SGPE3(1, 4, 16), SGPE3(1, 4, 32), SGPE3(2, 3, 16),
+    SGG(1, 6, 16, 8), SGG(1, 6, 16, 4), SGG(1, 5, 16, 8), SGG(1, 6, 32, 8), SGG(1, 5, 32, 8), SGG(1, 5, 16, 4),
+    SGG(1, 6, 16, 16), SGG(1, 5, 32, 4),
+    SGG(2, 4, 16, 8), SGG(2, 4, 32, 8), SGG(2, 4, 16, 4),
+    SG(1, 5, 16, 0), SG(2, 5, 16, 1),  // defaults (k <= 32 / k = 64)
+    SG(1, 5, 16, 1), SG(2, 5, 16, 0), SG(1, 4, 16, 0), SG(1, 4, 16, 1), SG(1, 5, 32, 0), SG(1, 5, 32, 1),
+    SG(2, 4, 16, 0), SG(2, 4, 16, 1), SG(2, 4, 32, 1),
+    SGP(1, 5, 16), SGP(1, 4, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
+    SGP2(2, 4, 16), SGP2(2, 3, 32), SGP2(2, 3, 16), SGP2(1, 5, 16), SGP2(1, 5, 32),
+    SGP3(1, 4, 16), SGP3(1, 4, 32), SGP3(1, 5, 16), SGP3(2, 3, 16), SGP3(2, 3, 32),
+};
+#undef SGP2
+#undef SGP3
+#undef SGG
+#undef SGPE
+#undef SGPE3
+#undef SG
+#undef SGP
+
+
+}  // namespace
+
+const SegVariant* seg_variants(size_t* n) {
+    *n = sizeof(kVariants) / sizeof(kVariants[0]);
+    return kVariants;
+}
+
+}  // namespace pospop_b200
