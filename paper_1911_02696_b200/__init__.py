@@ -18,8 +18,11 @@ Reference name              -> here
 
 Extensions on the same path (BASELINE.json north_star): k = 8/16/32/64
 (``pospopcnt_k``), the segmented/batched form (``pospopcnt_segmented``), a
-device-resident asynchronous launch (``count_async``) and the multi-GPU
-shard/reduce driver (``paper_1911_02696_b200.shard``).
+device-resident asynchronous launch (``count_async``), CUDA-graph replay
+(``CountGraph``), the fused FLAG statistics (``flagstats``), file/pipe
+ingestion (``pospopcnt_file``), the multi-GPU shard/reduce driver
+(``paper_1911_02696_b200.shard``) and the count fused with the cross-GPU
+exchange over peer memory (``paper_1911_02696_b200.exchange``).
 
 There is no CPU fallback: if the CUDA library or an sm_100 device is missing
 every counting call raises.
