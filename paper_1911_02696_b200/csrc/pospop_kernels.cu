@@ -359,7 +359,11 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
 // workspace, no cross-CTA atomics or ticket -- the latency path (SURVEY 8f
 // row f3; the reference's Auto switches kernels below 4096 words too,
 // pospop.cpp:84-86).
-constexpr int kSmallBytes = 128 << 10;  // measured crossover (tools/latency): 128 KiB 13.7 vs 15.5 us
+// measured (tools/latency, profiles/r01_latency_c_abi.csv): one CTA up to 64 KiB,
+// one 16-CTA cluster up to 3 MiB (512 KiB: 19.0 -> 13.3 us synchronous), the
+// multi-CTA stream kernel above
+constexpr int kSmallBytes = 64 << 10;
+constexpr int kClusterBytes = 3 << 20;
 
 static cudaError_t launch_small(int k, const void* data, size_t len_words, unsigned long long* d_out,
                                 bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
@@ -370,14 +374,64 @@ static cudaError_t launch_small(int k, const void* data, size_t len_words, unsig
     return launch_with_pdl(k == 64 ? small_kernel<2> : small_kernel<1>, 1, kSmallBlock, 0, stream, a, !opt.no_pdl);
 }
 
+// Medium inputs: one thread-block cluster (POSPOP_CLUSTER CTAs, default 16,
+// the non-portable maximum; 8 if 16 is refused).
+static cudaError_t launch_cluster(int k, const void* data, size_t len_words, unsigned long long* d_out,
+                                  bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
+                                  cudaStream_t stream, int* grid_used) {
+    StreamKernel fn = k == 64 ? cluster_kernel<2> : cluster_kernel<1>;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, bool> configured;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto key = std::make_pair(dev, reinterpret_cast<const void*>(fn));
+        if (!configured[key]) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaGetLastError();
+            configured[key] = true;
+        }
+    }
+    StreamArgs a;
+    fill_stream_args(a, k, data, len_words, 16, d_out, accumulate, opt, ws);
+    int csize = env_int("POSPOP_CLUSTER", 16);
+    for (;; csize = 8) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)csize);
+        cfg.blockDim = dim3((unsigned)kSmallBlock);
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = !opt.no_pdl && env_int("POSPOP_PDL", 1) ? 1 : 0;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = (unsigned)csize;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+        if (e == cudaSuccess) {
+            ++g_launches;
+            if (grid_used) *grid_used = csize;
+            return cudaGetLastError();
+        }
+        cudaGetLastError();
+        if (csize <= 8) return e;
+    }
+}
+
 cudaError_t launch_stream(int k, const void* data, size_t len_words, unsigned long long* d_out,
                           bool accumulate, const LaunchOptions& opt, const StreamWorkspace& ws,
                           cudaStream_t stream, int* grid_used) {
     env_refresh();
     const size_t nbytes = len_words * (size_t)(k / 8);
-    if (nbytes <= (size_t)env_int("POSPOP_SMALL_BYTES", kSmallBytes) && !opt.grid && !opt.block && !opt.trace &&
-        !opt.depth && !opt.peers && !env_get("POSPOP_STREAM_VARIANT"))
-        return launch_small(k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
+    if (!opt.grid && !opt.block && !opt.trace && !opt.depth && !opt.peers && !env_get("POSPOP_STREAM_VARIANT")) {
+        if (nbytes <= (size_t)env_int("POSPOP_SMALL_BYTES", kSmallBytes))
+            return launch_small(k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
+        if (nbytes <= (size_t)env_int("POSPOP_CLUSTER_BYTES", kClusterBytes))
+            return launch_cluster(k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
+    }
     return launch_stream_mode(0, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
 }
 

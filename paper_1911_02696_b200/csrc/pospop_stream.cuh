@@ -4,6 +4,7 @@
 // unit, which instantiates the kernels and owns the host-side launchers).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -750,6 +751,68 @@ __global__ void __launch_bounds__(kSmallBlock, 1) small_kernel(const StreamArgs 
         }
         a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Medium inputs (the latency path above the single-CTA size): ONE thread-block
+// cluster of gridDim.x CTAs (one per SM) counts the stream with the small
+// kernel's tree; each CTA reduces to shared-memory channel totals and, after a
+// cluster barrier, CTA 0 sums the other CTAs' totals through distributed
+// shared memory and writes out[k] -- still no workspace, no global atomics and
+// no last-CTA ticket, with gridDim.x times the single CTA's bandwidth.
+// ---------------------------------------------------------------------------
+template <int NBANK>
+__global__ void __launch_bounds__(kSmallBlock, 1) cluster_kernel(const StreamArgs a) {
+    namespace cg = cooperative_groups;
+    constexpr int VPT = 4, REGS = 16, L = NBANK == 1 ? 4 : 3;
+    const unsigned long long tile = (unsigned long long)VPT * kSmallBlock;
+    const unsigned long long stride = tile * gridDim.x;
+    __shared__ uint32_t s_ch[32 * NBANK];
+    for (int i = threadIdx.x; i < 32 * NBANK; i += kSmallBlock) s_ch[i] = 0;
+    pdl_allow_next();
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    for (unsigned long long t = a.v0 + blockIdx.x * tile; t < a.v1; t += stride) {
+        uint32_t r[REGS];
+        load_tree_block<16, 0, VPT>(a, t + threadIdx.x, kSmallBlock, t >= a.f0 && t + tile <= a.f1, r);
+        tree_block<NBANK, L>(r, carries, counter);
+    }
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        uint32_t d[16];
+        drain<L>(d, carries[b]);
+        const uint32_t tot = bank_warp_total(counter[b], L, d);
+        if (tot) atomicAdd(&s_ch[b * 32 + lane], tot);
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();  // every CTA's totals are in its shared memory
+    if (cluster.block_rank() == 0) {
+        pdl_wait_prev();  // out[] may belong to the previous launch on this stream
+        for (int c = threadIdx.x; c < 32 * NBANK; c += kSmallBlock) {
+            uint32_t sum = s_ch[c];
+            for (unsigned r = 1; r < cluster.num_blocks(); ++r) sum += cluster.map_shared_rank(s_ch, r)[c];
+            s_ch[c] = sum;
+        }
+        __syncthreads();
+        const int k = a.k;
+        for (int pos = threadIdx.x; pos < k; pos += kSmallBlock) {
+            unsigned long long sum = 0;
+            if (k == 64) {
+                sum = s_ch[pos];
+            } else {
+                for (int j = 0; j < channels_per_position(k); ++j) sum += s_ch[pos + j * k];
+            }
+            a.out[pos] = a.accumulate ? a.out[pos] + sum : sum;
+        }
+    }
+    cluster.sync();  // keep every CTA's shared memory alive until CTA 0 has read it
 }
 
 // ---------------------------------------------------------------------------

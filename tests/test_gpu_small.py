@@ -1,6 +1,7 @@
-"""The single-CTA small-input kernel (latency path):
+"""The latency-path kernels: the single-CTA small-input
+kernel and the one-cluster medium kernel (distributed-shared-memory reduce),
 bit-exact against the oracle for every k at every length up to the switch
-size, at unaligned starts inside 0xFF guard bytes, for overwrite and
+sizes, at unaligned starts inside 0xFF guard bytes, for overwrite and
 accumulate, and equal to the multi-CTA stream kernel on the same bytes."""
 import numpy as np
 import pytest
@@ -61,3 +62,24 @@ def test_small_path_launches_one_kernel(pp, dev, orc):
     n0 = pp.kernel_launches()
     assert pp.pospopcnt(d) == orc.pospopcnt(words, 16)
     assert pp.kernel_launches() - n0 == 1
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+@pytest.mark.parametrize("csize", ["16", "8"])
+def test_cluster_kernel_lengths_offsets_accumulate(pp, dev, orc, k, csize, monkeypatch):
+    monkeypatch.setenv("POSPOP_SMALL_BYTES", "0")
+    monkeypatch.setenv("POSPOP_CLUSTER_BYTES", str(64 << 20))
+    monkeypatch.setenv("POSPOP_CLUSTER", csize)
+    wb = k // 8
+    raw = orc.generate(6, 90 + k, (5 << 20) // 8).view(np.uint8)
+    for offset in sorted({0, wb, 3 * wb, 8, 16 - wb}):
+        for n in (0, 1, 33, 4097, 65537, 300_001, (1 << 20) // wb + 3, raw.size // wb - 8):
+            sub = raw[:n * wb]
+            view = guarded(sub, offset)
+            assert pp.pospopcnt_k(view, k) == orc.pospopcnt(sub, k, threads=4), (k, csize, offset, n)
+    d = torch.from_numpy(raw.copy()).cuda()
+    out = torch.zeros(k, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        pp.count_async(d, out, k, accumulate=True)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy().astype(np.uint64) == 3 * np.asarray(orc.pospopcnt(raw, k, threads=4), np.uint64)).all()
