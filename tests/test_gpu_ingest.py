@@ -93,6 +93,32 @@ def test_flagstats_cli(orc, tmp_path, golden):
     assert [out["pass"][f] for f in fields] + [out["fail"][f] for f in fields] == golden["flagstats_acceptance"][0]
 
 
+def test_flagstats_cli_text_and_modes(pp, orc, tmp_path, golden):
+    """Text output = the reference's format_flag_summary (flagstats.cpp:147-164);
+    --mode reference|pospopcnt|differential as the reference tool; a reserved
+    bit is a usage error (exit 2)."""
+    streams = orc.acceptance_flag_streams(count=1)
+    path = tmp_path / "flags.bin"
+    path.write_bytes(streams[0].astype("<u2").tobytes())
+    g = golden["flagstats_acceptance"][0]
+    names = ["total", "secondary", "supplementary", "n_pair_good", "n_read1", "n_read2", "n_sgltn", "pair_map",
+             "mapped", "dup"]
+    want = "field           QC-pass\tQC-fail\n" + "".join(
+        f"{n}{' ' * (16 - len(n))}{g[i]}\t{g[10 + i]}\n" for i, n in enumerate(names))
+    for mode in ("reference", "pospopcnt"):
+        r = cli("flagstats", "--input", str(path), "--mode", mode)
+        assert r.returncode == 0 and r.stdout.decode() == want, (mode, r.stdout, r.stderr)
+    r = cli("flagstats", "--input", str(path), "--mode", "differential")
+    assert r.returncode == 0
+    assert r.stdout.decode() == f"reference and pospopcnt summaries agree ({streams[0].size} words)\n" + want
+    assert cli("flagstats", "--input", str(path), "--mode", "bogus").returncode == 2
+    bad = streams[0].copy()
+    bad[5] |= 0x2000
+    path.write_bytes(bad.astype("<u2").tobytes())
+    r = cli("flagstats", "--input", str(path))
+    assert r.returncode == 2 and "offset 5" in r.stderr.decode()
+
+
 def test_plain_c_caller_counts_on_gpu(pp, tmp_path):
     """A strict-C11 caller of include/pospopcnt_b200.h (tests/c/abi_c_smoke.c)."""
     from test_abi import build_c_smoke
