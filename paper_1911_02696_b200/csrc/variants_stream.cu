@@ -7,6 +7,9 @@ namespace pospop_b200 {
 namespace {
 using namespace dev;
 #define SV(NB, L, VB, H, B, S) {NB, L, VB, H, B, S, 0, stream_kernel<NB, L, VB, H, B, S, 0>}
+// two CTAs per SM (<= 128 registers; hint slot 2 marks them): the next launch's
+// CTA can share an SM with the previous launch's tail CTA under PDL
+#define SV2(NB, L, VB, B, S) {NB, L, VB, 2, B, S, 0, stream_kernel<NB, L, VB, 0, B, S, 0, 2>}
 #define SVF(L, VB, B, S) {2, L, VB, 0, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1>}
 // FLAG variants that must fit 2 CTAs/SM (<= 128 registers); hint slot = 2 marks them.
 #define SVF2(L, VB, B, S) {2, L, VB, 2, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1, 2>}
@@ -22,10 +25,12 @@ const StreamVariant kVariants[] = {
     SV(1, 7, 32, 0, 0, 0), SV(2, 6, 32, 0, 0, 0),
     SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // per-warp guided chunks
     SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1), SV(1, 6, 32, 0, 256, 2), SV(1, 7, 16, 0, 256, 2),
+    SV2(1, 6, 32, 256, 2), SV2(1, 5, 32, 256, 2), SV2(2, 5, 32, 256, 2), SV2(1, 6, 16, 256, 2),
 
 };
 
 #undef SV
+#undef SV2
 #undef SVF
 #undef SVF2
 #undef SVB
