@@ -193,6 +193,16 @@ static void fill_stream_args(StreamArgs& a, int k, const void* data, size_t len_
     a.rank = opt.rank;
 }
 
+// Tree blocks between lane flushes: the caller's threshold, lowered by
+// POSPOP_FLUSH_THRESHOLD (tests: exercise the flush path) and, for the
+// byte-lane counters of the FLAG byte-frame kernel (MODE 2), at most 255.
+static uint32_t flush_threshold_for(int mode, const LaunchOptions& opt) {
+    uint32_t thr = opt.flush_threshold;
+    const int env_thr = env_int("POSPOP_FLUSH_THRESHOLD", 0);
+    if (env_thr > 0 && (uint32_t)env_thr < thr) thr = (uint32_t)env_thr;
+    return mode == 2 && thr > 255 ? 255 : thr;
+}
+
 static cudaError_t launch_with_pdl(StreamKernel fn, int grid, int threads, size_t smem, cudaStream_t stream,
                                    const StreamArgs& a, bool pdl) {
     cudaLaunchConfig_t cfg = {};
@@ -235,9 +245,7 @@ static cudaError_t launch_stream_tma(int mode, int nbank, int depth, int k, cons
     }
     StreamArgs a;
     fill_stream_args(a, k, data, len_words, 16, d_out, accumulate, opt, ws);
-    const int env_thr = env_int("POSPOP_FLUSH_THRESHOLD", 0);
-    if (env_thr > 0 && (uint32_t)env_thr < a.flush_threshold) a.flush_threshold = (uint32_t)env_thr;
-    if (mode == 2 && a.flush_threshold > 255) a.flush_threshold = 255;  // byte-lane counters
+    a.flush_threshold = flush_threshold_for(mode, opt);
     const int grid = device_info().sms;
     if (grid_used) *grid_used = grid;
     return launch_with_pdl(var->fn, grid, 32 * (var->nc + 1), var->smem, stream, a, !opt.no_pdl);
@@ -274,46 +282,13 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     const int vpt = (mode == 1 ? (1 << var->depth) : mode == 2 ? (2 << var->depth) : (nbank << var->depth)) /
                     (var->vb / 4);
 
-    const uintptr_t P = reinterpret_cast<uintptr_t>(data);
-    const size_t nbytes = len_words * (size_t)(k / 8);
-    const uintptr_t VBu = (uintptr_t)var->vb;
-    const uintptr_t group = 32 * VBu;
     StreamArgs a;
-    a.base = reinterpret_cast<const uint8_t*>(P & ~(group - 1));
-    if (nbytes == 0) {
-        a.v0 = a.v1 = a.f0 = a.f1 = a.g0 = a.ng = 0;
-        a.lo_byte = 0;
-        a.hi_byte = (int)VBu;
-    } else {
-        const uintptr_t B = reinterpret_cast<uintptr_t>(a.base);
-        a.v0 = (P - B) / VBu;
-        a.v1 = (P + nbytes - B + VBu - 1) / VBu;
-        a.lo_byte = (int)(P - (B + a.v0 * VBu));
-        a.hi_byte = (int)(P + nbytes - (B + (a.v1 - 1) * VBu));
-        a.f0 = a.v0 + (a.lo_byte != 0 ? 1 : 0);
-        a.f1 = a.v1 - (a.hi_byte != (int)VBu ? 1 : 0);
-        a.g0 = a.v0 / 32;
-        a.ng = (a.v1 + 31) / 32 - a.g0;
+    fill_stream_args(a, k, data, len_words, (uintptr_t)var->vb, d_out, accumulate, opt, ws);
+    a.flush_threshold = flush_threshold_for(mode, opt);
+    if (mode != 0) {  // the fused exchange is a count-mode feature
+        a.peers = nullptr;
+        a.n_peers = 0;
     }
-    a.k = k;
-    // byte-lane counters (MODE 2) take at most 255 tree blocks between flushes;
-    // POSPOP_FLUSH_THRESHOLD lowers the threshold (tests: exercise the flush path)
-    uint32_t thr = opt.flush_threshold;
-    const int env_thr = env_int("POSPOP_FLUSH_THRESHOLD", 0);
-    if (env_thr > 0 && (uint32_t)env_thr < thr) thr = (uint32_t)env_thr;
-    a.flush_threshold = mode == 2 && thr > 255 ? 255 : thr;
-    a.acc = ws.acc;
-    a.ticket = ws.ticket;
-    a.out = d_out;
-    a.accumulate = accumulate ? 1 : 0;
-    a.trace = opt.trace;
-    a.next = ws.next;
-    a.bad = ws.bad;
-    a.word_base = opt.word_base;
-    a.data_off = nbytes ? (unsigned long long)(P - reinterpret_cast<uintptr_t>(a.base)) : 0ull;
-    a.peers = mode == 0 ? opt.peers : nullptr;
-    a.n_peers = a.peers ? opt.n_peers : 0;
-    a.rank = opt.rank;
 
     int grid = opt.grid;
     if (grid <= 0) {
@@ -340,19 +315,7 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     if (a.pool > a.nwt) a.pool = a.nwt;
 
     if (grid_used) *grid_used = grid;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3((unsigned)threads);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = !opt.no_pdl && env_int("POSPOP_PDL", 1) ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, var->fn, a);
-    ++g_launches;
-    return e != cudaSuccess ? e : cudaGetLastError();
+    return launch_with_pdl(var->fn, grid, threads, 0, stream, a, !opt.no_pdl);
 }
 
 // Small inputs (<= POSPOP_SMALL_BYTES, default kSmallBytes): one CTA, no
