@@ -51,7 +51,9 @@ LIB_NAME = "libpospopcnt_b200.so"
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, LIB_NAME)
+    """The in-tree library; POSPOP_LIBRARY selects another build of it (tests:
+    the bounds-checked libpospopcnt_b200_debug.so)."""
+    return os.environ.get("POSPOP_LIBRARY") or os.path.join(_HERE, LIB_NAME)
 
 
 # -- errors (status codes of include/pospopcnt_b200.h) -----------------------

@@ -125,6 +125,23 @@ __device__ __forceinline__ uint32_t bank_warp_total_bytes(const uint32_t (&count
 }
 
 // ---------------------------------------------------------------------------
+// Debug bounds checks (libpospopcnt_b200_debug.so, built with
+// -DPOSPOP_DEBUG_BOUNDS): every vector load asserts that its index lies in the
+// valid range of the stream / array; a violation traps the kernel, which the
+// host sees as a CUDA error.  No-ops in the product build.
+// ---------------------------------------------------------------------------
+#ifdef POSPOP_DEBUG_BOUNDS
+#define POSPOP_CHECK(cond)          \
+    do {                            \
+        if (!(cond)) __trap();      \
+    } while (0)
+#else
+#define POSPOP_CHECK(cond) \
+    do {                   \
+    } while (0)
+#endif
+
+// ---------------------------------------------------------------------------
 // Streaming vector loads: read-only path, no L1 allocation (each byte is
 // touched exactly once).  VB = 16 -> LDG.E.NA.128 (512 B per warp),
 // VB = 32 -> LDG.E.NA.256 (1 KiB per warp; Blackwell's 256-bit load).

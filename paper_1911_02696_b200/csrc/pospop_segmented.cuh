@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
                     uint32_t x[RPV];
+                    POSPOP_CHECK(t + 32ull * v + lane < nv);
                     ldg_stream<VB, 0>(base + (t + 32ull * v + lane) * VB, x);
 #pragma unroll
                     for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
@@ -238,6 +239,7 @@ __device__ __forceinline__ void seg_load(const SegView& v, unsigned long long t,
 #pragma unroll
         for (int q = 0; q < VPT; ++q) {
             uint32_t x[RPV];
+            POSPOP_CHECK(t + 32ull * q + lane < v.nv);
             ldg_stream<VB, 0>(v.base + (t + 32ull * q + lane) * VB, x);
 #pragma unroll
             for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
@@ -521,6 +523,7 @@ __device__ __forceinline__ void seg_group_batch(const uint8_t* data, const unsig
 #pragma unroll
             for (int q = 0; q < VPT; ++q) {
                 uint32_t x[RPV];
+                POSPOP_CHECK(t + (unsigned long long)GX * q + gl < v.nv);
                 ldg_stream<VB, 0>(v.base + (t + (unsigned long long)GX * q + gl) * VB, x);
 #pragma unroll
                 for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];

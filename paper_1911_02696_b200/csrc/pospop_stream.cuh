@@ -110,6 +110,8 @@ __device__ __forceinline__ void load_tree_block(const StreamArgs& a, unsigned lo
 #pragma unroll
         for (int v = 0; v < VPT; ++v) {
             uint32_t x[RPV];
+            POSPOP_CHECK(first + (unsigned long long)v * stride >= a.v0 &&
+                         first + (unsigned long long)v * stride < a.v1);
             ldg_stream<VB, HINT>(p + (unsigned long long)v * stride * VB, x);
 #pragma unroll
             for (int j = 0; j < RPV; ++j) r[v * RPV + j] = x[j];
@@ -922,6 +924,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) stream_tma_kernel(const Stre
                 const unsigned long long lo = t0 > a.v0 ? t0 : a.v0;
                 const unsigned long long hi = t0 + STV < a.v1 ? t0 + STV : a.v1;
                 const uint32_t bytes = (uint32_t)((hi - lo) * 16);
+                POSPOP_CHECK(lo >= a.v0 && hi <= a.v1 && lo < hi);
                 mbar_arrive_expect_tx(&full[s], bytes);
                 tma_bulk_g2s(ring + (size_t)s * STB + (lo - t0) * 16, a.base + lo * 16, bytes, &full[s]);
             }
