@@ -53,7 +53,7 @@ WORKLOADS = {
     "cfg5_u64": (64, 6, 65536 * 4096, "cfg5 (u64): 65,536 arrays x 4096 u64 words (2 GiB), one k=64 row per array "
                                       "(32 MiB of rows); arrays split over the N GPUs, no exchange"),
     # SURVEY 8f row f1 (not the headline metric): flagstats_pospopcnt over SAM FLAG words
-    "flag": (16, 7, 1 << 32, "flag: 2^32 SAM FLAG words (12 valid bits, realistic flag mix), "
+    "flag": (16, 7, 1 << 32, "flag: 2^32 SAM FLAG words, uniform over the 4096 valid values (every flag combination equally likely, half QC-fail), "
                              "flagstats_pospopcnt pass/fail buckets in one fused pass; contiguous shards, "
                              "20-counter summary summed across GPUs"),
 }
