@@ -57,6 +57,9 @@ WORKLOADS = {
                              "flagstats_pospopcnt pass/fail buckets in one fused pass; contiguous shards, "
                              "20-counter summary summed across GPUs"),
 }
+WORKLOADS["flagmix"] = (16, 8, 1 << 32, "flagmix: 2^32 SAM FLAG words, a paired-end-like mix (proper pairs 86%, "
+                                        "duplicates 1/8, secondary/supplementary 1/128, QC-fail 2^-16), "
+                                        "flagstats_pospopcnt pass/fail buckets in one fused pass")
 FLAG_METRIC = "flagstats_pospopcnt input GB/s (SAM FLAG words) vs host CPU"
 
 
@@ -259,7 +262,7 @@ def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    if args.workload == "flag":
+    if args.workload in ("flag", "flagmix"):
         return run_reference_flag(args)
     if args.workload.startswith("cfg5"):
         return run_reference_seg(args)
@@ -310,7 +313,7 @@ def run_reference_flag(args):
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
-    k, gen_kind, total, desc = WORKLOADS["flag"]
+    k, gen_kind, total, desc = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     sample = min(total, 1 << 27)
     words = pyoracle.Oracle().generate(gen_kind, 1, sample, threads=threads)
@@ -569,7 +572,7 @@ def run_ours_flag(args):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    k, gen_kind, total, desc = WORKLOADS["flag"]
+    k, gen_kind, total, desc = WORKLOADS[args.workload]
     lo, hi = (rank * total, (rank + 1) * total) if args.scaling == "weak" else \
         (total * rank // world, total * (rank + 1) // world)
     words = hi - lo
@@ -667,7 +670,7 @@ def run_ours_flag(args):
         assert [int(x) for x in ref_out] == gpu.as_list(), "correctness gate: GPU and reference flagstats disagree"
         cpu = {"value": round(host_sample.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads,
                "kind": "reference",
-               "sample": f"first {sample} words ({sample * 2 >> 20} MiB) of the flag stream; "
+               "sample": f"first {sample} words ({sample * 2 >> 20} MiB) of the {args.workload} stream; "
                          f"pospop::flagstats_pospopcnt fork-joined over {threads} chunks, best of 3; "
                          f"summary equals the GPU's"}
 
@@ -683,7 +686,7 @@ def run_ours_flag(args):
                              "launch + 33-counter D2H per step"},
         "words_per_s": round(total_bytes / 2 / (ms_per_step * 1e-3), 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic("flag", world),
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, world),
                      "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
                      "kernel_ms_isolated": round(statistics.median(iso), 5),
                      "timing": "CUDA events around K synchronous C-ABI calls (kernel + 264-byte D2H each)",
@@ -950,7 +953,7 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if args.workload == "flag":
+    if args.workload in ("flag", "flagmix"):
         return run_ours_flag(args)
     if args.workload.startswith("cfg5"):
         return run_ours_seg(args)

@@ -237,7 +237,7 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
 
 /* ---- synthetic inputs and digests (device-side, for tests and bench) ---- */
 
-/* Fills n elements at d_out with generator `kind` (1..6):
+/* Fills n elements at d_out with generator `kind` (1..8, oracle/pospop_oracle.h):
  * element l is global element index_base + l.  Asynchronous on `stream`. */
 pospop_status pospop_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* d_out,
                               void* stream);

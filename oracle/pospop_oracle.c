@@ -464,6 +464,25 @@ static void gen_range(int kind, uint64_t key, uint64_t base, size_t lo, size_t h
             case 7:
                 ((uint16_t*)out)[l] = (uint16_t)((draw(key, i >> 2) >> (16 * (i & 3))) & 0x0FFF);
                 break;
+            case 8: { /* SAM FLAG words, a paired-end-like mix with rare QC-fail reads */
+                static const uint16_t proper[4] = {99, 147, 83, 163};
+                static const uint16_t paired[8] = {65, 129, 113, 177, 97, 145, 81, 161};
+                static const uint16_t half[8] = {73, 133, 89, 121, 137, 153, 185, 69};
+                const uint64_t u = draw(key, i);
+                const unsigned c = (unsigned)(u & 0xFF), sel = (unsigned)((u >> 8) & 7);
+                unsigned f;
+                if (c < 220) f = proper[sel & 3];
+                else if (c < 240) f = paired[sel];
+                else if (c < 250) f = half[sel];
+                else if (c < 254) f = (sel & 1) ? 141u : 77u;
+                else f = (sel & 1) ? 16u : 0u;
+                if (((u >> 16) & 0xF) < 2) f |= 0x400u;
+                if (((u >> 20) & 0x7F) == 0) f |= 0x100u;
+                if (((u >> 27) & 0x7F) == 1) f |= 0x800u;
+                if (((u >> 34) & 0xFFFF) == 0) f |= 0x200u;
+                ((uint16_t*)out)[l] = (uint16_t)f;
+                break;
+            }
         }
     }
 }
@@ -482,7 +501,7 @@ static void* gen_worker(void* arg) {
 }
 
 int orc_generate(int kind, uint64_t seed, uint64_t base, size_t n, void* out, int threads) {
-    if (kind < 1 || kind > 7) return 1;
+    if (kind < 1 || kind > 8) return 1;
     const uint64_t key = gen_key(seed, kind);
     if (threads < 1) threads = 1;
     if ((size_t)threads > n / 65536 + 1) threads = (int)(n / 65536 + 1);

@@ -115,6 +115,9 @@ void orc_mt64_draws(uint64_t seed, size_t n, uint64_t* out);
  *   kind 5: cfg5 uniform u32     (2 u32 per draw)
  *   kind 6: cfg5 uniform u64     (Bernoulli 0.5 per bit)
  *   kind 7: SAM FLAG words, uniform over the 12 defined bits (bits 12-15 clear)
+ *   kind 8: SAM FLAG words, a paired-end-like mix: proper pairs 86%, other paired 8%,
+ *           one end unmapped 4%, both unmapped 1.6%, single-end 0.8%; duplicate 1/8,
+ *           secondary 1/128, supplementary 1/128, QC-fail 2^-16 (one 64-bit draw per word)
  * Returns 0, or 1 for an unknown kind. */
 int orc_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* out, int threads);
 

@@ -154,7 +154,8 @@ class Oracle:
         self.lib.orc_mt_generate_stream(seed, n, _ptr(out))
         return out
 
-    GEN_DTYPE = {1: np.uint16, 2: np.uint16, 3: np.uint8, 4: np.uint16, 5: np.uint32, 6: np.uint64, 7: np.uint16}
+    GEN_DTYPE = {1: np.uint16, 2: np.uint16, 3: np.uint8, 4: np.uint16, 5: np.uint32, 6: np.uint64, 7: np.uint16,
+                 8: np.uint16}
 
     # -- FLAG statistics -----------------------------------------------------
     def flagstats(self, flags: np.ndarray, route: str = "reference"):

@@ -421,12 +421,12 @@ def segmented_async(data: Any, offsets: Any, out: Any, k: int, *, flush_threshol
                                              _stream_ptr(stream)))
 
 
-GEN_UNIFORM16, GEN_CFG2, GEN_CFG3, GEN_CFG4, GEN_U32, GEN_U64, GEN_FLAGS = 1, 2, 3, 4, 5, 6, 7
+GEN_UNIFORM16, GEN_CFG2, GEN_CFG3, GEN_CFG4, GEN_U32, GEN_U64, GEN_FLAGS, GEN_FLAGMIX = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 def generate(kind: int, seed: int, out: Any, base: int = 0, n: int | None = None, stream: Any = None) -> None:
     """Fills a device buffer with synthetic input `kind` (Synthetic inputs)."""
-    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8, 7: 2}[kind]
+    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8, 7: 2, 8: 2}[kind]
     addr, nbits = _addr_len(out, 8)
     count = nbits // esize if n is None else int(n)
     _check(_load().pospop_generate(int(kind), int(seed), int(base), count, addr or None, _stream_ptr(stream)))

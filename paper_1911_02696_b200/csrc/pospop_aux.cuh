@@ -61,6 +61,21 @@ __global__ void generate_kernel(int kind, uint64_t key, uint64_t index_base, uns
             case 7:  // SAM FLAG words: the 12 defined bits uniform, bits 12-15 clear
                 ((uint16_t*)out)[l] = (uint16_t)((mix64(key + ((i >> 2) + 1) * kGamma) >> (16 * (i & 3))) & 0x0FFF);
                 break;
+            case 8: {  // SAM FLAG words, a paired-end-like mix (oracle/pospop_oracle.c gen_range)
+                constexpr uint16_t kProper[4] = {99, 147, 83, 163};
+                constexpr uint16_t kPaired[8] = {65, 129, 113, 177, 97, 145, 81, 161};
+                constexpr uint16_t kHalf[8] = {73, 133, 89, 121, 137, 153, 185, 69};
+                const uint64_t u = mix64(key + (i + 1) * kGamma);
+                const uint32_t c = (uint32_t)(u & 0xFF), sel = (uint32_t)((u >> 8) & 7);
+                uint32_t f = c < 220 ? kProper[sel & 3] : c < 240 ? kPaired[sel] : c < 250 ? kHalf[sel]
+                           : c < 254 ? ((sel & 1) ? 141u : 77u) : ((sel & 1) ? 16u : 0u);
+                if (((u >> 16) & 0xF) < 2) f |= 0x400;     // duplicate, 1/8
+                if (((u >> 20) & 0x7F) == 0) f |= 0x100;   // secondary, 1/128
+                if (((u >> 27) & 0x7F) == 1) f |= 0x800;   // supplementary, 1/128
+                if (((u >> 34) & 0xFFFF) == 0) f |= 0x200; // QC-fail, 2^-16
+                ((uint16_t*)out)[l] = (uint16_t)f;
+                break;
+            }
         }
     }
 }

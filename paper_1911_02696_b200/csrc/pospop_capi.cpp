@@ -1129,7 +1129,7 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
 }
 
 pospop_status pospop_generate(int kind, uint64_t seed, uint64_t base, size_t n, void* d_out, void* stream) {
-    if (kind < 1 || kind > 7) return fail(POSPOP_EINVAL, "unknown generator kind %d", kind);
+    if (kind < 1 || kind > 8) return fail(POSPOP_EINVAL, "unknown generator kind %d", kind);
     if (!d_out && n) return fail(POSPOP_EINVAL, "NULL output");
     int dev = 0;
     pospop_status s = current_device(&dev);

@@ -195,12 +195,14 @@ static void fill_stream_args(StreamArgs& a, int k, const void* data, size_t len_
 
 // Tree blocks between lane flushes: the caller's threshold, lowered by
 // POSPOP_FLUSH_THRESHOLD (tests: exercise the flush path) and, for the
-// byte-lane counters of the FLAG byte-frame kernel (MODE 2), at most 255.
+// byte-lane counters of the FLAG byte-frame kernel (MODE 2; <= 255 per lane,
+// and a tile that takes the QC-fail fix-up extracts twice into bank 2), at
+// most 127.
 static uint32_t flush_threshold_for(int mode, const LaunchOptions& opt) {
     uint32_t thr = opt.flush_threshold;
     const int env_thr = env_int("POSPOP_FLUSH_THRESHOLD", 0);
     if (env_thr > 0 && (uint32_t)env_thr < thr) thr = (uint32_t)env_thr;
-    return mode == 2 && thr > 255 ? 255 : thr;
+    return mode == 2 && thr > 127 ? 127 : thr;
 }
 
 static cudaError_t launch_with_pdl(StreamKernel fn, int grid, int threads, size_t smem, cudaStream_t stream,

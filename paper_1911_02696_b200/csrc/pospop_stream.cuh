@@ -334,45 +334,68 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return d;
 }
 
-__device__ __forceinline__ void flag_leaf(uint32_t r0, uint32_t r1, uint32_t& al, uint32_t& fl, uint32_t& ahf,
-                                          uint32_t& hb) {
+// Plane sets (P): 0 = all three planes (AL, FL, AHF -> banks 0, 1, 2);
+// 1 = the QC-fail-free tile (AL, AH -> banks 0, 2: FL and the fail half of AHF
+// are zero); 2 = the fail planes only (FL, AH<<4 & mf -> banks 1, 2), added
+// to a tile first counted with P = 1.  AHF = AH | (AH<<4 & mf) has disjoint
+// halves, so counting them in two passes gives the same positional counts.
+template <int P>
+struct FlagPlanes {
+    static constexpr int N = P == 0 ? 3 : 2;
+    static __device__ __forceinline__ int bank(int i) { return P == 0 ? i : P == 1 ? (i == 0 ? 0 : 2) : (i == 0 ? 1 : 2); }
+};
+
+template <int P>
+__device__ __forceinline__ void flag_leaf(uint32_t r0, uint32_t r1, uint32_t (&o)[FlagPlanes<P>::N], uint32_t& hb) {
     constexpr uint32_t B1 = 0x01010101u;
     const uint32_t lb = prmt(r0, r1, 0x6420u);
     hb = prmt(r0, r1, 0x7531u);
     const uint32_t g = lb & ~hb & ~shr_fma<3>(hb) & B1;        // paired & !secondary & !supplementary
     const uint32_t gu = g & ~shr_fma<2>(lb);                    // ... & !unmapped
     const uint32_t t = g * 0xC0u + gu * 0x0Bu;                  // G -> bits 6,7 ; GU -> bits 0,1,3
-    al = lb & (t | 0x04040404u);
-    const uint32_t mf = prmt(shl_fma<6>(hb), 0u, 0xBA98u);     // 0xFF per QC-fail byte
-    fl = al & mf;
+    const uint32_t al = lb & (t | 0x04040404u);
     const uint32_t ah = hb & ~(shl_fma<3>(hb) & 0x08080808u);  // bit 3: supplementary & !secondary
-    ahf = ah | (shl_fma<4>(ah) & mf);
+    if constexpr (P == 1) {
+        o[0] = al;
+        o[1] = ah;
+    } else {
+        const uint32_t mf = prmt(shl_fma<6>(hb), 0u, 0xBA98u);  // 0xFF per QC-fail byte
+        if constexpr (P == 0) {
+            o[0] = al;
+            o[1] = al & mf;
+            o[2] = ah | (shl_fma<4>(ah) & mf);
+        } else {
+            o[0] = al & mf;
+            o[1] = shl_fma<4>(ah) & mf;
+        }
+    }
 }
 
-template <int CD, int L>
+template <int CD, int L, int P = 0>
 struct FlagByteTree {  // 2^L leaves = 2^(L+1) input registers; c[b][j] = carry of weight 2^j
-    static __device__ __forceinline__ void run(uint32_t (&c)[3][CD], const uint32_t* in, uint32_t (&top)[3],
+    static constexpr int N = FlagPlanes<P>::N;
+    static __device__ __forceinline__ void run(uint32_t (&c)[3][CD], const uint32_t* in, uint32_t (&top)[N],
                                                uint32_t& bad) {
-        uint32_t x[3], y[3];
+        uint32_t x[N], y[N];
         if constexpr (L == 1) {
             uint32_t hx, hy;
-            flag_leaf(in[0], in[1], x[0], x[1], x[2], hx);
-            flag_leaf(in[2], in[3], y[0], y[1], y[2], hy);
+            flag_leaf<P>(in[0], in[1], x, hx);
+            flag_leaf<P>(in[2], in[3], y, hy);
             bad = bad | hx | hy;  // one LOP3 per two leaves
         } else {
-            FlagByteTree<CD, L - 1>::run(c, in, x, bad);
-            FlagByteTree<CD, L - 1>::run(c, in + (2 << (L - 1)), y, bad);
+            FlagByteTree<CD, L - 1, P>::run(c, in, x, bad);
+            FlagByteTree<CD, L - 1, P>::run(c, in + (2 << (L - 1)), y, bad);
         }
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
+        for (int i = 0; i < N; ++i) {
+            const int b = FlagPlanes<P>::bank(i);
             uint32_t h, l;
-            csa(h, l, c[b][L - 1], x[b], y[b]);
+            csa(h, l, c[b][L - 1], x[i], y[i]);
             c[b][L - 1] = l;
-            top[b] = h;
+            top[i] = h;
         }
     }
 };
-
 
 // Rare path: this thread's tile holds a FLAG word with reserved bits 12-15
 // set; report the smallest such word index through a.bad (max of ~index).
@@ -410,12 +433,46 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
     } else if constexpr (MODE == 2) {
         static_assert(NBANK == 3 && REGS == (2 << L), "byte-frame FLAG mode: three banks, 2^(L+1) registers");
         constexpr int RPV = VB / 4;
+        if constexpr (!pair_tiles<MODE, L>()) {
+            // `phase` predicts whether this warp's tile has QC-fail reads:
+            // 0 = expect them (all three planes), 1/2 = expect none (AL and
+            // AH only; if a QC-fail word shows up after all -- bit 9 = bit 1
+            // of Hb -- reload the tile, an L2 hit, and add the fail planes).
+            // Two consecutive tiles with QC-fail reads switch to 0, one
+            // fail-free tile back to 1, so rare QC-fail reads cost one fix-up
+            // each and QC-fail-heavy streams run the three-plane tree.
+            // Warp-uniform throughout; exact either way.
+            uint32_t bad = 0;
+            if (phase) {
+                uint32_t top[2];
+                FlagByteTree<CD, L, 1>::run(carries, r, top, bad);
+                extract_bytes(counter[0], top[0]);
+                extract_bytes(counter[2], top[1]);
+                if (bad & 0xF0F0F0F0u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);  // r[] dies here
+                if (__any_sync(0xFFFFFFFFu, bad & 0x02020202u)) {
+                    uint32_t r2[REGS];
+                    load_tree_block<VB, 0, REGS / RPV>(a, first, stride, false, r2);
+                    uint32_t bad2 = 0, top2[2];
+                    FlagByteTree<CD, L, 2>::run(carries, r2, top2, bad2);
+                    extract_bytes(counter[1], top2[0]);
+                    extract_bytes(counter[2], top2[1]);
+                    phase = phase == 1u ? 2u : 0u;
+                } else {
+                    phase = 1u;
+                }
+            } else {
+                uint32_t top[3];
+                FlagByteTree<CD, L>::run(carries, r, top, bad);
+#pragma unroll
+                for (int b = 0; b < 3; ++b) extract_bytes(counter[b], top[b]);
+                if (bad & 0xF0F0F0F0u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
+                phase = __any_sync(0xFFFFFFFFu, bad & 0x02020202u) ? 0u : 1u;
+            }
+            return;
+        }
         uint32_t bad = 0, top[3];
         FlagByteTree<CD, L>::run(carries, r, top, bad);
-        if constexpr (!pair_tiles<MODE, L>()) {
-#pragma unroll
-            for (int b = 0; b < 3; ++b) extract_bytes(counter[b], top[b]);
-        } else if (phase) {  // second tile of the pair: level-L CSA, one extract per two tiles
+        if (phase) {  // second tile of the pair: level-L CSA, one extract per two tiles
 #pragma unroll
             for (int b = 0; b < 3; ++b) {
                 uint32_t h, l;

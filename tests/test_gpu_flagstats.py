@@ -128,3 +128,38 @@ def test_flag_byte_frame_full_size_flushes(pp, dev, orc, monkeypatch):
     rc, want, _ = orc.flagstats(host[: 1 << 26])
     monkeypatch.delenv("POSPOP_FLAG_VARIANT")
     assert pp.flagstats(host[: 1 << 26]).as_list() == list(want)
+
+
+@pytest.mark.parametrize("variant", ["", "5,16,0,512,2,2", "6,32,0,256,2,2"])
+def test_qcfail_fast_path_and_fixup(pp, dev, orc, variant, monkeypatch):
+    """The byte-frame kernel predicts fail-free tiles and counts only AL/AH
+    there; a tile that turns out to hold a QC-fail read is reloaded and its
+    fail planes added.  Paired-end-like mix (kind 8: QC-fail 2^-16, so most
+    tiles take the fast path and some the fix-up), plus hand-placed QC-fail
+    words at tile starts, ends and in isolated tiles, and a fail-free stream."""
+    if variant:
+        monkeypatch.setenv("POSPOP_FLAG_VARIANT", variant)
+    n = (1 << 24) + 77
+    d = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_FLAGMIX, 5, d)
+    host = d.cpu().numpy().view(np.uint16).copy()
+    assert 0 < int(((host & 0x200) != 0).sum()) < n // 1000  # rare but present
+    for w in (host, host & np.uint16(0x0DFF)):                # with and without any QC-fail read
+        rc, want, _ = orc.flagstats(w)
+        assert rc == 0
+        assert pp.flagstats(torch.from_numpy(w.view(np.int16).copy()).cuda()).as_list() == list(want)
+    w = host & np.uint16(0x0DFF)
+    for pos in (0, 1, 4095, 4096, 65535, 1 << 20, (1 << 20) + 1, n - 1):
+        w[pos] |= 0x200
+    rc, want, _ = orc.flagstats(w)
+    for off in (0, 2, 6):  # unaligned starts shift tile boundaries
+        buf = torch.zeros(n + 64, dtype=torch.int16, device="cuda")
+        buf[off // 2: off // 2 + n] = torch.from_numpy(w.view(np.int16).copy()).cuda()
+        assert pp.flagstats(buf[off // 2: off // 2 + n]).as_list() == list(want), off
+
+
+def test_flagmix_generator_matches_oracle(pp, dev, orc):
+    n = (1 << 20) + 3
+    d = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_FLAGMIX, 11, d, base=12345)
+    assert (d.cpu().numpy().view(np.uint16) == orc.generate(8, 11, n, base=12345)).all()

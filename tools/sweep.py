@@ -158,15 +158,14 @@ def main():
         os.environ.pop("POSPOP_STREAM_VARIANT", None)
         os.environ.pop("POSPOP_TMA", None)
 
-    if "flag" in what:
+    if "flag" in what or "flagmix" in what:
         lib = pp._load()
         nf = 1 << 32  # 8 GiB of FLAG words
-        pp.generate(pp.GEN_FLAGS, 1, data, n=nf, stream=s)
+        pp.generate(pp.GEN_FLAGMIX if "flagmix" in what else pp.GEN_FLAGS, 1, data, n=nf, stream=s)
         torch.cuda.synchronize()
         import ctypes as CC
         summ = pp._Summary()
-        for var in ["5,32,0,512,2,2", "5,32,0,512,5,2", "5,16,0,512,5,2", "6,32,0,256,5,2", "5,16,0,512,2,2",
-                    "4,32,0,512,4,2"]:
+        for var in ["5,32,0,512,2,2", "5,16,0,512,2,2", "4,32,0,512,2,2", "6,32,0,256,2,2", "6,32,0,512,2"]:
             var, _, tma = var.partition("/")
             os.environ["POSPOP_FLAG_VARIANT"] = var
             if tma:
