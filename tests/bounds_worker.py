@@ -59,6 +59,11 @@ def main():
             assert got == list(orc.flagstats(flags[off // 2: off // 2 + n])[1])
     for v in ("", "6,32,0,512,2", "5,32,0,512,5,2", "4,32,0,512,4,2"):
         run("flagstats", {"POSPOP_FLAG_VARIANT": v} if v else {}, flag)
+    # paired-end-like mix: rare QC-fail reads -> the fail-free fast path and its reload fix-up
+    flags = orc.generate(8, 2, (3 << 20) + 5)
+    flags[[0, 4097, 3 << 19]] |= 0x200
+    fdev = torch.from_numpy(flags.view(np.uint8).copy()).cuda()
+    run("flagstats, QC-fail prediction", {}, flag)
 
     rng = np.random.default_rng(5)
     for k in (8, 16, 32, 64):
