@@ -6,10 +6,15 @@
 One rank per GPU (torchrun for N > 1, NCCL).  A *step* is one pass of the hot
 path over the workload: for the default cfg4 (BASELINE.json configs[3]) every
 rank counts its contiguous shard of 2^32 u16 words (Bernoulli(0.1) bits,
-generated in place in HBM) with ONE kernel launch, and for N > 1 the
-16-entry u64 k-vector is summed across ranks with one NCCL all-reduce (on a
-communication stream, overlapping the next step's kernel; double-buffered
-outputs; every reduction completes inside the timed region).
+generated in place in HBM) with ONE kernel launch; for N > 1 that kernel's
+last CTA also stores the rank's 16-entry u64 k-vector into every GPU's gather
+slot through peer memory (paper_1911_02696_b200.exchange; two alternating
+slots), so every GPU holds the summable rows when the step's launches
+complete -- proven at setup against an NCCL all-reduce, which is the fallback
+(double-buffered, on a high-priority communication stream) when peer mapping
+is unavailable.  Every exchange completes inside the timed region.  Other
+workloads (--workload): cfg2, cfg3, cfg5 / cfg5_u64 (segmented), flag /
+flagmix (fused FLAG statistics).
 Device-timed with CUDA events on the launching stream, barrier +
 synchronize on both sides, max over ranks.  The input (8 GiB) is far larger
 than the 126 MB L2, so no L2 flush is needed between steps.
@@ -43,7 +48,8 @@ FALLBACK_HBM = 6650.0
 WORKLOADS = {
     # name: (k, generator kind, total words, description)
     "cfg4": (16, 4, 1 << 32, "cfg4: 2^32 u16 words, each bit Bernoulli(6554/65536), contiguous shards "
-                             "over the N GPUs, k=16 u64 counters summed across GPUs (NCCL all-reduce)"),
+                             "over the N GPUs, k=16 u64 counters summed across GPUs (delivered to every GPU "
+                             "by the counting kernel through peer memory; NCCL all-reduce as the fallback)"),
     "cfg2": (16, 2, 1 << 28, "cfg2: 2^28 u16 one-hot words, position Zipf(1.1), k=16 u64 counters"),
     "cfg3": (8, 3, (1 << 30) - 7, "cfg3: 2^30-7 u8 words at a +3 byte offset, 4 KiB runs one-hot/uniform, "
                                   "k=8 u64 counters"),
