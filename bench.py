@@ -758,25 +758,31 @@ def run_ours(args):
     # Fused exchange: set up the peer gather slots, prove they work on this
     # machine (every rank's rows land on every GPU and sum to the NCCL
     # all-reduce), else fall back to the NCCL all-reduce and say why.
+    # Every rank runs the same collectives in the same order whatever fails
+    # locally (PeerGather.create), so a failure on one rank cannot hang others.
     pg, collective = None, ("nccl" if world > 1 else "none")
     if world > 1 and args.collective == "p2p":
-        try:
-            from paper_1911_02696_b200.exchange import PeerGather
-            pg = PeerGather(k)
+        from paper_1911_02696_b200.exchange import PeerGather
+        pg, reason = PeerGather.create(k)
+        if pg is not None:
             probe = torch.zeros(k, dtype=torch.int64, device=dev)
-            pg.count(data, probe, 0, stream=stream, len_words=min(words, 1 << 20))
-            torch.cuda.synchronize(dev)
-            dist.barrier()
+            local_ok = 1
+            try:
+                pg.count(data, probe, 0, stream=stream, len_words=min(words, 1 << 20))
+                torch.cuda.synchronize(dev)
+            except Exception as e:  # noqa: BLE001
+                local_ok, reason = 0, f"fused count: {e}"
             ref = probe.clone()
-            dist.all_reduce(ref)
-            ok = torch.tensor([int(torch.equal(pg.result(0), ref))], device=dev)
+            dist.all_reduce(ref)  # every rank, always
+            ok = torch.tensor([local_ok * int(torch.equal(pg.result(0), ref))], device=dev)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if int(ok.item()) != 1:
-                raise RuntimeError("peer gather rows disagree with the NCCL all-reduce")
+                pg, reason = None, reason or "peer gather rows disagree with the NCCL all-reduce"
+        if pg is not None:
             collective = "p2p"
-        except Exception as e:  # noqa: BLE001 -- setup-time choice of collective, reported in config
-            print(f"[bench] p2p exchange unavailable ({e}); using NCCL all-reduce", file=sys.stderr)
-            pg, collective = None, f"nccl (p2p unavailable: {str(e)[:120]})"
+        else:
+            print(f"[bench] p2p exchange unavailable ({reason}); using NCCL all-reduce", file=sys.stderr)
+            collective = f"nccl (p2p unavailable: {str(reason)[:120]})"
 
     def step(i):
         o = outs[i % 2]

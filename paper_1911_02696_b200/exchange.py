@@ -53,6 +53,49 @@ class PeerGather:
                                     device=f"cuda:{dev}") for s in range(self.slots)]
         self.buffer = torch.as_tensor(_DeviceView(self.ptr, (self.slots, self.world, self.k)), device=f"cuda:{dev}")
 
+    @classmethod
+    def create(cls, k: int, slots: int = 2, group: Any = None) -> "tuple[PeerGather | None, str]":
+        """Collective-safe setup: every rank executes the same collectives
+        whatever fails locally, and either all ranks get a PeerGather or all
+        get (None, reason) -- a local failure never leaves peers blocked."""
+        import torch
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        self = cls.__new__(cls)
+        self.k, self.slots, self.world, self.rank = int(k), int(slots), world, rank
+        self._slot_bytes = world * self.k * 8
+        dev = torch.cuda.current_device()
+        reason = ""
+        try:
+            self.ptr, handle = ipc_alloc(self.slots * self._slot_bytes)
+        except Exception as e:  # noqa: BLE001
+            self.ptr, handle, reason = 0, None, f"ipc_alloc: {e}"
+        handles: list = [None] * world
+        dist.all_gather_object(handles, handle, group=group)  # every rank, always
+        opened: list[int] = []
+        ok = all(h is not None for h in handles)
+        if ok:
+            try:
+                for j in range(world):
+                    opened.append(self.ptr if j == rank else ipc_open(handles[j]))
+            except Exception as e:  # noqa: BLE001
+                ok, reason = False, f"ipc_open: {e}"
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=f"cuda:{dev}")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) != 1:
+            for j, p in enumerate(opened):
+                if j != rank:
+                    ipc_close(p)
+            if self.ptr:
+                ipc_free(self.ptr)
+            return None, reason or "a peer could not map the gather buffers"
+        self.peer_ptrs = opened
+        self.tables = [torch.tensor([p + s * self._slot_bytes for p in opened], dtype=torch.int64,
+                                    device=f"cuda:{dev}") for s in range(self.slots)]
+        self.buffer = torch.as_tensor(_DeviceView(self.ptr, (self.slots, world, self.k)), device=f"cuda:{dev}")
+        return self, ""
+
     def count(self, data: Any, out: Any, step: int, *, stream: Any = None, len_words: int | None = None) -> None:
         """One kernel: this rank's counts into `out` and into row `rank` of slot step % slots on every GPU."""
         count_allgather_async(data, out, self.k, self.tables[step % self.slots], self.world, self.rank,

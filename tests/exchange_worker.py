@@ -28,7 +28,8 @@ def main():
         want_all = orc.pospopcnt(host, k, threads=4)
         mine = host[lo * k // 8: hi * k // 8]
         d = torch.from_numpy(mine.copy()).cuda()
-        pg = PeerGather(k)
+        pg, reason = PeerGather.create(k)
+        assert pg is not None, reason
         out = torch.zeros(k, dtype=torch.int64, device="cuda")
         for step in range(3):  # slots 0, 1, 0: a slot is rewritten in place
             pg.count(d, out, step)
@@ -40,6 +41,22 @@ def main():
             assert (pg.result(step).cpu().numpy().astype(np.uint64) == want_all).all(), (k, step, rank)
             dist.barrier()
         pg.close()
+    # A local failure on one rank (here: rank 1 cannot map a peer) must make
+    # every rank fall back together, with no collective left waiting.
+    import paper_1911_02696_b200.exchange as ex
+    real_open = ex.ipc_open
+
+    def failing_open(h):
+        if rank == 1:
+            raise RuntimeError("injected ipc_open failure")
+        return real_open(h)
+    ex.ipc_open = failing_open
+    pg, reason = PeerGather.create(16)
+    ex.ipc_open = real_open
+    assert pg is None and reason, (rank, reason)
+    pg, reason = PeerGather.create(16)  # and a clean retry still works
+    assert pg is not None, reason
+    pg.close()
     dist.barrier()
     if rank == 0:
         print("exchange ok", world)
