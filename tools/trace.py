@@ -38,7 +38,8 @@ def main():
     for var in variants:
         if var:
             os.environ["POSPOP_STREAM_VARIANT"] = var
-        for nbytes in (1 << 29, 1 << 30, 1 << 33):
+        sizes = [int(x) for x in os.environ.get("TRACE_BYTES", "").split(",") if x] or [1 << 29, 1 << 30, 1 << 33]
+        for nbytes in sizes:
             for rep in range(4):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
