@@ -17,6 +17,8 @@ fixtures are exactly the cases those tests check:
 * bench.cpp:115-120        -- generate_stream words for several seeds; cfg1 (seed 1, 2^20)
 * acceptance.cpp:271-291   -- 100 FLAG streams of 10^5 words (seed 0xF1A6) and the 4096
                               single-value summaries, from flagstats_reference
+* k = 8/32/64              -- generate_stream bytes as k-bit words, counted by the
+                              reference's 16-bit API after the SURVEY 8c restatement
 
 Counts come from pospop::pospopcnt (Auto and every CSA width) and
 pospop::oracle_pospopcnt; the script asserts they agree before writing.
@@ -154,13 +156,30 @@ def main() -> None:
         single.append([int(x) for x in summ])
     out["flagstats_single"] = single
 
+    # k = 8 / 32 / 64 (no reference function): streams of the
+    # reference's generate_stream bytes read as k-bit words at several byte
+    # offsets and lengths, counted by the reference's own 16-bit pospopcnt
+    # after the 8c restatement (ref_segmented: k=8 fold with a direct odd
+    # head/tail byte, k=32/64 deinterleave).  [seed, k, byte_offset, n_words, counts...]
+    kw = []
+    for seed, k, off, n in ((21, 8, 0, 100003), (22, 8, 1, 65537), (23, 8, 3, 7), (24, 32, 0, 50001),
+                            (25, 32, 4, 4097), (26, 64, 0, 30011), (27, 64, 8, 513), (28, 64, 0, 1)):
+        wb = k // 8
+        raw = ref.generate_stream(seed, (off + n * wb) // 2 + 2).view(np.uint8)[off:off + n * wb]
+        dt = {8: np.uint8, 32: np.uint32, 64: np.uint64}[k]
+        words = np.frombuffer(raw.tobytes(), dt)
+        rows = ref.segmented(words, np.array([0, n], np.uint64), k, threads=1)
+        assert (rows[0] == orc.naive(raw, k)).all()
+        kw.append([seed, k, off, n] + [int(x) for x in rows[0]])
+    out["k_widths"] = kw
+
     with open(os.path.join(HERE, "reference_counts.json"), "w") as f:
         json.dump(out, f, separators=(",", ":"))
 
     # Generator fixtures (counter-based synthetic inputs).  These
     # pin the device generators; produced by the C restatement.
     gens = {}
-    for kind in range(1, 8):
+    for kind in range(1, 9):
         for seed, base in ((1, 0), (1, 123456789), (42, 2**33 + 17)):
             a = orc.generate(kind, seed, 1 << 16, base=base)
             gens[f"{kind}:{seed}:{base}"] = {"first16": [int(x) for x in a[:16]],

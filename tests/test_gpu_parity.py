@@ -463,3 +463,15 @@ def test_chained_async_launches_read_the_previous_output(pp, dev, orc):
         rows = seg.cpu().numpy().astype(np.uint64)
         assert (rows.sum(axis=0) == want).all()
         assert (out2.cpu().numpy().astype(np.uint64) == np.asarray(orc.pospopcnt(rows.ravel(), 64), np.uint64)).all()
+
+
+def test_k_widths_against_reference_fixtures(pp, dev, orc, golden):
+    """The GPU on the k = 8/32/64 fixtures counted by the reference library's
+    16-bit API (golden k_widths), at the fixture's byte offset inside 0xFF guards."""
+    for seed, k, off, n, *counts in golden["k_widths"]:
+        wb = k // 8
+        stream = orc.mt_generate_stream(seed, (off + n * wb) // 2 + 2).view(np.uint8)
+        buf = torch.full((stream.size + 128,), 0xFF, dtype=torch.uint8, device="cuda")
+        buf[64:64 + stream.size] = torch.from_numpy(stream.copy()).cuda()
+        view = buf[64 + off: 64 + off + n * wb]
+        assert [int(x) for x in pp.pospopcnt_k(view, k).counts] == counts, (seed, k, off, n)

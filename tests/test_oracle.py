@@ -325,3 +325,13 @@ def test_reference_segmented_restatement_matches_oracle(orc, ref, k):
     rng = np.random.default_rng(k)
     offs = np.concatenate([[0, 0, 1], np.sort(rng.integers(1, n, 40)), [n]]).astype(np.uint64)
     assert (ref.segmented(data, offs, k, threads=3) == orc.segmented(data, offs, k, threads=2)).all()
+
+
+def test_k_widths_against_reference_fixtures(orc, golden):
+    """k = 8/32/64 counts from the reference library's own 16-bit API (golden
+    k_widths, make_golden.py) reproduced by the oracle."""
+    ref_words = {}
+    for seed, k, off, n, *counts in golden["k_widths"]:
+        wb = k // 8
+        raw = orc.mt_generate_stream(seed, (off + n * wb) // 2 + 2).view(np.uint8)[off:off + n * wb]
+        assert [int(x) for x in orc.pospopcnt(raw, k)] == counts, (seed, k, off, n)
