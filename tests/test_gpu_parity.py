@@ -273,7 +273,7 @@ DT = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}
 # -- generators: device bytes == oracle bytes ------------------------------------------------
 
 def test_device_generators_match_oracle(pp, dev, orc, golden_generators):
-    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8, 7: 2}
+    esize = {1: 2, 2: 2, 3: 1, 4: 2, 5: 4, 6: 8, 7: 2, 8: 2}
     for key, v in golden_generators.items():
         kind, seed, base = (int(x) for x in key.split(":"))
         buf = torch.zeros((1 << 16) * esize[kind] + 8, dtype=torch.uint8, device="cuda")
