@@ -312,8 +312,16 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     unsigned long long tail = warps * (unsigned long long)env_int("POSPOP_TAIL_TILES_PER_WARP", 8);
     if (tail > a.nwt) tail = a.nwt;
     a.nA = (a.nwt - tail) / a.CA;
-    // SCHED 2: the global tail pool, in warp tiles.
-    a.pool = warps * (unsigned long long)env_int("POSPOP_POOL_TILES_PER_WARP", 16);
+    // SCHED 2: the global tail pool, in warp tiles: ~1/27 of each warp's
+    // share, 1..16 tiles per warp (measured, tools/size_curve.py, 16 KiB warp
+    // tiles at the default depth: 8 GiB (442 tiles per warp) wants 16 to
+    // absorb the tail; at 128 MiB a 16-tile pool would be 58 % of the input
+    // and costs 26 % -- pool chunks are claimed by global atomics with worse
+    // DRAM locality than the CTA ranges).
+    const unsigned long long share = warps ? a.nwt / warps : 0;
+    unsigned long long ppw = (unsigned long long)env_int("POSPOP_POOL_TILES_PER_WARP", 0);
+    if (ppw == 0) ppw = share / 27 < 1 ? 1 : (share / 27 > 16 ? 16 : share / 27);
+    a.pool = warps * ppw;
     if (a.pool > a.nwt) a.pool = a.nwt;
 
     if (grid_used) *grid_used = grid;
