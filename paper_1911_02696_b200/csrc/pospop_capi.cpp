@@ -14,6 +14,7 @@
 
 #include <cerrno>
 #include <condition_variable>
+#include <deque>
 #include <cstdarg>
 #include <functional>
 #include <thread>
@@ -223,6 +224,15 @@ struct Ctx {
     // grow-only device scratch for the synchronous segmented call (data, offsets, rows)
     void* scratch[3] = {};
     size_t scratch_cap[3] = {};
+    // pospopcnt_sharded: per shard on this device a stream, a workspace and a
+    // mapped pinned result (kept for reuse; no allocation per call)
+    struct ShardSlot {
+        cudaStream_t stream = nullptr;
+        StreamWorkspace ws;
+        unsigned long long* m_out = nullptr;
+        unsigned long long* m_out_dev = nullptr;
+    };
+    std::deque<ShardSlot> shard_slots;  // deque: push_back keeps references to earlier slots valid
     // pinned host ring for pageable / file input (lazily allocated)
     uint8_t* host_ring[kHostRing] = {};
     cudaEvent_t ev_h2d[kHostRing] = {};  // the H2D that last read host_ring[i] is done
@@ -873,51 +883,49 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
     pospop_status s = current_device(&dev0);
     if (s) return s;
     const size_t wb = (size_t)k / 8;
-    // Launch every shard before any synchronisation (launch skew, SURVEY 8e).
-    std::vector<unsigned long long*> partial((size_t)n_shards, nullptr);
-    std::vector<Ctx*> ctxs((size_t)n_shards, nullptr);
-    std::vector<cudaStream_t> streams((size_t)n_shards, nullptr);
-    LaunchOptions opt;
-    for (int i = 0; i < n_shards; ++i) {
+    for (int i = 0; i < n_shards; ++i) {  // validate everything before launching anything
         if (!shards[i] && lens[i]) return fail(POSPOP_EINVAL, "shard %d is NULL with len %zu", i, lens[i]);
         if ((uintptr_t)shards[i] % wb) return fail(POSPOP_EINVAL, "shard %d is misaligned", i);
-        int d = devices[i];
-        int pd = d;
+        int pd = devices[i];
         if (lens[i] && classify(shards[i], &pd) != Where::Device)
             return fail(POSPOP_EINVAL, "shard %d is not device memory", i);
-        if (lens[i] && pd != d) return fail(POSPOP_EINVAL, "shard %d lives on device %d, not %d", i, pd, d);
+        if (lens[i] && pd != devices[i])
+            return fail(POSPOP_EINVAL, "shard %d lives on device %d, not %d", i, pd, devices[i]);
+    }
+    // Launch every shard before any synchronisation (launch skew, SURVEY 8e).
+    // Shard i is the j-th shard of its device: it uses that device's slot j
+    // (own stream and workspace, so shards on one device may overlap), and
+    // its kernel writes the k counts straight into the slot's mapped buffer.
+    std::vector<Ctx::ShardSlot*> used((size_t)n_shards, nullptr);
+    std::map<int, size_t> per_dev;
+    LaunchOptions opt;
+    for (int i = 0; i < n_shards; ++i) {
+        const int d = devices[i];
         DeviceGuard g(d);
-        if ((s = get_ctx(d, &ctxs[(size_t)i]))) return s;
-        // Each shard gets its own stream + workspace so shards on one device
-        // may run back to back without sharing a ticket.
-        CU(cudaStreamCreateWithFlags(&streams[(size_t)i], cudaStreamDefault));
-        StreamWorkspace ws;
-        if ((s = stream_workspace(d, streams[(size_t)i], &ws))) return s;
-        CU(cudaMalloc(&partial[(size_t)i], 64 * sizeof(unsigned long long)));
+        Ctx* c = nullptr;
+        if ((s = get_ctx(d, &c))) return s;
+        const size_t j = per_dev[d]++;
+        if (c->shard_slots.size() <= j) {
+            Ctx::ShardSlot slot;
+            CU(cudaStreamCreateWithFlags(&slot.stream, cudaStreamDefault));
+            if ((s = alloc_workspace(&slot.ws))) return s;
+            CU(cudaHostAlloc(&slot.m_out, 64 * sizeof(unsigned long long), cudaHostAllocMapped));
+            CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&slot.m_out_dev), slot.m_out, 0));
+            c->shard_slots.push_back(slot);
+        }
+        Ctx::ShardSlot* slot = &c->shard_slots[j];
+        used[(size_t)i] = slot;
         if (lens[i]) {
-            CU(launch_stream(k, shards[i], lens[i], partial[(size_t)i], false, opt, ws, streams[(size_t)i]));
+            CU(launch_stream(k, shards[i], lens[i], slot->m_out_dev, false, opt, slot->ws, slot->stream));
         } else {
-            CU(cudaMemsetAsync(partial[(size_t)i], 0, 64 * sizeof(unsigned long long), streams[(size_t)i]));
+            for (int p = 0; p < k; ++p) slot->m_out[p] = 0;
         }
     }
     for (int p = 0; p < k; ++p) counts[p] = 0;
     for (int i = 0; i < n_shards; ++i) {  // merge_counts over shards
         DeviceGuard g(devices[i]);
-        unsigned long long h[64];
-        CU(cudaMemcpyAsync(h, partial[(size_t)i], (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                           streams[(size_t)i]));
-        CU(cudaStreamSynchronize(streams[(size_t)i]));
-        for (int p = 0; p < k; ++p) counts[p] += h[p];
-        cudaFree(partial[(size_t)i]);
-        {
-            std::lock_guard<std::mutex> lock(g_ws_mu);
-            auto it = g_ws.find(std::make_pair(devices[i], streams[(size_t)i]));
-            if (it != g_ws.end()) {
-                cudaFree(it->second.ws.acc);
-                g_ws.erase(it);
-            }
-        }
-        cudaStreamDestroy(streams[(size_t)i]);
+        CU(cudaStreamSynchronize(used[(size_t)i]->stream));
+        for (int p = 0; p < k; ++p) counts[p] += used[(size_t)i]->m_out[p];
     }
     return POSPOP_OK;
 }

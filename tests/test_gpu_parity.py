@@ -475,3 +475,19 @@ def test_k_widths_against_reference_fixtures(pp, dev, orc, golden):
         buf[64:64 + stream.size] = torch.from_numpy(stream.copy()).cuda()
         view = buf[64 + off: 64 + off + n * wb]
         assert [int(x) for x in pp.pospopcnt_k(view, k).counts] == counts, (seed, k, off, n)
+
+
+def test_sharded_repeated_calls_and_empty_shards(pp, dev, orc):
+    """pospopcnt_sharded reuses per-device shard slots across calls: repeated
+    calls, a varying shard count, empty shards, every k."""
+    for k in (8, 16, 32, 64):
+        raw = orc.generate(6, 60 + k, (3 << 20) // 8).view(np.uint8)
+        d = torch.from_numpy(raw.copy()).cuda()
+        want = orc.pospopcnt(raw, k, threads=4)
+        wb = k // 8
+        n = raw.size // wb
+        for parts in (1, 3, 5, 2, 5):
+            cuts = [n * i // parts for i in range(parts + 1)]
+            shards = [d[cuts[i] * wb: cuts[i + 1] * wb] for i in range(parts)]
+            shards.insert(1, d[:0])  # an empty shard
+            assert pp.pospopcnt_sharded(shards, [0] * len(shards), k) == want, (k, parts)
