@@ -674,7 +674,6 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
         dout = static_cast<unsigned long long*>(buf);
     }
     LaunchOptions opt;
-    opt.seg_avg_bytes = (hoff[n] - hoff[0]) * wb / n;  // picks the schedule for short arrays
     CU(launch_segmented(k, ddata ? ddata : (const void*)doff, doff, n, dout, opt, c->ws, c->stream));
     if (!c_dev)
         CU(cudaMemcpyAsync(counts, dout, n * (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));

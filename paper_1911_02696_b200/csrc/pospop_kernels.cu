@@ -414,6 +414,12 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
     return launch_stream_mode(2, 16, flags, len, d_out33, accumulate, opt, ws, stream, nullptr);
 }
 
+// Adaptive segmented kernel (sched 8) thresholds on the mean array length
+// (tools/seg_modes.py, u32: 64-word arrays lane 1523 vs G=4 1003 GB/s;
+// 256-word arrays G=4 4269 vs lane 2173; 1024 words G=4 ~ pipelined).
+constexpr int kSegLaneMeanBytes = 512;
+constexpr int kSegGroupMeanBytes = 2048;
+
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets, size_t n,
                              unsigned long long* d_out, const LaunchOptions& opt, const StreamWorkspace& ws,
                              cudaStream_t stream) {
@@ -421,17 +427,15 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     env_refresh();
     const int nbank = k == 64 ? 2 : 1;
     // Tuning override: POSPOP_SEG_VARIANT="depth,vb,sched[,lanes per array]".
-    // measured (r01, tools/sweep.py --what seg): pipelined with the bit-plane
-    // epilogue, 2 CTAs/SM (k <= 32: cfg5 6612 -> 6877 GB/s, 1024-word arrays
-    // 4360 -> 5990); dynamic claiming (k = 64)
-    int depth = 5, vb = 16, sched = nbank == 1 ? 6 : 1, group = 0;
-    // very short arrays: 4 lanes per array (grouped schedule)
-    if (nbank == 1 && opt.seg_avg_bytes && opt.seg_avg_bytes <= (unsigned long long)env_int("POSPOP_SEG_GROUP_BYTES", 2048))
-        depth = 6, sched = 5, group = 4;
+    // Default: the adaptive kernel (sched 8), which picks one lane per array,
+    // 4 lanes per array or the pipelined warp-per-array kernel with the
+    // bit-plane epilogue from the mean array length on the device
+    // (tools/seg_modes.py).
+    int depth = nbank == 1 ? 5 : 4, vb = 16, sched = 8, group = 0;  // (depth/vb name the sched-8 entry)
     if (const char* v = env_get("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &sched, &group);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb, sched, group);
-    if (!var) var = pick_segmented(nbank, 5, 16, nbank == 1 ? 6 : 1);
+    if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16, 8);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {
@@ -448,6 +452,11 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     unsigned extra = (unsigned)env_int("POSPOP_SEG_PER_GRAB", 1);
     if (extra < 1) extra = 1;
     if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
+    if (var->sched == 8) {  // mean-length thresholds, in 64-byte units (<= 4 MiB), for the lane and grouped modes
+        auto units = [](int bytes) { return (unsigned)(bytes < 0 ? 0 : (bytes / 64 > 0xFFFF ? 0xFFFF : bytes / 64)); };
+        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes)) |
+                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes)) << 16);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)block);

@@ -32,7 +32,6 @@ struct LaunchOptions {
     int depth = 0;                     // 0 = default tree depth (k=64: per bank)
     unsigned long long* trace = nullptr;  // diagnostics: 5 u64 per CTA (see pospopcnt_trace_async)
     unsigned long long word_base = 0;     // FLAG mode: global index of the first word
-    unsigned long long seg_avg_bytes = 0; // segmented: mean array length when known (0 = unknown)
     unsigned long long* const* peers = nullptr;  // fused exchange: device array of n_peers gather slots
     int n_peers = 0;
     int rank = 0;

@@ -26,23 +26,15 @@ namespace dev {
 // (SCHED 2 / 3: segmented_pipe_entry below, software-pipelined; 3 = bounded
 // to 2 CTAs/SM, which keeps it at <= 128 registers.)
 template <int NBANK, int L, int VB, int SCHED>
-__global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
-                                                        const unsigned long long* offsets,
-                                                        unsigned long long n_arrays, int k,
-                                                        uint32_t flush_threshold,
-                                                        unsigned long long* out,
-                                                        unsigned long long* next,
-                                                        unsigned int* ticket, unsigned per_grab) {
+__device__ __forceinline__ void seg_warp_loop(const uint8_t* data, const unsigned long long* offsets,
+                                              unsigned long long n_arrays, int k, uint32_t flush_threshold,
+                                              unsigned long long* out, unsigned long long* next, unsigned per_grab) {
     constexpr int REGS = NBANK << L;
     constexpr int RPV = VB / 4;
     constexpr int VPT = REGS / RPV;
     constexpr unsigned long long STEP = 32ull * VPT;
     const uint32_t lane = threadIdx.x & 31u;
     const int wb = k >> 3;
-    __shared__ int s_last;
-
-    pdl_allow_next();
-    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     unsigned long long mine = 0, run = 0, arr = warp, stop = n_arrays;
@@ -140,9 +132,12 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
         }
         arr += SCHED == 0 ? nwarps : 1;
     }
-    if (SCHED == 0) return;
-    // Every warp has drawn an index >= n_arrays; once all CTAs are past that
-    // point the counter can be reset.
+}
+
+// Every warp has drawn a claim index past the end; once all CTAs are past that
+// point the claim counter can be reset for the next launch.
+__device__ __forceinline__ void seg_claims_done(unsigned long long* next, unsigned int* ticket) {
+    __shared__ int s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -152,6 +147,20 @@ __global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
             *ticket = 0u;
         }
     }
+}
+
+template <int NBANK, int L, int VB, int SCHED>
+__global__ void __launch_bounds__(256) segmented_kernel(const uint8_t* data,
+                                                        const unsigned long long* offsets,
+                                                        unsigned long long n_arrays, int k,
+                                                        uint32_t flush_threshold,
+                                                        unsigned long long* out,
+                                                        unsigned long long* next,
+                                                        unsigned int* ticket, unsigned per_grab) {
+    pdl_allow_next();
+    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
+    seg_warp_loop<NBANK, L, VB, SCHED>(data, offsets, n_arrays, k, flush_threshold, out, next, per_grab);
+    if (SCHED == 1) seg_claims_done(next, ticket);
 }
 
 // ---------------------------------------------------------------------------
@@ -577,19 +586,16 @@ __device__ __forceinline__ void seg_group_batch(const uint8_t* data, const unsig
     }
 }
 
-template <int NBANK, int L, int VB, int G, int MINB>
-__global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_t* data,
-                                                                    const unsigned long long* offsets,
-                                                                    unsigned long long n_arrays, int k,
-                                                                    uint32_t flush_threshold, unsigned long long* out,
-                                                                    unsigned long long* next, unsigned int* ticket,
-                                                                    unsigned big_vectors) {
+// The claim loop of the grouped schedule (device function so the adaptive
+// kernel below can run it too).  `next` must be zero on entry.
+template <int NBANK, int L, int VB, int G>
+__device__ __forceinline__ void seg_group_loop(const uint8_t* data, const unsigned long long* offsets,
+                                               unsigned long long n_arrays, int k, uint32_t flush_threshold,
+                                               unsigned long long* out, unsigned long long* next,
+                                               unsigned big_vectors) {
     constexpr int NG = 32 / G;  // arrays per batch
     const uint32_t lane = threadIdx.x & 31u;
     const int wb = k >> 3;
-    __shared__ int s_last;
-    pdl_allow_next();
-    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
     mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
@@ -609,17 +615,154 @@ __global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_
         b = __shfl_sync(0xFFFFFFFFu, mine, 0);
         mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     }
-    // Every warp has drawn an index past the end; once all CTAs are past that
-    // point the counter can be reset.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-        if (s_last) {
-            *next = 0ull;
-            *ticket = 0u;
+}
+
+template <int NBANK, int L, int VB, int G, int MINB>
+__global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_t* data,
+                                                                    const unsigned long long* offsets,
+                                                                    unsigned long long n_arrays, int k,
+                                                                    uint32_t flush_threshold, unsigned long long* out,
+                                                                    unsigned long long* next, unsigned int* ticket,
+                                                                    unsigned big_vectors) {
+    pdl_allow_next();
+    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
+    seg_group_loop<NBANK, L, VB, G>(data, offsets, n_arrays, k, flush_threshold, out, next, big_vectors);
+    seg_claims_done(next, ticket);
+}
+
+// ---------------------------------------------------------------------------
+// One lane per array (tiny arrays): each lane walks its own array's 16-byte
+// vectors (masked edges), a depth-3 tree over pairs of vectors (k = 64: two
+// depth-2 banks), then drains and writes its own row -- no cross-lane
+// reduction at all.  Adjacent lanes take adjacent arrays, so a warp's loads
+// stay within one contiguous region.  Lanes stay within 16-bit counters for
+// arrays up to 2 MiB; the caller keeps arrays above `lane_cap_bytes` on the
+// full-warp path.
+// ---------------------------------------------------------------------------
+template <int NBANK>
+__device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsigned long long* offsets,
+                                               unsigned long long a, int k, unsigned long long* out) {
+    constexpr int L = NBANK == 1 ? 3 : 2;
+    constexpr int REGS = NBANK << L;  // 8 registers = two 16-byte vectors
+    constexpr int VPT = REGS / 4;
+    const int wb = k >> 3;
+    const SegView v = seg_view<16>(data, offsets[a], offsets[a + 1], wb);
+    uint32_t carries[NBANK][L];
+    uint32_t counter[NBANK][16];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    for (unsigned long long t = 0; t < v.nv; t += VPT) {
+        uint32_t r[REGS];
+#pragma unroll
+        for (int q = 0; q < VPT; ++q) {
+            const unsigned long long idx = t + q;
+            uint32_t x[4] = {0u, 0u, 0u, 0u};
+            if (idx < v.nv) {
+                POSPOP_CHECK(idx < v.nv);
+                ldg_stream<16, 0>(v.base + idx * 16, x);
+                if (idx == 0 || idx + 1 == v.nv) mask_bytes<16>(x, idx == 0 ? v.lo : 0, idx + 1 == v.nv ? v.hi : 16);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) r[q * 4 + j] = x[j];
+        }
+        tree_block<NBANK, L>(r, carries, counter);
+    }
+    unsigned long long* row = out + a * (unsigned long long)k;
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+        uint32_t d[16];
+        drain<L>(d, carries[b]);
+        uint32_t ch[32];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            ch[p] = ((counter[b][p] & 0xFFFFu) << L) + (d[p] & 0xFFFFu);
+            ch[p + 16] = ((counter[b][p] >> 16) << L) + (d[p] >> 16);
+        }
+        if (NBANK == 2 || k == 32) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 2)
+                *reinterpret_cast<ulonglong2*>(row + 32 * b + c) = make_ulonglong2(ch[c], ch[c + 1]);
+        } else if (k == 16) {
+#pragma unroll
+            for (int p = 0; p < 16; p += 2)
+                *reinterpret_cast<ulonglong2*>(row + p) =
+                    make_ulonglong2((unsigned long long)ch[p] + ch[p + 16], (unsigned long long)ch[p + 1] + ch[p + 17]);
+        } else {  // k == 8: channels p, p+8, p+16, p+24
+#pragma unroll
+            for (int p = 0; p < 8; p += 2)
+                *reinterpret_cast<ulonglong2*>(row + p) =
+                    make_ulonglong2((unsigned long long)ch[p] + ch[p + 8] + ch[p + 16] + ch[p + 24],
+                                    (unsigned long long)ch[p + 1] + ch[p + 9] + ch[p + 17] + ch[p + 25]);
         }
     }
+}
+
+// Lane mode claim loop: batches of 32 consecutive arrays per warp; a batch
+// holding an array above lane_cap_bytes is counted array by array by the
+// whole warp instead.
+template <int NBANK, int LW, int VBW>
+__device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigned long long* offsets,
+                                              unsigned long long n_arrays, int k, uint32_t flush_threshold,
+                                              unsigned long long* out, unsigned long long* next,
+                                              unsigned long long lane_cap_bytes) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const int wb = k >> 3;
+    unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
+    mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    for (;;) {
+        const unsigned long long a0 = b * 32;
+        if (a0 >= n_arrays) break;  // warp-uniform
+        const unsigned long long a = a0 + lane;
+        const unsigned long long nbytes = a < n_arrays ? (offsets[a + 1] - offsets[a]) * wb : 0;
+        if (!__any_sync(0xFFFFFFFFu, nbytes > lane_cap_bytes)) {
+            if (a < n_arrays) seg_lane_array<NBANK>(data, offsets, a, k, out);
+        } else {
+            for (int j = 0; j < 32; ++j)
+                if (a0 + j < n_arrays)
+                    seg_group_batch<NBANK, LW, VBW, 32>(data, offsets, a0 + j, n_arrays, k, flush_threshold, out, lane);
+        }
+        b = __shfl_sync(0xFFFFFFFFu, mine, 0);
+        mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Adaptive segmented kernel (SCHED 8, the asynchronous entry point's default
+// for k <= 32): every CTA reads offsets[0] and offsets[n] and picks, from the
+// mean array length, one lane per array (tiny arrays), G = 4 lanes per array
+// (short arrays) or the software-pipelined warp-per-array kernel with the
+// bit-plane epilogue -- the same choice for the whole grid, made on the
+// device, so device-resident offsets need no host round trip.
+// ---------------------------------------------------------------------------
+template <int NBANK>
+__global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* data,
+                                                                const unsigned long long* offsets,
+                                                                unsigned long long n_arrays, int k,
+                                                                uint32_t flush_threshold, unsigned long long* out,
+                                                                unsigned long long* next, unsigned int* ticket,
+                                                                unsigned thresholds) {
+    constexpr int LW = NBANK == 1 ? 5 : 4;  // full-warp fallback tree depth
+    pdl_allow_next();
+    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
+    const int wb = k >> 3;
+    const unsigned long long lane_max = (unsigned long long)(thresholds & 0xFFFFu) * 64;         // mean bytes
+    const unsigned long long group_max = (unsigned long long)(thresholds >> 16) * 64;             // mean bytes
+    const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
+    if (mean <= lane_max) {
+        seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10);
+    } else if (mean <= group_max) {
+        constexpr int LG = NBANK == 1 ? 6 : 4;  // grouped-mode tree depth (measured: 6 beats 5 by ~10 % at 1 KiB)
+        seg_group_loop<NBANK, LG, 16, 4>(data, offsets, n_arrays, k, flush_threshold, out, next, (256u << 10) / 16);
+    } else if constexpr (NBANK == 1) {
+        segmented_pipe_body<NBANK, LW, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out);
+    } else {  // k = 64: dynamic array claims measure best
+        seg_warp_loop<NBANK, 5, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out, next, 1u);
+    }
+    seg_claims_done(next, ticket);
 }
 
 }  // namespace dev

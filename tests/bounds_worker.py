@@ -78,6 +78,7 @@ def main():
         o = torch.from_numpy(offs.view(np.int64)).cuda()
         variants = ["5,16,0", "5,16,1", "5,16,3", "5,16,6", "6,16,5,4", "6,16,5,8"] if k < 64 else \
                    ["5,16,0", "5,16,1", "4,16,6", "4,16,5,8"]
+        auto = "4,16,8" if k == 64 else "5,16,8"
 
         def seg():
             out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
@@ -86,6 +87,9 @@ def main():
             assert (out.cpu().numpy().view(np.uint64) == want_rows).all()
         for v in variants:
             run(f"segmented k={k}", {"POSPOP_SEG_VARIANT": v, "POSPOP_SEG_BIG_KIB": "64"}, seg)
+        for lane, group in ((1 << 20, 1 << 20), (0, 1 << 20), (0, 0)):  # adaptive: lane / grouped / warp modes
+            run(f"segmented adaptive k={k}", {"POSPOP_SEG_VARIANT": auto, "POSPOP_SEG_LANE_MEAN_BYTES": str(lane),
+                                              "POSPOP_SEG_GROUP_MEAN_BYTES": str(group)}, seg)
     print("bounds ok")
 
 

@@ -358,13 +358,14 @@ def test_reference_verify_kernels_with_gpu_runner():
 
 
 _GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4", "6,16,5,16", "5,32,5,4",
-            "5,16,6", "5,32,6", "4,16,6", "4,32,6", "4,16,7", "4,32,7"]  # + bit-plane epilogue (sched 6/7)
+            "5,16,6", "5,32,6", "4,16,6", "4,32,6", "4,16,7", "4,32,7",  # + bit-plane epilogue (sched 6/7)
+            "5,16,8"]  # adaptive (sched 8)
 SEG_VARIANTS = {
     8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3",
-         "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7"],
+         "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7", "4,16,8"],
 }
 
 
@@ -491,3 +492,30 @@ def test_sharded_repeated_calls_and_empty_shards(pp, dev, orc):
             shards = [d[cuts[i] * wb: cuts[i + 1] * wb] for i in range(parts)]
             shards.insert(1, d[:0])  # an empty shard
             assert pp.pospopcnt_sharded(shards, [0] * len(shards), k) == want, (k, parts)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+@pytest.mark.parametrize("mode", ["lane", "grouped", "pipelined"])
+def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
+    """The adaptive kernel (sched 8) in each of its modes -- forced through the
+    mean-length thresholds -- on tiny, ragged, empty and large arrays; in lane
+    mode a batch with an array above the lane cap takes the full-warp path."""
+    monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
+    lane, group = {"lane": (1 << 20, 1 << 20), "grouped": (0, 1 << 20), "pipelined": (0, 0)}[mode]
+    monkeypatch.setenv("POSPOP_SEG_LANE_MEAN_BYTES", str(lane))
+    monkeypatch.setenv("POSPOP_SEG_GROUP_MEAN_BYTES", str(group))
+    rng = np.random.default_rng(40 + k)
+    n_words = 1_500_000
+    data = orc.generate(6, 51, n_words * k // 64 + 1).view(DT[k])[:n_words]
+    lens = rng.integers(0, 64, size=6000)
+    lens[rng.random(lens.size) < 0.2] = 0
+    lens[[10, 2000, 5999]] = [40_000, 100_001, 7]  # large arrays among tiny ones
+    offs = np.minimum(np.concatenate([[0], np.cumsum(lens)]), n_words).astype(np.uint64)
+    want = orc.segmented(data, offs, k, threads=8)
+    d = to_dev(data)
+    o = torch.from_numpy(offs.view(np.int64)).cuda()
+    for _ in range(2):  # claim counter and ticket are reset for the next launch
+        out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
+        pp.segmented_async(d, o, out, k)
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy().view(np.uint64) == want).all(), mode
