@@ -461,6 +461,22 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)block);
     cfg.stream = stream;
+    if (var->sched == 8 && nbank == 1 && !env_int("POSPOP_SEG_NO_STAGE", 0)) {
+        // the lane mode stages each warp's 32 rows (k*8 + 16 bytes each) in shared memory
+        cfg.dynamicSmemBytes = (size_t)(block / 32) * 32 * ((size_t)k * 8 + 16);
+        static std::mutex mu;
+        static std::map<std::pair<int, const void*>, size_t> configured;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lock(mu);
+        size_t& have = configured[std::make_pair(dev, reinterpret_cast<const void*>(var->fn))];
+        if (have < cfg.dynamicSmemBytes) {
+            const cudaError_t e = cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)cfg.dynamicSmemBytes);
+            if (e != cudaSuccess) return e;
+            have = cfg.dynamicSmemBytes;
+        }
+    }
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = env_int("POSPOP_PDL", 1) ? 1 : 0;

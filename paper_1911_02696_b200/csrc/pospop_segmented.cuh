@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_
 // ---------------------------------------------------------------------------
 template <int NBANK>
 __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsigned long long* offsets,
-                                               unsigned long long a, int k, unsigned long long* out) {
+                                               unsigned long long a, int k, unsigned long long* row) {
     constexpr int L = NBANK == 1 ? 3 : 2;
     constexpr int REGS = NBANK << L;  // 8 registers = two 16-byte vectors
     constexpr int VPT = REGS / 4;
@@ -670,7 +670,6 @@ __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsign
         }
         tree_block<NBANK, L>(r, carries, counter);
     }
-    unsigned long long* row = out + a * (unsigned long long)k;
 #pragma unroll
     for (int b = 0; b < NBANK; ++b) {
         uint32_t d[16];
@@ -681,21 +680,16 @@ __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsign
             ch[p] = ((counter[b][p] & 0xFFFFu) << L) + (d[p] & 0xFFFFu);
             ch[p + 16] = ((counter[b][p] >> 16) << L) + (d[p] >> 16);
         }
+        // row may be any 8-byte-aligned address (a caller's output rows)
         if (NBANK == 2 || k == 32) {
 #pragma unroll
-            for (int c = 0; c < 32; c += 2)
-                *reinterpret_cast<ulonglong2*>(row + 32 * b + c) = make_ulonglong2(ch[c], ch[c + 1]);
+            for (int c = 0; c < 32; ++c) row[32 * b + c] = ch[c];
         } else if (k == 16) {
 #pragma unroll
-            for (int p = 0; p < 16; p += 2)
-                *reinterpret_cast<ulonglong2*>(row + p) =
-                    make_ulonglong2((unsigned long long)ch[p] + ch[p + 16], (unsigned long long)ch[p + 1] + ch[p + 17]);
+            for (int p = 0; p < 16; ++p) row[p] = (unsigned long long)ch[p] + ch[p + 16];
         } else {  // k == 8: channels p, p+8, p+16, p+24
 #pragma unroll
-            for (int p = 0; p < 8; p += 2)
-                *reinterpret_cast<ulonglong2*>(row + p) =
-                    make_ulonglong2((unsigned long long)ch[p] + ch[p + 8] + ch[p + 16] + ch[p + 24],
-                                    (unsigned long long)ch[p + 1] + ch[p + 9] + ch[p + 17] + ch[p + 25]);
+            for (int p = 0; p < 8; ++p) row[p] = (unsigned long long)ch[p] + ch[p + 8] + ch[p + 16] + ch[p + 24];
         }
     }
 }
@@ -703,13 +697,19 @@ __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsign
 // Lane mode claim loop: batches of 32 consecutive arrays per warp; a batch
 // holding an array above lane_cap_bytes is counted array by array by the
 // whole warp instead.
+// With `stage` (shared memory, k <= 32: 32 rows of k*8 + 16 bytes per warp --
+// the 16-byte pad keeps each quarter-warp's row stores on distinct banks) the
+// warp's 32 rows are written to shared memory first and then copied out as one
+// contiguous block with coalesced 16-byte stores, instead of 32 scattered rows.
 template <int NBANK, int LW, int VBW>
 __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigned long long* offsets,
                                               unsigned long long n_arrays, int k, uint32_t flush_threshold,
                                               unsigned long long* out, unsigned long long* next,
-                                              unsigned long long lane_cap_bytes) {
+                                              unsigned long long lane_cap_bytes, uint8_t* stage) {
     const uint32_t lane = threadIdx.x & 31u;
     const int wb = k >> 3;
+    const int rowb = k * 8 + 16;  // staged row stride, bytes
+    uint8_t* wbuf = stage ? stage + (threadIdx.x >> 5) * 32 * rowb : nullptr;
     unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
     mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
@@ -719,7 +719,29 @@ __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigne
         const unsigned long long a = a0 + lane;
         const unsigned long long nbytes = a < n_arrays ? (offsets[a + 1] - offsets[a]) * wb : 0;
         if (!__any_sync(0xFFFFFFFFu, nbytes > lane_cap_bytes)) {
-            if (a < n_arrays) seg_lane_array<NBANK>(data, offsets, a, k, out);
+            if (wbuf) {
+                if (a < n_arrays)
+                    seg_lane_array<NBANK>(data, offsets, a, k, reinterpret_cast<unsigned long long*>(wbuf + lane * rowb));
+                __syncwarp();
+                const unsigned long long left = n_arrays - a0;
+                const int rows = left < 32 ? (int)left : 32;
+                const int cpr = k / 2;  // 16-byte chunks per row
+                uint8_t* dst = reinterpret_cast<uint8_t*>(out + a0 * (unsigned long long)k);
+                const bool v16 = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;  // else two 8-byte stores
+                for (int i = (int)lane; i < rows * cpr; i += 32) {
+                    const int r = i / cpr, c = i - r * cpr;
+                    const uint4 v = *reinterpret_cast<const uint4*>(wbuf + r * rowb + c * 16);
+                    if (v16) {
+                        *reinterpret_cast<uint4*>(dst + (size_t)i * 16) = v;
+                    } else {
+                        reinterpret_cast<unsigned long long*>(dst)[2 * i] = ((unsigned long long)v.y << 32) | v.x;
+                        reinterpret_cast<unsigned long long*>(dst)[2 * i + 1] = ((unsigned long long)v.w << 32) | v.z;
+                    }
+                }
+                __syncwarp();
+            } else if (a < n_arrays) {
+                seg_lane_array<NBANK>(data, offsets, a, k, out + a * (unsigned long long)k);
+            }
         } else {
             for (int j = 0; j < 32; ++j)
                 if (a0 + j < n_arrays)
@@ -753,7 +775,9 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
     const unsigned long long group_max = (unsigned long long)(thresholds >> 16) * 64;             // mean bytes
     const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
     if (mean <= lane_max) {
-        seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10);
+        extern __shared__ __align__(16) uint8_t seg_stage[];  // launcher: 32 rows per warp for k <= 32, else none
+        seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10,
+                                     NBANK == 1 && k <= 32 ? seg_stage : nullptr);
     } else if (mean <= group_max) {
         constexpr int LG = NBANK == 1 ? 6 : 4;  // grouped-mode tree depth (measured: 6 beats 5 by ~10 % at 1 KiB)
         seg_group_loop<NBANK, LG, 16, 4>(data, offsets, n_arrays, k, flush_threshold, out, next, (256u << 10) / 16);

@@ -519,3 +519,24 @@ def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
         pp.segmented_async(d, o, out, k)
         torch.cuda.synchronize()
         assert (out.cpu().numpy().view(np.uint64) == want).all(), mode
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_segmented_rows_at_8_byte_aligned_output(pp, dev, orc, k):
+    """Row stores (staged lane mode and direct) at an output that is only
+    8-byte aligned; tiny arrays select the lane mode."""
+    rng = np.random.default_rng(70 + k)
+    lens = rng.integers(0, 40, size=3001)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    total = int(offs[-1])
+    data = orc.generate(6, 71, total * k // 64 + 1).view(DT[k])[:total]
+    want = orc.segmented(data, offs, k, threads=4)
+    d = to_dev(data)
+    o = torch.from_numpy(offs.view(np.int64)).cuda()
+    n = offs.size - 1
+    buf = torch.full((n * k + 2,), -1, dtype=torch.int64, device="cuda")
+    out = buf[1:1 + n * k]  # 8-byte aligned, not 16
+    pp.segmented_async(d, o, out, k)
+    torch.cuda.synchronize()
+    assert (out.view(n, k).cpu().numpy().view(np.uint64) == want).all()
+    assert int(buf[0]) == -1 and int(buf[-1]) == -1
