@@ -44,8 +44,9 @@ static double median_us(F f, int reps) {
 
 int main(int argc, char** argv) {
     const int reps = argc > 1 ? std::atoi(argv[1]) : 200;
-    const size_t sizes[] = {1, 64, 1024, 4096, 16384, 32768, 65536, 131072, 262144, 524288, 1048576, 2097152, 4194304};
-    const size_t maxn = 4194304;
+    const size_t sizes[] = {1,       64,      1024,    4096,    16384,    32768,    65536,   131072,
+                            262144,  524288,  1048576, 2097152, 4194304, 8388608, 16777216, 33554432};
+    const size_t maxn = 33554432;
     uint16_t* h = nullptr;
     cudaMallocHost(&h, maxn * 2);
     for (size_t i = 0; i < maxn; ++i) h[i] = (uint16_t)(i * 2654435761u >> 7);
