@@ -423,7 +423,7 @@ def test_segmented_grouped_big_arrays_and_flushes(pp, dev, orc, k, monkeypatch):
 def test_graph_replay_counts_current_contents(pp, dev, orc):
     """CUDA-graph replay (latency path): bit-exact, and it recounts the buffer's
     current contents at every replay."""
-    for k, n_bytes in ((16, 8192), (8, 12345), (64, 1 << 20)):
+    for k, n_bytes in ((16, 8192), (8, 12345), (64, 1 << 20), (32, 5 << 20)):  # small, cluster, stream kernels
         a = orc.generate(6, 40 + k, (n_bytes + 7) // 8).view(np.uint8)[:n_bytes]
         b = orc.generate(6, 80 + k, (n_bytes + 7) // 8).view(np.uint8)[:n_bytes]
         buf = to_dev(a)
