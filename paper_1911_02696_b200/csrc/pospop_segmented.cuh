@@ -239,7 +239,7 @@ __device__ __forceinline__ SegView seg_view(const uint8_t* data, unsigned long l
     return v;
 }
 
-template <int VB, int VPT>
+template <int VB, int VPT, int HINT = 0>
 __device__ __forceinline__ void seg_load(const SegView& v, unsigned long long t, uint32_t lane,
                                          uint32_t (&r)[VPT * (VB / 4)]) {
     constexpr int RPV = VB / 4;
@@ -249,7 +249,7 @@ __device__ __forceinline__ void seg_load(const SegView& v, unsigned long long t,
         for (int q = 0; q < VPT; ++q) {
             uint32_t x[RPV];
             POSPOP_CHECK(t + 32ull * q + lane < v.nv);
-            ldg_stream<VB, 0>(v.base + (t + 32ull * q + lane) * VB, x);
+            ldg_stream<VB, HINT>(v.base + (t + 32ull * q + lane) * VB, x);
 #pragma unroll
             for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
         }
@@ -284,7 +284,7 @@ __device__ __forceinline__ void seg_store_row(unsigned long long* out, unsigned 
     }
 }
 
-template <int NBANK, int L, int VB, int EPI = 0>
+template <int NBANK, int L, int VB, int EPI = 0, int HINT = 0>
 __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const unsigned long long* offsets,
                                                     unsigned long long n_arrays, int k, uint32_t flush_threshold,
                                                     unsigned long long* out) {
@@ -338,7 +338,7 @@ __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const u
 
     unsigned long long t = 0;
     uint32_t rc[REGS];
-    seg_load<VB, VPT>(cur, t, lane, rc);
+    seg_load<VB, VPT, HINT>(cur, t, lane, rc);
     for (;;) {
         // Where the next step is: later in this array, or the next non-empty array.
         unsigned long long t_n = t + STEP, arr_n = arr;
@@ -366,7 +366,7 @@ __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const u
             }
         }
         uint32_t rn[REGS];
-        if (have_next) seg_load<VB, VPT>(nxt, t_n, lane, rn);
+        if (have_next) seg_load<VB, VPT, HINT>(nxt, t_n, lane, rn);
 
         if constexpr (EPI == 1) {
 #pragma unroll
@@ -436,12 +436,12 @@ __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const u
     }
 }
 
-template <int NBANK, int L, int VB, int MINB = 1, int EPI = 0>
+template <int NBANK, int L, int VB, int MINB = 1, int EPI = 0, int HINT = 0>
 __global__ void __launch_bounds__(256, MINB) segmented_pipe_entry(const uint8_t* data, const unsigned long long* offsets,
                                                             unsigned long long n, int k, uint32_t thr,
                                                             unsigned long long* out, unsigned long long*,
                                                             unsigned int*, unsigned) {
-    segmented_pipe_body<NBANK, L, VB, EPI>(data, offsets, n, k, thr, out);
+    segmented_pipe_body<NBANK, L, VB, EPI, HINT>(data, offsets, n, k, thr, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -20,6 +20,8 @@ import torch  # noqa: E402
 import paper_1911_02696_b200 as pp  # noqa: E402
 
 CASES = [("sched6", {"POSPOP_SEG_VARIANT": "5,16,6"}),
+         ("sched9-L2hint", {"POSPOP_SEG_VARIANT": "5,16,9"}),
+         ("sched9-L2hint-d4", {"POSPOP_SEG_VARIANT": "4,16,9"}),
          ("grouped4", {"POSPOP_SEG_VARIANT": "6,16,5,4"}),
          ("auto", {"POSPOP_SEG_VARIANT": "5,16,8"}),
          ("auto:lane", {"POSPOP_SEG_VARIANT": "5,16,8", "POSPOP_SEG_LANE_MEAN_BYTES": "1048576"}),
