@@ -143,7 +143,7 @@ const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched, int gr
     const SegVariant* v = seg_variants(&n);
     for (size_t i = 0; i < n; ++i)
         if (v[i].nbank == nbank && v[i].depth == depth && v[i].vb == vb && v[i].sched == sched &&
-            (sched != 5 || v[i].group == group))
+            ((sched != 5 && sched != 10) || v[i].group == group))
             return &v[i];
     return nullptr;
 }
@@ -461,9 +461,12 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)block);
     cfg.stream = stream;
-    if (var->sched == 8 && nbank == 1 && !env_int("POSPOP_SEG_NO_STAGE", 0)) {
-        // the lane mode stages each warp's 32 rows (k*8 + 16 bytes each) in shared memory
-        cfg.dynamicSmemBytes = (size_t)(block / 32) * 32 * ((size_t)k * 8 + 16);
+    if (var->sched == 10 || (var->sched == 8 && nbank == 1 && !env_int("POSPOP_SEG_NO_STAGE", 0))) {
+        // sched 8: the lane mode stages each warp's 32 rows (k*8 + 16 bytes each);
+        // sched 10: each warp's ring of `group` steps of 32 x VPT 16-byte vectors
+        cfg.dynamicSmemBytes = var->sched == 10
+                                   ? (size_t)(block / 32) * var->group * 32 * ((size_t)(nbank << var->depth) / 4) * 16
+                                   : (size_t)(block / 32) * 32 * ((size_t)k * 8 + 16);
         static std::mutex mu;
         static std::map<std::pair<int, const void*>, size_t> configured;
         int dev = 0;

@@ -445,6 +445,186 @@ __global__ void __launch_bounds__(256, MINB) segmented_pipe_entry(const uint8_t*
 }
 
 // ---------------------------------------------------------------------------
+// Multi-stage cp.async pipeline (SCHED 10): the warp-per-array walk of
+// segmented_pipe_body, but the steps ahead live in a per-warp shared-memory
+// ring of S slots filled with 16-byte cp.async copies (zero-filled past the
+// array), so S-1 steps per warp are in flight without holding registers; the
+// consumer reads its step with LDS.128.  No cross-warp synchronisation: each
+// warp owns its ring (cp.async.wait_group + __syncwarp).
+// ---------------------------------------------------------------------------
+struct SegCursor {
+    unsigned long long arr;  // n_arrays = exhausted
+    unsigned long long t;    // first vector of the step
+    SegView v;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(smem_dst)), "l"(gsrc),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NBANK>
+__device__ __forceinline__ void seg_zero_row(unsigned long long* out, unsigned long long arr, int k, uint32_t lane) {
+    unsigned long long z[NBANK];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) z[b] = 0;
+    seg_store_row<NBANK>(out, arr, k, lane, z);
+}
+
+// First non-empty array at or after `arr` (stride nwarps), zeroing the rows of
+// empty arrays on the way; c.arr = n_arrays when none is left.
+template <int NBANK>
+__device__ __forceinline__ void seg_cursor_seek(SegCursor& c, unsigned long long arr, const uint8_t* data,
+                                                const unsigned long long* offsets, unsigned long long n_arrays,
+                                                unsigned long long nwarps, int k, unsigned long long* out,
+                                                uint32_t lane) {
+    const int wb = k >> 3;
+    for (; arr < n_arrays; arr += nwarps) {
+        c.v = seg_view<16>(data, offsets[arr], offsets[arr + 1], wb);
+        if (c.v.nv) break;
+        seg_zero_row<NBANK>(out, arr, k, lane);
+    }
+    c.arr = arr;
+    c.t = 0;
+}
+
+template <int NBANK, int L, int S>
+__device__ __forceinline__ void segmented_cpasync_body(const uint8_t* data, const unsigned long long* offsets,
+                                                       unsigned long long n_arrays, int k, unsigned long long* out,
+                                                       uint8_t* ring) {
+    constexpr int M = 3;
+    constexpr int REGS = NBANK << L;
+    constexpr int VPT = REGS / 4;                     // 16-byte vectors per lane per step
+    constexpr unsigned long long STEP = 32ull * VPT;  // vectors per step
+    constexpr int SLOT = 32 * VPT * 16;               // bytes per ring slot
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    uint8_t* my = ring + (size_t)(threadIdx.x >> 5) * S * SLOT;
+
+    SegCursor fetch;
+    seg_cursor_seek<NBANK>(fetch, warp, data, offsets, n_arrays, nwarps, k, out, lane);
+    SegCursor desc[S];
+    auto issue = [&](int slot) {  // copy the fetch cursor's step into `slot`, then advance it
+        if (fetch.arr < n_arrays) {
+#pragma unroll
+            for (int q = 0; q < VPT; ++q) {
+                const unsigned long long idx = fetch.t + 32ull * q + lane;
+                const bool in = idx < fetch.v.nv;
+                POSPOP_CHECK(!in || idx < fetch.v.nv);
+                cp_async16(my + slot * SLOT + (32 * q + lane) * 16, fetch.v.base + (in ? idx : 0) * 16, in ? 16u : 0u);
+            }
+        }
+        cp_async_commit();  // one group per step, empty or not, so wait_group counts steps
+        if (fetch.arr < n_arrays) {
+            fetch.t += STEP;
+            if (fetch.t >= fetch.v.nv)
+                seg_cursor_seek<NBANK>(fetch, fetch.arr + nwarps, data, offsets, n_arrays, nwarps, k, out, lane);
+        }
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < S - 1; ++s0) {
+        desc[s0] = fetch;
+        issue(s0);
+    }
+
+    uint32_t carries[NBANK][L];
+    uint32_t U[NBANK][M];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) U[b][i] = 0;
+    }
+    const PlaneXpose xp(lane);
+    uint32_t nb = 0;
+    unsigned long long tot[NBANK];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+
+    for (bool more = true; more;) {
+#pragma unroll
+        for (int slot = 0; slot < S; ++slot) {  // unrolled: slot indices are compile-time
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int ahead = (slot + S - 1) % S;
+            desc[ahead] = fetch;
+            issue(ahead);
+            cp_async_wait<S - 1>();  // this lane's copies of the step in `slot` have landed
+            __syncwarp();            // ... and every other lane's
+            const SegCursor& d = desc[slot];
+            if (d.arr >= n_arrays) {
+                more = false;
+                break;
+            }
+            uint32_t r[REGS];
+#pragma unroll
+            for (int q = 0; q < VPT; ++q) {
+                const unsigned long long idx = d.t + 32ull * q + lane;
+                uint32_t x[4];
+                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3])
+                             : "r"(smem_addr(my + slot * SLOT + (32 * q + lane) * 16)));
+                if (idx == 0 || idx + 1 == d.v.nv) mask_bytes<16>(x, idx == 0 ? d.v.lo : 0, idx + 1 == d.v.nv ? d.v.hi : 16);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) r[q * 4 + j] = x[j];
+            }
+            __syncwarp();  // the slot may be refilled once every lane has read it
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b)
+                plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r) : Tree<L, 2>::run(carries[b], r + b));
+            if (++nb == (1u << M) - 1u) {
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                        U[b][i] = 0;
+                    }
+                nb = 0;
+            }
+            if (d.t + STEP >= d.v.nv) {  // the array's last step: bit-plane epilogue and row store
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b) {
+#pragma unroll
+                    for (int j = 0; j < L; ++j) {
+                        tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
+                        carries[b][j] = 0;
+                    }
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                        U[b][i] = 0;
+                    }
+                }
+                nb = 0;
+                seg_store_row<NBANK>(out, d.arr, k, lane, tot);
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int NBANK, int L, int S>
+__global__ void __launch_bounds__(256, 2) segmented_cpasync_kernel(const uint8_t* data,
+                                                                   const unsigned long long* offsets,
+                                                                   unsigned long long n_arrays, int k, uint32_t,
+                                                                   unsigned long long* out, unsigned long long*,
+                                                                   unsigned int*, unsigned) {
+    extern __shared__ __align__(16) uint8_t seg_ring[];
+    pdl_allow_next();
+    pdl_wait_prev();  // the rows may belong to the previous launch on this stream
+    segmented_cpasync_body<NBANK, L, S>(data, offsets, n_arrays, k, out, seg_ring);
+}
+
+// ---------------------------------------------------------------------------
 // Grouped segmented kernel (SCHED 4): G lanes per array, so one warp counts
 // 32/G arrays at once and the per-array epilogue (drain + reduction + row
 // store) is shared by 32/G arrays instead of paid per array by the whole

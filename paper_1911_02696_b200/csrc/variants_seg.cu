@@ -13,6 +13,8 @@ using namespace dev;
 // sched 6: pipelined, bit-plane epilogue, 2 CTAs/SM; sched 7: the same at 3 CTAs/SM
 #define SGPE(NB, L, VB) {NB, L, VB, 6, segmented_pipe_entry<NB, L, VB, 2, 1>}
 #define SGPE3(NB, L, VB) {NB, L, VB, 7, segmented_pipe_entry<NB, L, VB, 3, 1>}
+// sched 10: multi-stage cp.async ring per warp (group field = ring slots S)
+#define SGC(NB, L, S) {NB, L, 16, 10, segmented_cpasync_kernel<NB, L, S>, S}
 // sched 9: sched 6 with the L2::256B prefetch hint on the 16-byte loads
 #define SGPEH(NB, L) {NB, L, 16, 9, segmented_pipe_entry<NB, L, 16, 2, 1, 2>}
 // sched 8: adaptive (lane / grouped / pipelined chosen on the device from the mean array length)
@@ -21,6 +23,7 @@ using namespace dev;
 #define SGG(NB, L, VB, G) {NB, L, VB, 5, segmented_group_kernel<NB, L, VB, G, 2>, G}
 const SegVariant kVariants[] = {
     SGA(1, 5), SGA(2, 4), SGPEH(1, 5), SGPEH(1, 4), SGPEH(2, 4),
+    SGC(1, 5, 3), SGC(1, 5, 2), SGC(1, 4, 4), SGC(2, 3, 4), SGC(2, 4, 2),
     SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),
     SGPE3(1, 4, 16), SGPE3(1, 4, 32), SGPE3(2, 3, 16),
     SGG(1, 6, 16, 8), SGG(1, 6, 16, 4), SGG(1, 5, 16, 8), SGG(1, 6, 32, 8), SGG(1, 5, 32, 8), SGG(1, 5, 16, 4),
@@ -40,6 +43,7 @@ const SegVariant kVariants[] = {
 #undef SGPE
 #undef SGPE3
 #undef SGPEH
+#undef SGC
 #undef SG
 #undef SGP
 

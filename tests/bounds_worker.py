@@ -76,8 +76,8 @@ def main():
         want_rows = orc.segmented(data, offs, k, threads=4)
         d = torch.from_numpy(data.view(np.uint8).copy()).cuda()
         o = torch.from_numpy(offs.view(np.int64)).cuda()
-        variants = ["5,16,0", "5,16,1", "5,16,3", "5,16,6", "6,16,5,4", "6,16,5,8"] if k < 64 else \
-                   ["5,16,0", "5,16,1", "4,16,6", "4,16,5,8"]
+        variants = ["5,16,0", "5,16,1", "5,16,3", "5,16,6", "6,16,5,4", "6,16,5,8", "5,16,10,2"] if k < 64 else \
+                   ["5,16,0", "5,16,1", "4,16,6", "4,16,5,8", "3,16,10,4"]
         auto = "4,16,8" if k == 64 else "5,16,8"
 
         def seg():

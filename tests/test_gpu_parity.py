@@ -359,13 +359,13 @@ def test_reference_verify_kernels_with_gpu_runner():
 
 _GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4", "6,16,5,16", "5,32,5,4",
             "5,16,6", "5,32,6", "4,16,6", "4,32,6", "4,16,7", "4,32,7",  # + bit-plane epilogue (sched 6/7)
-            "5,16,8", "5,16,9"]  # adaptive (sched 8); L2::256B hint (sched 9)
+            "5,16,8", "5,16,9", "5,16,10,3", "5,16,10,2", "4,16,10,4"]  # sched 8/9/10
 SEG_VARIANTS = {
     8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
     64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3",
-         "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7", "4,16,8"],
+         "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7", "4,16,8", "3,16,10,4", "4,16,10,2"],
 }
 
 

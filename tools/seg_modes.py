@@ -20,8 +20,10 @@ import torch  # noqa: E402
 import paper_1911_02696_b200 as pp  # noqa: E402
 
 CASES = [("sched6", {"POSPOP_SEG_VARIANT": "5,16,6"}),
-         ("sched9-L2hint", {"POSPOP_SEG_VARIANT": "5,16,9"}),
-         ("sched9-L2hint-d4", {"POSPOP_SEG_VARIANT": "4,16,9"}),
+         ("cpasync-d5-s3", {"POSPOP_SEG_VARIANT": "5,16,10,3"}),
+         ("cpasync-d5-s2", {"POSPOP_SEG_VARIANT": "5,16,10,2"}),
+         ("cpasync-d5-s4", {"POSPOP_SEG_VARIANT": "5,16,10,4"}),
+         ("cpasync-d4-s4", {"POSPOP_SEG_VARIANT": "4,16,10,4"}),
          ("grouped4", {"POSPOP_SEG_VARIANT": "6,16,5,4"}),
          ("auto", {"POSPOP_SEG_VARIANT": "5,16,8"}),
          ("auto:lane", {"POSPOP_SEG_VARIANT": "5,16,8", "POSPOP_SEG_LANE_MEAN_BYTES": "1048576"}),
