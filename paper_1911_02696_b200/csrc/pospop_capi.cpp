@@ -12,6 +12,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cerrno>
 #include <condition_variable>
 #include <deque>
@@ -224,6 +225,13 @@ struct Ctx {
     // grow-only device scratch for the synchronous segmented call (data, offsets, rows)
     void* scratch[3] = {};
     size_t scratch_cap[3] = {};
+    // segmented calls on host data: rows come back on their own stream, per
+    // chunk, through a grow-only pinned staging buffer when the caller's rows
+    // are pageable; one event pair per chunk (grow-only pool)
+    cudaStream_t d2h = nullptr;
+    void* rows_pinned = nullptr;
+    size_t rows_pinned_cap = 0;
+    std::vector<cudaEvent_t> seg_ev;
     // pospopcnt_sharded: per shard on this device a stream, a workspace and a
     // mapped pinned result (kept for reuse; no allocation per call)
     struct ShardSlot {
@@ -341,6 +349,26 @@ pospop_status ctx_scratch(Ctx* c, int i, size_t bytes, void** out) {
         c->scratch_cap[i] = bytes;
     }
     *out = c->scratch[i];
+    return POSPOP_OK;
+}
+
+pospop_status ensure_seg_pipeline(Ctx* c, size_t events, size_t pinned_row_bytes) {
+    if (!c->d2h) CU(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    while (c->seg_ev.size() < events) {
+        cudaEvent_t e;
+        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->seg_ev.push_back(e);
+    }
+    if (c->rows_pinned_cap < pinned_row_bytes) {
+        if (c->rows_pinned) {
+            CU(cudaStreamSynchronize(c->d2h));
+            CU(cudaFreeHost(c->rows_pinned));
+            c->rows_pinned = nullptr;
+            c->rows_pinned_cap = 0;
+        }
+        CU(cudaMallocHost(&c->rows_pinned, pinned_row_bytes));
+        c->rows_pinned_cap = pinned_row_bytes;
+    }
     return POSPOP_OK;
 }
 
@@ -509,6 +537,122 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
     return POSPOP_OK;
 }
 
+// Segmented call on host data above kSegPipeMin bytes: the arrays are cut at
+// array boundaries into chunks of about kSegChunk bytes; chunk i's H2D (copy
+// stream), its segmented launch over the chunk's arrays (compute stream) and
+// the D2H of its rows (d2h stream) overlap the neighbouring chunks' work, so
+// the call runs at the H2D link rate instead of H2D + kernel + D2H in series.
+// The device copy of the data keeps the layout of the one-shot path (one
+// scratch buffer for the whole referenced range, same 32-byte phase), so the
+// kernels see exactly the addresses they would see there; a launch's masked
+// edge vectors may touch bytes of a chunk still in flight, which the masks
+// discard.
+constexpr size_t kSegPipeMin = 8u << 20;
+constexpr size_t kSegChunk = 32u << 20;
+
+pospop_status segmented_host_pipeline(Ctx* c, int k, const void* data, const uint64_t* offsets, bool o_dev,
+                                      const uint64_t* hoff, size_t n, uint64_t* counts, bool c_dev) {
+    pospop_status s;
+    const size_t wb = (size_t)k / 8, row_bytes = (size_t)k * sizeof(uint64_t);
+    const uint8_t* src = static_cast<const uint8_t*>(data) + hoff[0] * wb;
+    const size_t bytes = (hoff[n] - hoff[0]) * wb;
+    bool d_pinned = false, c_pinned = false;
+    int hdev = c->dev;
+    classify(data, &hdev, &d_pinned);
+    if (!c_dev) classify(counts, &hdev, &c_pinned);
+    const bool stage_rows = !c_dev && !c_pinned;
+
+    // chunk boundaries (array indices): a chunk ends at the last array
+    // boundary within kSegChunk bytes of its start, and holds >= 1 array
+    std::vector<size_t> cut{0};
+    const size_t chunk_words = kSegChunk / wb;
+    while (cut.back() < n) {
+        const size_t a0 = cut.back();
+        const uint64_t* hi = std::upper_bound(hoff + a0 + 1, hoff + n + 1, hoff[a0] + chunk_words);
+        size_t a1 = (size_t)(hi - hoff) - 1;
+        if (a1 <= a0) a1 = a0 + 1;
+        cut.push_back(a1);
+    }
+    const size_t chunks = cut.size() - 1;
+
+    const size_t pad = reinterpret_cast<uintptr_t>(src) & 31u;
+    void *buf = nullptr, *obuf = nullptr, *rbuf = nullptr;
+    if ((s = ctx_scratch(c, 0, bytes + pad + 64, &buf))) return s;
+    if (!o_dev && (s = ctx_scratch(c, 1, (n + 1) * sizeof(uint64_t), &obuf))) return s;
+    if (!c_dev && (s = ctx_scratch(c, 2, n * row_bytes, &rbuf))) return s;
+    if ((s = ensure_seg_pipeline(c, 2 * chunks, stage_rows ? n * row_bytes : 0))) return s;
+    if (!d_pinned && (s = ensure_host_ring(c))) return s;
+    const uint8_t* ddata = static_cast<const uint8_t*>(buf) + pad - hoff[0] * wb;
+    const unsigned long long* doff = reinterpret_cast<const unsigned long long*>(o_dev ? offsets : obuf);
+    unsigned long long* dout = reinterpret_cast<unsigned long long*>(c_dev ? counts : rbuf);
+    uint8_t* rows_dst = stage_rows ? static_cast<uint8_t*>(c->rows_pinned) : reinterpret_cast<uint8_t*>(counts);
+
+    // everything on the copy/d2h streams is ordered after the caller's prior
+    // legacy-stream work through c->stream, like the one-shot path
+    CU(cudaEventRecord(c->seg_ev[0], c->stream));
+    CU(cudaStreamWaitEvent(c->copy, c->seg_ev[0], 0));
+    CU(cudaStreamWaitEvent(c->d2h, c->seg_ev[0], 0));
+    if (!o_dev)
+        CU(cudaMemcpyAsync(obuf, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, c->copy));
+
+    size_t drained = 0;  // chunks whose staged rows are in `counts`
+    auto drain = [&](bool wait) -> pospop_status {
+        for (; drained < chunks; ++drained) {
+            cudaEvent_t done = c->seg_ev[2 * drained + 1];
+            if (wait) {
+                CU(cudaEventSynchronize(done));
+            } else {
+                const cudaError_t q = cudaEventQuery(done);
+                if (q == cudaErrorNotReady) return POSPOP_OK;
+                CU(q);
+            }
+            const size_t lo = cut[drained] * row_bytes, len = (cut[drained + 1] - cut[drained]) * row_bytes;
+            parallel_copy(reinterpret_cast<uint8_t*>(counts) + lo, rows_dst + lo, len);
+        }
+        return POSPOP_OK;
+    };
+
+    size_t piece = 0;  // host-ring slot counter (pageable data)
+    for (size_t i = 0; i < chunks; ++i) {
+        const size_t a0 = cut[i], a1 = cut[i + 1];
+        const size_t lo = (hoff[a0] - hoff[0]) * wb, hi = (hoff[a1] - hoff[0]) * wb;
+        uint8_t* dst = static_cast<uint8_t*>(buf) + pad;
+        if (d_pinned) {
+            if (hi > lo) CU(cudaMemcpyAsync(dst + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, c->copy));
+        } else {
+            for (size_t off = lo; off < hi; off += kHostChunk, ++piece) {
+                const size_t m = hi - off < kHostChunk ? hi - off : kHostChunk;
+                const int hs = (int)(piece % kHostRing);
+                if (c->host_used[hs]) CU(cudaEventSynchronize(c->ev_h2d[hs]));
+                parallel_copy(c->host_ring[hs], src + off, m);
+                CU(cudaMemcpyAsync(dst + off, c->host_ring[hs], m, cudaMemcpyHostToDevice, c->copy));
+                CU(cudaEventRecord(c->ev_h2d[hs], c->copy));
+                c->host_used[hs] = true;
+            }
+        }
+        CU(cudaEventRecord(c->seg_ev[2 * i], c->copy));
+        CU(cudaStreamWaitEvent(c->stream, c->seg_ev[2 * i], 0));
+        LaunchOptions opt;
+        CU(launch_segmented(k, ddata, doff + a0, a1 - a0, dout + a0 * k, opt, c->ws, c->stream));
+        if (!c_dev) {
+            CU(cudaEventRecord(c->seg_ev[2 * i + 1], c->stream));
+            CU(cudaStreamWaitEvent(c->d2h, c->seg_ev[2 * i + 1], 0));
+            CU(cudaMemcpyAsync(rows_dst + a0 * row_bytes, dout + a0 * k, (a1 - a0) * row_bytes,
+                               cudaMemcpyDeviceToHost, c->d2h));
+            CU(cudaEventRecord(c->seg_ev[2 * i + 1], c->d2h));
+            if (stage_rows && (s = drain(false))) return s;
+        }
+    }
+    if (stage_rows && (s = drain(true))) return s;
+    // the next call may reuse the scratch buffers: c->stream follows the d2h stream
+    if (!c_dev) {
+        CU(cudaEventRecord(c->seg_ev[1], c->d2h));
+        CU(cudaStreamWaitEvent(c->stream, c->seg_ev[1], 0));
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    return POSPOP_OK;
+}
+
 // flagstats.cpp:50-63 (bucket_from_counts): positions of the transformed word.
 void bucket_from_counts(const uint64_t* c, uint64_t total, pospop_flag_bucket* b) {
     b->total = total;
@@ -643,6 +787,9 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
     for (size_t a = 0; a < n; ++a)
         if (hoff[a + 1] < hoff[a]) return fail(POSPOP_EINVAL, "offsets must be non-decreasing (array %zu)", a);
     if (!data && hoff[n] != hoff[0]) return fail(POSPOP_EINVAL, "data is NULL but arrays are non-empty");
+
+    if (!d_dev && (hoff[n] - hoff[0]) * wb > kSegPipeMin)
+        return segmented_host_pipeline(c, k, data, offsets, o_dev, hoff, n, counts, c_dev);
 
     const void* ddata = data;
     if (!d_dev && hoff[n] > hoff[0]) {  // stage the referenced range [offsets[0], offsets[n]) words

@@ -270,6 +270,38 @@ def test_segmented_ragged(pp, dev, orc, k):
 DT = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}
 
 
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_segmented_host_pipeline(pp, dev, orc, k):
+    """Host data above 8 MiB takes the chunked path (H2D / launch / row D2H
+    overlapped, chunks cut at array boundaries): pinned and pageable data,
+    rows in pageable / pinned host memory and on the device, host and device
+    offsets, offsets[0] > 0 at an odd word, empty arrays, one array larger
+    than a chunk and arrays straddling every chunk edge."""
+    wb = k // 8
+    rng = np.random.default_rng(7 + k)
+    n_words = (72 << 20) // wb + 5
+    data = orc.generate(6, 21 + k, n_words * wb // 8 + 1, threads=8).view(DT[k])[:n_words]
+    big_lo = n_words // 3
+    cuts = np.concatenate([rng.integers(3, big_lo, size=5000),
+                           [big_lo, big_lo + (40 << 20) // wb, big_lo + (40 << 20) // wb],  # 40 MiB array + empty
+                           rng.integers(big_lo + (40 << 20) // wb, n_words - 1, size=3000)])
+    offs = np.concatenate([[3], np.sort(cuts), [n_words - 1]]).astype(np.uint64)
+    want = orc.segmented(data, offs, k, threads=8)
+    pinned = torch.empty(data.nbytes, dtype=torch.uint8).pin_memory()
+    pinned.numpy()[:] = data.view(np.uint8)
+    pinned_data = pinned.numpy().view(DT[k])
+    n = offs.size - 1
+    d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+    for src in (data, pinned_data):
+        assert (pp.pospopcnt_segmented(src, offs, k) == want).all()  # pageable rows
+        rows = torch.zeros((n, k), dtype=torch.int64).pin_memory()
+        pp.pospopcnt_segmented(src, d_offs, k, out=rows.numpy().view(np.uint64))  # pinned rows, device offsets
+        assert (rows.numpy().view(np.uint64) == want).all()
+        d_rows = torch.zeros((n, k), dtype=torch.int64, device="cuda")
+        pp.pospopcnt_segmented(src, offs, k, out=d_rows)  # device rows
+        assert (d_rows.cpu().numpy().view(np.uint64) == want).all()
+
+
 # -- generators: device bytes == oracle bytes ------------------------------------------------
 
 def test_device_generators_match_oracle(pp, dev, orc, golden_generators):
