@@ -409,7 +409,7 @@ std::map<std::pair<int, cudaStream_t>, StreamState> g_ws;
 
 pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out, const void* in = nullptr,
                                size_t in_bytes = 0, const void* dst = nullptr, size_t dst_bytes = 0,
-                               bool* no_pdl = nullptr) {
+                               bool* no_pdl = nullptr, const void* in2 = nullptr, size_t in2_bytes = 0) {
     std::lock_guard<std::mutex> lock(g_ws_mu);
     auto key = std::make_pair(dev, s);
     auto it = g_ws.find(key);
@@ -423,8 +423,11 @@ pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out, co
     if (no_pdl) {
         const uintptr_t lo = reinterpret_cast<uintptr_t>(in), hi = lo + in_bytes;
         *no_pdl = false;
-        for (int i = 0; i < StreamState::kHist; ++i)
+        const uintptr_t lo2 = reinterpret_cast<uintptr_t>(in2), hi2 = lo2 + in2_bytes;
+        for (int i = 0; i < StreamState::kHist; ++i) {
             if (in_bytes && st.out_hi[i] > lo && st.out_lo[i] < hi) *no_pdl = true;
+            if (in2_bytes && st.out_hi[i] > lo2 && st.out_lo[i] < hi2) *no_pdl = true;
+        }
         if (dst) {
             st.out_lo[st.next] = reinterpret_cast<uintptr_t>(dst);
             st.out_hi[st.next] = reinterpret_cast<uintptr_t>(dst) + dst_bytes;
@@ -433,6 +436,27 @@ pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out, co
     }
     *out = st.ws;
     return POSPOP_OK;
+}
+
+// The device allocation holding `p` (cuMemGetAddressRange through the runtime's
+// driver entry point): the bound on what a kernel indexing from `p` with
+// device-resident offsets can read.  False if it cannot be determined.
+bool alloc_range(const void* p, const void** base, size_t* bytes) {
+    using Fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<Fn>(f);
+    }();
+    unsigned long long b = 0;
+    size_t n = 0;
+    if (!fn || !p || fn(&b, &n, reinterpret_cast<unsigned long long>(p)) != 0) return false;
+    *base = reinterpret_cast<const void*>(b);
+    *bytes = n;
+    return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1272,8 +1296,15 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     StreamWorkspace ws;
     LaunchOptions opt;
-    bool unused = false;  // segmented kernels wait for the previous launch before reading anything
-    if ((s = stream_workspace(dev, st, &ws, nullptr, 0, d_counts, n * (size_t)k * 8, &unused))) return s;
+    // The default kernel reads (offsets and data) before waiting for the
+    // previous launch on the stream, so programmatic dependent launch is
+    // dropped when either allocation may hold a recent launch's output.
+    const void *dbase = nullptr, *obase = nullptr;
+    size_t dbytes = 0, obytes = 0;
+    const bool known = (!d_data || alloc_range(d_data, &dbase, &dbytes)) && (!n || alloc_range(d_offsets, &obase, &obytes));
+    if ((s = stream_workspace(dev, st, &ws, dbase, dbytes, d_counts, n * (size_t)k * 8, &opt.no_pdl, obase, obytes)))
+        return s;
+    if (!known) opt.no_pdl = true;
     opt.flush_threshold = flush;
     opt.grid = grid;
     opt.block = block;

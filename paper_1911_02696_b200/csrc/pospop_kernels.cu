@@ -143,7 +143,7 @@ const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched, int gr
     const SegVariant* v = seg_variants(&n);
     for (size_t i = 0; i < n; ++i)
         if (v[i].nbank == nbank && v[i].depth == depth && v[i].vb == vb && v[i].sched == sched &&
-            ((sched != 5 && sched != 10) || v[i].group == group))
+            ((sched != 5 && sched != 10 && sched < 11) || v[i].group == group))
             return &v[i];
     return nullptr;
 }
@@ -419,6 +419,7 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
 // 256-word arrays G=4 4269 vs lane 2173; 1024 words G=4 ~ pipelined).
 constexpr int kSegLaneMeanBytes = 512;
 constexpr int kSegGroupMeanBytes = 2048;
+constexpr int kSegTileMeanBytes = 8192;  // tile mode above this mean (tools/seg_vs_stream.py)
 
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets, size_t n,
                              unsigned long long* d_out, const LaunchOptions& opt, const StreamWorkspace& ws,
@@ -452,10 +453,14 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     unsigned extra = (unsigned)env_int("POSPOP_SEG_PER_GRAB", 1);
     if (extra < 1) extra = 1;
     if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
-    if (var->sched == 8) {  // mean-length thresholds, in 64-byte units (<= 4 MiB), for the lane and grouped modes
-        auto units = [](int bytes) { return (unsigned)(bytes < 0 ? 0 : (bytes / 64 > 0xFFFF ? 0xFFFF : bytes / 64)); };
-        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes)) |
-                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes)) << 16);
+    if (var->sched >= 11) extra = (unsigned)env_int("POSPOP_SEG_TAIL_ROUNDS", 4);  // tile kernels: dynamic tail
+    if (var->sched == 8) {  // mean-length thresholds in 64-byte units: lane / grouped mode (<= 64 KiB), tile mode
+        auto units = [](int bytes, unsigned cap) {
+            return (unsigned)(bytes < 0 ? 0 : ((unsigned)bytes / 64 > cap ? cap : (unsigned)bytes / 64));
+        };
+        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes), 0x3FF) |
+                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 0x3FF) << 10) |
+                (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 0xFFF) << 20);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -482,7 +487,7 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     }
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = env_int("POSPOP_PDL", 1) ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = !opt.no_pdl && env_int("POSPOP_PDL", 1) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, var->fn, static_cast<const uint8_t*>(data), d_offsets,

@@ -933,12 +933,228 @@ __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigne
 }
 
 // ---------------------------------------------------------------------------
-// Adaptive segmented kernel (SCHED 8, the asynchronous entry point's default
-// for k <= 32): every CTA reads offsets[0] and offsets[n] and picks, from the
-// mean array length, one lane per array (tiny arrays), G = 4 lanes per array
-// (short arrays) or the software-pipelined warp-per-array kernel with the
-// bit-plane epilogue -- the same choice for the whole grid, made on the
-// device, so device-resident offsets need no host round trip.
+// Warp-per-array tiles (SCHED 11): the stream kernel's shape applied to
+// arrays.  A step is one full-depth tree block per lane (2^L registers, e.g.
+// 16 x 32-byte loads at L = 7: 16 KiB per warp, one cfg5 u32 array), issued
+// all at once and consumed once it lands; latency is hidden by the other
+// warps of the SM, not by a register double buffer, so a deeper tree fits and
+// no registers are copied between steps.  The warp's next array offsets are
+// fetched one array ahead.  Counts are kept as bit planes (tree carries + a
+// 3-plane tops counter, folded every 7 blocks) and reduced with the warp bit
+// transpose (PlaneXpose), as in the pipelined kernel's EPI 1.
+// ---------------------------------------------------------------------------
+// Array order of one warp: `arr`, arr + stride, ... while below static_end,
+// then (dyn) single arrays claimed from the global counter `next` -- the last
+// rounds go to whichever warps finish first.  Claims are made one array ahead
+// (the following array's bounds are prefetched with it), and only after the
+// previous launch has completed (the counter is shared with it).
+struct TileCursor {
+    unsigned long long stride, static_end, n;
+    unsigned long long* next;
+    bool dyn;
+    __device__ __forceinline__ bool claims(unsigned long long a) const { return dyn && a + stride >= static_end; }
+    __device__ __forceinline__ unsigned long long following(unsigned long long a, uint32_t lane) const {
+        if (a + stride < static_end) return a + stride;
+        if (!dyn) return a + stride < n ? a + stride : n;
+        unsigned long long c = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+        c = __shfl_sync(0xFFFFFFFFu, c, 0);
+        return static_end + c < n ? static_end + c : n;
+    }
+};
+
+// EARLY: everything before the first row store -- reading the offsets and
+// data and counting the first array -- overlaps the previous launch on the
+// stream (programmatic dependent launch); the first row store, the first
+// dynamic claim and the warp's exit wait for it, so global rows (and the
+// claim counter) are only touched after the previous launch has completed.
+// (Parking the rows finished before the wait in shared memory, so that the
+// warp need not wait at its first store, measured slower: the carve-out it
+// takes shrinks the L1 that stages the in-flight loads.)
+template <int NBANK, int L, int VB, bool EARLY = false>
+__device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigned long long* offsets,
+                                              unsigned long long n_arrays, int k, unsigned long long* out,
+                                              unsigned long long arr, const TileCursor& cur) {
+    constexpr int M = 3;
+    constexpr int REGS = NBANK << L;
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr unsigned long long STEP = 32ull * VPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const int wb = k >> 3;
+    const PlaneXpose xp(lane);
+    bool waited = !EARLY;
+    auto ensure_waited = [&]() {
+        if (!waited) {
+            pdl_wait_prev();
+            waited = true;
+        }
+    };
+    auto store = [&](unsigned long long a, const unsigned long long (&tot)[NBANK]) {
+        ensure_waited();
+        seg_store_row<NBANK>(out, a, k, lane, tot);
+    };
+    auto next_of = [&](unsigned long long a) {
+        if (cur.claims(a)) ensure_waited();  // the claim counter belongs to the previous launch until it completes
+        return cur.following(a, lane);
+    };
+    const unsigned long long zero[NBANK] = {};
+    if (arr >= cur.static_end) arr = next_of(cur.static_end - cur.stride);  // this warp has no static array
+    // The loads of the next step -- later in this array or the first step of
+    // the warp's next non-empty array -- are issued as soon as the tree has
+    // consumed the registers, before the array's epilogue runs, so the warp
+    // keeps its memory requests in flight across array boundaries.
+    SegView v;
+    for (;; arr = next_of(arr)) {  // first non-empty array
+        if (arr >= n_arrays) {
+            ensure_waited();
+            return;
+        }
+        v = seg_view<VB>(data, offsets[arr], offsets[arr + 1], wb);
+        if (v.nv) break;
+        store(arr, zero);
+    }
+    unsigned long long nxt = next_of(arr), w0 = 0, w1 = 0;  // the array after it, bounds prefetched
+    if (nxt < n_arrays) {
+        w0 = offsets[nxt];
+        w1 = offsets[nxt + 1];
+    }
+    uint32_t carries[NBANK][L], U[NBANK][M];
+    unsigned long long tot[NBANK];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) U[b][i] = 0;
+        tot[b] = 0;
+    }
+    uint32_t nb = 0;
+    unsigned long long t = 0;
+    uint32_t r[REGS];
+    seg_load<VB, VPT>(v, t, lane, r);
+    for (;;) {
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b)
+            plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r) : Tree<L, 2>::run(carries[b], r + b));
+        ++nb;
+        t += STEP;
+        const bool array_done = t >= v.nv;
+        unsigned long long arr_n = arr;
+        SegView vn = v;
+        bool more = true;
+        if (array_done) {  // the warp's next non-empty array (rows of empty ones are zeroed on the way)
+            t = 0;
+            more = false;
+            while (nxt < n_arrays) {
+                arr_n = nxt;
+                vn = seg_view<VB>(data, w0, w1, wb);
+                nxt = next_of(arr_n);
+                if (nxt < n_arrays) {
+                    w0 = offsets[nxt];
+                    w1 = offsets[nxt + 1];
+                }
+                if (vn.nv) {
+                    more = true;
+                    break;
+                }
+                store(arr_n, zero);
+            }
+        }
+        if (more) seg_load<VB, VPT>(vn, t, lane, r);  // in flight during the fold / epilogue below
+        if (array_done || nb == (1u << M) - 1u) {  // warp-uniform: the step count is per array
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                    U[b][i] = 0;
+                }
+            nb = 0;
+        }
+        if (array_done) {
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) {
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
+                    carries[b][j] = 0;
+                }
+            }
+            store(arr, tot);
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+            if (!more) {
+                ensure_waited();
+                return;
+            }
+            arr = arr_n;
+            v = vn;
+        }
+    }
+}
+
+// Grid-strided tile schedule: warp w of the grid takes arrays w, w + nwarps,
+// ... (the whole GPU sweeps one window of consecutive arrays); with DYN the
+// last `tail_rounds` rounds are claimed dynamically from `next`.
+template <int NBANK, int L, int VB, bool EARLY, bool DYN>
+__device__ __forceinline__ void seg_tile_strided(const uint8_t* data, const unsigned long long* offsets,
+                                                 unsigned long long n_arrays, int k, unsigned long long* out,
+                                                 unsigned long long* next, unsigned tail_rounds) {
+    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    const unsigned long long rounds = n_arrays / nwarps;
+    TileCursor cur;
+    cur.next = next;
+    cur.dyn = DYN;
+    cur.stride = nwarps;
+    cur.n = n_arrays;
+    cur.static_end = DYN ? (rounds > tail_rounds ? rounds - tail_rounds : 0) * nwarps : n_arrays;
+    seg_tile_loop<NBANK, L, VB, EARLY>(data, offsets, n_arrays, k, out, warp, cur);
+}
+
+// MODE bit 0: CTA c takes the contiguous array range [c n / G, (c + 1) n / G)
+// and its warps stride over it (one DRAM region per SM, like the stream
+// kernel's CTA ranges; measured slower than the strided order); otherwise
+// seg_tile_strided.  Bit 1 (EARLY): reading and counting start before the
+// previous launch on the stream has completed (see seg_tile_loop; the
+// launcher drops programmatic dependent launch when the input may be that
+// launch's output).  Bit 2 (DYN, strided only): a dynamic tail.
+template <int NBANK, int L, int VB, int MINB, int MODE>
+__global__ void __launch_bounds__(256, MINB) segmented_tile_kernel(const uint8_t* data,
+                                                                   const unsigned long long* offsets,
+                                                                   unsigned long long n_arrays, int k, uint32_t,
+                                                                   unsigned long long* out, unsigned long long* next,
+                                                                   unsigned int* ticket, unsigned tail_rounds) {
+    constexpr bool EARLY = (MODE & 2) != 0;
+    constexpr bool DYN = (MODE & 4) != 0 && (MODE & 1) == 0;
+    pdl_allow_next();
+    if (!EARLY) pdl_wait_prev();  // the rows may belong to the previous launch on this stream
+    if constexpr (MODE & 1) {
+        const unsigned long long lo = n_arrays * blockIdx.x / gridDim.x;
+        const unsigned long long hi = n_arrays * (blockIdx.x + 1) / gridDim.x;
+        TileCursor cur;
+        cur.next = next;
+        cur.dyn = false;
+        cur.stride = blockDim.x >> 5;
+        cur.static_end = cur.n = hi;
+        seg_tile_loop<NBANK, L, VB, EARLY>(data, offsets, hi, k, out, lo + (threadIdx.x >> 5), cur);
+    } else {
+        seg_tile_strided<NBANK, L, VB, EARLY, DYN>(data, offsets, n_arrays, k, out, next, tail_rounds);
+    }
+    if constexpr (DYN) seg_claims_done(next, ticket);  // every warp has waited (seg_tile_loop exits after the wait)
+}
+
+// ---------------------------------------------------------------------------
+// Adaptive segmented kernel (SCHED 8, the asynchronous entry point's default):
+// every CTA reads offsets[0] and offsets[n] and picks, from the mean array
+// length, one lane per array (tiny arrays), G = 4 lanes per array (short
+// arrays), the software-pipelined warp-per-array kernel with the bit-plane
+// epilogue (medium arrays) or the warp-per-array tiles with a dynamic tail
+// (long arrays, cfg5) -- the same choice for the whole grid, made on the
+// device, so device-resident offsets need no host round trip.  The tile mode
+// starts counting before the previous launch on the stream has completed.
+// `thresholds`: mean-length bounds in 64-byte units, lane mode bits 0-9,
+// grouped mode bits 10-19, tile mode (above) bits 20-31.
 // ---------------------------------------------------------------------------
 template <int NBANK>
 __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* data,
@@ -949,11 +1165,19 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
                                                                 unsigned thresholds) {
     constexpr int LW = NBANK == 1 ? 5 : 4;  // full-warp fallback tree depth
     pdl_allow_next();
-    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     const int wb = k >> 3;
-    const unsigned long long lane_max = (unsigned long long)(thresholds & 0xFFFFu) * 64;         // mean bytes
-    const unsigned long long group_max = (unsigned long long)(thresholds >> 16) * 64;             // mean bytes
+    const unsigned long long lane_max = (unsigned long long)(thresholds & 0x3FFu) * 64;         // mean bytes
+    const unsigned long long group_max = (unsigned long long)((thresholds >> 10) & 0x3FFu) * 64;
+    const unsigned long long tile_min = (unsigned long long)(thresholds >> 20) * 64;
     const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
+    if (mean > tile_min && mean > group_max) {
+        // depth 5 per bank over 16-byte loads: 4 KiB (k <= 32) / 8 KiB (k = 64) steps per warp (measured
+        // best at two CTAs per SM: tools/seg_vs_stream.py)
+        seg_tile_strided<NBANK, 5, 16, true, true>(data, offsets, n_arrays, k, out, next, 4u);
+        seg_claims_done(next, ticket);  // every warp has waited
+        return;
+    }
+    pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     if (mean <= lane_max) {
         extern __shared__ __align__(16) uint8_t seg_stage[];  // launcher: 32 rows per warp for k <= 32, else none
         seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10,
@@ -963,7 +1187,7 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
         seg_group_loop<NBANK, LG, 16, 4>(data, offsets, n_arrays, k, flush_threshold, out, next, (256u << 10) / 16);
     } else if constexpr (NBANK == 1) {
         segmented_pipe_body<NBANK, LW, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out);
-    } else {  // k = 64: dynamic array claims measure best
+    } else {  // k = 64: dynamic array claims
         seg_warp_loop<NBANK, 5, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out, next, 1u);
     }
     seg_claims_done(next, ticket);

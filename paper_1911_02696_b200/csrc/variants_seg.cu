@@ -19,10 +19,24 @@ using namespace dev;
 #define SGPEH(NB, L) {NB, L, 16, 9, segmented_pipe_entry<NB, L, 16, 2, 1, 2>}
 // sched 8: adaptive (lane / grouped / pipelined chosen on the device from the mean array length)
 #define SGA(NB, L) {NB, L, 16, 8, segmented_auto_kernel<NB>}
+// sched 11: warp-per-array tiles, not pipelined (group field = CTAs per SM)
+#define SGT(NB, L, VB, MB) {NB, L, VB, 11, segmented_tile_kernel<NB, L, VB, MB, 0>, MB}
+// sched 13: sched 11 reading its first array before waiting for the previous launch
+#define SGTE(NB, L, VB, MB) {NB, L, VB, 13, segmented_tile_kernel<NB, L, VB, MB, 2>, MB}
+// sched 14: sched 13 with the last rounds of arrays claimed dynamically
+#define SGTD(NB, L, VB, MB) {NB, L, VB, 14, segmented_tile_kernel<NB, L, VB, MB, 6>, MB}
+// sched 12: the same with one contiguous array range per CTA
+#define SGTB(NB, L, VB, MB) {NB, L, VB, 12, segmented_tile_kernel<NB, L, VB, MB, 1>, MB}
 // sched 5: grouped, G lanes per array, 2 CTAs/SM
 #define SGG(NB, L, VB, G) {NB, L, VB, 5, segmented_group_kernel<NB, L, VB, G, 2>, G}
 const SegVariant kVariants[] = {
-    SGA(1, 5), SGA(2, 4), SGPEH(1, 5), SGPEH(1, 4), SGPEH(2, 4),
+    SGA(1, 5), SGA(2, 4),
+    SGT(1, 7, 32, 1), SGT(1, 7, 16, 1), SGT(1, 6, 32, 1), SGT(1, 6, 32, 2), SGT(1, 6, 16, 2), SGT(1, 5, 32, 2),
+    SGT(2, 6, 32, 1), SGT(2, 5, 32, 1), SGT(2, 5, 32, 2), SGT(2, 5, 16, 2),
+    SGTE(1, 7, 32, 1), SGTE(1, 6, 32, 1), SGTE(1, 6, 32, 2), SGTE(2, 6, 32, 1),
+    SGTD(1, 7, 32, 1), SGTD(1, 6, 32, 1), SGTD(1, 6, 32, 2), SGTD(2, 6, 32, 1), SGTD(2, 5, 32, 2), SGTD(2, 5, 16, 2),
+    SGTD(1, 6, 16, 2), SGTD(1, 5, 16, 2), SGTD(1, 5, 32, 2),
+    SGTB(1, 7, 32, 1), SGTB(1, 6, 32, 1), SGTB(1, 6, 32, 2), SGTB(2, 6, 32, 1), SGTB(2, 5, 32, 2), SGPEH(1, 5), SGPEH(1, 4), SGPEH(2, 4),
     SGC(1, 5, 3), SGC(1, 5, 2), SGC(1, 4, 4), SGC(2, 3, 4), SGC(2, 4, 2),
     SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),
     SGPE3(1, 4, 16), SGPE3(1, 4, 32), SGPE3(2, 3, 16),
@@ -39,6 +53,10 @@ const SegVariant kVariants[] = {
 #undef SGP2
 #undef SGP3
 #undef SGG
+#undef SGT
+#undef SGTB
+#undef SGTE
+#undef SGTD
 #undef SGA
 #undef SGPE
 #undef SGPE3

@@ -392,12 +392,15 @@ def test_reference_verify_kernels_with_gpu_runner():
 _GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4", "6,16,5,16", "5,32,5,4",
             "5,16,6", "5,32,6", "4,16,6", "4,32,6", "4,16,7", "4,32,7",  # + bit-plane epilogue (sched 6/7)
             "5,16,8", "5,16,9", "5,16,10,3", "5,16,10,2", "4,16,10,4"]  # sched 8/9/10
+_TILE = ["7,32,11,1", "7,16,11,1", "6,32,11,1", "6,32,11,2", "6,16,11,2", "5,32,11,2", "7,32,12,1", "6,32,12,1",
+         "6,32,12,2", "7,32,13,1", "6,32,13,2", "7,32,14,1", "6,32,14,1", "6,32,14,2"]
 SEG_VARIANTS = {
-    8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
-    16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
-    32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED,
+    8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
+    16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
+    32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
     64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3",
-         "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7", "4,16,8", "3,16,10,4", "4,16,10,2"],
+         "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7", "4,16,8", "3,16,10,4", "4,16,10,2",
+         "6,32,11,1", "5,32,11,1", "5,32,11,2", "5,16,11,2", "6,32,12,1", "5,32,12,2", "6,32,13,1", "6,32,14,1"],
 }
 
 
@@ -498,6 +501,48 @@ def test_chained_async_launches_read_the_previous_output(pp, dev, orc):
         assert (out2.cpu().numpy().astype(np.uint64) == np.asarray(orc.pospopcnt(rows.ravel(), 64), np.uint64)).all()
 
 
+@pytest.mark.parametrize("var", ["", "7,32,13,1", "7,32,14,1", "6,32,14,2"])
+def test_chained_segmented_launches(pp, dev, orc, var, monkeypatch):
+    """Segmented kernels that read (and count) before waiting for the previous
+    launch on the stream: a segmented input produced by the previous launch
+    (RAW: programmatic dependent launch dropped), rows overwritten by the next
+    launch (WAW) and rows written over the previous launch's input (WAR) --
+    rows reach global memory only after the previous launch completed."""
+    if var:
+        monkeypatch.setenv("POSPOP_SEG_VARIANT", var)
+    s = torch.cuda.current_stream()
+    k, arrays, words = 32, 8192, 4096
+    a = orc.generate(5, 61, arrays * words)  # u32 words
+    b = orc.generate(5, 62, arrays * words)
+    da, db = (torch.from_numpy(x.view(np.int64).copy()).cuda() for x in (a, b))
+    offs = torch.arange(arrays + 1, dtype=torch.int64, device="cuda") * words
+    want_b = orc.segmented(b, offs.cpu().numpy().view(np.uint64), k, threads=8)
+    rows = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
+    small_offs = torch.tensor([0, 3, 16], dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    for trial in range(10):
+        # WAW: the second launch's rows win
+        pp.segmented_async(da, offs, rows, k, stream=s)
+        pp.segmented_async(db, offs, rows, k, stream=s)
+        # RAW: the previous launch's rows as the next segmented input (k = 64 words)
+        rows2 = torch.empty((2, 64), dtype=torch.int64, device="cuda")
+        pp.segmented_async(rows, small_offs, rows2, 64, stream=s)
+        torch.cuda.synchronize()
+        got = rows.cpu().numpy().view(np.uint64)
+        assert (got == want_b).all(), trial
+        w64 = got.ravel()[:16]
+        want2 = orc.segmented(w64, np.array([0, 3, 16], np.uint64), 64)
+        assert (rows2.cpu().numpy().view(np.uint64) == want2).all(), trial
+        # WAR: a count reading `victim`, then rows written over it
+        victim = torch.from_numpy(a.view(np.int64).copy()).cuda()
+        pp.count_async(victim, cnt, 16, stream=s)
+        pp.segmented_async(db, offs, victim[:arrays * k].view(arrays, k), k, stream=s)
+        torch.cuda.synchronize()
+        assert (cnt.cpu().numpy().view(np.uint64) == np.asarray(orc.pospopcnt(a.view(np.uint16), 16, threads=8),
+                                                                np.uint64)).all(), trial
+        assert (victim[:arrays * k].view(arrays, k).cpu().numpy().view(np.uint64) == want_b).all()
+
+
 def test_k_widths_against_reference_fixtures(pp, dev, orc, golden):
     """The GPU on the k = 8/32/64 fixtures counted by the reference library's
     16-bit API (golden k_widths), at the fixture's byte offset inside 0xFF guards."""
@@ -527,15 +572,17 @@ def test_sharded_repeated_calls_and_empty_shards(pp, dev, orc):
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-@pytest.mark.parametrize("mode", ["lane", "grouped", "pipelined"])
+@pytest.mark.parametrize("mode", ["lane", "grouped", "pipelined", "tile"])
 def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
     """The adaptive kernel (sched 8) in each of its modes -- forced through the
     mean-length thresholds -- on tiny, ragged, empty and large arrays; in lane
     mode a batch with an array above the lane cap takes the full-warp path."""
     monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
-    lane, group = {"lane": (1 << 20, 1 << 20), "grouped": (0, 1 << 20), "pipelined": (0, 0)}[mode]
+    lane, group, tile = {"lane": (1 << 20, 1 << 20, 1 << 20), "grouped": (0, 1 << 20, 1 << 20),
+                         "pipelined": (0, 0, 1 << 20), "tile": (0, 0, 0)}[mode]
     monkeypatch.setenv("POSPOP_SEG_LANE_MEAN_BYTES", str(lane))
     monkeypatch.setenv("POSPOP_SEG_GROUP_MEAN_BYTES", str(group))
+    monkeypatch.setenv("POSPOP_SEG_TILE_MEAN_BYTES", str(tile))
     rng = np.random.default_rng(40 + k)
     n_words = 1_500_000
     data = orc.generate(6, 51, n_words * k // 64 + 1).view(DT[k])[:n_words]
