@@ -420,6 +420,9 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
 constexpr int kSegLaneMeanBytes = 512;
 constexpr int kSegGroupMeanBytes = 2048;
 constexpr int kSegTileMeanBytes = 8192;  // tile mode above this mean (tools/seg_vs_stream.py)
+constexpr int kSegRangeRounds = 4;       // range mode below this many arrays per warp
+static_assert(dev::kSegRangeSlots == kSegRangeSlotsHost && kAccChannels + 1 + 7 == 104,
+              "range-mode slots: workspace layout (pospop_launch.h) and dev::seg_range_slots disagree");
 
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets, size_t n,
                              unsigned long long* d_out, const LaunchOptions& opt, const StreamWorkspace& ws,
@@ -446,7 +449,8 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
         // measured (r01 sweep): 4 CTAs/SM for the strided schedule, one resident wave otherwise
         const int per_sm = env_int("POSPOP_SEG_BLOCKS_PER_SM", var->sched == 0 ? 4 : resident_blocks(var->fn, block));
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
-        grid = (int)(want < cap ? want : cap);
+        // the adaptive kernel's range mode and the range kernel spread few arrays over every warp
+        grid = (int)(want < cap && var->sched != 8 && var->sched != 16 ? want : cap);
     }
     // Last argument: SCHED 1 arrays per grab; SCHED 5 the vector count above
     // which a batch is counted one array at a time by the whole warp.
@@ -454,13 +458,15 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (extra < 1) extra = 1;
     if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
     if (var->sched >= 11) extra = (unsigned)env_int("POSPOP_SEG_TAIL_ROUNDS", 4);  // tile kernels: dynamic tail
-    if (var->sched == 8) {  // mean-length thresholds in 64-byte units: lane / grouped mode (<= 64 KiB), tile mode
-        auto units = [](int bytes, unsigned cap) {
-            return (unsigned)(bytes < 0 ? 0 : ((unsigned)bytes / 64 > cap ? cap : (unsigned)bytes / 64));
+    if (var->sched == 8) {  // mode bounds, 8 bits each: lane / grouped mean (64 B units), tile mean (256 B units),
+                            // range-mode rounds (arrays per warp below which the bytes are split evenly)
+        auto units = [](int v, unsigned unit) {
+            return (unsigned)(v < 0 ? 0 : ((unsigned)v / unit > 0xFF ? 0xFF : (unsigned)v / unit));
         };
-        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes), 0x3FF) |
-                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 0x3FF) << 10) |
-                (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 0xFFF) << 20);
+        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes), 64) |
+                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 64) << 8) |
+                (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 256) << 16) |
+                (units(env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds), 1) << 24);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);

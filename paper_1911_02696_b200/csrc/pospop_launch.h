@@ -20,10 +20,13 @@ struct StreamWorkspace {
     unsigned long long* bad = nullptr;   // FLAG mode: ~(first invalid word index), 0 = none
 };
 
-// Bytes of one workspace allocation: acc[96], ticket (u32 at +768), next (u64
-// at +776), bad (u64 at +784).
+// Bytes of one workspace allocation (u64 units): acc[0, 96), ticket (u32 at
+// u64 96), next (97), bad (98), then from u64 104 the segmented range mode's
+// kSegRangeSlots slots of 64 partial counts + 1 piece counter
+// (dev::seg_range_slots: `next` + 7).  Zero between launches.
 constexpr int kAccChannels = 96;
-constexpr size_t kWorkspaceBytes = kAccChannels * sizeof(unsigned long long) + 64;
+constexpr int kSegRangeSlotsHost = 4096;
+constexpr size_t kWorkspaceBytes = (104 + (size_t)kSegRangeSlotsHost * 65) * sizeof(unsigned long long);
 
 struct LaunchOptions {
     uint32_t flush_threshold = 65535;  // tree blocks between lane flushes, [1, 65535]

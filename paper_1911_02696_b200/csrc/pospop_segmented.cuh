@@ -1112,6 +1112,245 @@ __device__ __forceinline__ void seg_tile_strided(const uint8_t* data, const unsi
     seg_tile_loop<NBANK, L, VB, EARLY>(data, offsets, n_arrays, k, out, warp, cur);
 }
 
+// ---------------------------------------------------------------------------
+// Range mode (few or huge arrays): the referenced bytes [data + off[0]*wb,
+// data + off[n]*wb) are split into one contiguous, 16-byte-aligned range per
+// warp (equal bytes), so an array of any size is spread over as many warps as
+// it covers.  A warp finds the first array touching its range with a 32-ary
+// warp search over the offsets, then walks the arrays of its range in order
+// (the tile mode's step / load-before-epilogue loop).  An array inside the
+// range gets its row stored; an array spanning ranges adds its partial counts
+// into the slot of the range holding its first byte (u64 atomics into the
+// workspace), and the warp whose piece completes the array (a piece counter
+// per slot) moves the slot into the row with atomicExch, leaving the slot zero
+// for the next launch.  Empty arrays are written by the warp owning their
+// position.  Starts before the previous launch completes (EARLY semantics).
+// ---------------------------------------------------------------------------
+constexpr int kSegRangeSlots = 4096;   // = kSegRangeSlotsHost (pospop_launch.h)
+__device__ __forceinline__ unsigned long long* seg_range_slots(unsigned long long* next) { return next + 7; }
+
+struct RangeSplit {
+    unsigned long long base, total;  // byte positions relative to data: [base, base + total)
+    unsigned long long W;            // ranges (warps taking part)
+    // Start of range w (w <= W), 16-byte aligned in absolute address for w >= 1.
+    __device__ __forceinline__ unsigned long long start(unsigned long long w) const {
+        if (w >= W) return base + total;
+        return base + (((total * w) / W) & ~15ull);
+    }
+    // The range holding position p (base <= p < base + total); empty ranges hold none.
+    __device__ __forceinline__ unsigned long long owner(unsigned long long p) const {
+        unsigned long long w = total ? (p - base) * W / total : 0;
+        if (w >= W) w = W - 1;
+        while (w > 0 && start(w) > p) --w;
+        while (w + 1 < W && start(w + 1) <= p) ++w;
+        return w;
+    }
+};
+
+template <int NBANK, int L, int VB>
+__device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsigned long long* offsets,
+                                               unsigned long long n_arrays, int k, unsigned long long* out,
+                                               unsigned long long* next) {
+    constexpr int M = 3;
+    constexpr int REGS = NBANK << L;
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr unsigned long long STEP = 32ull * VPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned long long wb = (unsigned long long)(k >> 3);
+    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    unsigned long long* slots = seg_range_slots(next);
+    const PlaneXpose xp(lane);
+    bool waited = false;
+    auto ensure_waited = [&]() {
+        if (!waited) {
+            pdl_wait_prev();  // rows and slots may belong to the previous launch on this stream
+            waited = true;
+        }
+    };
+    const unsigned long long off0 = offsets[0], offn = offsets[n_arrays];
+    RangeSplit rs;
+    const unsigned long long p0 = off0 * wb;
+    rs.base = p0 - ((reinterpret_cast<uintptr_t>(data) + p0) & 15u);  // absolute 16-byte alignment
+    rs.total = offn * wb - rs.base;
+    // at least 512 bytes per range (so no range is empty), at most one per warp and slot
+    const unsigned long long wmax = nwarps < (unsigned long long)kSegRangeSlots ? nwarps : kSegRangeSlots;
+    rs.W = rs.total / 512 < wmax ? (rs.total / 512 ? rs.total / 512 : 1) : wmax;
+    if (warp >= rs.W) {
+        ensure_waited();
+        return;
+    }
+    const unsigned long long r0 = rs.start(warp), r1 = rs.start(warp + 1);
+    const bool last = warp + 1 == rs.W;
+    if (r0 == r1 && !last) {
+        ensure_waited();
+        return;
+    }
+    // First array touching [r0, r1): smallest a with end(a) > r0 or start(a) >= r0
+    // (the latter catches empty arrays placed at r0).  32-ary search.
+    auto touches = [&](unsigned long long i) {  // monotone in i
+        return offsets[i + 1] * wb > r0 || offsets[i] * wb >= r0;
+    };
+    unsigned long long lo = 0, hi = n_arrays;  // the answer lies in [lo, hi]; hi = n_arrays: none
+    for (;;) {
+        const unsigned long long span = hi - lo;
+        if (span <= 32) {  // one probe per candidate; lanes past the span stand for `hi`
+            const bool pred = lane >= span || touches(lo + lane);
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, pred);
+            lo = m ? lo + (unsigned long long)(__ffs(m) - 1) : hi;
+            break;
+        }
+        const unsigned long long probe = lo + span * lane / 32;  // lane 0 probes lo; all < hi <= n_arrays
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, touches(probe));
+        if (m & 1u) break;  // the answer is lo
+        const int j = m ? __ffs(m) - 1 : 32;  // first true probe; the answer is in (probe_{j-1}, probe_j]
+        const unsigned long long nlo = lo + span * (j - 1) / 32 + 1;
+        if (j < 32) hi = lo + span * j / 32;
+        lo = nlo;
+    }
+    unsigned long long a = lo;
+
+    uint32_t carries[NBANK][L], U[NBANK][M];
+    unsigned long long tot[NBANK];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) U[b][i] = 0;
+        tot[b] = 0;
+    }
+    const unsigned long long zero[NBANK] = {};
+    // Finishes array `arr` (bytes [s, e)) with this warp's counts `t`.
+    auto finish = [&](unsigned long long arr, unsigned long long s, unsigned long long e,
+                      const unsigned long long (&t)[NBANK]) {
+        ensure_waited();
+        if (s >= r0 && (e <= r1 || last)) {  // entirely in this range
+            seg_store_row<NBANK>(out, arr, k, lane, t);
+            return;
+        }
+        const unsigned long long key = rs.owner(s);
+        const unsigned long long pieces = rs.owner(e - 1) - key + 1;
+        unsigned long long* acc = slots + key * 65;
+        unsigned long long v0 = t[0];
+        if (NBANK == 1)
+            for (int w = 16; w >= k; w >>= 1) v0 += __shfl_down_sync(0xFFFFFFFFu, v0, w);
+        if (NBANK == 2) {
+            atomicAdd(acc + lane, v0);
+            atomicAdd(acc + 32 + lane, t[NBANK - 1]);
+        } else if ((int)lane < k) {
+            atomicAdd(acc + lane, v0);
+        }
+        __threadfence();
+        __syncwarp();
+        unsigned long long done = lane == 0 ? atomicAdd(acc + 64, 1ull) : 0ull;
+        done = __shfl_sync(0xFFFFFFFFu, done, 0);
+        if (done + 1 == pieces) {  // the last piece: move the slot into the row
+            __threadfence();
+            unsigned long long* row = out + arr * (unsigned long long)k;
+            for (int c = (int)lane; c < k; c += 32) row[c] = atomicExch(acc + c, 0ull);
+            if (lane == 0) atomicExch(acc + 64, 0ull);
+        }
+    };
+    // Segment of array `arr` inside the range, as a vector view; false if empty.
+    auto segment = [&](unsigned long long arr, unsigned long long& s, unsigned long long& e, SegView& v) {
+        s = offsets[arr] * wb;
+        e = offsets[arr + 1] * wb;
+        const unsigned long long lo_b = s > r0 ? s : r0, hi_b = e < r1 || last ? e : r1;
+        v = seg_view<VB>(data, lo_b / wb, hi_b > lo_b ? hi_b / wb : lo_b / wb, (int)wb);
+    };
+    auto in_range = [&](unsigned long long arr) {  // array `arr` still starts before r1 (or the last range)
+        return arr < n_arrays && (last || offsets[arr] * wb < r1);
+    };
+    // skip empty arrays (writing the zero rows this range owns) to the first non-empty segment
+    unsigned long long s = 0, e = 0;
+    SegView v;
+    for (;; ++a) {
+        if (!in_range(a)) {
+            ensure_waited();
+            return;
+        }
+        segment(a, s, e, v);
+        if (v.nv) break;
+        if (s == e && s >= r0) {  // an empty array at a position this range owns
+            ensure_waited();
+            seg_store_row<NBANK>(out, a, k, lane, zero);
+        }
+    }
+    uint32_t nb = 0;
+    unsigned long long t = 0;
+    uint32_t r[REGS];
+    seg_load<VB, VPT>(v, t, lane, r);
+    for (;;) {
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b)
+            plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r) : Tree<L, 2>::run(carries[b], r + b));
+        ++nb;
+        t += STEP;
+        const bool seg_done = t >= v.nv;
+        unsigned long long a_n = a, s_n = s, e_n = e;
+        SegView vn = v;
+        bool more = true;
+        if (seg_done) {  // next non-empty segment of this range
+            t = 0;
+            more = false;
+            for (a_n = a + 1; in_range(a_n); ++a_n) {
+                segment(a_n, s_n, e_n, vn);
+                if (vn.nv) {
+                    more = true;
+                    break;
+                }
+                if (s_n == e_n) {
+                    ensure_waited();
+                    seg_store_row<NBANK>(out, a_n, k, lane, zero);
+                }
+            }
+        }
+        if (more) seg_load<VB, VPT>(vn, t, lane, r);  // in flight during the epilogue below
+        if (seg_done || nb == (1u << M) - 1u) {
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                    U[b][i] = 0;
+                }
+            nb = 0;
+        }
+        if (seg_done) {
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
+                    carries[b][j] = 0;
+                }
+            finish(a, s, e, tot);
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+            if (!more) {
+                ensure_waited();
+                return;
+            }
+            a = a_n;
+            s = s_n;
+            e = e_n;
+            v = vn;
+        }
+    }
+}
+
+template <int NBANK, int L, int VB, int MINB>
+__global__ void __launch_bounds__(256, MINB) segmented_range_kernel(const uint8_t* data,
+                                                                    const unsigned long long* offsets,
+                                                                    unsigned long long n_arrays, int k, uint32_t,
+                                                                    unsigned long long* out, unsigned long long* next,
+                                                                    unsigned int*, unsigned) {
+    pdl_allow_next();
+    seg_range_loop<NBANK, L, VB>(data, offsets, n_arrays, k, out, next);
+}
+
 // MODE bit 0: CTA c takes the contiguous array range [c n / G, (c + 1) n / G)
 // and its warps stride over it (one DRAM region per SM, like the stream
 // kernel's CTA ranges; measured slower than the strided order); otherwise
@@ -1151,10 +1390,12 @@ __global__ void __launch_bounds__(256, MINB) segmented_tile_kernel(const uint8_t
 // arrays), the software-pipelined warp-per-array kernel with the bit-plane
 // epilogue (medium arrays) or the warp-per-array tiles with a dynamic tail
 // (long arrays, cfg5) -- the same choice for the whole grid, made on the
-// device, so device-resident offsets need no host round trip.  The tile mode
-// starts counting before the previous launch on the stream has completed.
-// `thresholds`: mean-length bounds in 64-byte units, lane mode bits 0-9,
-// grouped mode bits 10-19, tile mode (above) bits 20-31.
+// device, so device-resident offsets need no host round trip.  With fewer
+// than `rounds` arrays per warp (few arrays, typically huge ones) the range
+// mode splits the bytes evenly over the warps instead.  The tile and range
+// modes start counting before the previous launch on the stream completed.
+// `thresholds` (8 bits each): lane-mode mean bound / 64 B, grouped / 64 B,
+// tile-mode lower bound / 256 B, range-mode rounds.
 // ---------------------------------------------------------------------------
 template <int NBANK>
 __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* data,
@@ -1166,9 +1407,16 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
     constexpr int LW = NBANK == 1 ? 5 : 4;  // full-warp fallback tree depth
     pdl_allow_next();
     const int wb = k >> 3;
-    const unsigned long long lane_max = (unsigned long long)(thresholds & 0x3FFu) * 64;         // mean bytes
-    const unsigned long long group_max = (unsigned long long)((thresholds >> 10) & 0x3FFu) * 64;
-    const unsigned long long tile_min = (unsigned long long)(thresholds >> 20) * 64;
+    const unsigned long long lane_max = (unsigned long long)(thresholds & 0xFFu) * 64;  // mean bytes
+    const unsigned long long group_max = (unsigned long long)((thresholds >> 8) & 0xFFu) * 64;
+    const unsigned long long tile_min = (unsigned long long)((thresholds >> 16) & 0xFFu) * 256;
+    const unsigned long long range_rounds = thresholds >> 24;
+    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+    if (n_arrays < range_rounds * nwarps) {
+        seg_range_loop<NBANK, NBANK == 1 ? 5 : 4, 16>(data, offsets, n_arrays, k, out, next);
+        seg_claims_done(next, ticket);  // every warp has waited
+        return;
+    }
     const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
     if (mean > tile_min && mean > group_max) {
         // depth 5 per bank over 16-byte loads: 4 KiB (k <= 32) / 8 KiB (k = 64) steps per warp (measured

@@ -25,6 +25,8 @@ using namespace dev;
 #define SGTE(NB, L, VB, MB) {NB, L, VB, 13, segmented_tile_kernel<NB, L, VB, MB, 2>, MB}
 // sched 14: sched 13 with the last rounds of arrays claimed dynamically
 #define SGTD(NB, L, VB, MB) {NB, L, VB, 14, segmented_tile_kernel<NB, L, VB, MB, 6>, MB}
+// sched 16: even byte ranges per warp (the adaptive kernel's range mode)
+#define SGR(NB, L, VB, MB) {NB, L, VB, 16, segmented_range_kernel<NB, L, VB, MB>, MB}
 // sched 12: the same with one contiguous array range per CTA
 #define SGTB(NB, L, VB, MB) {NB, L, VB, 12, segmented_tile_kernel<NB, L, VB, MB, 1>, MB}
 // sched 5: grouped, G lanes per array, 2 CTAs/SM
@@ -36,6 +38,7 @@ const SegVariant kVariants[] = {
     SGTE(1, 7, 32, 1), SGTE(1, 6, 32, 1), SGTE(1, 6, 32, 2), SGTE(2, 6, 32, 1),
     SGTD(1, 7, 32, 1), SGTD(1, 6, 32, 1), SGTD(1, 6, 32, 2), SGTD(2, 6, 32, 1), SGTD(2, 5, 32, 2), SGTD(2, 5, 16, 2),
     SGTD(1, 6, 16, 2), SGTD(1, 5, 16, 2), SGTD(1, 5, 32, 2),
+    SGR(1, 5, 16, 2), SGR(2, 5, 16, 2), SGR(1, 7, 32, 1), SGR(2, 6, 32, 1),
     SGTB(1, 7, 32, 1), SGTB(1, 6, 32, 1), SGTB(1, 6, 32, 2), SGTB(2, 6, 32, 1), SGTB(2, 5, 32, 2), SGPEH(1, 5), SGPEH(1, 4), SGPEH(2, 4),
     SGC(1, 5, 3), SGC(1, 5, 2), SGC(1, 4, 4), SGC(2, 3, 4), SGC(2, 4, 2),
     SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),
@@ -57,6 +60,7 @@ const SegVariant kVariants[] = {
 #undef SGTB
 #undef SGTE
 #undef SGTD
+#undef SGR
 #undef SGA
 #undef SGPE
 #undef SGPE3

@@ -87,11 +87,13 @@ def main():
             assert (out.cpu().numpy().view(np.uint64) == want_rows).all()
         for v in variants:
             run(f"segmented k={k}", {"POSPOP_SEG_VARIANT": v, "POSPOP_SEG_BIG_KIB": "64"}, seg)
-        for lane, group, tile in ((1 << 20,) * 3, (0, 1 << 20, 1 << 20), (0, 0, 1 << 20), (0, 0, 0)):
-            # adaptive: lane / grouped / pipelined warp / tile modes
+        for lane, group, tile, rounds in ((1 << 20,) * 3 + (0,), (0, 1 << 20, 1 << 20, 0), (0, 0, 1 << 20, 0),
+                                          (0, 0, 0, 0), (0, 0, 0, 255)):
+            # adaptive: lane / grouped / pipelined warp / tile / range modes
             run(f"segmented adaptive k={k}", {"POSPOP_SEG_VARIANT": auto, "POSPOP_SEG_LANE_MEAN_BYTES": str(lane),
                                               "POSPOP_SEG_GROUP_MEAN_BYTES": str(group),
-                                              "POSPOP_SEG_TILE_MEAN_BYTES": str(tile)}, seg)
+                                              "POSPOP_SEG_TILE_MEAN_BYTES": str(tile),
+                                              "POSPOP_SEG_RANGE_ROUNDS": str(rounds)}, seg)
     print("bounds ok")
 
 

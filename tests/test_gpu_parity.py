@@ -393,14 +393,14 @@ _GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,
             "5,16,6", "5,32,6", "4,16,6", "4,32,6", "4,16,7", "4,32,7",  # + bit-plane epilogue (sched 6/7)
             "5,16,8", "5,16,9", "5,16,10,3", "5,16,10,2", "4,16,10,4"]  # sched 8/9/10
 _TILE = ["7,32,11,1", "7,16,11,1", "6,32,11,1", "6,32,11,2", "6,16,11,2", "5,32,11,2", "7,32,12,1", "6,32,12,1",
-         "6,32,12,2", "7,32,13,1", "6,32,13,2", "7,32,14,1", "6,32,14,1", "6,32,14,2"]
+         "6,32,12,2", "7,32,13,1", "6,32,13,2", "7,32,14,1", "6,32,14,1", "6,32,14,2", "5,16,16,2", "7,32,16,1"]
 SEG_VARIANTS = {
     8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
     16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
     32: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
     64: ["5,16,0", "5,16,1", "4,16,2", "3,32,2", "4,32,2", "4,16,3", "3,32,3", "3,16,3",
          "4,16,5,8", "4,32,5,8", "4,16,5,4", "4,16,6", "4,32,6", "3,32,6", "3,16,7", "4,16,8", "3,16,10,4", "4,16,10,2",
-         "6,32,11,1", "5,32,11,1", "5,32,11,2", "5,16,11,2", "6,32,12,1", "5,32,12,2", "6,32,13,1", "6,32,14,1"],
+         "6,32,11,1", "5,32,11,1", "5,32,11,2", "5,16,11,2", "6,32,12,1", "5,32,12,2", "6,32,13,1", "6,32,14,1", "5,16,16,2", "6,32,16,1"],
 }
 
 
@@ -501,6 +501,33 @@ def test_chained_async_launches_read_the_previous_output(pp, dev, orc):
         assert (out2.cpu().numpy().astype(np.uint64) == np.asarray(orc.pospopcnt(rows.ravel(), 64), np.uint64)).all()
 
 
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_segmented_few_huge_arrays(pp, dev, orc, k, monkeypatch):
+    """Few arrays, some far larger than a warp's share (the adaptive kernel's
+    range mode: even byte ranges per warp, arrays spanning ranges summed
+    through workspace slots): one array over everything, a few hundred-MiB
+    arrays with empty and tiny ones between them, offsets[0] > 0 at an odd
+    word, repeated launches (the slots are left zero)."""
+    wb = k // 8
+    n_words = (300 << 20) // wb + 3
+    data = orc.generate(6, 90 + k, n_words * wb // 8 + 1, threads=8).view(DT[k])[:n_words]
+    d = to_dev(data)
+    cases = [np.array([0, n_words], np.uint64),
+             np.array([5, 5, 6, 6 + (100 << 20) // wb, 6 + (100 << 20) // wb, 7 + (100 << 20) // wb,
+                       n_words - 9, n_words - 1, n_words - 1], np.uint64),
+             np.array([1, 2, 3, 4], np.uint64),  # tiny arrays only
+             np.array([17, 17], np.uint64)]       # one empty array
+    for offs in cases:
+        want = orc.segmented(data, offs, k, threads=8)
+        o = torch.from_numpy(offs.view(np.int64)).cuda()
+        for _ in range(3):
+            out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
+            pp.segmented_async(d, o, out, k)
+            torch.cuda.synchronize()
+            assert (out.cpu().numpy().view(np.uint64) == want).all(), offs[:4]
+        assert (pp.pospopcnt_segmented(d, offs, k) == want).all()  # synchronous entry, host offsets
+
+
 @pytest.mark.parametrize("var", ["", "7,32,13,1", "7,32,14,1", "6,32,14,2"])
 def test_chained_segmented_launches(pp, dev, orc, var, monkeypatch):
     """Segmented kernels that read (and count) before waiting for the previous
@@ -572,17 +599,18 @@ def test_sharded_repeated_calls_and_empty_shards(pp, dev, orc):
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-@pytest.mark.parametrize("mode", ["lane", "grouped", "pipelined", "tile"])
+@pytest.mark.parametrize("mode", ["lane", "grouped", "pipelined", "tile", "range"])
 def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
     """The adaptive kernel (sched 8) in each of its modes -- forced through the
     mean-length thresholds -- on tiny, ragged, empty and large arrays; in lane
     mode a batch with an array above the lane cap takes the full-warp path."""
     monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
-    lane, group, tile = {"lane": (1 << 20, 1 << 20, 1 << 20), "grouped": (0, 1 << 20, 1 << 20),
-                         "pipelined": (0, 0, 1 << 20), "tile": (0, 0, 0)}[mode]
+    lane, group, tile, rounds = {"lane": (1 << 20, 1 << 20, 1 << 20, 0), "grouped": (0, 1 << 20, 1 << 20, 0),
+                                 "pipelined": (0, 0, 1 << 20, 0), "tile": (0, 0, 0, 0), "range": (0, 0, 0, 255)}[mode]
     monkeypatch.setenv("POSPOP_SEG_LANE_MEAN_BYTES", str(lane))
     monkeypatch.setenv("POSPOP_SEG_GROUP_MEAN_BYTES", str(group))
     monkeypatch.setenv("POSPOP_SEG_TILE_MEAN_BYTES", str(tile))
+    monkeypatch.setenv("POSPOP_SEG_RANGE_ROUNDS", str(rounds))
     rng = np.random.default_rng(40 + k)
     n_words = 1_500_000
     data = orc.generate(6, 51, n_words * k // 64 + 1).view(DT[k])[:n_words]
