@@ -547,6 +547,24 @@ def test_chained_segmented_launches(pp, dev, orc, var, monkeypatch):
     rows = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
     small_offs = torch.tensor([0, 3, 16], dtype=torch.int64, device="cuda")
     cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    # RAW on the offsets: a count's output (non-decreasing by construction:
+    # word i of a 16-word block sets bits i..15, so counts[p] = (p + 1) * blocks)
+    # is the next segmented launch's offsets array
+    blk = np.array([sum(1 << p for p in range(16) if p >= i) for i in range(16)], np.uint16)
+    blocks = 1 << 16
+    d_blk = torch.from_numpy(np.tile(blk, blocks).view(np.int16)).cuda()
+    seg_words = torch.from_numpy(a[:blocks * 16].view(np.int64).copy()).cuda()
+    off_dev = torch.zeros(16, dtype=torch.int64, device="cuda")
+    want_offs = np.arange(1, 17, dtype=np.uint64) * blocks
+    want_rows = orc.segmented(a[:blocks * 16].view(np.uint32), want_offs, 32, threads=8)
+    for trial in range(5):
+        off_dev.zero_()
+        pp.count_async(d_blk, off_dev, 16, stream=s)
+        rows_o = torch.empty((15, 32), dtype=torch.int64, device="cuda")
+        pp.segmented_async(seg_words, off_dev, rows_o, 32, stream=s)
+        torch.cuda.synchronize()
+        assert (off_dev.cpu().numpy().view(np.uint64) == want_offs).all()
+        assert (rows_o.cpu().numpy().view(np.uint64) == want_rows).all(), trial
     for trial in range(10):
         # WAW: the second launch's rows win
         pp.segmented_async(da, offs, rows, k, stream=s)
