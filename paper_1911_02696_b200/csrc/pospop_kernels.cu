@@ -419,10 +419,12 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
 // 256-word arrays G=4 4269 vs lane 2173; 1024 words G=4 ~ pipelined).
 constexpr int kSegLaneMeanBytes = 512;
 constexpr int kSegGroupMeanBytes = 2048;
-constexpr int kSegTileMeanBytes = 8192;  // tile mode above this mean (tools/seg_vs_stream.py)
+constexpr int kSegTileMeanBytes = 2048;  // tile mode above this mean (= the grouped bound; tools/seg_vs_stream.py)
 constexpr int kSegRangeRounds = 4;       // range mode below this many arrays per warp
-static_assert(dev::kSegRangeSlots == kSegRangeSlotsHost && kAccChannels + 1 + 7 == 104,
-              "range-mode slots: workspace layout (pospop_launch.h) and dev::seg_range_slots disagree");
+constexpr int kSegGiantKib = 1024;       // arrays above this go through the giant queue
+static_assert(dev::kSegRangeSlots == kSegRangeSlotsHost && dev::kGiantQ == kGiantQHost &&
+                  dev::kGiantEntry == kGiantEntryHost && kAccChannels + 1 + 7 == 104,
+              "segmented workspace regions: pospop_launch.h and pospop_segmented.cuh disagree");
 
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets, size_t n,
                              unsigned long long* d_out, const LaunchOptions& opt, const StreamWorkspace& ws,
@@ -458,15 +460,16 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (extra < 1) extra = 1;
     if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
     if (var->sched >= 11) extra = (unsigned)env_int("POSPOP_SEG_TAIL_ROUNDS", 4);  // tile kernels: dynamic tail
-    if (var->sched == 8) {  // mode bounds, 8 bits each: lane / grouped mean (64 B units), tile mean (256 B units),
-                            // range-mode rounds (arrays per warp below which the bytes are split evenly)
-        auto units = [](int v, unsigned unit) {
-            return (unsigned)(v < 0 ? 0 : ((unsigned)v / unit > 0xFF ? 0xFF : (unsigned)v / unit));
+    if (var->sched == 8) {  // mode bounds: lane / grouped mean (64 B units), tile mean (256 B units), range-mode
+                            // rounds (6 bits each), giant-array bound (16 KiB units, 8 bits)
+        auto units = [](int v, unsigned unit, unsigned cap) {
+            return (unsigned)(v < 0 ? 0 : ((unsigned)v / unit > cap ? cap : (unsigned)v / unit));
         };
-        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes), 64) |
-                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 64) << 8) |
-                (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 256) << 16) |
-                (units(env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds), 1) << 24);
+        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes), 64, 0x3F) |
+                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 64, 0x3F) << 6) |
+                (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 256, 0x3F) << 12) |
+                (units(env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds), 1, 0x3F) << 18) |
+                (units(env_int("POSPOP_SEG_GIANT_KIB", kSegGiantKib), 16, 0xFF) << 24);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);

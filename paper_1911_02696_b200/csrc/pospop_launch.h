@@ -23,10 +23,15 @@ struct StreamWorkspace {
 // Bytes of one workspace allocation (u64 units): acc[0, 96), ticket (u32 at
 // u64 96), next (97), bad (98), then from u64 104 the segmented range mode's
 // kSegRangeSlots slots of 64 partial counts + 1 piece counter
-// (dev::seg_range_slots: `next` + 7).  Zero between launches.
+// (dev::seg_range_slots: `next` + 7), then the segmented giant-array queue
+// (8 + kGiantQ entries of kGiantEntry u64; dev::GiantQueue).  Zero between
+// launches.
 constexpr int kAccChannels = 96;
 constexpr int kSegRangeSlotsHost = 4096;
-constexpr size_t kWorkspaceBytes = (104 + (size_t)kSegRangeSlotsHost * 65) * sizeof(unsigned long long);
+constexpr int kGiantQHost = 512;
+constexpr int kGiantEntryHost = 72;
+constexpr size_t kWorkspaceBytes =
+    (104 + (size_t)kSegRangeSlotsHost * 65 + 8 + (size_t)kGiantQHost * kGiantEntryHost) * sizeof(unsigned long long);
 
 struct LaunchOptions {
     uint32_t flush_threshold = 65535;  // tree blocks between lane flushes, [1, 65535]

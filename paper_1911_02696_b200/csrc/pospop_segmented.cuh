@@ -284,6 +284,195 @@ __device__ __forceinline__ void seg_store_row(unsigned long long* out, unsigned 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Workspace regions after the stream scratch (pospop_launch.h), addressed
+// from the claim counter `next` (u64 97 of the workspace): the range mode's
+// slots (u64 104 on) and the giant-array queue after them.  Zero between
+// launches.
+// ---------------------------------------------------------------------------
+constexpr int kSegRangeSlots = 4096;   // = kSegRangeSlotsHost (pospop_launch.h)
+constexpr int kGiantQ = 512;           // = kGiantQHost
+constexpr int kGiantEntry = 72;        // u64 per queue entry
+__device__ __forceinline__ unsigned long long* seg_range_slots(unsigned long long* next) { return next + 7; }
+
+// Giant arrays (above `giant_bytes`) met by the array-per-warp / per-lane
+// schedules are not counted by one warp: the warp publishes the array in this
+// queue and counts its chunks together with every warp that reaches a claim
+// point (or its exit) while chunks are left; chunk partials are summed in the
+// entry with u64 atomics and the warp finishing the last chunk moves them into
+// the row.  The publisher keeps helping until its entry has no chunk left, so
+// no array waits for a warp that already exited.  Entry: [0] array, [1]
+// chunks, [2] chunk claim counter, [3] ready flag, [4, 68) counts, [68] chunks
+// done.  [0] of the queue = entries published (beyond kGiantQ the publisher
+// counts the array alone).  The last CTA resets the queue (seg_launch_done).
+struct GiantQueue {
+    unsigned long long* base;
+    unsigned long long giant_bytes;  // 0: off
+    __device__ __forceinline__ unsigned long long* entry(unsigned long long e) const {
+        return base + 8 + e * kGiantEntry;
+    }
+    __device__ __forceinline__ unsigned long long chunk_bytes() const { return giant_bytes / 4; }
+};
+__device__ __forceinline__ GiantQueue seg_giant_queue(unsigned long long* next, unsigned long long giant_bytes) {
+    return GiantQueue{next + 7 + (unsigned long long)kSegRangeSlots * 65, giant_bytes};
+}
+
+// Warp totals (lane c: channel c) of one vector view, depth-L tree steps.
+template <int NBANK, int L, int VB>
+__device__ __forceinline__ void seg_count_view(const SegView& v, uint32_t lane, const PlaneXpose& xp,
+                                               unsigned long long (&tot)[NBANK]) {
+    constexpr int M = 3;
+    constexpr int REGS = NBANK << L;
+    constexpr int VPT = REGS / (VB / 4);
+    constexpr unsigned long long STEP = 32ull * VPT;
+    uint32_t carries[NBANK][L], U[NBANK][M];
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) carries[b][j] = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) U[b][i] = 0;
+        tot[b] = 0;
+    }
+    uint32_t nb = 0;
+    for (unsigned long long t = 0; t < v.nv; t += STEP) {
+        uint32_t r[REGS];
+        seg_load<VB, VPT>(v, t, lane, r);
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b)
+            plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r) : Tree<L, 2>::run(carries[b], r + b));
+        if (++nb == (1u << M) - 1u) {
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                    U[b][i] = 0;
+                }
+            nb = 0;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
+#pragma unroll
+        for (int i = 0; i < M; ++i) tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+    }
+}
+
+// Publishes array `arr` of `bytes` bytes; false if the queue is full (the
+// caller then counts it itself).  Warp-uniform.
+__device__ __forceinline__ bool giant_publish(const GiantQueue& q, unsigned long long arr, unsigned long long bytes,
+                                              uint32_t lane) {
+    unsigned long long e = lane == 0 ? atomicAdd(q.base, 1ull) : 0ull;
+    e = __shfl_sync(0xFFFFFFFFu, e, 0);
+    if (e >= (unsigned long long)kGiantQ) return false;
+    if (lane == 0) {
+        unsigned long long* p = q.entry(e);
+        p[0] = arr;
+        p[1] = (bytes + q.chunk_bytes() - 1) / q.chunk_bytes();
+        __threadfence();
+        atomicExch(p + 3, 1ull);
+    }
+    __syncwarp();
+    return true;
+}
+
+// Counts chunks of published arrays until no chunk is left to claim.
+// Warp-uniform; called at a warp's exit.
+template <int NBANK, int L, int VB>
+__device__ __noinline__ void giant_help(const GiantQueue q, const uint8_t* data, const unsigned long long* offsets,
+                                        int k, unsigned long long* out, uint32_t lane) {
+    const int wb = k >> 3;
+    unsigned long long cursor = 0;
+    const unsigned long long cw = q.chunk_bytes() / (unsigned long long)wb;  // words per chunk
+    const PlaneXpose xp(lane);
+    for (;;) {
+        unsigned long long cnt = __ldcg(q.base);
+        if (cnt > (unsigned long long)kGiantQ) cnt = kGiantQ;
+        if (cursor >= cnt) return;
+        unsigned long long* p = q.entry(cursor);
+        unsigned long long arr = 0, chunks = 0, c = 0;
+        if (lane == 0) {
+            while (atomicAdd(p + 3, 0ull) == 0ull) {  // its publisher is running: ready momentarily
+            }
+            __threadfence();
+            arr = __ldcg(p);
+            chunks = __ldcg(p + 1);
+            c = atomicAdd(p + 2, 1ull);
+        }
+        arr = __shfl_sync(0xFFFFFFFFu, arr, 0);
+        chunks = __shfl_sync(0xFFFFFFFFu, chunks, 0);
+        c = __shfl_sync(0xFFFFFFFFu, c, 0);
+        if (c >= chunks) {
+            ++cursor;
+            continue;
+        }
+        const unsigned long long w0 = offsets[arr] + c * cw, e1 = offsets[arr + 1];
+        const unsigned long long w1 = w0 + cw < e1 ? w0 + cw : e1;
+        unsigned long long tot[NBANK];
+        seg_count_view<NBANK, L, VB>(seg_view<VB>(data, w0, w1, wb), lane, xp, tot);
+        unsigned long long* acc = p + 4;
+        unsigned long long v0 = tot[0];
+        if (NBANK == 1)
+            for (int w = 16; w >= k; w >>= 1) v0 += __shfl_down_sync(0xFFFFFFFFu, v0, w);
+        if (NBANK == 2) {
+            atomicAdd(acc + lane, v0);
+            atomicAdd(acc + 32 + lane, tot[NBANK - 1]);
+        } else if ((int)lane < k) {
+            atomicAdd(acc + lane, v0);
+        }
+        __threadfence();
+        __syncwarp();
+        unsigned long long done = lane == 0 ? atomicAdd(p + 68, 1ull) : 0ull;
+        done = __shfl_sync(0xFFFFFFFFu, done, 0);
+        if (done + 1 == chunks) {  // the last chunk: move the counts into the row
+            __threadfence();
+            unsigned long long* row = out + arr * (unsigned long long)k;
+            for (int ch = (int)lane; ch < k; ch += 32) row[ch] = atomicExch(acc + ch, 0ull);
+            if (lane == 0) atomicExch(p + 68, 0ull);
+        }
+    }
+}
+
+// A warp meeting array `arr` (of `bytes` bytes): true if it was published to
+// the giant queue (the caller skips it; every warp counts queued chunks when
+// its own work is done -- giant_help at the warp's exit, where none of the
+// schedule's registers are live -- and the publisher is among them, so every
+// queued array is finished before the launch ends).
+__device__ __forceinline__ bool giant_divert(const GiantQueue& q, unsigned long long arr, unsigned long long bytes,
+                                             uint32_t lane) {
+    if (!q.giant_bytes || bytes <= q.giant_bytes) return false;
+    return giant_publish(q, arr, bytes, lane);
+}
+
+// End of a launch that may have used the claim counter and the giant queue:
+// the last CTA (every warp has finished) resets both for the next launch.
+__device__ __forceinline__ void seg_launch_done(unsigned long long* next, unsigned int* ticket, const GiantQueue& q) {
+    __shared__ int s_last_q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last_q = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last_q) return;
+    __threadfence();
+    unsigned long long cnt = __ldcg(q.base);
+    if (cnt > (unsigned long long)kGiantQ) cnt = kGiantQ;
+    for (unsigned long long e = threadIdx.x; e < cnt; e += blockDim.x) {
+        q.entry(e)[2] = 0ull;
+        q.entry(e)[3] = 0ull;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *q.base = 0ull;
+        *next = 0ull;
+        *ticket = 0u;
+    }
+}
+
 template <int NBANK, int L, int VB, int EPI = 0, int HINT = 0>
 __device__ __forceinline__ void segmented_pipe_body(const uint8_t* data, const unsigned long long* offsets,
                                                     unsigned long long n_arrays, int k, uint32_t flush_threshold,
@@ -772,10 +961,11 @@ template <int NBANK, int L, int VB, int G>
 __device__ __forceinline__ void seg_group_loop(const uint8_t* data, const unsigned long long* offsets,
                                                unsigned long long n_arrays, int k, uint32_t flush_threshold,
                                                unsigned long long* out, unsigned long long* next,
-                                               unsigned big_vectors) {
+                                               unsigned big_vectors, unsigned long long giant_bytes = 0) {
     constexpr int NG = 32 / G;  // arrays per batch
     const uint32_t lane = threadIdx.x & 31u;
     const int wb = k >> 3;
+    const GiantQueue q = seg_giant_queue(next, giant_bytes);
     unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
     mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
@@ -788,13 +978,17 @@ __device__ __forceinline__ void seg_group_loop(const uint8_t* data, const unsign
         if (!__any_sync(0xFFFFFFFFu, nbytes > (unsigned long long)big_vectors * VB)) {
             seg_group_batch<NBANK, L, VB, G>(data, offsets, a0, n_arrays, k, flush_threshold, out, lane);
         } else {
-            for (int j = 0; j < NG; ++j)
-                if (a0 + j < n_arrays)
+            for (int j = 0; j < NG; ++j) {
+                if (a0 + j >= n_arrays) break;
+                const unsigned long long bytes = __shfl_sync(0xFFFFFFFFu, nbytes, j);
+                if (!giant_divert(q, a0 + j, bytes, lane))
                     seg_group_batch<NBANK, L, VB, 32>(data, offsets, a0 + j, n_arrays, k, flush_threshold, out, lane);
+            }
         }
         b = __shfl_sync(0xFFFFFFFFu, mine, 0);
         mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     }
+    if (giant_bytes) giant_help<NBANK, NBANK == 1 ? 5 : 4, 16>(q, data, offsets, k, out, lane);
 }
 
 template <int NBANK, int L, int VB, int G, int MINB>
@@ -885,9 +1079,11 @@ template <int NBANK, int LW, int VBW>
 __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigned long long* offsets,
                                               unsigned long long n_arrays, int k, uint32_t flush_threshold,
                                               unsigned long long* out, unsigned long long* next,
-                                              unsigned long long lane_cap_bytes, uint8_t* stage) {
+                                              unsigned long long lane_cap_bytes, uint8_t* stage,
+                                              unsigned long long giant_bytes = 0) {
     const uint32_t lane = threadIdx.x & 31u;
     const int wb = k >> 3;
+    const GiantQueue q = seg_giant_queue(next, giant_bytes);
     const int rowb = k * 8 + 16;  // staged row stride, bytes
     uint8_t* wbuf = stage ? stage + (threadIdx.x >> 5) * 32 * rowb : nullptr;
     unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
@@ -923,13 +1119,17 @@ __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigne
                 seg_lane_array<NBANK>(data, offsets, a, k, out + a * (unsigned long long)k);
             }
         } else {
-            for (int j = 0; j < 32; ++j)
-                if (a0 + j < n_arrays)
+            for (int j = 0; j < 32; ++j) {
+                if (a0 + j >= n_arrays) break;
+                const unsigned long long bytes = __shfl_sync(0xFFFFFFFFu, nbytes, j);
+                if (!giant_divert(q, a0 + j, bytes, lane))
                     seg_group_batch<NBANK, LW, VBW, 32>(data, offsets, a0 + j, n_arrays, k, flush_threshold, out, lane);
+            }
         }
         b = __shfl_sync(0xFFFFFFFFu, mine, 0);
         mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     }
+    if (giant_bytes) giant_help<NBANK, NBANK == 1 ? 5 : 4, 16>(q, data, offsets, k, out, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -973,7 +1173,8 @@ struct TileCursor {
 template <int NBANK, int L, int VB, bool EARLY = false>
 __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigned long long* offsets,
                                               unsigned long long n_arrays, int k, unsigned long long* out,
-                                              unsigned long long arr, const TileCursor& cur) {
+                                              unsigned long long arr, const TileCursor& cur,
+                                              unsigned long long giant_bytes = 0) {
     constexpr int M = 3;
     constexpr int REGS = NBANK << L;
     constexpr int RPV = VB / 4;
@@ -997,6 +1198,17 @@ __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigne
         if (cur.claims(a)) ensure_waited();  // the claim counter belongs to the previous launch until it completes
         return cur.following(a, lane);
     };
+    // giant arrays go through the queue (which belongs to the previous launch until it completes)
+    const GiantQueue q = seg_giant_queue(cur.next, giant_bytes);
+    auto diverted = [&](unsigned long long a, unsigned long long w0, unsigned long long w1) {
+        if (!giant_bytes || (w1 - w0) * (unsigned long long)wb <= giant_bytes) return false;
+        ensure_waited();
+        return giant_divert(q, a, (w1 - w0) * (unsigned long long)wb, lane);
+    };
+    auto finish_warp = [&]() {
+        ensure_waited();
+        if (giant_bytes) giant_help<NBANK, NBANK == 1 ? 5 : 4, 16>(q, data, offsets, k, out, lane);
+    };
     const unsigned long long zero[NBANK] = {};
     if (arr >= cur.static_end) arr = next_of(cur.static_end - cur.stride);  // this warp has no static array
     // The loads of the next step -- later in this array or the first step of
@@ -1006,10 +1218,12 @@ __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigne
     SegView v;
     for (;; arr = next_of(arr)) {  // first non-empty array
         if (arr >= n_arrays) {
-            ensure_waited();
+            finish_warp();
             return;
         }
-        v = seg_view<VB>(data, offsets[arr], offsets[arr + 1], wb);
+        const unsigned long long a_w0 = offsets[arr], a_w1 = offsets[arr + 1];
+        if (diverted(arr, a_w0, a_w1)) continue;
+        v = seg_view<VB>(data, a_w0, a_w1, wb);
         if (v.nv) break;
         store(arr, zero);
     }
@@ -1047,12 +1261,14 @@ __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigne
             more = false;
             while (nxt < n_arrays) {
                 arr_n = nxt;
-                vn = seg_view<VB>(data, w0, w1, wb);
+                const unsigned long long n_w0 = w0, n_w1 = w1;
+                vn = seg_view<VB>(data, n_w0, n_w1, wb);
                 nxt = next_of(arr_n);
                 if (nxt < n_arrays) {
                     w0 = offsets[nxt];
                     w1 = offsets[nxt + 1];
                 }
+                if (diverted(arr_n, n_w0, n_w1)) continue;
                 if (vn.nv) {
                     more = true;
                     break;
@@ -1084,7 +1300,7 @@ __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigne
 #pragma unroll
             for (int b = 0; b < NBANK; ++b) tot[b] = 0;
             if (!more) {
-                ensure_waited();
+                finish_warp();
                 return;
             }
             arr = arr_n;
@@ -1126,8 +1342,6 @@ __device__ __forceinline__ void seg_tile_strided(const uint8_t* data, const unsi
 // for the next launch.  Empty arrays are written by the warp owning their
 // position.  Starts before the previous launch completes (EARLY semantics).
 // ---------------------------------------------------------------------------
-constexpr int kSegRangeSlots = 4096;   // = kSegRangeSlotsHost (pospop_launch.h)
-__device__ __forceinline__ unsigned long long* seg_range_slots(unsigned long long* next) { return next + 7; }
 
 struct RangeSplit {
     unsigned long long base, total;  // byte positions relative to data: [base, base + total)
@@ -1385,17 +1599,20 @@ __global__ void __launch_bounds__(256, MINB) segmented_tile_kernel(const uint8_t
 
 // ---------------------------------------------------------------------------
 // Adaptive segmented kernel (SCHED 8, the asynchronous entry point's default):
-// every CTA reads offsets[0] and offsets[n] and picks, from the mean array
-// length, one lane per array (tiny arrays), G = 4 lanes per array (short
-// arrays), the software-pipelined warp-per-array kernel with the bit-plane
-// epilogue (medium arrays) or the warp-per-array tiles with a dynamic tail
-// (long arrays, cfg5) -- the same choice for the whole grid, made on the
-// device, so device-resident offsets need no host round trip.  With fewer
-// than `rounds` arrays per warp (few arrays, typically huge ones) the range
-// mode splits the bytes evenly over the warps instead.  The tile and range
-// modes start counting before the previous launch on the stream completed.
-// `thresholds` (8 bits each): lane-mode mean bound / 64 B, grouped / 64 B,
-// tile-mode lower bound / 256 B, range-mode rounds.
+// every CTA reads offsets[0] and offsets[n] and picks, from the array count and
+// the mean array length, the same schedule for the whole grid -- on the
+// device, so device-resident offsets need no host round trip:
+//   fewer than `rounds` arrays per warp   -> range mode (even byte ranges)
+//   mean <= lane bound                    -> one lane per array
+//   mean <= grouped bound                 -> four lanes per array
+//   otherwise                             -> warp-per-array tiles
+// Arrays above `giant` bytes met by the last three go through the giant queue.
+// The tile and range modes start counting before the previous launch on the
+// stream completed.  `thresholds`: lane bound / 64 B (bits 0-5), grouped bound
+// / 64 B (6-11), tile lower bound / 256 B (12-17), rounds (18-23), giant /
+// 16 KiB (24-31, 0 = off).  A mean between the grouped and the tile bound
+// (only when set so) takes the pipelined warp kernel (k <= 32) / dynamic
+// claims (k = 64) without the giant queue.
 // ---------------------------------------------------------------------------
 template <int NBANK>
 __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* data,
@@ -1407,38 +1624,49 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
     constexpr int LW = NBANK == 1 ? 5 : 4;  // full-warp fallback tree depth
     pdl_allow_next();
     const int wb = k >> 3;
-    const unsigned long long lane_max = (unsigned long long)(thresholds & 0xFFu) * 64;  // mean bytes
-    const unsigned long long group_max = (unsigned long long)((thresholds >> 8) & 0xFFu) * 64;
-    const unsigned long long tile_min = (unsigned long long)((thresholds >> 16) & 0xFFu) * 256;
-    const unsigned long long range_rounds = thresholds >> 24;
+    const unsigned long long lane_max = (unsigned long long)(thresholds & 0x3Fu) * 64;  // mean bytes
+    const unsigned long long group_max = (unsigned long long)((thresholds >> 6) & 0x3Fu) * 64;
+    const unsigned long long tile_min = (unsigned long long)((thresholds >> 12) & 0x3Fu) * 256;
+    const unsigned long long range_rounds = (thresholds >> 18) & 0x3Fu;
+    const unsigned long long giant = (unsigned long long)(thresholds >> 24) << 14;
+    const GiantQueue q = seg_giant_queue(next, giant);
     const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     if (n_arrays < range_rounds * nwarps) {
         seg_range_loop<NBANK, NBANK == 1 ? 5 : 4, 16>(data, offsets, n_arrays, k, out, next);
-        seg_claims_done(next, ticket);  // every warp has waited
+        seg_launch_done(next, ticket, q);  // every warp has waited
         return;
     }
     const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
     if (mean > tile_min && mean > group_max) {
         // depth 5 per bank over 16-byte loads: 4 KiB (k <= 32) / 8 KiB (k = 64) steps per warp (measured
         // best at two CTAs per SM: tools/seg_vs_stream.py)
-        seg_tile_strided<NBANK, 5, 16, true, true>(data, offsets, n_arrays, k, out, next, 4u);
-        seg_claims_done(next, ticket);  // every warp has waited
+        const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+        const unsigned long long rounds = n_arrays / nwarps;
+        TileCursor cur;
+        cur.next = next;
+        cur.dyn = true;
+        cur.stride = nwarps;
+        cur.n = n_arrays;
+        cur.static_end = (rounds > 4 ? rounds - 4 : 0) * nwarps;
+        seg_tile_loop<NBANK, 5, 16, true>(data, offsets, n_arrays, k, out, warp, cur, giant);
+        seg_launch_done(next, ticket, q);  // every warp has waited
         return;
     }
     pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     if (mean <= lane_max) {
         extern __shared__ __align__(16) uint8_t seg_stage[];  // launcher: 32 rows per warp for k <= 32, else none
         seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10,
-                                     NBANK == 1 && k <= 32 ? seg_stage : nullptr);
+                                     NBANK == 1 && k <= 32 ? seg_stage : nullptr, giant);
     } else if (mean <= group_max) {
         constexpr int LG = NBANK == 1 ? 6 : 4;  // grouped-mode tree depth (measured: 6 beats 5 by ~10 % at 1 KiB)
-        seg_group_loop<NBANK, LG, 16, 4>(data, offsets, n_arrays, k, flush_threshold, out, next, (256u << 10) / 16);
+        seg_group_loop<NBANK, LG, 16, 4>(data, offsets, n_arrays, k, flush_threshold, out, next, (256u << 10) / 16,
+                                         giant);
     } else if constexpr (NBANK == 1) {
         segmented_pipe_body<NBANK, LW, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out);
     } else {  // k = 64: dynamic array claims
         seg_warp_loop<NBANK, 5, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out, next, 1u);
     }
-    seg_claims_done(next, ticket);
+    seg_launch_done(next, ticket, q);
 }
 
 }  // namespace dev

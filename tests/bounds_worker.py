@@ -90,10 +90,12 @@ def main():
         for lane, group, tile, rounds in ((1 << 20,) * 3 + (0,), (0, 1 << 20, 1 << 20, 0), (0, 0, 1 << 20, 0),
                                           (0, 0, 0, 0), (0, 0, 0, 255)):
             # adaptive: lane / grouped / pipelined warp / tile / range modes
-            run(f"segmented adaptive k={k}", {"POSPOP_SEG_VARIANT": auto, "POSPOP_SEG_LANE_MEAN_BYTES": str(lane),
-                                              "POSPOP_SEG_GROUP_MEAN_BYTES": str(group),
-                                              "POSPOP_SEG_TILE_MEAN_BYTES": str(tile),
-                                              "POSPOP_SEG_RANGE_ROUNDS": str(rounds)}, seg)
+            for giant in ("1024", "16"):  # a 16 KiB giant bound: the queue carries the longer arrays
+                run(f"segmented adaptive k={k}", {"POSPOP_SEG_VARIANT": auto, "POSPOP_SEG_LANE_MEAN_BYTES": str(lane),
+                                                  "POSPOP_SEG_GROUP_MEAN_BYTES": str(group),
+                                                  "POSPOP_SEG_TILE_MEAN_BYTES": str(tile),
+                                                  "POSPOP_SEG_RANGE_ROUNDS": str(rounds),
+                                                  "POSPOP_SEG_GIANT_KIB": giant}, seg)
     print("bounds ok")
 
 

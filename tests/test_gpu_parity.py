@@ -528,6 +528,42 @@ def test_segmented_few_huge_arrays(pp, dev, orc, k, monkeypatch):
         assert (pp.pospopcnt_segmented(d, offs, k) == want).all()  # synchronous entry, host offsets
 
 
+@pytest.mark.parametrize("k", [8, 32, 64])
+@pytest.mark.parametrize("mode", ["lane", "grouped", "tile"])
+def test_segmented_giant_queue(pp, dev, orc, k, mode, monkeypatch):
+    """Giant arrays among many short ones: the lane / grouped / tile schedules
+    publish arrays above the giant bound to the queue and every warp counts
+    their chunks at its exit.  A 16 KiB bound makes hundreds of giants (more
+    than the 512 queue entries: the overflow is counted by the publisher), with
+    empty arrays, odd starts and a few huge arrays; repeated launches (the
+    queue is reset by the last CTA)."""
+    monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
+    lane, group, tile = {"lane": (4096, 4096, 4096), "grouped": (0, 4096, 4096), "tile": (0, 0, 0)}[mode]
+    monkeypatch.setenv("POSPOP_SEG_LANE_MEAN_BYTES", str(lane))
+    monkeypatch.setenv("POSPOP_SEG_GROUP_MEAN_BYTES", str(group))
+    monkeypatch.setenv("POSPOP_SEG_TILE_MEAN_BYTES", str(tile))
+    monkeypatch.setenv("POSPOP_SEG_RANGE_ROUNDS", "0")
+    monkeypatch.setenv("POSPOP_SEG_GIANT_KIB", "16")
+    wb = k // 8
+    rng = np.random.default_rng(700 + k)
+    lens = rng.integers(0, 24 if mode != "tile" else 600, size=40000)
+    lens[rng.random(lens.size) < 0.1] = 0
+    big = rng.choice(lens.size, size=800, replace=False)
+    lens[big] = rng.integers((16 << 10) // wb + 1, (64 << 10) // wb, size=big.size)  # > 16 KiB
+    lens[[17, 20000, 39999]] = [(40 << 20) // wb + 3, (5 << 20) // wb, (9 << 20) // wb + 1]
+    offs = np.concatenate([[3], 3 + np.cumsum(lens)]).astype(np.uint64)
+    n_words = int(offs[-1]) + 8
+    data = orc.generate(6, 71, n_words * wb // 8 + 1, threads=8).view(DT[k])[:n_words]
+    want = orc.segmented(data, offs, k, threads=8)
+    d = to_dev(data)
+    o = torch.from_numpy(offs.view(np.int64)).cuda()
+    for _ in range(3):
+        out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
+        pp.segmented_async(d, o, out, k)
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy().view(np.uint64) == want).all(), mode
+
+
 @pytest.mark.parametrize("var", ["", "7,32,13,1", "7,32,14,1", "6,32,14,2"])
 def test_chained_segmented_launches(pp, dev, orc, var, monkeypatch):
     """Segmented kernels that read (and count) before waiting for the previous

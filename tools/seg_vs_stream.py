@@ -46,6 +46,13 @@ def main():
     ap.add_argument("--words", default="4096,16384")
     ap.add_argument("--k", type=int, default=32, choices=[32, 64])
     ap.add_argument("--rounds", type=int, default=1, help="alternate the variants this many times")
+    ap.add_argument("--rows-in", type=int, default=0, help="carve the rows from a buffer of this many MiB")
+    ap.add_argument("--rows-init", default="empty", choices=["empty", "zeros", "ones"])
+    ap.add_argument("--prealloc", type=int, default=0,
+                    help="allocate (and zero, if negative: leave unwritten) then free this many MiB before the rows")
+    ap.add_argument("--offs-in", type=int, default=0, help="carve the offsets from a buffer of this many MiB")
+    ap.add_argument("--giant-frac", type=float, default=0.0,
+                    help="replace this fraction of the arrays (in the middle) by ONE giant array")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     s = torch.cuda.current_stream()
@@ -59,7 +66,30 @@ def main():
     for words in [int(w) for w in args.words.split(",")]:
         arrays = total // (k // 8) // words
         offs = torch.arange(arrays + 1, dtype=torch.int64, device="cuda") * words
-        out = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
+        if args.giant_frac > 0:  # arrays [g0, g1) merged into one
+            g0 = int(arrays * (0.5 - args.giant_frac / 2))
+            g1 = int(arrays * (0.5 + args.giant_frac / 2))
+            offs = torch.cat([offs[:g0 + 1], offs[g1:]])
+            arrays = offs.numel() - 1
+        if args.offs_in:
+            ob = torch.empty(args.offs_in << 17, dtype=torch.int64, device="cuda")
+            ob[:offs.numel()].copy_(offs)
+            offs = ob[:offs.numel()]
+        if args.prealloc:
+            tmp = torch.empty(abs(args.prealloc) << 20, dtype=torch.uint8, device="cuda")
+            if args.prealloc > 0:
+                tmp.zero_()
+            torch.cuda.synchronize()
+            del tmp
+        if args.rows_in:
+            rb = torch.empty(args.rows_in << 17, dtype=torch.int64, device="cuda")
+            if args.rows_init == "zeros":
+                rb.zero_()
+            out = rb[:arrays * k].view(arrays, k)
+        else:
+            out = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
+        if args.rows_init != "empty" and not args.rows_in:
+            out.fill_(0 if args.rows_init == "zeros" else -1)
         for var in args.variants.split(";") * args.rounds:
             if var:
                 os.environ["POSPOP_SEG_VARIANT"] = var
