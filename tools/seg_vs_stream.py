@@ -48,6 +48,8 @@ def main():
     ap.add_argument("--rounds", type=int, default=1, help="alternate the variants this many times")
     ap.add_argument("--rows-in", type=int, default=0, help="carve the rows from a buffer of this many MiB")
     ap.add_argument("--rows-init", default="empty", choices=["empty", "zeros", "ones"])
+    ap.add_argument("--rows-at", type=int, default=0, help="MiB offset of the rows inside the --rows-in buffer")
+    ap.add_argument("--zero-mib", default="", help="lo,hi: zero only this MiB range of the --rows-in buffer")
     ap.add_argument("--prealloc", type=int, default=0,
                     help="allocate (and zero, if negative: leave unwritten) then free this many MiB before the rows")
     ap.add_argument("--offs-in", type=int, default=0, help="carve the offsets from a buffer of this many MiB")
@@ -85,7 +87,10 @@ def main():
             rb = torch.empty(args.rows_in << 17, dtype=torch.int64, device="cuda")
             if args.rows_init == "zeros":
                 rb.zero_()
-            out = rb[:arrays * k].view(arrays, k)
+            if args.zero_mib:
+                zlo, zhi = (int(x) for x in args.zero_mib.split(","))
+                rb[zlo << 17:zhi << 17].zero_()
+            out = rb[(args.rows_at << 17):(args.rows_at << 17) + arrays * k].view(arrays, k)
         else:
             out = torch.empty((arrays, k), dtype=torch.int64, device="cuda")
         if args.rows_init != "empty" and not args.rows_in:
