@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--k", type=int, default=32, choices=[32, 64])
     ap.add_argument("--rounds", type=int, default=1, help="alternate the variants this many times")
     ap.add_argument("--rows-in", type=int, default=0, help="carve the rows from a buffer of this many MiB")
+    ap.add_argument("--data-extra", type=int, default=0,
+                    help="allocate the 1 GiB input inside a buffer this many MiB larger (negative: leave the extra unwritten)")
     ap.add_argument("--rows-init", default="empty", choices=["empty", "zeros", "ones"])
     ap.add_argument("--rows-at", type=int, default=0, help="MiB offset of the rows inside the --rows-in buffer")
     ap.add_argument("--zero-mib", default="", help="lo,hi: zero only this MiB range of the --rows-in buffer")
@@ -59,7 +61,13 @@ def main():
     torch.cuda.set_device(0)
     s = torch.cuda.current_stream()
     k, total = args.k, 1 << 30
-    data = torch.empty(total, dtype=torch.uint8, device="cuda")
+    if args.data_extra:
+        big = torch.empty(total + (abs(args.data_extra) << 20), dtype=torch.uint8, device="cuda")
+        if args.data_extra > 0:
+            big.zero_()
+        data = big[:total]
+    else:
+        data = torch.empty(total, dtype=torch.uint8, device="cuda")
     pp.generate(pp.GEN_U32 if k == 32 else pp.GEN_U64, 1, data, stream=s)
     cnt = torch.zeros(k, dtype=torch.int64, device="cuda")
     b2b, iso = timed(lambda: pp.count_async(data, cnt, k, stream=s), args.reps, s)
