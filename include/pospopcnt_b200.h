@@ -130,6 +130,17 @@ pospop_status pospopcnt_u16_c32(const uint16_t* data, uint32_t len, uint32_t cou
 pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offsets, size_t n_arrays,
                                   uint64_t* counts);
 
+/* Typed forms (the shape SURVEY.md 8b recommends): pospopcnt_segmented with
+ * k = 8 / 16 / 32 / 64; counts is n_arrays x k, row-major. */
+pospop_status pospopcnt_u8_segmented(const uint8_t* data, const uint64_t* offsets, size_t n_arrays,
+                                     uint64_t* counts);
+pospop_status pospopcnt_u16_segmented(const uint16_t* data, const uint64_t* offsets, size_t n_arrays,
+                                      uint64_t* counts);
+pospop_status pospopcnt_u32_segmented(const uint32_t* data, const uint64_t* offsets, size_t n_arrays,
+                                      uint64_t* counts);
+pospop_status pospopcnt_u64_segmented(const uint64_t* data, const uint64_t* offsets, size_t n_arrays,
+                                      uint64_t* counts);
+
 /* ---- file / pipe ingestion (the reference CLI's input path) ------------- */
 
 /* Counts a raw little-endian stream of k-bit words read from `fd` (a regular
@@ -176,6 +187,10 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
 pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* lens,
                                 const int* devices, int n_shards, uint64_t* counts);
 
+/* The 16-bit form (BASELINE cfg4): pospopcnt_sharded with k = 16. */
+pospop_status pospopcnt_u16_sharded(const uint16_t* const* shards, const size_t* lens, const int* devices,
+                                    int n_devices, uint64_t counts[16]);
+
 /* ---- asynchronous device-resident entry points (timing / integration) --- */
 
 /* Enqueues one count of device-resident data on `stream` (a cudaStream_t,
@@ -188,6 +203,9 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
 pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
                               int accumulate, uint32_t flush_threshold_blocks, int grid, int block,
                               void* stream);
+
+/* The 16-bit form: d_counts[16] overwritten, default flush threshold and grid. */
+pospop_status pospopcnt_u16_async(const uint16_t* d_data, size_t len, uint64_t* d_counts, void* stream);
 
 /* Diagnostics: pospopcnt_async with per-CTA %globaltimer timestamps.
  * d_trace (device, >= 5 * trace_ctas u64, trace_ctas >= 32 * SMs) receives,

@@ -852,6 +852,19 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
     return POSPOP_OK;
 }
 
+pospop_status pospopcnt_u8_segmented(const uint8_t* data, const uint64_t* offsets, size_t n, uint64_t* counts) {
+    return pospopcnt_segmented(8, data, offsets, n, counts);
+}
+pospop_status pospopcnt_u16_segmented(const uint16_t* data, const uint64_t* offsets, size_t n, uint64_t* counts) {
+    return pospopcnt_segmented(16, data, offsets, n, counts);
+}
+pospop_status pospopcnt_u32_segmented(const uint32_t* data, const uint64_t* offsets, size_t n, uint64_t* counts) {
+    return pospopcnt_segmented(32, data, offsets, n, counts);
+}
+pospop_status pospopcnt_u64_segmented(const uint64_t* data, const uint64_t* offsets, size_t n, uint64_t* counts) {
+    return pospopcnt_segmented(64, data, offsets, n, counts);
+}
+
 pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_summary* out, uint64_t* bad_offset,
                                uint16_t* bad_word) {
     if (!out) return fail(POSPOP_EINVAL, "out must not be NULL");
@@ -1098,6 +1111,15 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
         for (int p = 0; p < k; ++p) counts[p] += used[(size_t)i]->m_out[p];
     }
     return POSPOP_OK;
+}
+
+pospop_status pospopcnt_u16_sharded(const uint16_t* const* shards, const size_t* lens, const int* devices,
+                                    int n_devices, uint64_t counts[16]) {
+    return pospopcnt_sharded(16, reinterpret_cast<const void* const*>(shards), lens, devices, n_devices, counts);
+}
+
+pospop_status pospopcnt_u16_async(const uint16_t* d_data, size_t len, uint64_t* d_counts, void* stream) {
+    return pospopcnt_async(16, d_data, len, d_counts, 0, 65535, 0, 0, stream);
 }
 
 pospop_status pospopcnt_async(int k, const void* d_data, size_t len, uint64_t* d_counts, int accumulate,

@@ -701,3 +701,38 @@ def test_segmented_rows_at_8_byte_aligned_output(pp, dev, orc, k):
     torch.cuda.synchronize()
     assert (out.view(n, k).cpu().numpy().view(np.uint64) == want).all()
     assert int(buf[0]) == -1 and int(buf[-1]) == -1
+
+
+def test_typed_entry_points(pp, dev, orc):
+    """The typed C entry points of SURVEY.md 8b (pospopcnt_u{8,16,32,64}_segmented,
+    pospopcnt_u16_sharded, pospopcnt_u16_async) equal the generic ones."""
+    import ctypes as C
+    lib = pp._load()
+    u64p = C.POINTER(C.c_uint64)
+    raw = orc.generate(6, 33, 1 << 16).view(np.uint8)
+    for k in (8, 16, 32, 64):
+        wb = k // 8
+        n_words = raw.size // wb
+        offs = np.array([0, 1, 1, 777, n_words // 2, n_words], np.uint64)
+        rows = np.zeros((offs.size - 1, k), np.uint64)
+        fn = getattr(lib, f"pospopcnt_u{k}_segmented")
+        fn.argtypes = [C.c_void_p, u64p, C.c_size_t, u64p]
+        assert fn(raw.ctypes.data, offs.ctypes.data_as(u64p), offs.size - 1, rows.ctypes.data_as(u64p)) == 0
+        assert (rows == orc.segmented(raw.view(DT[k]), offs, k)).all(), k
+    d = to_dev(raw)
+    lib.pospopcnt_u16_sharded.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.POINTER(C.c_int), C.c_int,
+                                          u64p]
+    half = raw.size // 4  # words per shard (two shards)
+    ptrs = (C.c_void_p * 2)(d.data_ptr(), d.data_ptr() + 2 * half)
+    lens = (C.c_size_t * 2)(half, raw.size // 2 - half)
+    devs = (C.c_int * 2)(0, 0)
+    out = np.zeros(16, np.uint64)
+    assert lib.pospopcnt_u16_sharded(ptrs, lens, devs, 2, out.ctypes.data_as(u64p)) == 0
+    want = orc.naive(raw, 16)
+    assert [int(x) for x in out] == [int(x) for x in want]
+    lib.pospopcnt_u16_async.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+    d_out = torch.full((16,), -1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    assert lib.pospopcnt_u16_async(d.data_ptr(), raw.size // 2, d_out.data_ptr(), C.c_void_p(s.cuda_stream)) == 0
+    torch.cuda.synchronize()
+    assert [int(x) for x in d_out.cpu().numpy()] == [int(x) for x in want]
