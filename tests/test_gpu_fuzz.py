@@ -1,7 +1,8 @@
 """Property-based fuzzing of the product paths against the oracle (hypothesis):
 random k, lengths, byte offsets inside 0xFF guards, flush thresholds, value
-distributions (generator kinds), accumulate, segmented offsets with empty and
-tiny arrays, and every host/device placement.  Bit-exact."""
+distributions (generator kinds), accumulate, segmented offsets with empty,
+tiny and giant arrays in every adaptive-kernel mode (lane / grouped / tile /
+range, giant queue on and off), and every host/device placement.  Bit-exact."""
 import numpy as np
 import pytest
 
@@ -50,14 +51,41 @@ def test_fuzz_counts(pp, dev, orc, k, n, off_words, kind, seed, flush, where):
     assert pp.pospopcnt_k(data, k, flush_threshold_blocks=flush) == want
 
 
-@SETTINGS
+# Adaptive-kernel mode forced through its bounds (lane, grouped, tile, range mean bytes / rounds).
+MODES = {"auto": {}, "lane": {"LANE_MEAN_BYTES": 4000, "GROUP_MEAN_BYTES": 4000, "RANGE_ROUNDS": 0},
+         "grouped": {"LANE_MEAN_BYTES": 0, "GROUP_MEAN_BYTES": 4000, "RANGE_ROUNDS": 0},
+         "tile": {"LANE_MEAN_BYTES": 0, "GROUP_MEAN_BYTES": 0, "TILE_MEAN_BYTES": 0, "RANGE_ROUNDS": 0},
+         "range": {"RANGE_ROUNDS": 63}}
+
+
+@settings(SETTINGS, max_examples=200)
 @given(k=st.sampled_from([8, 16, 32, 64]), n_arrays=st.integers(1, 3000), max_len=st.sampled_from([1, 17, 300, 5000]),
-       seed=st.integers(0, 2**32 - 1), empty_frac=st.floats(0, 0.5), flush=st.sampled_from([1, 3, 65535]))
-def test_fuzz_segmented(pp, dev, orc, k, n_arrays, max_len, seed, empty_frac, flush):
+       seed=st.integers(0, 2**32 - 1), empty_frac=st.floats(0, 0.5), flush=st.sampled_from([1, 3, 65535]),
+       mode=st.sampled_from(sorted(MODES)), giant_kib=st.sampled_from([1024, 16]), start=st.integers(0, 9),
+       huge=st.booleans())
+def test_fuzz_segmented(pp, dev, orc, k, n_arrays, max_len, seed, empty_frac, flush, mode, giant_kib, start, huge):
+    import os
     rng = np.random.default_rng(seed)
     lens = rng.integers(0, max_len + 1, size=n_arrays)
     lens[rng.random(n_arrays) < empty_frac] = 0
-    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    if huge:  # a few arrays far above the giant bound
+        lens[rng.integers(0, n_arrays, size=3)] = rng.integers(1 << 16, 1 << 19, size=3) * 8 // k
+    offs = np.concatenate([[start], start + np.cumsum(lens)]).astype(np.uint64)
+    env = {f"POSPOP_SEG_{key}": str(v) for key, v in MODES[mode].items()}
+    env["POSPOP_SEG_GIANT_KIB"] = str(giant_kib)
+    saved = {key: os.environ.get(key) for key in env}
+    os.environ.update(env)
+    try:
+        _check_segmented(pp, orc, k, offs, n_arrays, seed, flush)
+    finally:
+        for key, v in saved.items():
+            if v is None:
+                os.environ.pop(key, None)
+            else:
+                os.environ[key] = v
+
+
+def _check_segmented(pp, orc, k, offs, n_arrays, seed, flush):
     total = int(offs[-1])
     dt = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}[k]
     data = orc.generate(6, seed, total * k // 64 + 1).view(dt)[:total]
