@@ -499,8 +499,9 @@ def run_ours_seg(args):
         e2e = {"value": round(total_bytes / float(tt[0]) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": words * wb + (arrays + 1) * 8, "d2h_bytes_per_step": arrays * k * 8,
                "steps": e2e_steps, "step_ms": [round(x, 2) for x in step_ms],
-               "path": "pospopcnt_segmented C ABI: pinned host data + pageable host offsets and rows; 32 MiB chunks cut at "
-                       "array boundaries, chunk H2D / segmented launch / row D2H overlapped on three streams"}
+               "path": "pospopcnt_segmented C ABI: pinned host data + pageable host offsets and rows; <= 32 MiB units cut "
+                       "at array boundaries through a 3-slot device staging ring, unit H2D / segmented launch / "
+                       "row D2H overlapped on three streams"}
         link = h2d_link_gbs(host, dev)
         if link:
             e2e["h2d_link_gbs"] = link

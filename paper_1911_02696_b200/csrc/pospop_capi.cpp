@@ -561,68 +561,85 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
     return POSPOP_OK;
 }
 
-// Segmented call on host data above kSegPipeMin bytes: the arrays are cut at
-// array boundaries into chunks of about kSegChunk bytes; chunk i's H2D (copy
-// stream), its segmented launch over the chunk's arrays (compute stream) and
-// the D2H of its rows (d2h stream) overlap the neighbouring chunks' work, so
-// the call runs at the H2D link rate instead of H2D + kernel + D2H in series.
-// The device copy of the data keeps the layout of the one-shot path (one
-// scratch buffer for the whole referenced range, same 32-byte phase), so the
-// kernels see exactly the addresses they would see there; a launch's masked
-// edge vectors may touch bytes of a chunk still in flight, which the masks
-// discard.
+// Segmented call on host data above kSegPipeMin bytes.  The arrays are cut
+// at array boundaries into units of at most kSegChunk bytes; an array longer
+// than that is a unit of its own, sent in kSegChunk pieces.  Unit i goes
+// through device staging slot i % kRing (the count path's 3 x 64 MiB ring, so
+// device memory stays bounded whatever the input size): its H2D on the copy
+// stream (pageable data through the pinned host ring), its launch on the
+// compute stream -- the segmented kernel over the unit's arrays, or for a
+// piece of a long array the stream kernel accumulating into that array's row
+// -- and the D2H of its rows on a third stream (pageable rows through a
+// grow-only pinned row buffer, copied out as each D2H completes) all overlap
+// the neighbouring units, so the call runs at the H2D link rate.  Each unit is
+// staged at the same 32-byte phase as in host memory, with slack on both sides
+// for the kernels' masked edge vectors.
 constexpr size_t kSegPipeMin = 8u << 20;
-constexpr size_t kSegChunk = 32u << 20;
+constexpr size_t kSegChunk = 32u << 20;  // <= stage_bytes - 128
+
+struct SegUnit {
+    size_t a0, a1;   // arrays [a0, a1); a long array: a1 = a0 + 1
+    size_t lo, hi;   // bytes relative to the first referenced byte
+    bool piece;      // a piece of a long array (stream kernel, accumulating)
+    bool first_piece, last_piece;
+};
 
 pospop_status segmented_host_pipeline(Ctx* c, int k, const void* data, const uint64_t* offsets, bool o_dev,
                                       const uint64_t* hoff, size_t n, uint64_t* counts, bool c_dev) {
     pospop_status s;
     const size_t wb = (size_t)k / 8, row_bytes = (size_t)k * sizeof(uint64_t);
     const uint8_t* src = static_cast<const uint8_t*>(data) + hoff[0] * wb;
-    const size_t bytes = (hoff[n] - hoff[0]) * wb;
     bool d_pinned = false, c_pinned = false;
     int hdev = c->dev;
     classify(data, &hdev, &d_pinned);
     if (!c_dev) classify(counts, &hdev, &c_pinned);
     const bool stage_rows = !c_dev && !c_pinned;
+    if ((s = ensure_stage(c))) return s;
+    const size_t piece_bytes = kSegChunk < c->stage_bytes - 128 ? kSegChunk : (c->stage_bytes - 128) & ~(size_t)63;
 
-    // chunk boundaries (array indices): a chunk ends at the last array
-    // boundary within kSegChunk bytes of its start, and holds >= 1 array
-    std::vector<size_t> cut{0};
-    const size_t chunk_words = kSegChunk / wb;
-    while (cut.back() < n) {
-        const size_t a0 = cut.back();
-        const uint64_t* hi = std::upper_bound(hoff + a0 + 1, hoff + n + 1, hoff[a0] + chunk_words);
-        size_t a1 = (size_t)(hi - hoff) - 1;
+    // units (rows of a unit go back once its last launch is done)
+    std::vector<SegUnit> units;
+    const size_t chunk_words = piece_bytes / wb;
+    for (size_t a0 = 0; a0 < n;) {
+        const size_t lo = (hoff[a0] - hoff[0]) * wb;
+        if ((hoff[a0 + 1] - hoff[a0]) * wb > piece_bytes) {  // a long array, in pieces
+            const size_t hi = (hoff[a0 + 1] - hoff[0]) * wb;
+            for (size_t p = lo; p < hi; p += piece_bytes)
+                units.push_back({a0, a0 + 1, p, hi - p < piece_bytes ? hi : p + piece_bytes, true, p == lo,
+                                 p + piece_bytes >= hi});
+            ++a0;
+            continue;
+        }
+        const uint64_t* e = std::upper_bound(hoff + a0 + 1, hoff + n + 1, hoff[a0] + chunk_words);
+        size_t a1 = (size_t)(e - hoff) - 1;
         if (a1 <= a0) a1 = a0 + 1;
-        cut.push_back(a1);
+        units.push_back({a0, a1, lo, (hoff[a1] - hoff[0]) * wb, false, true, true});
+        a0 = a1;
     }
-    const size_t chunks = cut.size() - 1;
+    const size_t nu = units.size();
 
-    const size_t pad = reinterpret_cast<uintptr_t>(src) & 31u;
-    void *buf = nullptr, *obuf = nullptr, *rbuf = nullptr;
-    if ((s = ctx_scratch(c, 0, bytes + pad + 64, &buf))) return s;
+    void *obuf = nullptr, *rbuf = nullptr;
     if (!o_dev && (s = ctx_scratch(c, 1, (n + 1) * sizeof(uint64_t), &obuf))) return s;
     if (!c_dev && (s = ctx_scratch(c, 2, n * row_bytes, &rbuf))) return s;
-    if ((s = ensure_seg_pipeline(c, 2 * chunks, stage_rows ? n * row_bytes : 0))) return s;
+    if ((s = ensure_seg_pipeline(c, nu + 1, stage_rows ? n * row_bytes : 0))) return s;
     if (!d_pinned && (s = ensure_host_ring(c))) return s;
-    const uint8_t* ddata = static_cast<const uint8_t*>(buf) + pad - hoff[0] * wb;
     const unsigned long long* doff = reinterpret_cast<const unsigned long long*>(o_dev ? offsets : obuf);
     unsigned long long* dout = reinterpret_cast<unsigned long long*>(c_dev ? counts : rbuf);
     uint8_t* rows_dst = stage_rows ? static_cast<uint8_t*>(c->rows_pinned) : reinterpret_cast<uint8_t*>(counts);
 
-    // everything on the copy/d2h streams is ordered after the caller's prior
-    // legacy-stream work through c->stream, like the one-shot path
-    CU(cudaEventRecord(c->seg_ev[0], c->stream));
-    CU(cudaStreamWaitEvent(c->copy, c->seg_ev[0], 0));
-    CU(cudaStreamWaitEvent(c->d2h, c->seg_ev[0], 0));
+    // the copy/d2h streams start after the caller's prior legacy-stream work (through c->stream)
+    CU(cudaEventRecord(c->seg_ev[nu], c->stream));
+    CU(cudaStreamWaitEvent(c->copy, c->seg_ev[nu], 0));
+    CU(cudaStreamWaitEvent(c->d2h, c->seg_ev[nu], 0));
     if (!o_dev)
         CU(cudaMemcpyAsync(obuf, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, c->copy));
 
-    size_t drained = 0;  // chunks whose staged rows are in `counts`
-    auto drain = [&](bool wait) -> pospop_status {
-        for (; drained < chunks; ++drained) {
-            cudaEvent_t done = c->seg_ev[2 * drained + 1];
+    size_t drained = 0;  // units whose staged rows are in `counts` (or that have no rows of their own)
+    auto drain = [&](bool wait, size_t issued) -> pospop_status {  // units [0, issued) have been enqueued
+        for (; drained < issued; ++drained) {
+            const SegUnit& u = units[drained];
+            if (!u.last_piece) continue;
+            cudaEvent_t done = c->seg_ev[drained];
             if (wait) {
                 CU(cudaEventSynchronize(done));
             } else {
@@ -630,49 +647,55 @@ pospop_status segmented_host_pipeline(Ctx* c, int k, const void* data, const uin
                 if (q == cudaErrorNotReady) return POSPOP_OK;
                 CU(q);
             }
-            const size_t lo = cut[drained] * row_bytes, len = (cut[drained + 1] - cut[drained]) * row_bytes;
-            parallel_copy(reinterpret_cast<uint8_t*>(counts) + lo, rows_dst + lo, len);
+            parallel_copy(reinterpret_cast<uint8_t*>(counts) + u.a0 * row_bytes, rows_dst + u.a0 * row_bytes,
+                          (u.a1 - u.a0) * row_bytes);
         }
         return POSPOP_OK;
     };
 
     size_t piece = 0;  // host-ring slot counter (pageable data)
-    for (size_t i = 0; i < chunks; ++i) {
-        const size_t a0 = cut[i], a1 = cut[i + 1];
-        const size_t lo = (hoff[a0] - hoff[0]) * wb, hi = (hoff[a1] - hoff[0]) * wb;
-        uint8_t* dst = static_cast<uint8_t*>(buf) + pad;
+    for (size_t i = 0; i < nu; ++i) {
+        const SegUnit& u = units[i];
+        const int slot = (int)(i % kRing);
+        const size_t pad = reinterpret_cast<uintptr_t>(src + u.lo) & 31u;
+        uint8_t* dst = static_cast<uint8_t*>(c->stage[slot]) + 64 + pad;  // 64 B of slack before the unit
+        if (i >= (size_t)kRing) CU(cudaStreamWaitEvent(c->copy, c->ev_done[slot], 0));
         if (d_pinned) {
-            if (hi > lo) CU(cudaMemcpyAsync(dst + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, c->copy));
+            CU(cudaMemcpyAsync(dst, src + u.lo, u.hi - u.lo, cudaMemcpyHostToDevice, c->copy));
         } else {
-            for (size_t off = lo; off < hi; off += kHostChunk, ++piece) {
-                const size_t m = hi - off < kHostChunk ? hi - off : kHostChunk;
+            for (size_t off = u.lo; off < u.hi; off += kHostChunk, ++piece) {
+                const size_t m = u.hi - off < kHostChunk ? u.hi - off : kHostChunk;
                 const int hs = (int)(piece % kHostRing);
                 if (c->host_used[hs]) CU(cudaEventSynchronize(c->ev_h2d[hs]));
                 parallel_copy(c->host_ring[hs], src + off, m);
-                CU(cudaMemcpyAsync(dst + off, c->host_ring[hs], m, cudaMemcpyHostToDevice, c->copy));
+                CU(cudaMemcpyAsync(dst + (off - u.lo), c->host_ring[hs], m, cudaMemcpyHostToDevice, c->copy));
                 CU(cudaEventRecord(c->ev_h2d[hs], c->copy));
                 c->host_used[hs] = true;
             }
         }
-        CU(cudaEventRecord(c->seg_ev[2 * i], c->copy));
-        CU(cudaStreamWaitEvent(c->stream, c->seg_ev[2 * i], 0));
+        CU(cudaEventRecord(c->ev_copied[slot], c->copy));
+        CU(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
         LaunchOptions opt;
-        CU(launch_segmented(k, ddata, doff + a0, a1 - a0, dout + a0 * k, opt, c->ws, c->stream));
-        if (!c_dev) {
-            CU(cudaEventRecord(c->seg_ev[2 * i + 1], c->stream));
-            CU(cudaStreamWaitEvent(c->d2h, c->seg_ev[2 * i + 1], 0));
-            CU(cudaMemcpyAsync(rows_dst + a0 * row_bytes, dout + a0 * k, (a1 - a0) * row_bytes,
+        if (u.piece) {
+            CU(launch_stream(k, dst, (u.hi - u.lo) / wb, dout + u.a0 * k, !u.first_piece, opt, c->ws, c->stream));
+        } else {
+            // device pointer whose word hoff[a0] is at dst
+            const uint8_t* ddata = dst - u.lo - hoff[0] * wb;
+            CU(launch_segmented(k, ddata, doff + u.a0, u.a1 - u.a0, dout + u.a0 * k, opt, c->ws, c->stream));
+        }
+        CU(cudaEventRecord(c->ev_done[slot], c->stream));
+        if (!c_dev && u.last_piece) {
+            CU(cudaStreamWaitEvent(c->d2h, c->ev_done[slot], 0));
+            CU(cudaMemcpyAsync(rows_dst + u.a0 * row_bytes, dout + u.a0 * k, (u.a1 - u.a0) * row_bytes,
                                cudaMemcpyDeviceToHost, c->d2h));
-            CU(cudaEventRecord(c->seg_ev[2 * i + 1], c->d2h));
-            if (stage_rows && (s = drain(false))) return s;
+            CU(cudaEventRecord(c->seg_ev[i], c->d2h));
+            if (stage_rows && (s = drain(false, i + 1))) return s;
         }
     }
-    if (stage_rows && (s = drain(true))) return s;
-    // the next call may reuse the scratch buffers: c->stream follows the d2h stream
-    if (!c_dev) {
-        CU(cudaEventRecord(c->seg_ev[1], c->d2h));
-        CU(cudaStreamWaitEvent(c->stream, c->seg_ev[1], 0));
-    }
+    if (stage_rows && (s = drain(true, nu))) return s;
+    // the next call may reuse the staging slots and scratch: c->stream follows the d2h stream
+    CU(cudaEventRecord(c->seg_ev[nu], c->d2h));
+    CU(cudaStreamWaitEvent(c->stream, c->seg_ev[nu], 0));
     CU(cudaStreamSynchronize(c->stream));
     return POSPOP_OK;
 }

@@ -273,18 +273,20 @@ DT = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
 def test_segmented_host_pipeline(pp, dev, orc, k):
     """Host data above 8 MiB takes the chunked path (H2D / launch / row D2H
-    overlapped, chunks cut at array boundaries): pinned and pageable data,
-    rows in pageable / pinned host memory and on the device, host and device
-    offsets, offsets[0] > 0 at an odd word, empty arrays, one array larger
-    than a chunk and arrays straddling every chunk edge."""
+    overlapped through the bounded staging ring, units cut at array
+    boundaries): pinned and pageable data, rows in pageable / pinned host
+    memory and on the device, host and device offsets, offsets[0] > 0 at an
+    odd word, empty arrays, a 100 MiB array counted in pieces by the stream
+    kernel, a 33 MiB one, and arrays straddling every unit edge."""
     wb = k // 8
     rng = np.random.default_rng(7 + k)
-    n_words = (72 << 20) // wb + 5
+    n_words = (170 << 20) // wb + 5
     data = orc.generate(6, 21 + k, n_words * wb // 8 + 1, threads=8).view(DT[k])[:n_words]
-    big_lo = n_words // 3
+    big_lo = n_words // 5
+    big = (100 << 20) // wb + 1  # longer than a staging unit: four pieces through the stream kernel
     cuts = np.concatenate([rng.integers(3, big_lo, size=5000),
-                           [big_lo, big_lo + (40 << 20) // wb, big_lo + (40 << 20) // wb],  # 40 MiB array + empty
-                           rng.integers(big_lo + (40 << 20) // wb, n_words - 1, size=3000)])
+                           [big_lo, big_lo + big, big_lo + big, big_lo + big + (33 << 20) // wb],  # + empty, 33 MiB
+                           rng.integers(big_lo + big + (33 << 20) // wb, n_words - 1, size=3000)])
     offs = np.concatenate([[3], np.sort(cuts), [n_words - 1]]).astype(np.uint64)
     want = orc.segmented(data, offs, k, threads=8)
     pinned = torch.empty(data.nbytes, dtype=torch.uint8).pin_memory()
