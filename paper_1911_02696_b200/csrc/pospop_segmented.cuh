@@ -1153,12 +1153,15 @@ struct TileCursor {
     unsigned long long* next;
     bool dyn;
     __device__ __forceinline__ bool claims(unsigned long long a) const { return dyn && a + stride >= static_end; }
-    __device__ __forceinline__ unsigned long long following(unsigned long long a, uint32_t lane) const {
-        if (a + stride < static_end) return a + stride;
-        if (!dyn) return a + stride < n ? a + stride : n;
+    __device__ __forceinline__ unsigned long long claim(uint32_t lane) const {  // warp-uniform
         unsigned long long c = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
         c = __shfl_sync(0xFFFFFFFFu, c, 0);
         return static_end + c < n ? static_end + c : n;
+    }
+    __device__ __forceinline__ unsigned long long following(unsigned long long a, uint32_t lane) const {
+        if (a + stride < static_end) return a + stride;
+        if (!dyn) return a + stride < n ? a + stride : n;
+        return claim(lane);
     }
 };
 
@@ -1210,7 +1213,14 @@ __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigne
         if (giant_bytes) giant_help<NBANK, NBANK == 1 ? 5 : 4, 16>(q, data, offsets, k, out, lane);
     };
     const unsigned long long zero[NBANK] = {};
-    if (arr >= cur.static_end) arr = next_of(cur.static_end - cur.stride);  // this warp has no static array
+    if (arr >= cur.static_end) {  // this warp has no static array
+        if (cur.dyn) {
+            ensure_waited();  // the claim counter belongs to the previous launch until it completes
+            arr = cur.claim(lane);
+        } else {
+            arr = n_arrays;
+        }
+    }
     // The loads of the next step -- later in this array or the first step of
     // the warp's next non-empty array -- are issued as soon as the tree has
     // consumed the registers, before the array's epilogue runs, so the warp
