@@ -247,7 +247,15 @@ pospop_status pospopcnt_graph_create(int k, const void* d_data, size_t len, uint
 pospop_status pospopcnt_graph_launch(pospop_graph graph, void* stream);
 void pospopcnt_graph_destroy(pospop_graph graph);
 
-/* Segmented, device-resident, asynchronous. */
+/* Segmented, device-resident, asynchronous: one launch of the adaptive kernel,
+ * which picks its schedule on the device from n_arrays and the mean array
+ * length (no host round trip for device offsets).  Consecutive launches on a
+ * stream overlap (programmatic dependent launch): a launch starts reading and
+ * counting while the previous one finishes, writes rows only after it has
+ * completed, and runs fully serialised when the device allocation holding
+ * d_data or d_offsets may hold one of the stream's recent outputs.  Rows are
+ * overwritten; the flush threshold is accepted for API symmetry (every
+ * schedule gives the same counts). */
 pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_t* d_offsets,
                                         size_t n_arrays, uint64_t* d_counts,
                                         uint32_t flush_threshold_blocks, int grid, int block,
