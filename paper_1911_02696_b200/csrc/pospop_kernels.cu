@@ -441,6 +441,7 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (const char* v = env_get("POSPOP_SEG_VARIANT")) std::sscanf(v, "%d,%d,%d,%d", &depth, &vb, &sched, &group);
     if (opt.depth) depth = opt.depth;
     const SegVariant* var = pick_segmented(nbank, depth, vb, sched, group);
+    if (var && var->sched == 16 && n > (size_t)kSegRangeSlotsHost) var = nullptr;  // range kernel: a slot per array
     if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16, 8);
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;

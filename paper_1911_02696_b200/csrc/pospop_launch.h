@@ -22,12 +22,12 @@ struct StreamWorkspace {
 
 // Bytes of one workspace allocation (u64 units): acc[0, 96), ticket (u32 at
 // u64 96), next (97), bad (98), then from u64 104 the segmented range mode's
-// kSegRangeSlots slots of 64 partial counts + 1 piece counter
+// kSegRangeSlots slots (one per array) of 64 partial counts + 1 byte counter
 // (dev::seg_range_slots: `next` + 7), then the segmented giant-array queue
 // (8 + kGiantQ entries of kGiantEntry u64; dev::GiantQueue).  Zero between
 // launches.
 constexpr int kAccChannels = 96;
-constexpr int kSegRangeSlotsHost = 4096;
+constexpr int kSegRangeSlotsHost = 16384;
 constexpr int kGiantQHost = 512;
 constexpr int kGiantEntryHost = 72;
 constexpr size_t kWorkspaceBytes =

@@ -290,7 +290,7 @@ __device__ __forceinline__ void seg_store_row(unsigned long long* out, unsigned 
 // slots (u64 104 on) and the giant-array queue after them.  Zero between
 // launches.
 // ---------------------------------------------------------------------------
-constexpr int kSegRangeSlots = 4096;   // = kSegRangeSlotsHost (pospop_launch.h)
+constexpr int kSegRangeSlots = 16384;  // = kSegRangeSlotsHost (pospop_launch.h); range mode: one per array
 constexpr int kGiantQ = 512;           // = kGiantQHost
 constexpr int kGiantEntry = 72;        // u64 per queue entry
 __device__ __forceinline__ unsigned long long* seg_range_slots(unsigned long long* next) { return next + 7; }
@@ -1340,36 +1340,38 @@ __device__ __forceinline__ void seg_tile_strided(const uint8_t* data, const unsi
 
 // ---------------------------------------------------------------------------
 // Range mode (few or huge arrays): the referenced bytes [data + off[0]*wb,
-// data + off[n]*wb) are split into one contiguous, 16-byte-aligned range per
-// warp (equal bytes), so an array of any size is spread over as many warps as
-// it covers.  A warp finds the first array touching its range with a 32-ary
-// warp search over the offsets, then walks the arrays of its range in order
-// (the tile mode's step / load-before-epilogue loop).  An array inside the
-// range gets its row stored; an array spanning ranges adds its partial counts
-// into the slot of the range holding its first byte (u64 atomics into the
-// workspace), and the warp whose piece completes the array (a piece counter
-// per slot) moves the slot into the row with atomicExch, leaving the slot zero
-// for the next launch.  Empty arrays are written by the warp owning their
-// position.  Starts before the previous launch completes (EARLY semantics).
+// data + off[n]*wb) are cut into pieces, so an array of any size is spread
+// over as many warps as it covers: 7/8 of the bytes as one contiguous,
+// 16-byte-aligned range per warp, the rest (inputs of 64 MiB and more) as
+// 128 KiB chunks that warps claim from the global counter when their range is
+// done, so faster SMs absorb the tail.  For a piece, a warp finds the first
+// array touching it with a 32-ary warp search over the offsets, then walks
+// the piece's arrays in order (the tile mode's step / load-before-epilogue
+// loop).  An array inside the piece gets its row stored; an array spanning
+// pieces adds its partial counts and its byte count into its slot (u64
+// atomics into the workspace; slot = array index), and the warp whose bytes
+// complete the array moves the slot into the row with atomicExch, leaving the
+// slot zero for the next launch.  Empty arrays are written by the piece
+// holding their position.  Starts before the previous launch completes (EARLY
+// semantics: the first row store / slot update / claim waits for it).
 // ---------------------------------------------------------------------------
 
-struct RangeSplit {
-    unsigned long long base, total;  // byte positions relative to data: [base, base + total)
-    unsigned long long W;            // ranges (warps taking part)
-    // Start of range w (w <= W), 16-byte aligned in absolute address for w >= 1.
-    __device__ __forceinline__ unsigned long long start(unsigned long long w) const {
-        if (w >= W) return base + total;
-        return base + (((total * w) / W) & ~15ull);
-    }
-    // The range holding position p (base <= p < base + total); empty ranges hold none.
-    __device__ __forceinline__ unsigned long long owner(unsigned long long p) const {
-        unsigned long long w = total ? (p - base) * W / total : 0;
-        if (w >= W) w = W - 1;
-        while (w > 0 && start(w) > p) --w;
-        while (w + 1 < W && start(w + 1) <= p) ++w;
-        return w;
-    }
+struct RangePieces {
+    unsigned long long base, end;  // byte positions relative to data: [base, end)
+    unsigned long long W;          // static pieces, one per warp taking part
+    unsigned long long S;          // bytes in the static pieces (16-byte multiple)
+    unsigned long long NC;         // dynamic chunks of kRangeChunk bytes after them
+    __device__ __forceinline__ unsigned long long pieces() const { return W + NC; }
+    // Start of piece i (i <= pieces()); 16-byte aligned in absolute address for i >= 1.
+    __device__ __forceinline__ unsigned long long start(unsigned long long i) const;
 };
+constexpr unsigned long long kRangeChunk = 128ull << 10;
+constexpr unsigned long long kRangeDynMin = 64ull << 20;  // inputs with a dynamic tail
+__device__ __forceinline__ unsigned long long RangePieces::start(unsigned long long i) const {
+    if (i <= W) return base + (((S * i) / W) & ~15ull);
+    const unsigned long long p = base + S + (i - W) * kRangeChunk;
+    return p < end ? p : end;
+}
 
 template <int NBANK, int L, int VB>
 __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsigned long long* offsets,
@@ -1389,52 +1391,23 @@ __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsign
     bool waited = false;
     auto ensure_waited = [&]() {
         if (!waited) {
-            pdl_wait_prev();  // rows and slots may belong to the previous launch on this stream
+            pdl_wait_prev();  // rows, slots and the claim counter may belong to the previous launch
             waited = true;
         }
     };
-    const unsigned long long off0 = offsets[0], offn = offsets[n_arrays];
-    RangeSplit rs;
-    const unsigned long long p0 = off0 * wb;
-    rs.base = p0 - ((reinterpret_cast<uintptr_t>(data) + p0) & 15u);  // absolute 16-byte alignment
-    rs.total = offn * wb - rs.base;
-    // at least 512 bytes per range (so no range is empty), at most one per warp and slot
-    const unsigned long long wmax = nwarps < (unsigned long long)kSegRangeSlots ? nwarps : kSegRangeSlots;
-    rs.W = rs.total / 512 < wmax ? (rs.total / 512 ? rs.total / 512 : 1) : wmax;
-    if (warp >= rs.W) {
-        ensure_waited();
-        return;
-    }
-    const unsigned long long r0 = rs.start(warp), r1 = rs.start(warp + 1);
-    const bool last = warp + 1 == rs.W;
-    if (r0 == r1 && !last) {
-        ensure_waited();
-        return;
-    }
-    // First array touching [r0, r1): smallest a with end(a) > r0 or start(a) >= r0
-    // (the latter catches empty arrays placed at r0).  32-ary search.
-    auto touches = [&](unsigned long long i) {  // monotone in i
-        return offsets[i + 1] * wb > r0 || offsets[i] * wb >= r0;
-    };
-    unsigned long long lo = 0, hi = n_arrays;  // the answer lies in [lo, hi]; hi = n_arrays: none
-    for (;;) {
-        const unsigned long long span = hi - lo;
-        if (span <= 32) {  // one probe per candidate; lanes past the span stand for `hi`
-            const bool pred = lane >= span || touches(lo + lane);
-            const uint32_t m = __ballot_sync(0xFFFFFFFFu, pred);
-            lo = m ? lo + (unsigned long long)(__ffs(m) - 1) : hi;
-            break;
-        }
-        const unsigned long long probe = lo + span * lane / 32;  // lane 0 probes lo; all < hi <= n_arrays
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, touches(probe));
-        if (m & 1u) break;  // the answer is lo
-        const int j = m ? __ffs(m) - 1 : 32;  // first true probe; the answer is in (probe_{j-1}, probe_j]
-        const unsigned long long nlo = lo + span * (j - 1) / 32 + 1;
-        if (j < 32) hi = lo + span * j / 32;
-        lo = nlo;
-    }
-    unsigned long long a = lo;
+    RangePieces rp;
+    const unsigned long long p0 = offsets[0] * wb;
+    rp.base = p0 - ((reinterpret_cast<uintptr_t>(data) + p0) & 15u);  // absolute 16-byte alignment
+    rp.end = offsets[n_arrays] * wb;
+    const unsigned long long total = rp.end - rp.base;
+    const bool dyn = total >= kRangeDynMin;
+    rp.S = dyn ? (total - total / 8) & ~15ull : total;
+    rp.NC = dyn ? (rp.end - (rp.base + rp.S) + kRangeChunk - 1) / kRangeChunk : 0;
+    // at least 512 bytes per static piece (so no piece is empty), at most one per warp
+    rp.W = rp.S / 512 < nwarps ? (rp.S / 512 ? rp.S / 512 : 1) : nwarps;
+    const unsigned long long last_piece = rp.pieces() - 1;
 
+    const unsigned long long zero[NBANK] = {};
     uint32_t carries[NBANK][L], U[NBANK][M];
     unsigned long long tot[NBANK];
 #pragma unroll
@@ -1445,124 +1418,160 @@ __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsign
         for (int i = 0; i < M; ++i) U[b][i] = 0;
         tot[b] = 0;
     }
-    const unsigned long long zero[NBANK] = {};
-    // Finishes array `arr` (bytes [s, e)) with this warp's counts `t`.
-    auto finish = [&](unsigned long long arr, unsigned long long s, unsigned long long e,
-                      const unsigned long long (&t)[NBANK]) {
-        ensure_waited();
-        if (s >= r0 && (e <= r1 || last)) {  // entirely in this range
-            seg_store_row<NBANK>(out, arr, k, lane, t);
-            return;
-        }
-        const unsigned long long key = rs.owner(s);
-        const unsigned long long pieces = rs.owner(e - 1) - key + 1;
-        unsigned long long* acc = slots + key * 65;
-        unsigned long long v0 = t[0];
-        if (NBANK == 1)
-            for (int w = 16; w >= k; w >>= 1) v0 += __shfl_down_sync(0xFFFFFFFFu, v0, w);
-        if (NBANK == 2) {
-            atomicAdd(acc + lane, v0);
-            atomicAdd(acc + 32 + lane, t[NBANK - 1]);
-        } else if ((int)lane < k) {
-            atomicAdd(acc + lane, v0);
-        }
-        __threadfence();
-        __syncwarp();
-        unsigned long long done = lane == 0 ? atomicAdd(acc + 64, 1ull) : 0ull;
-        done = __shfl_sync(0xFFFFFFFFu, done, 0);
-        if (done + 1 == pieces) {  // the last piece: move the slot into the row
-            __threadfence();
-            unsigned long long* row = out + arr * (unsigned long long)k;
-            for (int c = (int)lane; c < k; c += 32) row[c] = atomicExch(acc + c, 0ull);
-            if (lane == 0) atomicExch(acc + 64, 0ull);
-        }
-    };
-    // Segment of array `arr` inside the range, as a vector view; false if empty.
-    auto segment = [&](unsigned long long arr, unsigned long long& s, unsigned long long& e, SegView& v) {
-        s = offsets[arr] * wb;
-        e = offsets[arr + 1] * wb;
-        const unsigned long long lo_b = s > r0 ? s : r0, hi_b = e < r1 || last ? e : r1;
-        v = seg_view<VB>(data, lo_b / wb, hi_b > lo_b ? hi_b / wb : lo_b / wb, (int)wb);
-    };
-    auto in_range = [&](unsigned long long arr) {  // array `arr` still starts before r1 (or the last range)
-        return arr < n_arrays && (last || offsets[arr] * wb < r1);
-    };
-    // skip empty arrays (writing the zero rows this range owns) to the first non-empty segment
-    unsigned long long s = 0, e = 0;
-    SegView v;
-    for (;; ++a) {
-        if (!in_range(a)) {
-            ensure_waited();
-            return;
-        }
-        segment(a, s, e, v);
-        if (v.nv) break;
-        if (s == e && s >= r0) {  // an empty array at a position this range owns
-            ensure_waited();
-            seg_store_row<NBANK>(out, a, k, lane, zero);
-        }
-    }
-    uint32_t nb = 0;
-    unsigned long long t = 0;
-    uint32_t r[REGS];
-    seg_load<VB, VPT>(v, t, lane, r);
-    for (;;) {
-#pragma unroll
-        for (int b = 0; b < NBANK; ++b)
-            plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r) : Tree<L, 2>::run(carries[b], r + b));
-        ++nb;
-        t += STEP;
-        const bool seg_done = t >= v.nv;
-        unsigned long long a_n = a, s_n = s, e_n = e;
-        SegView vn = v;
-        bool more = true;
-        if (seg_done) {  // next non-empty segment of this range
-            t = 0;
-            more = false;
-            for (a_n = a + 1; in_range(a_n); ++a_n) {
-                segment(a_n, s_n, e_n, vn);
-                if (vn.nv) {
-                    more = true;
-                    break;
-                }
-                if (s_n == e_n) {
-                    ensure_waited();
-                    seg_store_row<NBANK>(out, a_n, k, lane, zero);
-                }
+
+    // Counts piece `pc` = bytes [r0, r1).
+    auto run_piece = [&](unsigned long long pc) {
+        const unsigned long long r0 = rp.start(pc), r1 = rp.start(pc + 1);
+        const bool last = pc == last_piece;
+        // First array touching the piece: smallest a with end(a) > r0 or start(a) >= r0
+        // (the latter catches empty arrays placed at r0).  32-ary search.
+        auto touches = [&](unsigned long long i) {  // monotone in i
+            return offsets[i + 1] * wb > r0 || offsets[i] * wb >= r0;
+        };
+        unsigned long long lo = 0, hi = n_arrays;  // the answer lies in [lo, hi]; hi = n_arrays: none
+        for (;;) {
+            const unsigned long long span = hi - lo;
+            if (span <= 32) {  // one probe per candidate; lanes past the span stand for `hi`
+                const bool pred = lane >= span || touches(lo + lane);
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, pred);
+                lo = m ? lo + (unsigned long long)(__ffs(m) - 1) : hi;
+                break;
             }
+            const unsigned long long probe = lo + span * lane / 32;  // lane 0 probes lo; all < hi <= n_arrays
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, touches(probe));
+            if (m & 1u) break;  // the answer is lo
+            const int j = m ? __ffs(m) - 1 : 32;  // first true probe; the answer is in (probe_{j-1}, probe_j]
+            const unsigned long long nlo = lo + span * (j - 1) / 32 + 1;
+            if (j < 32) hi = lo + span * j / 32;
+            lo = nlo;
         }
-        if (more) seg_load<VB, VPT>(vn, t, lane, r);  // in flight during the epilogue below
-        if (seg_done || nb == (1u << M) - 1u) {
-#pragma unroll
-            for (int b = 0; b < NBANK; ++b)
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
-                    U[b][i] = 0;
-                }
-            nb = 0;
-        }
-        if (seg_done) {
-#pragma unroll
-            for (int b = 0; b < NBANK; ++b)
-#pragma unroll
-                for (int j = 0; j < L; ++j) {
-                    tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
-                    carries[b][j] = 0;
-                }
-            finish(a, s, e, tot);
-#pragma unroll
-            for (int b = 0; b < NBANK; ++b) tot[b] = 0;
-            if (!more) {
-                ensure_waited();
+        unsigned long long a = lo;
+        // Finishes array `arr` (bytes [s, e)) with this piece's counts `t` over `seg` bytes.
+        auto finish = [&](unsigned long long arr, unsigned long long s, unsigned long long e, unsigned long long seg,
+                          const unsigned long long (&t)[NBANK]) {
+            ensure_waited();
+            if (s >= r0 && (e <= r1 || last)) {  // entirely in this piece
+                seg_store_row<NBANK>(out, arr, k, lane, t);
                 return;
             }
-            a = a_n;
-            s = s_n;
-            e = e_n;
-            v = vn;
+            unsigned long long* acc = slots + arr * 65;
+            unsigned long long v0 = t[0];
+            if (NBANK == 1)
+                for (int w = 16; w >= k; w >>= 1) v0 += __shfl_down_sync(0xFFFFFFFFu, v0, w);
+            if (NBANK == 2) {
+                atomicAdd(acc + lane, v0);
+                atomicAdd(acc + 32 + lane, t[NBANK - 1]);
+            } else if ((int)lane < k) {
+                atomicAdd(acc + lane, v0);
+            }
+            __threadfence();
+            __syncwarp();
+            unsigned long long done = lane == 0 ? atomicAdd(acc + 64, seg) : 0ull;
+            done = __shfl_sync(0xFFFFFFFFu, done, 0);
+            if (done + seg == e - s) {  // this piece completes the array: move the slot into the row
+                __threadfence();
+                unsigned long long* row = out + arr * (unsigned long long)k;
+                for (int c = (int)lane; c < k; c += 32) row[c] = atomicExch(acc + c, 0ull);
+                if (lane == 0) atomicExch(acc + 64, 0ull);
+            }
+        };
+        // Segment of array `arr` inside the piece, as a vector view (nv = 0: empty).
+        auto segment = [&](unsigned long long arr, unsigned long long& s, unsigned long long& e,
+                           unsigned long long& seg, SegView& v) {
+            s = offsets[arr] * wb;
+            e = offsets[arr + 1] * wb;
+            const unsigned long long lo_b = s > r0 ? s : r0, hi_b = e < r1 || last ? e : r1;
+            seg = hi_b > lo_b ? hi_b - lo_b : 0;
+            v = seg_view<VB>(data, lo_b / wb, hi_b > lo_b ? hi_b / wb : lo_b / wb, (int)wb);
+        };
+        auto in_piece = [&](unsigned long long arr) {  // array `arr` still starts in this piece
+            return arr < n_arrays && (last || offsets[arr] * wb < r1);
+        };
+        // skip empty arrays (writing the zero rows this piece owns) to the first non-empty segment
+        unsigned long long s = 0, e = 0, seg = 0;
+        SegView v;
+        for (;; ++a) {
+            if (!in_piece(a)) return;
+            segment(a, s, e, seg, v);
+            if (v.nv) break;
+            if (s == e && s >= r0) {  // an empty array at a position this piece owns
+                ensure_waited();
+                seg_store_row<NBANK>(out, a, k, lane, zero);
+            }
+        }
+        uint32_t nb = 0;
+        unsigned long long t = 0;
+        uint32_t r[REGS];
+        seg_load<VB, VPT>(v, t, lane, r);
+        for (;;) {
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b)
+                plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r)
+                                                    : Tree<L, 2>::run(carries[b], r + b));
+            ++nb;
+            t += STEP;
+            const bool seg_done = t >= v.nv;
+            unsigned long long a_n = a, s_n = s, e_n = e, seg_n = seg;
+            SegView vn = v;
+            bool more = true;
+            if (seg_done) {  // next non-empty segment of this piece
+                t = 0;
+                more = false;
+                for (a_n = a + 1; in_piece(a_n); ++a_n) {
+                    segment(a_n, s_n, e_n, seg_n, vn);
+                    if (vn.nv) {
+                        more = true;
+                        break;
+                    }
+                    if (s_n == e_n) {
+                        ensure_waited();
+                        seg_store_row<NBANK>(out, a_n, k, lane, zero);
+                    }
+                }
+            }
+            if (more) seg_load<VB, VPT>(vn, t, lane, r);  // in flight during the epilogue below
+            if (seg_done || nb == (1u << M) - 1u) {
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                        U[b][i] = 0;
+                    }
+                nb = 0;
+            }
+            if (seg_done) {
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                    for (int j = 0; j < L; ++j) {
+                        tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
+                        carries[b][j] = 0;
+                    }
+                finish(a, s, e, seg, tot);
+#pragma unroll
+                for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+                if (!more) return;
+                a = a_n;
+                s = s_n;
+                e = e_n;
+                seg = seg_n;
+                v = vn;
+            }
+        }
+    };
+
+    if (warp < rp.W) run_piece(warp);
+    if (rp.NC) {  // the dynamic tail: chunks claimed one at a time (the counter belongs to the previous launch)
+        ensure_waited();
+        for (;;) {
+            unsigned long long c = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+            c = __shfl_sync(0xFFFFFFFFu, c, 0);
+            if (c >= rp.NC) break;
+            run_piece(rp.W + c);
         }
     }
+    ensure_waited();
 }
 
 template <int NBANK, int L, int VB, int MINB>
@@ -1570,9 +1579,10 @@ __global__ void __launch_bounds__(256, MINB) segmented_range_kernel(const uint8_
                                                                     const unsigned long long* offsets,
                                                                     unsigned long long n_arrays, int k, uint32_t,
                                                                     unsigned long long* out, unsigned long long* next,
-                                                                    unsigned int*, unsigned) {
+                                                                    unsigned int* ticket, unsigned) {
     pdl_allow_next();
-    seg_range_loop<NBANK, L, VB>(data, offsets, n_arrays, k, out, next);
+    seg_range_loop<NBANK, L, VB>(data, offsets, n_arrays, k, out, next);  // n_arrays <= kSegRangeSlots (launcher)
+    seg_claims_done(next, ticket);  // every warp has waited
 }
 
 // MODE bit 0: CTA c takes the contiguous array range [c n / G, (c + 1) n / G)
@@ -1641,7 +1651,7 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
     const unsigned long long giant = (unsigned long long)(thresholds >> 24) << 14;
     const GiantQueue q = seg_giant_queue(next, giant);
     const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
-    if (n_arrays < range_rounds * nwarps) {
+    if (n_arrays < range_rounds * nwarps && n_arrays <= (unsigned long long)kSegRangeSlots) {
         seg_range_loop<NBANK, NBANK == 1 ? 5 : 4, 16>(data, offsets, n_arrays, k, out, next);
         seg_launch_done(next, ticket, q);  // every warp has waited
         return;
