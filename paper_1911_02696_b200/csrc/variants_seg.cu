@@ -38,7 +38,7 @@ const SegVariant kVariants[] = {
     SGTE(1, 7, 32, 1), SGTE(1, 6, 32, 1), SGTE(1, 6, 32, 2), SGTE(2, 6, 32, 1),
     SGTD(1, 7, 32, 1), SGTD(1, 6, 32, 1), SGTD(1, 6, 32, 2), SGTD(2, 6, 32, 1), SGTD(2, 5, 32, 2), SGTD(2, 5, 16, 2),
     SGTD(1, 6, 16, 2), SGTD(1, 5, 16, 2), SGTD(1, 5, 32, 2),
-    SGR(1, 5, 16, 2), SGR(2, 5, 16, 2), SGR(1, 7, 32, 1), SGR(2, 6, 32, 1),
+    SGR(1, 5, 16, 2), SGR(2, 5, 16, 2), SGR(1, 7, 32, 1), SGR(2, 6, 32, 1), SGR(1, 5, 32, 2), SGR(1, 6, 32, 1),
     SGTB(1, 7, 32, 1), SGTB(1, 6, 32, 1), SGTB(1, 6, 32, 2), SGTB(2, 6, 32, 1), SGTB(2, 5, 32, 2), SGPEH(1, 5), SGPEH(1, 4), SGPEH(2, 4),
     SGC(1, 5, 3), SGC(1, 5, 2), SGC(1, 4, 4), SGC(2, 3, 4), SGC(2, 4, 2),
     SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),

@@ -395,7 +395,8 @@ _GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,
             "5,16,6", "5,32,6", "4,16,6", "4,32,6", "4,16,7", "4,32,7",  # + bit-plane epilogue (sched 6/7)
             "5,16,8", "5,16,9", "5,16,10,3", "5,16,10,2", "4,16,10,4"]  # sched 8/9/10
 _TILE = ["7,32,11,1", "7,16,11,1", "6,32,11,1", "6,32,11,2", "6,16,11,2", "5,32,11,2", "7,32,12,1", "6,32,12,1",
-         "6,32,12,2", "7,32,13,1", "6,32,13,2", "7,32,14,1", "6,32,14,1", "6,32,14,2", "5,16,16,2", "7,32,16,1"]
+         "6,32,12,2", "7,32,13,1", "6,32,13,2", "7,32,14,1", "6,32,14,1", "6,32,14,2", "5,16,16,2", "7,32,16,1", "5,32,16,2",
+         "6,32,16,1"]
 SEG_VARIANTS = {
     8: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
     16: ["5,16,0", "5,16,1", "4,16,2", "5,16,2", "4,32,2", "5,32,2", "5,16,3", "5,32,3"] + _GROUPED + _TILE,
