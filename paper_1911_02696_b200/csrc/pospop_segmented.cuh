@@ -270,6 +270,39 @@ __device__ __forceinline__ void seg_load(const SegView& v, unsigned long long t,
     }
 }
 
+// seg_load for a whole CTA counting one view together: thread `tid` of
+// `nthreads` loads vectors t + tid + q * nthreads (q < VPT), so each step of
+// the CTA reads one contiguous window of nthreads * VPT vectors.
+template <int VB, int VPT>
+__device__ __forceinline__ void seg_load_cta(const SegView& v, unsigned long long t, unsigned tid, unsigned nthreads,
+                                             uint32_t (&r)[VPT * (VB / 4)]) {
+    constexpr int RPV = VB / 4;
+    if (t >= v.f0 && t + (unsigned long long)nthreads * VPT <= v.f1) {
+#pragma unroll
+        for (int q = 0; q < VPT; ++q) {
+            uint32_t x[RPV];
+            POSPOP_CHECK(t + tid + (unsigned long long)nthreads * q < v.nv);
+            ldg_stream<VB, 0>(v.base + (t + tid + (unsigned long long)nthreads * q) * VB, x);
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < VPT; ++q) {
+            const unsigned long long idx = t + tid + (unsigned long long)nthreads * q;
+            uint32_t x[RPV];
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) x[j] = 0;
+            if (idx < v.nv) {
+                ldg_stream<VB, 0>(v.base + idx * VB, x);
+                if (idx == 0 || idx + 1 == v.nv) mask_bytes<VB>(x, idx == 0 ? v.lo : 0, idx + 1 == v.nv ? v.hi : VB);
+            }
+#pragma unroll
+            for (int j = 0; j < RPV; ++j) r[q * RPV + j] = x[j];
+        }
+    }
+}
+
 template <int NBANK>
 __device__ __forceinline__ void seg_store_row(unsigned long long* out, unsigned long long arr, int k, uint32_t lane,
                                               const unsigned long long (&tot)[NBANK]) {
@@ -1340,38 +1373,40 @@ __device__ __forceinline__ void seg_tile_strided(const uint8_t* data, const unsi
 
 // ---------------------------------------------------------------------------
 // Range mode (few or huge arrays): the referenced bytes [data + off[0]*wb,
-// data + off[n]*wb) are cut into pieces, so an array of any size is spread
-// over as many warps as it covers: 7/8 of the bytes as one contiguous,
-// 16-byte-aligned range per warp, the rest (inputs of 64 MiB and more) as
-// 128 KiB chunks that warps claim from the global counter when their range is
-// done, so faster SMs absorb the tail.  For a piece, a warp finds the first
-// array touching it with a 32-ary warp search over the offsets, then walks
-// the piece's arrays in order (the tile mode's step / load-before-epilogue
-// loop).  An array inside the piece gets its row stored; an array spanning
-// pieces adds its partial counts and its byte count into its slot (u64
-// atomics into the workspace; slot = array index), and the warp whose bytes
-// complete the array moves the slot into the row with atomicExch, leaving the
-// slot zero for the next launch.  Empty arrays are written by the piece
-// holding their position.  Starts before the previous launch completes (EARLY
-// semantics: the first row store / slot update / claim waits for it).
+// data + off[n]*wb) are split into one contiguous, 16-byte-aligned range per
+// CTA (equal bytes), so an array of any size is spread over as many SMs as it
+// covers.  The CTA's warps count its range together: a 32-ary warp search over
+// the offsets finds the first array touching the range, then the CTA walks
+// the range's arrays in order, every thread loading vectors tid, tid +
+// nthreads, ... of each step (one contiguous window per CTA step, like the
+// stream kernel's CTA tiles; the next step's loads -- possibly the next
+// array's -- are issued before a segment's epilogue).  At the end of a segment
+// the warps' counts are summed in shared memory; warp 0 stores the row of an
+// array inside the range, or adds the partial counts of an array spanning
+// ranges into that array's workspace slot (u64 atomics; slot = array index)
+// and, if its range completes the array (a per-slot counter of the ranges it
+// covers), moves the slot into the row with atomicExch, leaving the slot zero
+// for the next launch.  Empty arrays are written by the CTA owning their
+// position.  Starts before the previous launch completes (EARLY semantics:
+// the first row store / slot update waits for it).
 // ---------------------------------------------------------------------------
-
-struct RangePieces {
-    unsigned long long base, end;  // byte positions relative to data: [base, end)
-    unsigned long long W;          // static pieces, one per warp taking part
-    unsigned long long S;          // bytes in the static pieces (16-byte multiple)
-    unsigned long long NC;         // dynamic chunks of kRangeChunk bytes after them
-    __device__ __forceinline__ unsigned long long pieces() const { return W + NC; }
-    // Start of piece i (i <= pieces()); 16-byte aligned in absolute address for i >= 1.
-    __device__ __forceinline__ unsigned long long start(unsigned long long i) const;
+struct RangeSplit {
+    unsigned long long base, total;  // byte positions relative to data: [base, base + total)
+    unsigned long long W;            // ranges (CTAs taking part)
+    // Start of range w (w <= W), 16-byte aligned in absolute address for w >= 1.
+    __device__ __forceinline__ unsigned long long start(unsigned long long w) const {
+        if (w >= W) return base + total;
+        return base + (((total * w) / W) & ~15ull);
+    }
+    // The range holding position p (base <= p < base + total); empty ranges hold none.
+    __device__ __forceinline__ unsigned long long owner(unsigned long long p) const {
+        unsigned long long w = total ? (p - base) * W / total : 0;
+        if (w >= W) w = W - 1;
+        while (w > 0 && start(w) > p) --w;
+        while (w + 1 < W && start(w + 1) <= p) ++w;
+        return w;
+    }
 };
-constexpr unsigned long long kRangeChunk = 128ull << 10;
-constexpr unsigned long long kRangeDynMin = 64ull << 20;  // inputs with a dynamic tail
-__device__ __forceinline__ unsigned long long RangePieces::start(unsigned long long i) const {
-    if (i <= W) return base + (((S * i) / W) & ~15ull);
-    const unsigned long long p = base + S + (i - W) * kRangeChunk;
-    return p < end ? p : end;
-}
 
 template <int NBANK, int L, int VB>
 __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsigned long long* offsets,
@@ -1381,33 +1416,122 @@ __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsign
     constexpr int REGS = NBANK << L;
     constexpr int RPV = VB / 4;
     constexpr int VPT = REGS / RPV;
-    constexpr unsigned long long STEP = 32ull * VPT;
-    const uint32_t lane = threadIdx.x & 31u;
+    constexpr int kMaxWarps = 8;  // blockDim.x <= 256
+    __shared__ unsigned long long s_tot[kMaxWarps][64];
+    const uint32_t lane = threadIdx.x & 31u, wic = threadIdx.x >> 5, nwc = blockDim.x >> 5;
+    const unsigned long long step = (unsigned long long)blockDim.x * VPT;  // vectors per CTA step
     const unsigned long long wb = (unsigned long long)(k >> 3);
-    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
-    const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
     unsigned long long* slots = seg_range_slots(next);
     const PlaneXpose xp(lane);
     bool waited = false;
-    auto ensure_waited = [&]() {
+    auto ensure_waited = [&]() {  // block-uniform
         if (!waited) {
-            pdl_wait_prev();  // rows, slots and the claim counter may belong to the previous launch
+            pdl_wait_prev();  // rows and slots may belong to the previous launch on this stream
             waited = true;
         }
     };
-    RangePieces rp;
+    RangeSplit rs;
     const unsigned long long p0 = offsets[0] * wb;
-    rp.base = p0 - ((reinterpret_cast<uintptr_t>(data) + p0) & 15u);  // absolute 16-byte alignment
-    rp.end = offsets[n_arrays] * wb;
-    const unsigned long long total = rp.end - rp.base;
-    const bool dyn = total >= kRangeDynMin;
-    rp.S = dyn ? (total - total / 8) & ~15ull : total;
-    rp.NC = dyn ? (rp.end - (rp.base + rp.S) + kRangeChunk - 1) / kRangeChunk : 0;
-    // at least 512 bytes per static piece (so no piece is empty), at most one per warp
-    rp.W = rp.S / 512 < nwarps ? (rp.S / 512 ? rp.S / 512 : 1) : nwarps;
-    const unsigned long long last_piece = rp.pieces() - 1;
+    rs.base = p0 - ((reinterpret_cast<uintptr_t>(data) + p0) & 15u);  // absolute 16-byte alignment
+    rs.total = offsets[n_arrays] * wb - rs.base;
+    // at least 4 KiB per range (so no range is empty), at most one per CTA
+    rs.W = rs.total / 4096 < gridDim.x ? (rs.total / 4096 ? rs.total / 4096 : 1) : gridDim.x;
+    if (blockIdx.x >= rs.W) {
+        ensure_waited();
+        return;
+    }
+    const unsigned long long r0 = rs.start(blockIdx.x), r1 = rs.start(blockIdx.x + 1);
+    const bool last = blockIdx.x + 1 == rs.W;
+    // First array touching [r0, r1): smallest a with end(a) > r0 or start(a) >= r0
+    // (the latter catches empty arrays placed at r0).  32-ary search, every warp.
+    auto touches = [&](unsigned long long i) {  // monotone in i
+        return offsets[i + 1] * wb > r0 || offsets[i] * wb >= r0;
+    };
+    unsigned long long lo = 0, hi = n_arrays;  // the answer lies in [lo, hi]; hi = n_arrays: none
+    for (;;) {
+        const unsigned long long span = hi - lo;
+        if (span <= 32) {  // one probe per candidate; lanes past the span stand for `hi`
+            const bool pred = lane >= span || touches(lo + lane);
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, pred);
+            lo = m ? lo + (unsigned long long)(__ffs(m) - 1) : hi;
+            break;
+        }
+        const unsigned long long probe = lo + span * lane / 32;  // lane 0 probes lo; all < hi <= n_arrays
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, touches(probe));
+        if (m & 1u) break;  // the answer is lo
+        const int j = m ? __ffs(m) - 1 : 32;  // first true probe; the answer is in (probe_{j-1}, probe_j]
+        const unsigned long long nlo = lo + span * (j - 1) / 32 + 1;
+        if (j < 32) hi = lo + span * j / 32;
+        lo = nlo;
+    }
+    unsigned long long a = lo;
 
     const unsigned long long zero[NBANK] = {};
+    // The CTA finishes array `arr` (bytes [s, e)) with its warps' counts `t`.  Block-uniform.
+    auto finish = [&](unsigned long long arr, unsigned long long s, unsigned long long e,
+                      const unsigned long long (&t)[NBANK]) {
+        ensure_waited();
+        unsigned long long v0 = t[0];
+        if (NBANK == 1)
+            for (int w = 16; w >= k; w >>= 1) v0 += __shfl_down_sync(0xFFFFFFFFu, v0, w);
+        s_tot[wic][lane] = v0;
+        if (NBANK == 2) s_tot[wic][32 + lane] = t[NBANK - 1];
+        __syncthreads();
+        if (wic == 0) {
+            unsigned long long sum0 = 0, sum1 = 0;
+            for (uint32_t w = 0; w < nwc; ++w) {
+                sum0 += s_tot[w][lane];
+                if (NBANK == 2) sum1 += s_tot[w][32 + lane];
+            }
+            const bool mine = (int)lane < (NBANK == 2 ? 32 : k);
+            if (s >= r0 && (e <= r1 || last)) {  // entirely in this range
+                unsigned long long* row = out + arr * (unsigned long long)k;
+                if (mine) row[lane] = sum0;
+                if (NBANK == 2) row[32 + lane] = sum1;
+            } else {
+                const unsigned long long pieces = rs.owner(e - 1) - rs.owner(s) + 1;
+                unsigned long long* acc = slots + arr * 65;
+                if (mine) atomicAdd(acc + lane, sum0);
+                if (NBANK == 2) atomicAdd(acc + 32 + lane, sum1);
+                __threadfence();
+                __syncwarp();
+                unsigned long long done = lane == 0 ? atomicAdd(acc + 64, 1ull) : 0ull;
+                done = __shfl_sync(0xFFFFFFFFu, done, 0);
+                if (done + 1 == pieces) {  // this range completes the array: move the slot into the row
+                    __threadfence();
+                    unsigned long long* row = out + arr * (unsigned long long)k;
+                    for (int c = (int)lane; c < k; c += 32) row[c] = atomicExch(acc + c, 0ull);
+                    if (lane == 0) atomicExch(acc + 64, 0ull);
+                }
+            }
+        }
+        __syncthreads();  // s_tot is reused by the next segment
+    };
+    // Segment of array `arr` inside the range, as a vector view (nv = 0: empty).
+    auto segment = [&](unsigned long long arr, unsigned long long& s, unsigned long long& e, SegView& v) {
+        s = offsets[arr] * wb;
+        e = offsets[arr + 1] * wb;
+        const unsigned long long lo_b = s > r0 ? s : r0, hi_b = e < r1 || last ? e : r1;
+        v = seg_view<VB>(data, lo_b / wb, hi_b > lo_b ? hi_b / wb : lo_b / wb, (int)wb);
+    };
+    auto in_range = [&](unsigned long long arr) {  // array `arr` still starts in this range
+        return arr < n_arrays && (last || offsets[arr] * wb < r1);
+    };
+    auto zero_row = [&](unsigned long long arr) {  // an empty array at a position this range owns
+        ensure_waited();
+        if (wic == 0) seg_store_row<NBANK>(out, arr, k, lane, zero);
+    };
+    unsigned long long s = 0, e = 0;
+    SegView v;
+    for (;; ++a) {  // first non-empty segment
+        if (!in_range(a)) {
+            ensure_waited();
+            return;
+        }
+        segment(a, s, e, v);
+        if (v.nv) break;
+        if (s == e && s >= r0) zero_row(a);
+    }
     uint32_t carries[NBANK][L], U[NBANK][M];
     unsigned long long tot[NBANK];
 #pragma unroll
@@ -1418,160 +1542,64 @@ __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsign
         for (int i = 0; i < M; ++i) U[b][i] = 0;
         tot[b] = 0;
     }
-
-    // Counts piece `pc` = bytes [r0, r1).
-    auto run_piece = [&](unsigned long long pc) {
-        const unsigned long long r0 = rp.start(pc), r1 = rp.start(pc + 1);
-        const bool last = pc == last_piece;
-        // First array touching the piece: smallest a with end(a) > r0 or start(a) >= r0
-        // (the latter catches empty arrays placed at r0).  32-ary search.
-        auto touches = [&](unsigned long long i) {  // monotone in i
-            return offsets[i + 1] * wb > r0 || offsets[i] * wb >= r0;
-        };
-        unsigned long long lo = 0, hi = n_arrays;  // the answer lies in [lo, hi]; hi = n_arrays: none
-        for (;;) {
-            const unsigned long long span = hi - lo;
-            if (span <= 32) {  // one probe per candidate; lanes past the span stand for `hi`
-                const bool pred = lane >= span || touches(lo + lane);
-                const uint32_t m = __ballot_sync(0xFFFFFFFFu, pred);
-                lo = m ? lo + (unsigned long long)(__ffs(m) - 1) : hi;
-                break;
-            }
-            const unsigned long long probe = lo + span * lane / 32;  // lane 0 probes lo; all < hi <= n_arrays
-            const uint32_t m = __ballot_sync(0xFFFFFFFFu, touches(probe));
-            if (m & 1u) break;  // the answer is lo
-            const int j = m ? __ffs(m) - 1 : 32;  // first true probe; the answer is in (probe_{j-1}, probe_j]
-            const unsigned long long nlo = lo + span * (j - 1) / 32 + 1;
-            if (j < 32) hi = lo + span * j / 32;
-            lo = nlo;
-        }
-        unsigned long long a = lo;
-        // Finishes array `arr` (bytes [s, e)) with this piece's counts `t` over `seg` bytes.
-        auto finish = [&](unsigned long long arr, unsigned long long s, unsigned long long e, unsigned long long seg,
-                          const unsigned long long (&t)[NBANK]) {
-            ensure_waited();
-            if (s >= r0 && (e <= r1 || last)) {  // entirely in this piece
-                seg_store_row<NBANK>(out, arr, k, lane, t);
-                return;
-            }
-            unsigned long long* acc = slots + arr * 65;
-            unsigned long long v0 = t[0];
-            if (NBANK == 1)
-                for (int w = 16; w >= k; w >>= 1) v0 += __shfl_down_sync(0xFFFFFFFFu, v0, w);
-            if (NBANK == 2) {
-                atomicAdd(acc + lane, v0);
-                atomicAdd(acc + 32 + lane, t[NBANK - 1]);
-            } else if ((int)lane < k) {
-                atomicAdd(acc + lane, v0);
-            }
-            __threadfence();
-            __syncwarp();
-            unsigned long long done = lane == 0 ? atomicAdd(acc + 64, seg) : 0ull;
-            done = __shfl_sync(0xFFFFFFFFu, done, 0);
-            if (done + seg == e - s) {  // this piece completes the array: move the slot into the row
-                __threadfence();
-                unsigned long long* row = out + arr * (unsigned long long)k;
-                for (int c = (int)lane; c < k; c += 32) row[c] = atomicExch(acc + c, 0ull);
-                if (lane == 0) atomicExch(acc + 64, 0ull);
-            }
-        };
-        // Segment of array `arr` inside the piece, as a vector view (nv = 0: empty).
-        auto segment = [&](unsigned long long arr, unsigned long long& s, unsigned long long& e,
-                           unsigned long long& seg, SegView& v) {
-            s = offsets[arr] * wb;
-            e = offsets[arr + 1] * wb;
-            const unsigned long long lo_b = s > r0 ? s : r0, hi_b = e < r1 || last ? e : r1;
-            seg = hi_b > lo_b ? hi_b - lo_b : 0;
-            v = seg_view<VB>(data, lo_b / wb, hi_b > lo_b ? hi_b / wb : lo_b / wb, (int)wb);
-        };
-        auto in_piece = [&](unsigned long long arr) {  // array `arr` still starts in this piece
-            return arr < n_arrays && (last || offsets[arr] * wb < r1);
-        };
-        // skip empty arrays (writing the zero rows this piece owns) to the first non-empty segment
-        unsigned long long s = 0, e = 0, seg = 0;
-        SegView v;
-        for (;; ++a) {
-            if (!in_piece(a)) return;
-            segment(a, s, e, seg, v);
-            if (v.nv) break;
-            if (s == e && s >= r0) {  // an empty array at a position this piece owns
-                ensure_waited();
-                seg_store_row<NBANK>(out, a, k, lane, zero);
+    uint32_t nb = 0;
+    unsigned long long t = 0;
+    uint32_t r[REGS];
+    seg_load_cta<VB, VPT>(v, t, threadIdx.x, blockDim.x, r);
+    for (;;) {
+#pragma unroll
+        for (int b = 0; b < NBANK; ++b)
+            plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r) : Tree<L, 2>::run(carries[b], r + b));
+        ++nb;
+        t += step;
+        const bool seg_done = t >= v.nv;
+        unsigned long long a_n = a, s_n = s, e_n = e;
+        SegView vn = v;
+        bool more = true;
+        if (seg_done) {  // next non-empty segment of this range
+            t = 0;
+            more = false;
+            for (a_n = a + 1; in_range(a_n); ++a_n) {
+                segment(a_n, s_n, e_n, vn);
+                if (vn.nv) {
+                    more = true;
+                    break;
+                }
+                if (s_n == e_n) zero_row(a_n);
             }
         }
-        uint32_t nb = 0;
-        unsigned long long t = 0;
-        uint32_t r[REGS];
-        seg_load<VB, VPT>(v, t, lane, r);
-        for (;;) {
+        if (more) seg_load_cta<VB, VPT>(vn, t, threadIdx.x, blockDim.x, r);  // in flight during the epilogue
+        if (seg_done || nb == (1u << M) - 1u) {
 #pragma unroll
             for (int b = 0; b < NBANK; ++b)
-                plane_count_add<M>(U[b], NBANK == 1 ? Tree<L, 1>::run(carries[b], r)
-                                                    : Tree<L, 2>::run(carries[b], r + b));
-            ++nb;
-            t += STEP;
-            const bool seg_done = t >= v.nv;
-            unsigned long long a_n = a, s_n = s, e_n = e, seg_n = seg;
-            SegView vn = v;
-            bool more = true;
-            if (seg_done) {  // next non-empty segment of this piece
-                t = 0;
-                more = false;
-                for (a_n = a + 1; in_piece(a_n); ++a_n) {
-                    segment(a_n, s_n, e_n, seg_n, vn);
-                    if (vn.nv) {
-                        more = true;
-                        break;
-                    }
-                    if (s_n == e_n) {
-                        ensure_waited();
-                        seg_store_row<NBANK>(out, a_n, k, lane, zero);
-                    }
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
+                    U[b][i] = 0;
                 }
-            }
-            if (more) seg_load<VB, VPT>(vn, t, lane, r);  // in flight during the epilogue below
-            if (seg_done || nb == (1u << M) - 1u) {
-#pragma unroll
-                for (int b = 0; b < NBANK; ++b)
-#pragma unroll
-                    for (int i = 0; i < M; ++i) {
-                        tot[b] += (unsigned long long)xp.column_popc(U[b][i]) << (L + i);
-                        U[b][i] = 0;
-                    }
-                nb = 0;
-            }
-            if (seg_done) {
-#pragma unroll
-                for (int b = 0; b < NBANK; ++b)
-#pragma unroll
-                    for (int j = 0; j < L; ++j) {
-                        tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
-                        carries[b][j] = 0;
-                    }
-                finish(a, s, e, seg, tot);
-#pragma unroll
-                for (int b = 0; b < NBANK; ++b) tot[b] = 0;
-                if (!more) return;
-                a = a_n;
-                s = s_n;
-                e = e_n;
-                seg = seg_n;
-                v = vn;
-            }
+            nb = 0;
         }
-    };
-
-    if (warp < rp.W) run_piece(warp);
-    if (rp.NC) {  // the dynamic tail: chunks claimed one at a time (the counter belongs to the previous launch)
-        ensure_waited();
-        for (;;) {
-            unsigned long long c = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
-            c = __shfl_sync(0xFFFFFFFFu, c, 0);
-            if (c >= rp.NC) break;
-            run_piece(rp.W + c);
+        if (seg_done) {
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    tot[b] += (unsigned long long)xp.column_popc(carries[b][j]) << j;
+                    carries[b][j] = 0;
+                }
+            finish(a, s, e, tot);
+#pragma unroll
+            for (int b = 0; b < NBANK; ++b) tot[b] = 0;
+            if (!more) {
+                ensure_waited();
+                return;
+            }
+            a = a_n;
+            s = s_n;
+            e = e_n;
+            v = vn;
         }
     }
-    ensure_waited();
 }
 
 template <int NBANK, int L, int VB, int MINB>
