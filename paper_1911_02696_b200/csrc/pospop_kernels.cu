@@ -443,6 +443,17 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     const SegVariant* var = pick_segmented(nbank, depth, vb, sched, group);
     if (var && var->sched == 16 && n > (size_t)kSegRangeSlotsHost) var = nullptr;  // range kernel: a slot per array
     if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16, 8);
+    if (var->sched == 8 && !opt.grid && !opt.block && !env_get("POSPOP_SEG_VARIANT") && n <= (size_t)kSegRangeSlotsHost) {
+        // The adaptive kernel's range-mode test depends only on n and its grid, so it is made here:
+        // few arrays go to the standalone range kernel at one CTA per SM with depth-7 / 32-byte steps
+        // (twice the bytes in flight of the adaptive kernel's two-CTA launch).
+        const unsigned long long auto_warps = (unsigned long long)device_info().sms *
+                                              resident_blocks(var->fn, kDefaultBlock) * (kDefaultBlock / 32);
+        if (n < (unsigned long long)env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds) * auto_warps) {
+            const SegVariant* r = pick_segmented(nbank, nbank == 1 ? 7 : 6, 32, 16, 1);
+            if (r) var = r;
+        }
+    }
     const int block = opt.block ? opt.block : env_int("POSPOP_SEG_BLOCK", kDefaultBlock);
     int grid = opt.grid;
     if (grid <= 0) {
