@@ -418,8 +418,8 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
 // (tools/seg_modes.py, u32: 64-word arrays lane 1523 vs G=4 1003 GB/s;
 // 256-word arrays G=4 4269 vs lane 2173; 1024 words G=4 ~ pipelined).
 constexpr int kSegLaneMeanBytes = 512;
-constexpr int kSegGroupMeanBytes = 2048;
-constexpr int kSegTileMeanBytes = 2048;  // tile mode above this mean (= the grouped bound; tools/seg_vs_stream.py)
+constexpr int kSegGroupMeanBytes = 16128; // grouped mode up to here unless tiles fit
+constexpr int kSegTileMeanBytes = 8192;  // tile mode from here when whole tile steps cover the mean
 constexpr int kSegRangeRounds = 4;       // range mode below this many arrays per warp
 constexpr int kSegGiantKib = 1024;       // arrays above this go through the giant queue
 static_assert(dev::kSegRangeSlots == kSegRangeSlotsHost && dev::kGiantQ == kGiantQHost &&
@@ -472,13 +472,13 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (extra < 1) extra = 1;
     if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
     if (var->sched >= 11) extra = (unsigned)env_int("POSPOP_SEG_TAIL_ROUNDS", 4);  // tile kernels: dynamic tail
-    if (var->sched == 8) {  // mode bounds: lane / grouped mean (64 B units), tile mean (256 B units), range-mode
+    if (var->sched == 8) {  // mode bounds: lane mean (64 B units), grouped / tile mean (256 B units), range-mode
                             // rounds (6 bits each), giant-array bound (16 KiB units, 8 bits)
         auto units = [](int v, unsigned unit, unsigned cap) {
             return (unsigned)(v < 0 ? 0 : ((unsigned)v / unit > cap ? cap : (unsigned)v / unit));
         };
         extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes), 64, 0x3F) |
-                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 64, 0x3F) << 6) |
+                (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 256, 0x3F) << 6) |
                 (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 256, 0x3F) << 12) |
                 (units(env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds), 1, 0x3F) << 18) |
                 (units(env_int("POSPOP_SEG_GIANT_KIB", kSegGiantKib), 16, 0xFF) << 24);

@@ -1652,15 +1652,15 @@ __global__ void __launch_bounds__(256, MINB) segmented_tile_kernel(const uint8_t
 // device, so device-resident offsets need no host round trip:
 //   fewer than `rounds` arrays per warp   -> range mode (even byte ranges)
 //   mean <= lane bound                    -> one lane per array
-//   mean <= grouped bound                 -> four lanes per array
-//   otherwise                             -> warp-per-array tiles
+//   mean > grouped bound, or >= the tile bound and a near multiple of the
+//   tile step (NBANK x 4 KiB per warp)    -> warp-per-array tiles
+//   otherwise                             -> four lanes per array
 // Arrays above `giant` bytes met by the last three go through the giant queue.
 // The tile and range modes start counting before the previous launch on the
 // stream completed.  `thresholds`: lane bound / 64 B (bits 0-5), grouped bound
-// / 64 B (6-11), tile lower bound / 256 B (12-17), rounds (18-23), giant /
-// 16 KiB (24-31, 0 = off).  A mean between the grouped and the tile bound
-// (only when set so) takes the pipelined warp kernel (k <= 32) / dynamic
-// claims (k = 64) without the giant queue.
+// / 256 B (6-11), tile lower bound / 256 B (12-17), rounds (18-23), giant /
+// 16 KiB (24-31, 0 = off).  (The software-pipelined warp kernel and the
+// dynamic-claim warp loop remain standalone schedules, sched 1-9.)
 // ---------------------------------------------------------------------------
 template <int NBANK>
 __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* data,
@@ -1673,7 +1673,7 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
     pdl_allow_next();
     const int wb = k >> 3;
     const unsigned long long lane_max = (unsigned long long)(thresholds & 0x3Fu) * 64;  // mean bytes
-    const unsigned long long group_max = (unsigned long long)((thresholds >> 6) & 0x3Fu) * 64;
+    const unsigned long long group_max = (unsigned long long)((thresholds >> 6) & 0x3Fu) * 256;
     const unsigned long long tile_min = (unsigned long long)((thresholds >> 12) & 0x3Fu) * 256;
     const unsigned long long range_rounds = (thresholds >> 18) & 0x3Fu;
     const unsigned long long giant = (unsigned long long)(thresholds >> 24) << 14;
@@ -1685,7 +1685,12 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
         return;
     }
     const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
-    if (mean > tile_min && mean > group_max) {
+    // Tile mode: above the grouped bound, or from tile_min on when whole warp steps cover the mean array
+    // (less than 1/8 of the last step idle; a step is NBANK x 4 KiB per warp).
+    constexpr unsigned long long kStepBytes = NBANK * 4096ull;
+    const unsigned long long steps = (mean + kStepBytes - 1) / kStepBytes;
+    const bool whole_steps = 8 * (steps * kStepBytes - mean) < steps * kStepBytes;
+    if (mean > lane_max && (mean > group_max || (mean >= tile_min && whole_steps))) {
         // depth 5 per bank over 16-byte loads: 4 KiB (k <= 32) / 8 KiB (k = 64) steps per warp (measured
         // best at two CTAs per SM: tools/seg_vs_stream.py)
         const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
@@ -1705,14 +1710,10 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
         extern __shared__ __align__(16) uint8_t seg_stage[];  // launcher: 32 rows per warp for k <= 32, else none
         seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10,
                                      NBANK == 1 && k <= 32 ? seg_stage : nullptr, giant);
-    } else if (mean <= group_max) {
+    } else {
         constexpr int LG = NBANK == 1 ? 6 : 4;  // grouped-mode tree depth (measured: 6 beats 5 by ~10 % at 1 KiB)
         seg_group_loop<NBANK, LG, 16, 4>(data, offsets, n_arrays, k, flush_threshold, out, next, (256u << 10) / 16,
                                          giant);
-    } else if constexpr (NBANK == 1) {
-        segmented_pipe_body<NBANK, LW, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out);
-    } else {  // k = 64: dynamic array claims
-        seg_warp_loop<NBANK, 5, 16, 1>(data, offsets, n_arrays, k, flush_threshold, out, next, 1u);
     }
     seg_launch_done(next, ticket, q);
 }

@@ -87,9 +87,9 @@ def main():
             assert (out.cpu().numpy().view(np.uint64) == want_rows).all()
         for v in variants:
             run(f"segmented k={k}", {"POSPOP_SEG_VARIANT": v, "POSPOP_SEG_BIG_KIB": "64"}, seg)
-        for lane, group, tile, rounds in ((1 << 20,) * 3 + (0,), (0, 1 << 20, 1 << 20, 0), (0, 0, 1 << 20, 0),
-                                          (0, 0, 0, 0), (0, 0, 0, 255)):
-            # adaptive: lane / grouped / pipelined warp / tile / range modes
+        for lane, group, tile, rounds in ((1 << 20,) * 3 + (0,), (0, 1 << 20, 1 << 20, 0), (0, 0, 0, 0),
+                                          (0, 0, 0, 255)):
+            # adaptive: lane / grouped / tile / range modes
             for giant in ("1024", "16"):  # a 16 KiB giant bound: the queue carries the longer arrays
                 run(f"segmented adaptive k={k}", {"POSPOP_SEG_VARIANT": auto, "POSPOP_SEG_LANE_MEAN_BYTES": str(lane),
                                                   "POSPOP_SEG_GROUP_MEAN_BYTES": str(group),

@@ -656,14 +656,14 @@ def test_sharded_repeated_calls_and_empty_shards(pp, dev, orc):
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-@pytest.mark.parametrize("mode", ["lane", "grouped", "pipelined", "tile", "range"])
+@pytest.mark.parametrize("mode", ["lane", "grouped", "tile", "range"])
 def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
     """The adaptive kernel (sched 8) in each of its modes -- forced through the
     mean-length thresholds -- on tiny, ragged, empty and large arrays; in lane
     mode a batch with an array above the lane cap takes the full-warp path."""
     monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
     lane, group, tile, rounds = {"lane": (1 << 20, 1 << 20, 1 << 20, 0), "grouped": (0, 1 << 20, 1 << 20, 0),
-                                 "pipelined": (0, 0, 1 << 20, 0), "tile": (0, 0, 0, 0), "range": (0, 0, 0, 255)}[mode]
+                                 "tile": (0, 0, 0, 0), "range": (0, 0, 0, 255)}[mode]
     monkeypatch.setenv("POSPOP_SEG_LANE_MEAN_BYTES", str(lane))
     monkeypatch.setenv("POSPOP_SEG_GROUP_MEAN_BYTES", str(group))
     monkeypatch.setenv("POSPOP_SEG_TILE_MEAN_BYTES", str(tile))
