@@ -146,13 +146,17 @@ __device__ __forceinline__ uint32_t bank_warp_total_bytes(const uint32_t (&count
 // touched exactly once).  VB = 16 -> LDG.E.NA.128 (512 B per warp),
 // VB = 32 -> LDG.E.NA.256 (1 KiB per warp; Blackwell's 256-bit load).
 // HINT 0: default L2 policy; 1: L2 evict_first (256-bit form only);
-// 2: L2 256 B prefetch hint (128-bit form only).
+// 2: L2 256 B prefetch hint (128-bit form only); 3: allocate in L1 (128-bit
+// form only).
 // ---------------------------------------------------------------------------
 template <int VB, int HINT>
 __device__ __forceinline__ void ldg_stream(const uint8_t* p, uint32_t (&r)[VB / 4]) {
     static_assert(VB == 16 || VB == 32, "vector width");
     if constexpr (VB == 16) {
-        if constexpr (HINT == 2) {
+        if constexpr (HINT == 3) {  // L1-allocating (lanes reading half sectors: the other half hits L1)
+            asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p));
+        } else if constexpr (HINT == 2) {
             asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p));
         } else {

@@ -417,7 +417,8 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
 // Adaptive segmented kernel (sched 8) thresholds on the mean array length
 // (tools/seg_modes.py, u32: 64-word arrays lane 1523 vs G=4 1003 GB/s;
 // 256-word arrays G=4 4269 vs lane 2173; 1024 words G=4 ~ pipelined).
-constexpr int kSegLaneMeanBytes = 512;
+constexpr int kSegLaneMeanBytes = 768;    // one lane per array up to here (k <= 32)
+constexpr int kSegLaneMeanBytes64 = 512;  // the same for k = 64
 constexpr int kSegGroupMeanBytes = 16128; // grouped mode up to here unless tiles fit
 constexpr int kSegTileMeanBytes = 8192;  // tile mode from here when whole tile steps cover the mean
 constexpr int kSegRangeRounds = 4;       // range mode below this many arrays per warp
@@ -477,7 +478,8 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
         auto units = [](int v, unsigned unit, unsigned cap) {
             return (unsigned)(v < 0 ? 0 : ((unsigned)v / unit > cap ? cap : (unsigned)v / unit));
         };
-        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", kSegLaneMeanBytes), 64, 0x3F) |
+        extra = units(env_int("POSPOP_SEG_LANE_MEAN_BYTES", nbank == 1 ? kSegLaneMeanBytes : kSegLaneMeanBytes64), 64,
+                      0x3F) |
                 (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 256, 0x3F) << 6) |
                 (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 256, 0x3F) << 12) |
                 (units(env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds), 1, 0x3F) << 18) |

@@ -1046,6 +1046,9 @@ __global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_
 // arrays up to 2 MiB; the caller keeps arrays above `lane_cap_bytes` on the
 // full-warp path.
 // ---------------------------------------------------------------------------
+#ifndef POSPOP_LANE_HINT
+#define POSPOP_LANE_HINT 3  // L1-allocating: lanes read half sectors (64-word arrays 1626 -> 2205 GB/s)
+#endif
 template <int NBANK>
 __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsigned long long* offsets,
                                                unsigned long long a, int k, unsigned long long* row) {
@@ -1069,7 +1072,7 @@ __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsign
             uint32_t x[4] = {0u, 0u, 0u, 0u};
             if (idx < v.nv) {
                 POSPOP_CHECK(idx < v.nv);
-                ldg_stream<16, 0>(v.base + idx * 16, x);
+                ldg_stream<16, POSPOP_LANE_HINT>(v.base + idx * 16, x);
                 if (idx == 0 || idx + 1 == v.nv) mask_bytes<16>(x, idx == 0 ? v.lo : 0, idx + 1 == v.nv ? v.hi : 16);
             }
 #pragma unroll
