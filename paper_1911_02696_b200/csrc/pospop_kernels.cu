@@ -418,7 +418,7 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
 // (tools/seg_modes.py, u32: 64-word arrays lane 1523 vs G=4 1003 GB/s;
 // 256-word arrays G=4 4269 vs lane 2173; 1024 words G=4 ~ pipelined).
 constexpr int kSegLaneMeanBytes = 768;    // one lane per array up to here (k <= 32)
-constexpr int kSegLaneMeanBytes64 = 512;  // the same for k = 64
+constexpr int kSegLaneMeanBytes64 = 1024; // the same for k = 64 (rows staged one bank half at a time)
 constexpr int kSegGroupMeanBytes = 16128; // grouped mode up to here unless tiles fit
 constexpr int kSegTileMeanBytes = 8192;  // tile mode from here when whole tile steps cover the mean
 constexpr int kSegRangeRounds = 4;       // range mode below this many arrays per warp
@@ -489,12 +489,13 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)block);
     cfg.stream = stream;
-    if (var->sched == 10 || (var->sched == 8 && nbank == 1 && !env_int("POSPOP_SEG_NO_STAGE", 0))) {
-        // sched 8: the lane mode stages each warp's 32 rows (k*8 + 16 bytes each);
-        // sched 10: each warp's ring of `group` steps of 32 x VPT 16-byte vectors
+    if (var->sched == 10 || (var->sched == 8 && !env_int("POSPOP_SEG_NO_STAGE", 0))) {
+        // sched 8: the lane mode stages each warp's 32 rows (k*8 + 16 bytes each; k = 64: 8 rows' 256-byte
+        // bank halves at a time); sched 10: each warp's ring of `group` steps of 32 x VPT 16-byte vectors
         cfg.dynamicSmemBytes = var->sched == 10
                                    ? (size_t)(block / 32) * var->group * 32 * ((size_t)(nbank << var->depth) / 4) * 16
-                                   : (size_t)(block / 32) * 32 * ((size_t)k * 8 + 16);
+                               : k > 32 ? (size_t)(block / 32) * 8 * (32 * 8 + 16)
+                                        : (size_t)(block / 32) * 32 * ((size_t)k * 8 + 16);
         static std::mutex mu;
         static std::map<std::pair<int, const void*>, size_t> configured;
         int dev = 0;

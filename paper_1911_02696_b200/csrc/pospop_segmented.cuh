@@ -1049,14 +1049,24 @@ __global__ void __launch_bounds__(256, MINB) segmented_group_kernel(const uint8_
 #ifndef POSPOP_LANE_HINT
 #define POSPOP_LANE_HINT 3  // L1-allocating: lanes read half sectors (64-word arrays 1626 -> 2205 GB/s)
 #endif
-template <int NBANK>
-__device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsigned long long* offsets,
-                                               unsigned long long a, int k, unsigned long long* row) {
+// Counts array `a` (nothing when !valid) on this lane and hands each bank's
+// 32 channel totals to sink(bank, ch).
+template <int NBANK, class Sink>
+__device__ __forceinline__ void seg_lane_counts(const uint8_t* data, const unsigned long long* offsets,
+                                                unsigned long long a, bool valid, int k, Sink&& sink) {
     constexpr int L = NBANK == 1 ? 3 : 2;
     constexpr int REGS = NBANK << L;  // 8 registers = two 16-byte vectors
     constexpr int VPT = REGS / 4;
     const int wb = k >> 3;
-    const SegView v = seg_view<16>(data, offsets[a], offsets[a + 1], wb);
+    SegView v;
+    if (valid) {
+        v = seg_view<16>(data, offsets[a], offsets[a + 1], wb);
+    } else {
+        v.base = data;
+        v.nv = v.f0 = v.f1 = 0;
+        v.lo = 0;
+        v.hi = 16;
+    }
     uint32_t carries[NBANK][L];
     uint32_t counter[NBANK][16];
 #pragma unroll
@@ -1090,7 +1100,15 @@ __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsign
             ch[p] = ((counter[b][p] & 0xFFFFu) << L) + (d[p] & 0xFFFFu);
             ch[p + 16] = ((counter[b][p] >> 16) << L) + (d[p] >> 16);
         }
-        // row may be any 8-byte-aligned address (a caller's output rows)
+        sink(b, ch);
+    }
+}
+
+// Array a's row written straight to `row` (any 8-byte-aligned address).
+template <int NBANK>
+__device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsigned long long* offsets,
+                                               unsigned long long a, int k, unsigned long long* row) {
+    seg_lane_counts<NBANK>(data, offsets, a, true, k, [&](int b, const uint32_t (&ch)[32]) {
         if (NBANK == 2 || k == 32) {
 #pragma unroll
             for (int c = 0; c < 32; ++c) row[32 * b + c] = ch[c];
@@ -1100,6 +1118,26 @@ __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsign
         } else {  // k == 8: channels p, p+8, p+16, p+24
 #pragma unroll
             for (int p = 0; p < 8; ++p) row[p] = (unsigned long long)ch[p] + ch[p + 8] + ch[p + 16] + ch[p + 24];
+        }
+    });
+}
+
+// Copies `rows` staged rows of `half_bytes` each (stage stride `rowb`) to
+// dst + r * dst_stride with coalesced 16-byte stores (two 8-byte stores when
+// dst is only 8-byte aligned).  The whole warp.
+__device__ __forceinline__ void seg_copy_staged(const uint8_t* wbuf, int rowb, int rows, int half_bytes, uint8_t* dst,
+                                                size_t dst_stride, uint32_t lane) {
+    const int cpr = half_bytes / 16;  // 16-byte chunks per row
+    const bool v16 = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (dst_stride & 15u) == 0;
+    for (int i = (int)lane; i < rows * cpr; i += 32) {
+        const int r = i / cpr, c = i - r * cpr;
+        const uint4 v = *reinterpret_cast<const uint4*>(wbuf + r * rowb + c * 16);
+        uint8_t* p = dst + (size_t)r * dst_stride + (size_t)c * 16;
+        if (v16) {
+            *reinterpret_cast<uint4*>(p) = v;
+        } else {
+            reinterpret_cast<unsigned long long*>(p)[0] = ((unsigned long long)v.y << 32) | v.x;
+            reinterpret_cast<unsigned long long*>(p)[1] = ((unsigned long long)v.w << 32) | v.z;
         }
     }
 }
@@ -1120,8 +1158,8 @@ __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigne
     const uint32_t lane = threadIdx.x & 31u;
     const int wb = k >> 3;
     const GiantQueue q = seg_giant_queue(next, giant_bytes);
-    const int rowb = k * 8 + 16;  // staged row stride, bytes
-    uint8_t* wbuf = stage ? stage + (threadIdx.x >> 5) * 32 * rowb : nullptr;
+    const int rowb = (k > 32 ? 32 : k) * 8 + 16;  // staged row stride, bytes (k = 64: half rows, one bank at a time)
+    uint8_t* wbuf = stage ? stage + (threadIdx.x >> 5) * (NBANK == 2 ? 8 : 32) * rowb : nullptr;
     unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
     mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
@@ -1132,25 +1170,32 @@ __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigne
         const unsigned long long nbytes = a < n_arrays ? (offsets[a + 1] - offsets[a]) * wb : 0;
         if (!__any_sync(0xFFFFFFFFu, nbytes > lane_cap_bytes)) {
             if (wbuf) {
-                if (a < n_arrays)
-                    seg_lane_array<NBANK>(data, offsets, a, k, reinterpret_cast<unsigned long long*>(wbuf + lane * rowb));
-                __syncwarp();
                 const unsigned long long left = n_arrays - a0;
                 const int rows = left < 32 ? (int)left : 32;
-                const int cpr = k / 2;  // 16-byte chunks per row
                 uint8_t* dst = reinterpret_cast<uint8_t*>(out + a0 * (unsigned long long)k);
-                const bool v16 = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;  // else two 8-byte stores
-                for (int i = (int)lane; i < rows * cpr; i += 32) {
-                    const int r = i / cpr, c = i - r * cpr;
-                    const uint4 v = *reinterpret_cast<const uint4*>(wbuf + r * rowb + c * 16);
-                    if (v16) {
-                        *reinterpret_cast<uint4*>(dst + (size_t)i * 16) = v;
-                    } else {
-                        reinterpret_cast<unsigned long long*>(dst)[2 * i] = ((unsigned long long)v.y << 32) | v.x;
-                        reinterpret_cast<unsigned long long*>(dst)[2 * i + 1] = ((unsigned long long)v.w << 32) | v.z;
-                    }
+                if (NBANK == 2) {  // 512-byte rows: one 256-byte bank half of 8 rows at a time (a small stage
+                                   // keeps the L1 that the other modes' in-flight loads need)
+                    seg_lane_counts<NBANK>(data, offsets, a, a < n_arrays, k, [&](int bank, const uint32_t (&ch)[32]) {
+#pragma unroll 1
+                        for (int g = 0; g < 4; ++g) {
+                            if ((int)(lane >> 3) == g) {
+                                unsigned long long* srow = reinterpret_cast<unsigned long long*>(wbuf + (lane & 7u) * rowb);
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) srow[c] = ch[c];
+                            }
+                            __syncwarp();
+                            const int gr = rows - 8 * g;
+                            if (gr > 0) seg_copy_staged(wbuf, rowb, gr < 8 ? gr : 8, 256, dst + 256 * bank + 4096 * g, 512, lane);
+                            __syncwarp();
+                        }
+                    });
+                } else {
+                    if (a < n_arrays)
+                        seg_lane_array<NBANK>(data, offsets, a, k, reinterpret_cast<unsigned long long*>(wbuf + lane * rowb));
+                    __syncwarp();
+                    seg_copy_staged(wbuf, rowb, rows, k * 8, dst, (size_t)k * 8, lane);
+                    __syncwarp();
                 }
-                __syncwarp();
             } else if (a < n_arrays) {
                 seg_lane_array<NBANK>(data, offsets, a, k, out + a * (unsigned long long)k);
             }
@@ -1710,9 +1755,9 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
     }
     pdl_wait_prev();  // the claim counter, the ticket and the rows may belong to the previous launch
     if (mean <= lane_max) {
-        extern __shared__ __align__(16) uint8_t seg_stage[];  // launcher: 32 rows per warp for k <= 32, else none
-        seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10,
-                                     NBANK == 1 && k <= 32 ? seg_stage : nullptr, giant);
+        extern __shared__ __align__(16) uint8_t seg_stage[];  // launcher: 32 (half) rows per warp
+        seg_lane_loop<NBANK, LW, 16>(data, offsets, n_arrays, k, flush_threshold, out, next, 16u << 10, seg_stage,
+                                     giant);
     } else {
         constexpr int LG = NBANK == 1 ? 6 : 4;  // grouped-mode tree depth (measured: 6 beats 5 by ~10 % at 1 KiB)
         seg_group_loop<NBANK, LG, 16, 4>(data, offsets, n_arrays, k, flush_threshold, out, next, (256u << 10) / 16,
