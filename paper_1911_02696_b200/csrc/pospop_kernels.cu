@@ -490,12 +490,12 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     cfg.blockDim = dim3((unsigned)block);
     cfg.stream = stream;
     if (var->sched == 10 || (var->sched == 8 && !env_int("POSPOP_SEG_NO_STAGE", 0))) {
-        // sched 8: the lane mode stages each warp's 32 rows (k*8 + 16 bytes each; k = 64: 8 rows' 256-byte
-        // bank halves at a time); sched 10: each warp's ring of `group` steps of 32 x VPT 16-byte vectors
+        // sched 8: the lane mode stages dev::seg_stage_rows(k) rows per warp at a time (k*8 + 16 bytes
+        // each; k = 64: 256-byte bank halves); sched 10: each warp's ring of `group` steps of 32 x VPT
+        // 16-byte vectors
         cfg.dynamicSmemBytes = var->sched == 10
                                    ? (size_t)(block / 32) * var->group * 32 * ((size_t)(nbank << var->depth) / 4) * 16
-                               : k > 32 ? (size_t)(block / 32) * 8 * (32 * 8 + 16)
-                                        : (size_t)(block / 32) * 32 * ((size_t)k * 8 + 16);
+                                   : (size_t)(block / 32) * dev::seg_stage_rows(k) * ((size_t)(k > 32 ? 32 : k) * 8 + 16);
         static std::mutex mu;
         static std::map<std::pair<int, const void*>, size_t> configured;
         int dev = 0;

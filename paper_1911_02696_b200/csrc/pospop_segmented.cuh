@@ -1122,6 +1122,13 @@ __device__ __forceinline__ void seg_lane_array(const uint8_t* data, const unsign
     });
 }
 
+// Rows staged per warp at a time in the lane mode (stride (min(k, 32) * 8 +
+// 16) bytes): all 32 for the short rows of k <= 16, 16 for k = 32, 8 bank
+// halves for k = 64 -- the stage's carve-out takes L1 from every mode of the
+// adaptive kernel.  The launcher sizes the dynamic shared
+// memory with the same rule.
+__host__ __device__ __forceinline__ int seg_stage_rows(int k) { return k <= 16 ? 32 : k == 32 ? 16 : 8; }
+
 // Copies `rows` staged rows of `half_bytes` each (stage stride `rowb`) to
 // dst + r * dst_stride with coalesced 16-byte stores (two 8-byte stores when
 // dst is only 8-byte aligned).  The whole warp.
@@ -1159,7 +1166,7 @@ __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigne
     const int wb = k >> 3;
     const GiantQueue q = seg_giant_queue(next, giant_bytes);
     const int rowb = (k > 32 ? 32 : k) * 8 + 16;  // staged row stride, bytes (k = 64: half rows, one bank at a time)
-    uint8_t* wbuf = stage ? stage + (threadIdx.x >> 5) * (NBANK == 2 ? 8 : 32) * rowb : nullptr;
+    uint8_t* wbuf = stage ? stage + (threadIdx.x >> 5) * seg_stage_rows(k) * rowb : nullptr;
     unsigned long long mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     unsigned long long b = __shfl_sync(0xFFFFFFFFu, mine, 0);
     mine = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
@@ -1173,29 +1180,36 @@ __device__ __forceinline__ void seg_lane_loop(const uint8_t* data, const unsigne
                 const unsigned long long left = n_arrays - a0;
                 const int rows = left < 32 ? (int)left : 32;
                 uint8_t* dst = reinterpret_cast<uint8_t*>(out + a0 * (unsigned long long)k);
-                if (NBANK == 2) {  // 512-byte rows: one 256-byte bank half of 8 rows at a time (a small stage
-                                   // keeps the L1 that the other modes' in-flight loads need)
-                    seg_lane_counts<NBANK>(data, offsets, a, a < n_arrays, k, [&](int bank, const uint32_t (&ch)[32]) {
+                // `rp` rows at a time (k = 64: their 256-byte bank halves): a small stage keeps the L1 that
+                // the other modes' in-flight loads need
+                const size_t row_bytes = (size_t)k * 8;
+                const int rp = seg_stage_rows(k);
+                seg_lane_counts<NBANK>(data, offsets, a, a < n_arrays, k, [&](int bank, const uint32_t (&ch)[32]) {
 #pragma unroll 1
-                        for (int g = 0; g < 4; ++g) {
-                            if ((int)(lane >> 3) == g) {
-                                unsigned long long* srow = reinterpret_cast<unsigned long long*>(wbuf + (lane & 7u) * rowb);
+                    for (int g = 0; g < 32 / rp; ++g) {
+                        if ((int)lane / rp == g) {
+                            unsigned long long* srow =
+                                reinterpret_cast<unsigned long long*>(wbuf + ((int)lane - g * rp) * rowb);
+                            if (NBANK == 2 || k == 32) {
 #pragma unroll
                                 for (int c = 0; c < 32; ++c) srow[c] = ch[c];
+                            } else if (k == 16) {
+#pragma unroll
+                                for (int p = 0; p < 16; ++p) srow[p] = (unsigned long long)ch[p] + ch[p + 16];
+                            } else {  // k == 8
+#pragma unroll
+                                for (int p = 0; p < 8; ++p)
+                                    srow[p] = (unsigned long long)ch[p] + ch[p + 8] + ch[p + 16] + ch[p + 24];
                             }
-                            __syncwarp();
-                            const int gr = rows - 8 * g;
-                            if (gr > 0) seg_copy_staged(wbuf, rowb, gr < 8 ? gr : 8, 256, dst + 256 * bank + 4096 * g, 512, lane);
-                            __syncwarp();
                         }
-                    });
-                } else {
-                    if (a < n_arrays)
-                        seg_lane_array<NBANK>(data, offsets, a, k, reinterpret_cast<unsigned long long*>(wbuf + lane * rowb));
-                    __syncwarp();
-                    seg_copy_staged(wbuf, rowb, rows, k * 8, dst, (size_t)k * 8, lane);
-                    __syncwarp();
-                }
+                        __syncwarp();
+                        const int gr = rows - rp * g;
+                        if (gr > 0)
+                            seg_copy_staged(wbuf, rowb, gr < rp ? gr : rp, NBANK == 2 ? 256 : (int)row_bytes,
+                                            dst + (NBANK == 2 ? 256 * bank : 0) + rp * g * row_bytes, row_bytes, lane);
+                        __syncwarp();
+                    }
+                });
             } else if (a < n_arrays) {
                 seg_lane_array<NBANK>(data, offsets, a, k, out + a * (unsigned long long)k);
             }
