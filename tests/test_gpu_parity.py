@@ -686,9 +686,14 @@ def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-def test_segmented_rows_at_8_byte_aligned_output(pp, dev, orc, k):
-    """Row stores (staged lane mode and direct) at an output that is only
-    8-byte aligned; tiny arrays select the lane mode."""
+@pytest.mark.parametrize("mode", ["default", "lane"])
+def test_segmented_rows_at_8_byte_aligned_output(pp, dev, orc, k, mode, monkeypatch):
+    """Row stores at an output that is only 8-byte aligned: the default path
+    (few arrays: the range kernel) and the adaptive kernel's lane mode (staged
+    rows copied out with 8-byte stores)."""
+    if mode == "lane":
+        monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
+        monkeypatch.setenv("POSPOP_SEG_RANGE_ROUNDS", "0")
     rng = np.random.default_rng(70 + k)
     lens = rng.integers(0, 40, size=3001)
     offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
