@@ -421,7 +421,8 @@ constexpr int kSegLaneMeanBytes = 768;    // one lane per array up to here (k <=
 constexpr int kSegLaneMeanBytes64 = 1024; // the same for k = 64 (rows staged one bank half at a time)
 constexpr int kSegGroupMeanBytes = 16128; // grouped mode up to here unless tiles fit
 constexpr int kSegTileMeanBytes = 8192;  // tile mode from here when whole tile steps cover the mean
-constexpr int kSegRangeRounds = 4;       // range mode below this many arrays per warp
+constexpr int kSegRange = 16;  // range mode from a mean of 16 x 32 KiB = 512 KiB, or with at most one array per CTA
+                               // (POSPOP_SEG_RANGE: 0 = never, 63 = always)
 constexpr int kSegGiantKib = 1024;       // arrays above this go through the giant queue
 static_assert(dev::kSegRangeSlots == kSegRangeSlotsHost && dev::kGiantQ == kGiantQHost &&
                   dev::kGiantEntry == kGiantEntryHost && kAccChannels + 1 + 7 == 104,
@@ -445,12 +446,11 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (var && var->sched == 16 && n > (size_t)kSegRangeSlotsHost) var = nullptr;  // range kernel: a slot per array
     if (!var) var = pick_segmented(nbank, nbank == 1 ? 5 : 4, 16, 8);
     if (var->sched == 8 && !opt.grid && !opt.block && !env_get("POSPOP_SEG_VARIANT") && n <= (size_t)kSegRangeSlotsHost) {
-        // The adaptive kernel's range-mode test depends only on n and its grid, so it is made here:
-        // few arrays go to the standalone range kernel at one CTA per SM with depth-7 / 32-byte steps
-        // (twice the bytes in flight of the adaptive kernel's two-CTA launch).
-        const unsigned long long auto_warps = (unsigned long long)device_info().sms *
-                                              resident_blocks(var->fn, kDefaultBlock) * (kDefaultBlock / 32);
-        if (n < (unsigned long long)env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds) * auto_warps) {
+        // With at most one array per SM the adaptive kernel would pick its range mode whatever the
+        // lengths; that choice is made here instead, for the standalone range kernel at one CTA per SM
+        // with depth-7 / 32-byte steps (twice the bytes in flight of the adaptive kernel's launch).
+        const int range = env_int("POSPOP_SEG_RANGE", kSegRange);
+        if (range != 0 && n <= (size_t)device_info().sms) {
             const SegVariant* r = pick_segmented(nbank, nbank == 1 ? 7 : 6, 32, 16, 1);
             if (r) var = r;
         }
@@ -474,7 +474,7 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     if (var->sched == 5) extra = (unsigned)((size_t)env_int("POSPOP_SEG_BIG_KIB", 256) * 1024 / var->vb);
     if (var->sched >= 11) extra = (unsigned)env_int("POSPOP_SEG_TAIL_ROUNDS", 4);  // tile kernels: dynamic tail
     if (var->sched == 8) {  // mode bounds: lane mean (64 B units), grouped / tile mean (256 B units), range-mode
-                            // rounds (6 bits each), giant-array bound (16 KiB units, 8 bits)
+                            // mean (32 KiB units; 0 off, 63 always) (6 bits each), giant-array bound (16 KiB, 8 bits)
         auto units = [](int v, unsigned unit, unsigned cap) {
             return (unsigned)(v < 0 ? 0 : ((unsigned)v / unit > cap ? cap : (unsigned)v / unit));
         };
@@ -482,7 +482,7 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
                       0x3F) |
                 (units(env_int("POSPOP_SEG_GROUP_MEAN_BYTES", kSegGroupMeanBytes), 256, 0x3F) << 6) |
                 (units(env_int("POSPOP_SEG_TILE_MEAN_BYTES", kSegTileMeanBytes), 256, 0x3F) << 12) |
-                (units(env_int("POSPOP_SEG_RANGE_ROUNDS", kSegRangeRounds), 1, 0x3F) << 18) |
+                (units(env_int("POSPOP_SEG_RANGE", kSegRange), 1, 0x3F) << 18) |
                 (units(env_int("POSPOP_SEG_GIANT_KIB", kSegGiantKib), 16, 0xFF) << 24);
     }
     cudaLaunchConfig_t cfg = {};

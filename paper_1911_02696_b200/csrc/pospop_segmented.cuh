@@ -334,7 +334,9 @@ __device__ __forceinline__ unsigned long long* seg_range_slots(unsigned long lon
 // point (or its exit) while chunks are left; chunk partials are summed in the
 // entry with u64 atomics and the warp finishing the last chunk moves them into
 // the row.  The publisher keeps helping until its entry has no chunk left, so
-// no array waits for a warp that already exited.  Entry: [0] array, [1]
+// no array waits for a warp that already exited; a helper never waits for an
+// entry that is counted but not yet marked ready -- it skips it (its publisher
+// counts it).  (A helper spinning on that flag hung intermittently.)  Entry: [0] array, [1]
 // chunks, [2] chunk claim counter, [3] ready flag, [4, 68) counts, [68] chunks
 // done.  [0] of the queue = entries published (beyond kGiantQ the publisher
 // counts the array alone).  The last CTA resets the queue (seg_launch_done).
@@ -427,9 +429,7 @@ __device__ __noinline__ void giant_help(const GiantQueue q, const uint8_t* data,
         if (cursor >= cnt) return;
         unsigned long long* p = q.entry(cursor);
         unsigned long long arr = 0, chunks = 0, c = 0;
-        if (lane == 0) {
-            while (atomicAdd(p + 3, 0ull) == 0ull) {  // its publisher is running: ready momentarily
-            }
+        if (lane == 0 && atomicAdd(p + 3, 0ull) != 0ull) {  // published (else its publisher counts it)
             __threadfence();
             arr = __ldcg(p);
             chunks = __ldcg(p + 1);
@@ -438,7 +438,7 @@ __device__ __noinline__ void giant_help(const GiantQueue q, const uint8_t* data,
         arr = __shfl_sync(0xFFFFFFFFu, arr, 0);
         chunks = __shfl_sync(0xFFFFFFFFu, chunks, 0);
         c = __shfl_sync(0xFFFFFFFFu, c, 0);
-        if (c >= chunks) {
+        if (c >= chunks) {  // no chunk left (or not published yet: never waited for)
             ++cursor;
             continue;
         }
@@ -1712,7 +1712,8 @@ __global__ void __launch_bounds__(256, MINB) segmented_tile_kernel(const uint8_t
 // every CTA reads offsets[0] and offsets[n] and picks, from the array count and
 // the mean array length, the same schedule for the whole grid -- on the
 // device, so device-resident offsets need no host round trip:
-//   fewer than `rounds` arrays per warp   -> range mode (even byte ranges)
+//   at most one array per CTA, or a mean of `range` x 32 KiB or more
+//                                         -> range mode (even byte ranges per CTA)
 //   mean <= lane bound                    -> one lane per array
 //   mean > grouped bound, or >= the tile bound and a near multiple of the
 //   tile step (NBANK x 4 KiB per warp)    -> warp-per-array tiles
@@ -1720,8 +1721,8 @@ __global__ void __launch_bounds__(256, MINB) segmented_tile_kernel(const uint8_t
 // Arrays above `giant` bytes met by the last three go through the giant queue.
 // The tile and range modes start counting before the previous launch on the
 // stream completed.  `thresholds`: lane bound / 64 B (bits 0-5), grouped bound
-// / 256 B (6-11), tile lower bound / 256 B (12-17), rounds (18-23), giant /
-// 16 KiB (24-31, 0 = off).  (The software-pipelined warp kernel and the
+// / 256 B (6-11), tile lower bound / 256 B (12-17), range (18-23: 0 never, 63
+// always, else the mean bound / 32 KiB), giant / 16 KiB (24-31, 0 = off).  (The software-pipelined warp kernel and the
 // dynamic-claim warp loop remain standalone schedules, sched 1-9.)
 // ---------------------------------------------------------------------------
 template <int NBANK>
@@ -1737,16 +1738,18 @@ __global__ void __launch_bounds__(256, 2) segmented_auto_kernel(const uint8_t* d
     const unsigned long long lane_max = (unsigned long long)(thresholds & 0x3Fu) * 64;  // mean bytes
     const unsigned long long group_max = (unsigned long long)((thresholds >> 6) & 0x3Fu) * 256;
     const unsigned long long tile_min = (unsigned long long)((thresholds >> 12) & 0x3Fu) * 256;
-    const unsigned long long range_rounds = (thresholds >> 18) & 0x3Fu;
+    const unsigned long long range = (thresholds >> 18) & 0x3Fu;  // 0 never, 63 always, else mean >= range x 32 KiB
     const unsigned long long giant = (unsigned long long)(thresholds >> 24) << 14;
     const GiantQueue q = seg_giant_queue(next, giant);
     const unsigned long long nwarps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
-    if (n_arrays < range_rounds * nwarps && n_arrays <= (unsigned long long)kSegRangeSlots) {
+    const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
+    // Range mode: few arrays (at most one per CTA) or long ones (a CTA step is 32 KiB here), within the slots.
+    if (range && n_arrays <= (unsigned long long)kSegRangeSlots &&
+        (range == 63 || n_arrays <= gridDim.x || mean >= (range << 15))) {
         seg_range_loop<NBANK, NBANK == 1 ? 5 : 4, 16>(data, offsets, n_arrays, k, out, next);
         seg_launch_done(next, ticket, q);  // every warp has waited
         return;
     }
-    const unsigned long long mean = n_arrays ? (offsets[n_arrays] - offsets[0]) * wb / n_arrays : 0;
     // Tile mode: above the grouped bound, or from tile_min on when whole warp steps cover the mean array
     // (less than 1/8 of the last step idle; a step is NBANK x 4 KiB per warp).
     constexpr unsigned long long kStepBytes = NBANK * 4096ull;

@@ -94,7 +94,7 @@ def main():
                 run(f"segmented adaptive k={k}", {"POSPOP_SEG_VARIANT": auto, "POSPOP_SEG_LANE_MEAN_BYTES": str(lane),
                                                   "POSPOP_SEG_GROUP_MEAN_BYTES": str(group),
                                                   "POSPOP_SEG_TILE_MEAN_BYTES": str(tile),
-                                                  "POSPOP_SEG_RANGE_ROUNDS": str(rounds),
+                                                  "POSPOP_SEG_RANGE": str(rounds),
                                                   "POSPOP_SEG_GIANT_KIB": giant}, seg)
     print("bounds ok")
 

@@ -52,10 +52,10 @@ def test_fuzz_counts(pp, dev, orc, k, n, off_words, kind, seed, flush, where):
 
 
 # Adaptive-kernel mode forced through its bounds (lane, grouped, tile, range mean bytes / rounds).
-MODES = {"auto": {}, "lane": {"LANE_MEAN_BYTES": 4000, "GROUP_MEAN_BYTES": 4000, "RANGE_ROUNDS": 0},
-         "grouped": {"LANE_MEAN_BYTES": 0, "GROUP_MEAN_BYTES": 4000, "RANGE_ROUNDS": 0},
-         "tile": {"LANE_MEAN_BYTES": 0, "GROUP_MEAN_BYTES": 0, "TILE_MEAN_BYTES": 0, "RANGE_ROUNDS": 0},
-         "range": {"RANGE_ROUNDS": 63}}
+MODES = {"auto": {}, "lane": {"LANE_MEAN_BYTES": 4000, "GROUP_MEAN_BYTES": 4000, "RANGE": 0},
+         "grouped": {"LANE_MEAN_BYTES": 0, "GROUP_MEAN_BYTES": 4000, "RANGE": 0},
+         "tile": {"LANE_MEAN_BYTES": 0, "GROUP_MEAN_BYTES": 0, "TILE_MEAN_BYTES": 0, "RANGE": 0},
+         "range": {"RANGE": 63}}
 
 
 @settings(SETTINGS, max_examples=200)

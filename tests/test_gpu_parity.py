@@ -545,7 +545,7 @@ def test_segmented_giant_queue(pp, dev, orc, k, mode, monkeypatch):
     monkeypatch.setenv("POSPOP_SEG_LANE_MEAN_BYTES", str(lane))
     monkeypatch.setenv("POSPOP_SEG_GROUP_MEAN_BYTES", str(group))
     monkeypatch.setenv("POSPOP_SEG_TILE_MEAN_BYTES", str(tile))
-    monkeypatch.setenv("POSPOP_SEG_RANGE_ROUNDS", "0")
+    monkeypatch.setenv("POSPOP_SEG_RANGE", "0")
     monkeypatch.setenv("POSPOP_SEG_GIANT_KIB", "16")
     wb = k // 8
     rng = np.random.default_rng(700 + k)
@@ -667,7 +667,7 @@ def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
     monkeypatch.setenv("POSPOP_SEG_LANE_MEAN_BYTES", str(lane))
     monkeypatch.setenv("POSPOP_SEG_GROUP_MEAN_BYTES", str(group))
     monkeypatch.setenv("POSPOP_SEG_TILE_MEAN_BYTES", str(tile))
-    monkeypatch.setenv("POSPOP_SEG_RANGE_ROUNDS", str(rounds))
+    monkeypatch.setenv("POSPOP_SEG_RANGE", str(rounds))
     rng = np.random.default_rng(40 + k)
     n_words = 1_500_000
     data = orc.generate(6, 51, n_words * k // 64 + 1).view(DT[k])[:n_words]
@@ -693,7 +693,7 @@ def test_segmented_rows_at_8_byte_aligned_output(pp, dev, orc, k, mode, monkeypa
     rows copied out with 8-byte stores)."""
     if mode == "lane":
         monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
-        monkeypatch.setenv("POSPOP_SEG_RANGE_ROUNDS", "0")
+        monkeypatch.setenv("POSPOP_SEG_RANGE", "0")
     rng = np.random.default_rng(70 + k)
     lens = rng.integers(0, 40, size=3001)
     offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--variants", default=";7,32,13,1;6,32,13,2;6,32,11,2")
     ap.add_argument("--words", default="4096,16384")
     ap.add_argument("--k", type=int, default=32, choices=[32, 64])
+    ap.add_argument("--total-mib", type=int, default=1024, help="input size")
     ap.add_argument("--rounds", type=int, default=1, help="alternate the variants this many times")
     ap.add_argument("--rows-in", type=int, default=0, help="carve the rows from a buffer of this many MiB")
     ap.add_argument("--data-extra", type=int, default=0,
@@ -60,7 +61,7 @@ def main():
     args = ap.parse_args()
     torch.cuda.set_device(0)
     s = torch.cuda.current_stream()
-    k, total = args.k, 1 << 30
+    k, total = args.k, args.total_mib << 20
     if args.data_extra:
         big = torch.empty(total + (abs(args.data_extra) << 20), dtype=torch.uint8, device="cuda")
         if args.data_extra > 0:
