@@ -421,7 +421,7 @@ constexpr int kSegLaneMeanBytes = 768;    // one lane per array up to here (k <=
 constexpr int kSegLaneMeanBytes64 = 1024; // the same for k = 64 (rows staged one bank half at a time)
 constexpr int kSegGroupMeanBytes = 16128; // grouped mode up to here unless tiles fit
 constexpr int kSegTileMeanBytes = 8192;  // tile mode from here when whole tile steps cover the mean
-constexpr int kSegRange = 16;  // range mode from a mean of 16 x 32 KiB = 512 KiB, or with at most one array per CTA
+constexpr int kSegRange = 8;   // range mode from a mean of 8 x 32 KiB = 256 KiB, or with at most one array per CTA
                                // (POSPOP_SEG_RANGE: 0 = never, 63 = always)
 constexpr int kSegGiantKib = 1024;       // arrays above this go through the giant queue
 static_assert(dev::kSegRangeSlots == kSegRangeSlotsHost && dev::kGiantQ == kGiantQHost &&
