@@ -336,9 +336,9 @@ __device__ __forceinline__ unsigned long long* seg_range_slots(unsigned long lon
 // the row.  The publisher keeps helping until its entry has no chunk left, so
 // no array waits for a warp that already exited; a helper never waits for an
 // entry that is counted but not yet marked ready -- it skips it (its publisher
-// counts it).  (A helper spinning on that flag hung intermittently.)  Entry: [0] array, [1]
-// chunks, [2] chunk claim counter, [3] ready flag, [4, 68) counts, [68] chunks
-// done.  [0] of the queue = entries published (beyond kGiantQ the publisher
+// counts it; a helper spinning on that flag hung intermittently).  Entry: [0]
+// array, [1] chunks, [2] chunk claim counter, [3] ready flag, [4, 68) counts,
+// [68] chunks done.  [0] of the queue = entries published (beyond kGiantQ the publisher
 // counts the array alone).  The last CTA resets the queue (seg_launch_done).
 struct GiantQueue {
     unsigned long long* base;
