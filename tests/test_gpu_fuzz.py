@@ -58,8 +58,9 @@ MODES = {"auto": {}, "lane": {"LANE_MEAN_BYTES": 4000, "GROUP_MEAN_BYTES": 4000,
          "range": {"RANGE": 63}}
 
 
-@settings(SETTINGS, max_examples=200)
-@given(k=st.sampled_from([8, 16, 32, 64]), n_arrays=st.integers(1, 3000), max_len=st.sampled_from([1, 17, 300, 5000]),
+@settings(SETTINGS, max_examples=300)
+@given(k=st.sampled_from([8, 16, 32, 64]), n_arrays=st.integers(1, 12000),
+       max_len=st.sampled_from([1, 17, 300, 5000, 40000]),
        seed=st.integers(0, 2**32 - 1), empty_frac=st.floats(0, 0.5), flush=st.sampled_from([1, 3, 65535]),
        mode=st.sampled_from(sorted(MODES)), giant_kib=st.sampled_from([1024, 16]), start=st.integers(0, 9),
        huge=st.booleans())
