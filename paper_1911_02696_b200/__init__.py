@@ -330,18 +330,54 @@ def pospopcnt_u16_c32(words: Any, counters: np.ndarray) -> np.ndarray:
     return counters
 
 
+def _offsets_addr(offsets: Any) -> tuple[int, int]:
+    """(address, n_arrays) of an offsets array: int64/uint64, contiguous, >= 1 element."""
+    if isinstance(offsets, np.ndarray):
+        if offsets.dtype not in (np.dtype(np.uint64), np.dtype(np.int64)):
+            raise InvalidArgument(f"offsets must be uint64 or int64, got {offsets.dtype}")
+        if not offsets.flags.c_contiguous:
+            raise InvalidArgument("offsets must be C-contiguous")
+        n = offsets.size
+    elif hasattr(offsets, "data_ptr") and hasattr(offsets, "element_size"):
+        import torch
+        if offsets.dtype not in (torch.int64, torch.uint64):
+            raise InvalidArgument(f"offsets must be int64 or uint64, got {offsets.dtype}")
+        if not offsets.is_contiguous():
+            raise InvalidArgument("offsets must be contiguous")
+        n = offsets.numel()
+    else:
+        raise TypeError(f"unsupported offsets type {type(offsets)!r}")
+    if n < 1:
+        raise InvalidArgument("offsets needs at least one element (n_arrays + 1)")
+    return (_addr_len(offsets, 64)[0] if n else 0), n - 1
+
+
+def _rows_addr(out: Any, n: int, k: int) -> int:
+    """Address of a row buffer holding exactly n * k 8-byte elements."""
+    if isinstance(out, np.ndarray):
+        ok = out.dtype.itemsize == 8 and out.dtype.kind in "iu"
+        size = out.size
+    elif hasattr(out, "data_ptr") and hasattr(out, "element_size"):
+        ok = out.element_size() == 8 and not out.is_floating_point()
+        size = out.numel()
+    else:
+        raise TypeError(f"unsupported row buffer type {type(out)!r}")
+    if not ok:
+        raise InvalidArgument("rows must be an 8-byte integer array")
+    if size != n * k:
+        raise InvalidArgument(f"rows must hold n_arrays * k = {n * k} elements, got {size}")
+    return _addr_len(out, 64)[0]
+
+
 def pospopcnt_segmented(data: Any, offsets: Any, k: int, out: Any = None) -> Any:
     """Row a = counts of words [offsets[a], offsets[a+1]); returns (n_arrays, k) uint64."""
     addr, _ = _addr_len(data, k)
-    if isinstance(offsets, np.ndarray):
+    if isinstance(offsets, np.ndarray) and offsets.dtype != np.uint64 and offsets.dtype.kind in "iu":
         offsets = np.ascontiguousarray(offsets, np.uint64)
-        n = offsets.size - 1
-    else:
-        n = offsets.numel() - 1
-    off_addr, _ = _addr_len(offsets, 64)
+    off_addr, n = _offsets_addr(offsets)
     if out is None:
-        out = np.zeros((max(n, 0), k), np.uint64)
-    out_addr, _ = _addr_len(out, 64)
+        out = np.zeros((n, k), np.uint64)
+    out_addr = _rows_addr(out, n, k)
     if n > 0:
         _check(_load().pospopcnt_segmented(int(k), addr or None, off_addr, n, out_addr))
     return out
@@ -414,9 +450,9 @@ def ipc_free(ptr: int) -> None:
 def segmented_async(data: Any, offsets: Any, out: Any, k: int, *, flush_threshold_blocks: int = 65535,
                     grid: int = 0, block: int = 0, stream: Any = None) -> None:
     addr, _ = _addr_len(data, k)
-    off_addr, noff = _addr_len(offsets, 64)
-    out_addr, _ = _addr_len(out, 64)
-    _check(_load().pospopcnt_segmented_async(int(k), addr or None, off_addr, noff - 1, out_addr,
+    off_addr, n = _offsets_addr(offsets)
+    out_addr = _rows_addr(out, n, k)
+    _check(_load().pospopcnt_segmented_async(int(k), addr or None, off_addr, n, out_addr,
                                              int(flush_threshold_blocks), int(grid), int(block),
                                              _stream_ptr(stream)))
 

@@ -1492,10 +1492,16 @@ __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsign
             waited = true;
         }
     };
+    // Byte positions are taken relative to `data` rounded down to 16 bytes
+    // (`dal`): word i sits at pos(i) = sh + i * wb, so the 16-byte-aligned
+    // range starts below never go negative whatever the caller's alignment.
+    const unsigned long long sh = reinterpret_cast<uintptr_t>(data) & 15u;  // a multiple of wb
+    const uint8_t* dal = data - sh;
+    auto pos = [&](unsigned long long i) { return sh + offsets[i] * wb; };
     RangeSplit rs;
-    const unsigned long long p0 = offsets[0] * wb;
-    rs.base = p0 - ((reinterpret_cast<uintptr_t>(data) + p0) & 15u);  // absolute 16-byte alignment
-    rs.total = offsets[n_arrays] * wb - rs.base;
+    const unsigned long long p0 = pos(0);
+    rs.base = p0 & ~15ull;  // absolute 16-byte alignment
+    rs.total = pos(n_arrays) - rs.base;
     // at least 4 KiB per range (so no range is empty), at most one per CTA
     rs.W = rs.total / 4096 < gridDim.x ? (rs.total / 4096 ? rs.total / 4096 : 1) : gridDim.x;
     if (blockIdx.x >= rs.W) {
@@ -1507,7 +1513,7 @@ __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsign
     // First array touching [r0, r1): smallest a with end(a) > r0 or start(a) >= r0
     // (the latter catches empty arrays placed at r0).  32-ary search, every warp.
     auto touches = [&](unsigned long long i) {  // monotone in i
-        return offsets[i + 1] * wb > r0 || offsets[i] * wb >= r0;
+        return pos(i + 1) > r0 || pos(i) >= r0;
     };
     unsigned long long lo = 0, hi = n_arrays;  // the answer lies in [lo, hi]; hi = n_arrays: none
     for (;;) {
@@ -1571,13 +1577,13 @@ __device__ __forceinline__ void seg_range_loop(const uint8_t* data, const unsign
     };
     // Segment of array `arr` inside the range, as a vector view (nv = 0: empty).
     auto segment = [&](unsigned long long arr, unsigned long long& s, unsigned long long& e, SegView& v) {
-        s = offsets[arr] * wb;
-        e = offsets[arr + 1] * wb;
+        s = pos(arr);
+        e = pos(arr + 1);
         const unsigned long long lo_b = s > r0 ? s : r0, hi_b = e < r1 || last ? e : r1;
-        v = seg_view<VB>(data, lo_b / wb, hi_b > lo_b ? hi_b / wb : lo_b / wb, (int)wb);
+        v = seg_view<VB>(dal, lo_b / wb, hi_b > lo_b ? hi_b / wb : lo_b / wb, (int)wb);
     };
     auto in_range = [&](unsigned long long arr) {  // array `arr` still starts in this range
-        return arr < n_arrays && (last || offsets[arr] * wb < r1);
+        return arr < n_arrays && (last || pos(arr) < r1);
     };
     auto zero_row = [&](unsigned long long arr) {  // an empty array at a position this range owns
         ensure_waited();

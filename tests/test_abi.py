@@ -42,10 +42,22 @@ def test_library_is_sm100a_only(pp):
     assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", "")), out
 
 
-def test_sass_uses_lop3_csa_and_128bit_loads(pp):
-    sass = subprocess.run(["cuobjdump", "-sass", pp.library_path()], capture_output=True, text=True).stdout
+def _kernel_sass(pp, pattern):
+    """SASS of the kernels whose mangled names match `pattern` (cuobjdump -fun)."""
+    names = subprocess.run(["cuobjdump", "-symbols", pp.library_path()], capture_output=True, text=True).stdout
+    funs = sorted(set(re.findall(r"STO_ENTRY\s+(\S*" + pattern + r"\S*)", names)))
+    assert funs, pattern
+    return funs, subprocess.run(["cuobjdump", "-sass", "-fun", funs[0], pp.library_path()],
+                                capture_output=True, text=True).stdout
+
+
+def test_sass_uses_lop3_csa_and_256bit_loads(pp):
+    """The default k <= 32 counting kernel, stream_kernel<1,7,32,0,256,2,0,1>
+    (DESIGN.md 3.1): LOP3 CSAs with the reference's vpternlogd immediates and
+    256-bit non-allocating vector loads."""
+    funs, sass = _kernel_sass(pp, r"stream_kernelILi1ELi7ELi32ELi0ELi256ELi2ELi0ELi1E")
     assert "LOP3.LUT" in sass and "0xe8" in sass and "0x96" in sass
-    assert "LDG.E.NA.128.CONSTANT" in sass
+    assert "LDG.E.NA.ENL2.256.CONSTANT" in sass, funs
 
 
 def test_validate_like_reference(pp):  # test_core.cpp:184-201
@@ -141,3 +153,24 @@ def test_header_is_plain_c_and_fails_loudly_without_gpu(pp, tmp_path):
         assert r.returncode == 0, r.stdout
     else:
         assert r.returncode == 2, (r.returncode, r.stdout)
+
+
+def test_segmented_wrappers_check_offsets_and_rows(pp):
+    """Offsets must be 64-bit integers with >= 1 element; rows must hold
+    exactly n_arrays * k 8-byte integers (checked before any device work)."""
+    data = np.zeros(64, np.uint16)
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt_segmented(data, np.zeros(0, np.uint64), 16)
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt_segmented(data, np.array([0, 4], np.float64), 16)
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt_segmented(data, np.array([0, 4, 8], np.uint64), 16, out=np.zeros((1, 16), np.uint64))
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt_segmented(data, np.array([0, 4], np.uint64), 16, out=np.zeros(16, np.float64))
+    torch = pytest.importorskip("torch")
+    with pytest.raises(pp.InvalidArgument):
+        pp.segmented_async(data, torch.tensor([0, 4], dtype=torch.int32), np.zeros(16, np.uint64), 16)
+    with pytest.raises(pp.InvalidArgument):
+        pp.segmented_async(data, torch.zeros(0, dtype=torch.int64), np.zeros(0, np.uint64), 16)
+    with pytest.raises(pp.InvalidArgument):
+        pp.segmented_async(data, torch.tensor([0, 4], dtype=torch.int64), torch.zeros(15, dtype=torch.int64), 16)

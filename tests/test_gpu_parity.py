@@ -744,3 +744,42 @@ def test_typed_entry_points(pp, dev, orc):
     assert lib.pospopcnt_u16_async(d.data_ptr(), raw.size // 2, d_out.data_ptr(), C.c_void_p(s.cuda_stream)) == 0
     torch.cuda.synchronize()
     assert [int(x) for x in d_out.cpu().numpy()] == [int(x) for x in want]
+
+
+@pytest.mark.parametrize("k", [16, 32, 64])
+@pytest.mark.parametrize("mode", ["range_kernel", "adaptive_range"])
+def test_segmented_range_mode_misaligned_data(pp, dev, orc, k, mode, monkeypatch):
+    """Range mode with data that is word-aligned but not 16-byte aligned
+    (+wb, +2wb, +3wb bytes) and offsets[0] = 0, so the first referenced byte
+    sits in the first 16-byte block: every range must be counted and no
+    workspace slot may be left dirty.  Misaligned and aligned calls alternate
+    on one stream (a dirty slot would corrupt the next call's rows); the host
+    path (pageable data staged at the caller's 32-byte phase) is checked too."""
+    if mode == "adaptive_range":
+        monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
+        monkeypatch.setenv("POSPOP_SEG_RANGE", "63")
+    wb = k // 8
+    n_words = (3 << 20) // wb
+    raw = orc.generate(6, 300 + k, n_words * wb // 8 + 8, threads=8).view(np.uint8)
+    rng = np.random.default_rng(k)
+    # few arrays (<= SM count: the host routes to the range kernel), some spanning many ranges
+    cuts = np.sort(rng.choice(np.arange(1, n_words - 1), size=40, replace=False))
+    offs = np.concatenate([[0, 0, 5], cuts, [n_words - 1, n_words]]).astype(np.uint64)
+    if mode == "adaptive_range":  # more arrays than SMs: the adaptive kernel, range mode forced
+        offs = np.unique(np.concatenate([offs, rng.integers(0, n_words, size=400).astype(np.uint64)]))
+        offs = np.concatenate([[0], offs]).astype(np.uint64)
+    o = torch.from_numpy(offs.view(np.int64)).cuda()
+    buf = torch.from_numpy(raw.copy()).cuda()  # 256-byte aligned base
+    s = torch.cuda.Stream()
+    for rep in range(2):
+        for shift in (wb, 2 * wb, 3 * wb, 0):
+            words = raw[shift:shift + n_words * wb].view(DT[k])
+            want = orc.segmented(words, offs, k, threads=8)
+            d = buf[shift:shift + n_words * wb]
+            out = torch.full((offs.size - 1, k), -1, dtype=torch.int64, device="cuda")
+            pp.segmented_async(d, o, out, k, stream=s)
+            s.synchronize()
+            assert (out.cpu().numpy().view(np.uint64) == want).all(), (k, shift, rep)
+            if rep == 0:  # synchronous entry point: device data, host offsets; then pageable host data
+                assert (pp.pospopcnt_segmented(d, offs, k) == want).all(), (k, shift)
+                assert (pp.pospopcnt_segmented(words, offs, k) == want).all(), (k, shift, "host")
