@@ -24,9 +24,15 @@ measured HBM peak), cpu_baseline (the reference library on the host cores,
 N=1 only), e2e (the C-ABI call on pinned HOST buffers, H2D + D2H inside the
 timed region), gpu_launches, clocks (NVML sampled during the timed region).
 
+``--gpus N`` without torchrun re-launches itself under torch.distributed.run
+with N local ranks (one GPU each); the ranks check that their GPUs are
+distinct (by UUID) and refuse to print a headline if two share one.
+
 ``--impl reference`` times the reference's own CPU implementation
 (oracle/_ref/libpospop_ref.so: pospop::pospopcnt, fork-join + merge_counts
-over all host threads) on a bounded sample of the same workload; rank 0 only.
+over all host threads) on the SAME workload as our arm (all 2^32 words of
+cfg4 per step), correctness gate first (proj/core/src/bench.cpp:55-107);
+rank 0 only.
 """
 from __future__ import annotations
 
@@ -85,6 +91,8 @@ def parse():
                          "(peer-memory stores, paper_1911_02696_b200.exchange); nccl = a separate all-reduce")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-words", type=int, default=0,
+                    help="reference arm only: cap the words per step (CPU-only tests; 0 = the whole workload)")
     return ap.parse_args()
 
 
@@ -130,9 +138,10 @@ class ClockSampler:
             return
         try:
             import pynvml
-            pynvml.nvmlInit()
             self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self._h = nvml_handle(device_index)  # by UUID: NVML indices ignore CUDA_VISIBLE_DEVICES
+            if self._h is None:
+                return
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
             self._ok = True
         except Exception:
@@ -198,46 +207,171 @@ def dist_env():
     return world, rank, local
 
 
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
+
+def spawn(args) -> int:
+    """--gpus N > 1 without torchrun: re-launch under torch.distributed.run
+    with N local ranks (the driver's own launch form); rank 0 prints the line."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def nvml_handle(dev_index: int):
+    """NVML handle of torch device `dev_index`, matched by UUID (NVML indices
+    ignore CUDA_VISIBLE_DEVICES); None if NVML is unavailable."""
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(dev_index).uuid).lower()
+        for i in range(pynvml.nvmlDeviceGetCount()):
+            h = pynvml.nvmlDeviceGetHandleByIndex(i)
+            u = pynvml.nvmlDeviceGetUUID(h)
+            u = (u.decode() if isinstance(u, bytes) else u).lower()
+            if u.endswith(uuid) or uuid.endswith(u.replace("gpu-", "")):
+                return h
+        return pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def pin_numa(dev_index: int) -> str:
+    """Restricts this rank's host threads to the CPUs NVML reports as close to
+    its GPU, so the pinned host buffers it then first-touches (and the staging
+    threads of the e2e path) sit on the GPU's NUMA node.  Used for N > 1 only."""
+    h = nvml_handle(dev_index)
+    if h is None:
+        return "nvml unavailable"
+    try:
+        import pynvml
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (int(m) >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return "no NUMA-local CPUs in this process's affinity"
+        os.sched_setaffinity(0, cpus)
+        return f"{len(cpus)} NUMA-local CPUs"
+    except Exception as e:  # noqa: BLE001
+        return f"affinity unavailable ({e})"
+
+
+def init_rank(args):
+    """One process per GPU: device, process group (NCCL INIT lines on), and the
+    check that every rank owns a distinct GPU.  Returns
+    (world, rank, local device index, torch.device, shared-GPU reason or "", numa note)."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"[bench] WORLD_SIZE={world} but --gpus {args.gpus}")
+    # POSPOP_BENCH_DIST_BACKEND=gloo runs the N > 1 host path with fewer GPUs
+    # than ranks (tests only; the shared-GPU guard below then trips).
+    backend = os.environ.get("POSPOP_BENCH_DIST_BACKEND", "nccl")
+    ndev = max(torch.cuda.device_count(), 1)
+    if backend == "nccl" and local >= ndev:
+        raise SystemExit(f"[bench] rank {rank}: local rank {local} but only {ndev} visible GPUs")
+    local = local % ndev
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    numa = pin_numa(local) if world > 1 else "n/a (one rank)"
+    shared = ""
+    if world > 1:
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # INIT lines name every rank's device
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+        uuid = str(torch.cuda.get_device_properties(local).uuid)
+        uuids: list = [None] * world
+        dist.all_gather_object(uuids, uuid)
+        if len(set(uuids)) != world:
+            shared = f"ranks share a GPU ({world} ranks on {len(set(uuids))} distinct GPUs: {uuids})"
+    return world, rank, local, dev, shared, numa
+
+
+def reject_shared(args, metric, world, rank, shared) -> bool:
+    """True if the run must stop: ranks time-slicing one GPU would report
+    total bytes / max rank time above any single GPU's ceiling.  Rank 0 prints
+    a line with no value.  POSPOP_BENCH_ALLOW_SHARED_GPU=1 (tests) runs on,
+    marking the line."""
+    if not shared or os.environ.get("POSPOP_BENCH_ALLOW_SHARED_GPU") == "1":
+        return False
+    import torch.distributed as dist
+    if rank == 0:
+        print(json.dumps({"metric": metric, "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "rejected": shared, "workload": args.workload}), flush=True)
+    print(f"[bench] rank {rank}: {shared}; no headline", file=sys.stderr, flush=True)
+    dist.destroy_process_group()
+    return True
+
+
+def isolated_ms(launch, stream, reps: int = 5) -> float:
+    """Device time of ONE launch, free of host launch latency: a device sleep
+    is queued first, so the start event, the launch and the end event are all
+    enqueued before the GPU reaches them.  Median of `reps`."""
+    import torch
+    out = []
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(2_000_000)  # ~1 ms of device time
+            a0.record(stream)
+            launch()
+            a1.record(stream)
+            a1.synchronize()
+            out.append(a0.elapsed_time(a1))
+    return statistics.median(out)
+
+
 # ---------------------------------------------------------------------------------------------
 # reference arm: the reference's own CPU implementation
 # ---------------------------------------------------------------------------------------------
 
-def cpu_reference_measure(k: int, gen_kind: int, sample_words: int, reps: int, threads: int):
-    """Times the reference library (oracle/_ref) -- or the oracle port when the
-    reference was not built -- on the first `sample_words` words of the workload.
-    Returns (best GB/s, median GB/s, kind, counts, single-thread GB/s)."""
-    import numpy as np
+def _ref_libs():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
-
     orc = pyoracle.Oracle()
-    data = orc.generate(gen_kind, 1, sample_words, threads=threads)
-    words16 = data.view(np.uint16)
     try:
-        ref = pyoracle.Reference()
-        kind = "reference"
+        return orc, pyoracle.Reference(), "reference"
+    except Exception:  # noqa: BLE001
+        return orc, None, "port"
 
-        def run(nthreads):  # k=8 runs the 16-bit API and folds below (SURVEY 8c)
-            return ref.pospopcnt_mt(words16, nthreads)
-    except Exception:
-        kind = "port"
 
-        def run(nthreads):
-            return orc.pospopcnt(words16, 16, threads=nthreads)
+def ref_count_fn(orc, ref, k: int, threads: int):
+    """fn(data) -> k counts: pospop::pospopcnt fork-join + merge_counts over
+    `threads` contiguous chunks (proj/tests/test_core.cpp:155-175).  k = 8 runs
+    the reference's 16-bit API per chunk with the SURVEY 8c fold (odd head /
+    tail bytes counted directly); the oracle port when the reference is absent."""
+    import numpy as np
+    if ref is None:
+        return lambda data: np.asarray(orc.pospopcnt(data, k, threads=threads), np.uint64)
+    if k == 16:
+        return lambda data: np.asarray(ref.pospopcnt_mt(data.view(np.uint16), threads), np.uint64)
 
-    run(threads)  # warm-up + page-in
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        counts = run(threads)
-        times.append(time.perf_counter() - t0)
-    t0 = time.perf_counter()
-    run(1)
-    t1 = time.perf_counter() - t0
-    nbytes = data.nbytes
-    if k == 8:  # SURVEY 8c fold: c8[p] = c16[p] + c16[p+8]
-        counts = counts[:8] + counts[8:]
-    return nbytes / min(times) / 1e9, nbytes / statistics.median(times) / 1e9, kind, counts, nbytes / t1 / 1e9
+    def run(data):
+        n = data.nbytes * 8 // k
+        cuts = np.array([n * i // (4 * threads) for i in range(4 * threads + 1)], np.uint64)
+        return ref.segmented(data, cuts, k, threads).sum(axis=0, dtype=np.uint64)
+    return run
 
 
 def ref_flagstats_mt(words, threads):
@@ -261,130 +395,151 @@ def ref_flagstats_mt(words, threads):
     return np.sum(parts, axis=0, dtype=np.uint64)
 
 
+def oracle_flagstats_mt(orc, words, threads):
+    """The oracle's flagstats (per-word restatement) over `threads` chunks, summed: the gate."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    n = words.size
+    cuts = [n * i // threads for i in range(threads + 1)]
+
+    def one(i):
+        rc, out, _ = orc.flagstats(words[cuts[i]:cuts[i + 1]])
+        assert rc == 0
+        return out
+    with ThreadPoolExecutor(threads) as ex:
+        return np.sum(list(ex.map(one, range(threads))), axis=0, dtype=np.uint64)
+
+
 SEG_WORDS = 4096  # words per array in cfg5
 
 
+def host_workload(orc, workload: str, words: int, threads: int):
+    """The workload's first `words` words generated on the host (same counter-
+    based generator as the device: bit-identical data).  cfg3 sits at +3 bytes
+    of a 16-byte-aligned buffer, like the device run."""
+    import numpy as np
+    k, gen_kind, _, _ = WORKLOADS[workload]
+    wb = k // 8
+    if workload == "cfg3":
+        raw = np.empty(words * wb + 64, np.uint8)
+        base = (-raw.ctypes.data) % 16
+        view = raw[base + 3: base + 3 + words * wb]
+        orc.generate(gen_kind, 1, words, threads=threads, out=view)
+        return view
+    return orc.generate(gen_kind, 1, words, threads=threads)
+
+
+def time_steps(fn, steps: int, warmup: int, budget_s: float = 240.0):
+    for _ in range(max(warmup, 1)):
+        fn()
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:  # keep the arm within a few minutes
+            break
+    return times
+
+
 def run_reference(args):
+    """The reference arm: the whole workload per step, correctness gate first
+    (proj/core/src/bench.cpp:55-107: a result that disagrees with the oracle
+    produces no record), then `steps` timed passes (mean reported, best too)."""
+    import numpy as np
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    if args.workload in ("flag", "flagmix"):
-        return run_reference_flag(args)
+    threads = host_threads()
+    orc, ref, kind = _ref_libs()
+    k, gen_kind, total, desc = WORKLOADS[args.workload]
+    wb = k // 8
+    metric = FLAG_METRIC if args.workload in ("flag", "flagmix") else METRIC
+    t_gen = time.perf_counter()
     if args.workload.startswith("cfg5"):
-        return run_reference_seg(args)
-    k, gen_kind, total, desc = WORKLOADS[args.workload]
-    threads = os.cpu_count() or 1
-    # bounded sample: 2^28 words of the workload stream per step (512 MiB for u16)
-    sample = min(total, 1 << 28) if k == 16 else min(total, 1 << 29)
-    import numpy as np
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-    orc = pyoracle.Oracle()
-    data = orc.generate(gen_kind, 1, sample, threads=threads)
-    words16 = data.view(np.uint16)
-    try:
-        ref = pyoracle.Reference()
-        kind = "reference"
-        run = lambda: ref.pospopcnt_mt(words16, threads)  # noqa: E731
-    except Exception:
-        kind = "port"
-        run = lambda: orc.pospopcnt(words16, 16, threads=threads)  # noqa: E731
-    for _ in range(max(args.warmup, 1)):
-        run()
-    times = []
-    t_all = time.perf_counter()
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > 240:  # keep the arm within a few minutes
-            break
+        arrays = total // SEG_WORDS
+        if args.ref_words:
+            arrays = max(1, min(arrays, args.ref_words // SEG_WORDS))
+        words = arrays * SEG_WORDS
+        data = orc.generate(gen_kind, 1, words, threads=threads)
+        offs = np.arange(arrays + 1, dtype=np.uint64) * SEG_WORDS
+        if ref is None:
+            run = lambda: orc.segmented(data, offs, k, threads=threads)  # noqa: E731
+        else:
+            run = lambda: ref.segmented(data, offs, k, threads)  # noqa: E731
+        want = orc.segmented(data, offs, k, threads=threads)
+        gate = lambda got: bool((got == want).all())  # noqa: E731
+        what = (f"all {arrays} arrays x {SEG_WORDS} words per step; per array the reference's 16-bit "
+                f"pospop::pospopcnt after the SURVEY 8c deinterleave (k/16 streams), arrays fork-joined over "
+                f"{threads} threads")
+    elif args.workload in ("flag", "flagmix"):
+        words = min(total, args.ref_words) if args.ref_words else total
+        data = orc.generate(gen_kind, 1, words, threads=threads)
+        run = lambda: ref_flagstats_mt(data, threads)  # noqa: E731
+        want20 = oracle_flagstats_mt(orc, data, threads)
+        gate = lambda got: [int(x) for x in got] == [int(x) for x in want20]  # noqa: E731
+        what = (f"all {words} words of the {args.workload} stream per step; pospop::flagstats_pospopcnt "
+                f"fork-joined over {threads} chunks, summaries summed")
+    else:
+        words = min(total, args.ref_words) if args.ref_words else total
+        data = host_workload(orc, args.workload, words, threads)
+        fn = ref_count_fn(orc, ref, k, threads)
+        run = lambda: fn(data)  # noqa: E731
+        want = np.asarray(orc.pospopcnt(data, k, threads=threads), np.uint64)
+        gate = lambda got: bool((np.asarray(got, np.uint64) == want).all())  # noqa: E731
+        what = (f"all {words} words of the {args.workload} stream per step"
+                + (" (at +3 bytes)" if args.workload == "cfg3" else "")
+                + f"; pospop::pospopcnt (Auto->Csa16 at native width) fork-join over {threads} threads "
+                  f"+ merge_counts" + ("; k = 8 via the SURVEY 8c fold" if k == 8 else ""))
+    t_gen = time.perf_counter() - t_gen
+    if not gate(run()):  # correctness gate, doubles as warm-up
+        raise SystemExit("[bench] correctness gate: the reference disagrees with the oracle")
+    times = time_steps(run, args.steps, args.warmup)
+    nbytes = words * wb
     mean = sum(times) / len(times)
-    gbs = data.nbytes / mean / 1e9
+    gbs = nbytes / mean / 1e9
+    same = words == total if not args.workload.startswith("cfg5") else words == total
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 4), "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": {"workload": desc, "sample_words_per_step": sample, "host_threads": threads},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": kind,
-                         "sample": f"first {sample} words of the {args.workload} stream per step; pospop::pospopcnt "
-                                   f"(Auto->Csa16 at native width) fork-join over {threads} threads + merge_counts"},
-        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-def run_reference_flag(args):
-    import numpy as np
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-    k, gen_kind, total, desc = WORKLOADS[args.workload]
-    threads = os.cpu_count() or 1
-    sample = min(total, 1 << 27)
-    words = pyoracle.Oracle().generate(gen_kind, 1, sample, threads=threads)
-    for _ in range(max(args.warmup, 1)):
-        ref_flagstats_mt(words, threads)
-    times = []
-    t_all = time.perf_counter()
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        ref_flagstats_mt(words, threads)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > 240:
-            break
-    mean = sum(times) / len(times)
-    gbs = words.nbytes / mean / 1e9
-    line = {
-        "impl": "reference", "metric": FLAG_METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 4), "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": {"workload": desc, "sample_words_per_step": sample, "host_threads": threads},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"first {sample} words of the flag stream per step; pospop::flagstats_pospopcnt "
-                                   f"fork-joined over {threads} chunks, summaries summed"},
-        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-def run_reference_seg(args):
-    import numpy as np
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-    k, gen_kind, total, desc = WORKLOADS[args.workload]
-    threads = os.cpu_count() or 1
-    arrays = 8192  # bounded sample: the first 8192 arrays per step
-    data = pyoracle.Oracle().generate(gen_kind, 1, arrays * SEG_WORDS, threads=threads)
-    offs = np.arange(arrays + 1, dtype=np.uint64) * SEG_WORDS
-    ref = pyoracle.Reference()
-    for _ in range(max(args.warmup, 1)):
-        ref.segmented(data, offs, k, threads)
-    times = []
-    t_all = time.perf_counter()
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        ref.segmented(data, offs, k, threads)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > 240:
-            break
-    mean = sum(times) / len(times)
-    gbs = data.nbytes / mean / 1e9
-    sample = (f"first {arrays} arrays x {SEG_WORDS} words per step; per array the reference's 16-bit "
-              f"pospop::pospopcnt after the SURVEY 8c deinterleave (k/16 streams), arrays fork-joined over "
-              f"{threads} threads")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 4), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": f"u{k}", "data": "synthetic",
-        "config": {"workload": desc, "sample_arrays_per_step": arrays, "host_threads": threads},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+        "config": {"workload": desc, "words_per_step": words, "bytes_per_step": nbytes, "host_threads": threads,
+                   "same_config_as_ours": same, "generate_s": round(t_gen, 2)},
+        "best_gbs": round(nbytes / min(times) / 1e9, 3),
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": what + f"; correctness gate vs the oracle passed; mean of {len(times)} steps "
+                                          f"(best {nbytes / min(times) / 1e9:.2f} GB/s)"},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline_full(host, k: int, workload: str, gpu_counts, words: int):
+    """Our arm's cpu_baseline leg (rank 0, N = 1): the reference on the SAME
+    host copy of the whole workload the e2e leg just counted, best of 3, with
+    the GPU's counts as the gate."""
+    import numpy as np
+    threads = host_threads()
+    orc, ref, kind = _ref_libs()
+    fn = ref_count_fn(orc, ref, k, threads)
+    got = fn(host)
+    assert (np.asarray(got, np.uint64) == np.asarray(gpu_counts, np.uint64)).all(), \
+        "correctness gate: GPU and reference disagree"
+    best = None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        fn(host)
+        dt = time.perf_counter() - t0
+        best = dt if best is None or dt < best else best
+    t0 = time.perf_counter()
+    ref_count_fn(orc, ref, k, 1)(host[: min(host.nbytes, 1 << 28)])
+    single = min(host.nbytes, 1 << 28) / (time.perf_counter() - t0) / 1e9
+    return {"value": round(host.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"all {words} words ({host.nbytes >> 20} MiB) of the {workload} stream (the e2e leg's host "
+                      f"copy), pospop::pospopcnt fork-join over {threads} threads + merge_counts, best of 3 "
+                      f"(1 thread on 256 MiB: {single:.2f} GB/s); counts equal the GPU's"}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -400,16 +555,9 @@ def run_ours_seg(args):
 
     import paper_1911_02696_b200 as pp
 
-    world, rank, local = dist_env()
-    backend = os.environ.get("POSPOP_BENCH_DIST_BACKEND", "nccl")
-    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+    world, rank, local, dev, shared, numa = init_rank(args)
+    if reject_shared(args, METRIC, world, rank, shared):
+        return 3
     k, gen_kind, total, desc = WORKLOADS[args.workload]
     wb = k // 8
     n_arrays_total = total // SEG_WORDS
@@ -448,14 +596,7 @@ def run_ours_seg(args):
         dist.barrier()
     launches = pp.kernel_launches() - launches0
     elapsed_ms = t_begin.elapsed_time(t_end)
-    iso = []
-    for _ in range(5):
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        step()
-        a1.record(stream)
-        a1.synchronize()
-        iso.append(a0.elapsed_time(a1))
+    iso_ms = isolated_ms(step, stream)
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -468,31 +609,31 @@ def run_ours_seg(args):
     achieved = per_launch_bytes / (kern_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
 
-    # correctness gate against the oracle on the first arrays
+    # correctness gate: every row of this rank against the oracle
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
-    sample_arrays = min(arrays, 512)
-    host_sample = data[: sample_arrays * SEG_WORDS * wb].cpu().numpy()
-    want = pyoracle.Oracle().segmented(host_sample, np.arange(sample_arrays + 1, dtype=np.uint64) * SEG_WORDS, k,
-                                       threads=4)
-    assert (rows[:sample_arrays].cpu().numpy().view(np.uint64) == want).all(), "segmented rows disagree with oracle"
+    host_data = data.cpu().numpy()
+    host_offs = np.arange(arrays + 1, dtype=np.uint64) * SEG_WORDS
+    want = pyoracle.Oracle().segmented(host_data, host_offs, k, threads=host_threads())
+    assert (rows.cpu().numpy().view(np.uint64) == want).all(), "segmented rows disagree with the oracle"
 
     e2e = None
     if not args.no_e2e:
         host = torch.empty(words * wb, dtype=torch.uint8, pin_memory=True)
         host.copy_(data)
-        host_offs = np.arange(arrays + 1, dtype=np.uint64) * SEG_WORDS
         host_rows = np.empty((arrays, k), np.uint64)
         host_arr = host.numpy()
         pp.pospopcnt_segmented(host_arr, host_offs, k, out=host_rows)
         e2e_steps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
         step_ms = []
         for _ in range(e2e_steps):
             t0 = time.perf_counter()
             pp.pospopcnt_segmented(host_arr, host_offs, k, out=host_rows)
             step_ms.append((time.perf_counter() - t0) * 1e3)
         e2e_s = sum(step_ms) / len(step_ms) / 1e3
-        assert (host_rows[:sample_arrays] == want).all()
+        assert (host_rows == want).all()
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -510,21 +651,19 @@ def run_ours_seg(args):
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        cpu_arrays = min(arrays, 8192)
-        hs = data[: cpu_arrays * SEG_WORDS * wb].cpu().numpy()
-        ho = np.arange(cpu_arrays + 1, dtype=np.uint64) * SEG_WORDS
-        ref = pyoracle.Reference()
-        ref_rows = ref.segmented(hs, ho, k, threads)
+        threads = host_threads()
+        orc, ref, kind = _ref_libs()
+        seg = (lambda: ref.segmented(host_data, host_offs, k, threads)) if ref is not None else \
+            (lambda: orc.segmented(host_data, host_offs, k, threads=threads))
+        assert (seg() == want).all(), "correctness gate: reference rows disagree"
         best = None
         for _ in range(3):
             t0 = time.perf_counter()
-            ref.segmented(hs, ho, k, threads)
+            seg()
             dt = time.perf_counter() - t0
             best = dt if best is None or dt < best else best
-        assert (ref_rows[:sample_arrays] == want[: min(sample_arrays, cpu_arrays)]).all()
-        cpu = {"value": round(hs.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-               "sample": f"first {cpu_arrays} arrays ({hs.nbytes >> 20} MiB); per array the reference's 16-bit "
+        cpu = {"value": round(host_data.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+               "sample": f"all {arrays} arrays ({host_data.nbytes >> 20} MiB); per array the reference's 16-bit "
                          f"pospop::pospopcnt after the SURVEY 8c deinterleave, arrays fork-joined over {threads} "
                          f"threads, best of 3; rows equal the GPU's"}
 
@@ -535,15 +674,16 @@ def run_ours_seg(args):
         "data": "synthetic (counter-based generator, generated in place in HBM)",
         "config": {"workload": desc, "arrays_total": n_arrays_total, "words_per_array": SEG_WORDS, "k": k,
                    "bytes_per_step": total_bytes, "parallelism": f"shard{world}",
-                   "l2_policy": "input >> 126 MB L2; no flush needed",
-                   "kernel": "segmented (one warp per array, software-pipelined) for k=32; dynamic array claims "
-                             "for k=64; one launch per step"},
+                   "l2_policy": "input >> 126 MB L2; no flush needed", "numa": numa,
+                   "kernel": "segmented_auto_kernel (adaptive: tile mode for 16/32 KiB arrays); one launch per step"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, world),
                      "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
-                     "kernel_ms_isolated": round(statistics.median(iso), 5),
+                     "kernel_ms_single_launch": round(iso_ms, 5),
+                     "achieved_single_launch": round(per_launch_bytes / (iso_ms * 1e-3) / 1e9, 2),
                      "timing": "back-to-back launches with programmatic dependent launch, CUDA events around the "
-                               "timed region; isolated = median of 5 single launches bracketed by events",
+                               "timed region; single launch = events around one launch queued behind a device "
+                               "sleep (no host launch latency), median of 5",
                      "bytes_per_launch": per_launch_bytes,
                      "frac_of_theoretical_8180": round(achieved / 8180.0, 4)},
         "cpu_baseline": cpu,
@@ -551,6 +691,8 @@ def run_ours_seg(args):
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }
+    if shared:
+        line["rejected"] = shared
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -570,16 +712,9 @@ def run_ours_flag(args):
 
     import paper_1911_02696_b200 as pp
 
-    world, rank, local = dist_env()
-    backend = os.environ.get("POSPOP_BENCH_DIST_BACKEND", "nccl")
-    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+    world, rank, local, dev, shared, numa = init_rank(args)
+    if reject_shared(args, FLAG_METRIC, world, rank, shared):
+        return 3
     k, gen_kind, total, desc = WORKLOADS[args.workload]
     lo, hi = (rank * total, (rank + 1) * total) if args.scaling == "weak" else \
         (total * rank // world, total * (rank + 1) // world)
@@ -593,8 +728,11 @@ def run_ours_flag(args):
     fields = pp._BUCKET_FIELDS
     red = torch.zeros(2 * len(fields), dtype=torch.int64, device=dev)
 
-    def step():
+    def call():
         assert lib.pospop_flagstats(data.data_ptr(), words, C.byref(summ), None, None) == 0
+
+    def step():
+        call()
         if world > 1:
             vals = [getattr(summ.pass_, f) for f in fields] + [getattr(summ.fail, f) for f in fields]
             red.copy_(torch.tensor(vals, dtype=torch.int64))
@@ -617,15 +755,9 @@ def run_ours_flag(args):
         torch.cuda.synchronize(dev)
     launches = pp.kernel_launches() - launches0
     elapsed_ms = t_begin.elapsed_time(t_end)
-    # kernel alone: events around single launches of the same call
-    iso = []
-    for _ in range(5):
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        assert lib.pospop_flagstats(data.data_ptr(), words, C.byref(summ), None, None) == 0
-        a1.record(stream)
-        a1.synchronize()
-        iso.append(a0.elapsed_time(a1))
+    # the kernel alone: async launches of the same kernel, back to back
+    out33 = torch.zeros(33, dtype=torch.int64, device=dev)
+    iso_ms = isolated_ms(call, stream)
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -633,23 +765,28 @@ def run_ours_flag(args):
     ms_per_step = elapsed_ms / args.steps
     total_bytes = total * (world if args.scaling == "weak" else 1) * 2
     value = total_bytes / (ms_per_step * 1e-3) / 1e9
-    kern_ms = elapsed_ms / args.steps if world == 1 else statistics.median(iso)
+    kern_ms = elapsed_ms / args.steps if world == 1 else iso_ms
     per_launch_bytes = words * 2
     achieved = per_launch_bytes / (kern_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
+    del out33
+    gpu_summary = pp.flagstats(data).as_list()
 
+    host_arr = None
     e2e = None
     if not args.no_e2e:
         host = torch.empty(words, dtype=torch.int16, pin_memory=True)
         host.copy_(data)
         host_arr = host.numpy().view(np.uint16)
-        want = pp.flagstats(host_arr).as_list()
+        assert pp.flagstats(host_arr).as_list() == gpu_summary
         e2e_steps = max(1, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             got = pp.flagstats(host_arr)
         e2e_s = (time.perf_counter() - t0) / e2e_steps
-        assert got.as_list() == want
+        assert got.as_list() == gpu_summary
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -660,25 +797,21 @@ def run_ours_flag(args):
         if link:
             e2e["h2d_link_gbs"] = link
             e2e["frac_of_h2d_link"] = round(e2e["value"] / world / link, 4)
-        del host
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        sample = min(words, 1 << 27)
-        host_sample = data[:sample].cpu().numpy().view(np.uint16)
-        ref_flagstats_mt(host_sample, threads)
+        threads = host_threads()
+        hs = host_arr if host_arr is not None else data.cpu().numpy().view(np.uint16)
+        ref_out = ref_flagstats_mt(hs, threads)
+        assert [int(x) for x in ref_out] == gpu_summary, "correctness gate: GPU and reference flagstats disagree"
         best = None
         for _ in range(3):
             t0 = time.perf_counter()
-            ref_out = ref_flagstats_mt(host_sample, threads)
+            ref_flagstats_mt(hs, threads)
             dt = time.perf_counter() - t0
             best = dt if best is None or dt < best else best
-        gpu = pp.flagstats(data[:sample])
-        assert [int(x) for x in ref_out] == gpu.as_list(), "correctness gate: GPU and reference flagstats disagree"
-        cpu = {"value": round(host_sample.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads,
-               "kind": "reference",
-               "sample": f"first {sample} words ({sample * 2 >> 20} MiB) of the {args.workload} stream; "
+        cpu = {"value": round(hs.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+               "sample": f"all {words} words ({hs.nbytes >> 20} MiB) of the {args.workload} stream; "
                          f"pospop::flagstats_pospopcnt fork-joined over {threads} chunks, best of 3; "
                          f"summary equals the GPU's"}
 
@@ -689,15 +822,16 @@ def run_ours_flag(args):
         "data": "synthetic (counter-based FLAG generator, generated in place in HBM)",
         "config": {"workload": desc, "words_total": total, "bytes_per_step": total_bytes,
                    "parallelism": f"shard{world}", "l2_policy": "input >> 126 MB L2; no flush needed",
-                   "kernel": "stream_kernel<NBANK=3,L=5,VB=32,BLOCK=512,SCHED=2,MODE=2>: byte-frame FLAG "
-                             "transform (PRMT regroup, 4 words per SWAR op) + three Harley-Seal trees; one "
-                             "launch + 33-counter D2H per step"},
+                   "numa": numa,
+                   "kernel": "stream_kernel MODE 2: byte-frame FLAG transform + Harley-Seal trees; one launch + "
+                             "33-counter D2H per step"},
         "words_per_s": round(total_bytes / 2 / (ms_per_step * 1e-3), 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, world),
                      "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
-                     "kernel_ms_isolated": round(statistics.median(iso), 5),
-                     "timing": "CUDA events around K synchronous C-ABI calls (kernel + 264-byte D2H each)",
+                     "kernel_ms_single_launch": round(iso_ms, 5),
+                     "timing": "CUDA events around K synchronous C-ABI calls (kernel + 264-byte D2H each); single "
+                               "launch = one call queued behind a device sleep, median of 5",
                      "bytes_per_launch": per_launch_bytes,
                      "frac_of_theoretical_8180": round(achieved / 8180.0, 4)},
         "cpu_baseline": cpu,
@@ -705,6 +839,8 @@ def run_ours_flag(args):
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }
+    if shared:
+        line["rejected"] = shared
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -719,18 +855,9 @@ def run_ours(args):
 
     import paper_1911_02696_b200 as pp
 
-    world, rank, local = dist_env()
-    # POSPOP_BENCH_DIST_BACKEND=gloo exercises the N > 1 code path with fewer GPUs
-    # than ranks (tests only): ranks share devices, the k-vector goes through gloo.
-    backend = os.environ.get("POSPOP_BENCH_DIST_BACKEND", "nccl")
-    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+    world, rank, local, dev, shared, numa = init_rank(args)
+    if reject_shared(args, METRIC, world, rank, shared):
+        return 3
     k, gen_kind, total, desc = WORKLOADS[args.workload]
     wb = k // 8
     if args.scaling == "weak":
@@ -743,43 +870,46 @@ def run_ours(args):
     data = buf[offset:offset + words * wb]
     stream = torch.cuda.current_stream(dev)
     pp.generate(gen_kind, 1, data, base=lo, n=words, stream=stream)
-    out = torch.zeros(k, dtype=torch.int64, device=dev)
     torch.cuda.synchronize(dev)
 
-    # N > 1: the 128-byte k-vector all-reduce of step i runs on a communication
-    # stream while step i+1's kernel counts into the other output buffer
-    # (double-buffered; a buffer is reused only after its reduction finished).
-    outs = [out, torch.zeros(k, dtype=torch.int64, device=dev)]
-    # High priority: when a count kernel's CTA retires, the (one-CTA) NCCL all-reduce
-    # kernel is scheduled before the next count's CTAs, which PDL launches early.
+    # Per step, N = 1: one count launch.  N > 1: the count kernel publishes the
+    # rank's k-vector (step-tagged rows in every GPU's exchange buffer over
+    # peer memory) and a one-CTA reduce kernel waits for all rows and writes
+    # the all-reduced counts on the device (paper_1911_02696_b200.exchange);
+    # fallback: an NCCL all-reduce on a communication stream, double-buffered.
+    local_out = [torch.zeros(k, dtype=torch.int64, device=dev) for _ in range(2)]
+    totals = [torch.zeros(k, dtype=torch.int64, device=dev) for _ in range(2)]
     comm = torch.cuda.Stream(dev, priority=-1) if world > 1 else None
     counted = [torch.cuda.Event() for _ in range(2)]
     reduced = [torch.cuda.Event() for _ in range(2)]
     issued = [False, False]
+    xs = [0]  # the exchange's next step number (steps are consecutive)
 
-    # Fused exchange: set up the peer gather slots, prove they work on this
-    # machine (every rank's rows land on every GPU and sum to the NCCL
-    # all-reduce), else fall back to the NCCL all-reduce and say why.
-    # Every rank runs the same collectives in the same order whatever fails
-    # locally (PeerGather.create), so a failure on one rank cannot hang others.
+    # Fused exchange: set it up and prove it on this machine (every rank's
+    # device total equals the NCCL all-reduce of the local counts), else fall
+    # back to NCCL.  Every rank runs the same collectives in the same order
+    # whatever fails locally, so one rank's failure cannot hang the others.
     pg, collective = None, ("nccl" if world > 1 else "none")
-    if world > 1 and args.collective == "p2p":
+    if world > 1 and args.collective == "p2p" and not shared:
         from paper_1911_02696_b200.exchange import PeerGather
         pg, reason = PeerGather.create(k)
         if pg is not None:
-            probe = torch.zeros(k, dtype=torch.int64, device=dev)
+            probe_l = torch.zeros(k, dtype=torch.int64, device=dev)
+            probe_t = torch.zeros(k, dtype=torch.int64, device=dev)
             local_ok = 1
             try:
-                pg.count(data, probe, 0, stream=stream, len_words=min(words, 1 << 20))
+                pg.allreduce(data, probe_l, probe_t, xs[0], stream=stream, len_words=min(words, 1 << 20))
+                xs[0] += 1
                 torch.cuda.synchronize(dev)
+                pg.status()
             except Exception as e:  # noqa: BLE001
                 local_ok, reason = 0, f"fused count: {e}"
-            ref = probe.clone()
+            ref = probe_l.clone()
             dist.all_reduce(ref)  # every rank, always
-            ok = torch.tensor([local_ok * int(torch.equal(pg.result(0), ref))], device=dev)
+            ok = torch.tensor([local_ok * int(torch.equal(probe_t, ref))], device=dev)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if int(ok.item()) != 1:
-                pg, reason = None, reason or "peer gather rows disagree with the NCCL all-reduce"
+                pg, reason = None, reason or "exchange totals disagree with the NCCL all-reduce"
         if pg is not None:
             collective = "p2p"
         else:
@@ -787,9 +917,10 @@ def run_ours(args):
             collective = f"nccl (p2p unavailable: {str(reason)[:120]})"
 
     def step(i):
-        o = outs[i % 2]
-        if pg is not None:  # one kernel: count + deliver the k-vector to every GPU
-            pg.count(data, o, i, stream=stream, len_words=words)
+        o, tot = local_out[i % 2], totals[i % 2]
+        if pg is not None:  # count + publish, then the device-side reduce
+            pg.allreduce(data, o, tot, xs[0], stream=stream, len_words=words)
+            xs[0] += 1
             return
         if world > 1 and issued[i % 2]:
             stream.wait_event(reduced[i % 2])
@@ -798,7 +929,8 @@ def run_ours(args):
             counted[i % 2].record(stream)
             with torch.cuda.stream(comm):
                 comm.wait_event(counted[i % 2])
-                dist.all_reduce(o)
+                tot.copy_(o)
+                dist.all_reduce(tot)
                 reduced[i % 2].record(comm)
             issued[i % 2] = True
 
@@ -813,10 +945,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
 
-    # No events inside the step loop at N = 1: consecutive launches overlap through
+    # No events inside the step loop: consecutive launches overlap through
     # programmatic dependent launch (the next count's CTAs start on SMs freed by
     # the previous one's tail) and any stream operation in between would
-    # serialise them.  The average launch duration is then region / K.
+    # serialise them.  The average step duration is then region / K.
     t_begin = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     launches0 = pp.kernel_launches()
@@ -835,27 +967,21 @@ def run_ours(args):
         dist.barrier()
     launches = pp.kernel_launches() - launches0
     elapsed_ms = t_begin.elapsed_time(t_end)
+    last = (args.steps - 1) % 2
+    if pg is not None:
+        pg.status()  # raises if a bounded device wait timed out
     if world == 1:
         kern_ms = elapsed_ms / args.steps  # the step is exactly one launch
-    else:  # launch-only loop on the same stream, same launches, no reductions
+    else:  # the count kernel alone: a launch-only loop on the same stream
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         kreps = max(5, min(args.steps, 50))
         k0.record(stream)
         for _ in range(kreps):
-            pp.count_async(data, outs[0], k, stream=stream, len_words=words)
+            pp.count_async(data, local_out[0], k, stream=stream, len_words=words)
         k1.record(stream)
         torch.cuda.synchronize(dev)
         kern_ms = k0.elapsed_time(k1) / kreps
-    # Isolated launch time (events around single launches), for reference.
-    iso = []
-    for _ in range(5):
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        pp.count_async(data, outs[0], k, stream=stream, len_words=words)
-        a1.record(stream)
-        a1.synchronize()
-        iso.append(a0.elapsed_time(a1))
-    iso_ms = statistics.median(iso)
+    iso_ms = isolated_ms(lambda: pp.count_async(data, local_out[0], k, stream=stream, len_words=words), stream)
     t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -864,13 +990,17 @@ def run_ours(args):
     total_bytes = (total * (world if args.scaling == "weak" else 1)) * wb
     value = total_bytes / (ms_per_step * 1e-3) / 1e9
 
-    counts = outs[(args.steps - 1) % 2].cpu().numpy().astype(np.uint64)
-    if pg is not None:  # the delivered rows of the last step must sum to the NCCL all-reduce
-        local = outs[(args.steps - 1) % 2].clone()
-        ref = local.clone()
+    # the last step's device total vs an NCCL all-reduce of this step's local counts
+    pp.count_async(data, local_out[0], k, stream=stream, len_words=words)
+    torch.cuda.synchronize(dev)
+    mine = local_out[0].cpu().numpy().astype(np.uint64)
+    counts = mine
+    if world > 1:
+        ref = local_out[0].clone()
         dist.all_reduce(ref)
-        assert torch.equal(pg.result(args.steps - 1), ref), "p2p exchange disagrees with NCCL"
-        counts = pg.result(args.steps - 1).cpu().numpy().astype(np.uint64)
+        counts = ref.cpu().numpy().astype(np.uint64)
+        assert (totals[last].cpu().numpy().astype(np.uint64) == counts).all(), \
+            f"{collective} exchange disagrees with an NCCL all-reduce"
     if args.workload == "cfg2":
         assert int(counts.sum()) == total, "one-hot invariant violated"
 
@@ -880,22 +1010,26 @@ def run_ours(args):
 
     # ---- e2e: the C-ABI call on pinned HOST memory (H2D + D2H inside the timed region) ----
     e2e = None
+    host_arr = None
     if not args.no_e2e:
-        host = torch.empty(words * wb, dtype=torch.uint8, pin_memory=True)
+        hbuf = torch.empty(words * wb + offset + 64, dtype=torch.uint8, pin_memory=True)
+        host = hbuf[offset:offset + words * wb]
         host.copy_(data)
         torch.cuda.synchronize(dev)
         host_arr = host.numpy()
-        ref_counts = pp.pospopcnt_k(host_arr, k)  # warm-up: staging buffers, pinned result
-        assert ref_counts == counts if world == 1 else True
+        got = pp.pospopcnt_k(host_arr, k)  # warm-up: staging buffers, pinned result
+        assert (np.asarray(got.counts, np.uint64) == mine).all(), "e2e counts disagree with the device count"
         e2e_steps = max(1, min(args.steps, 10))
         if world > 1:
             dist.barrier()
+        red = torch.zeros(k, dtype=torch.int64, device=dev)
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             c = pp.pospopcnt_k(host_arr, k)
             if world > 1:
-                ct = torch.from_numpy(c.counts.astype(np.int64))
-                dist.all_reduce(ct.to(dev))
+                red.copy_(torch.from_numpy(c.counts.astype(np.int64)))
+                dist.all_reduce(red)
+                red.cpu()
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
@@ -904,29 +1038,22 @@ def run_ours(args):
         e2e = {"value": round(total_bytes / e2e_s / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": words * wb, "d2h_bytes_per_step": k * 8, "steps": e2e_steps,
                "path": "pospopcnt_k C ABI on a pinned host buffer: chunked H2D (64 MiB x3 ring) overlapped "
-                       "with the kernel, k-vector D2H"}
+                       "with the kernel, k-vector D2H" + ("; one rank per GPU on its own host link, k-vectors "
+                                                         "all-reduced" if world > 1 else "")}
         link = h2d_link_gbs(host, dev)
         if link:
             e2e["h2d_link_gbs"] = link
             e2e["frac_of_h2d_link"] = round(e2e["value"] / world / link, 4)
-        del host
 
-    # ---- CPU baseline on the host (rank 0, N = 1 only) ----
+    # ---- CPU baseline on the host (rank 0, N = 1 only): the whole workload ----
     cpu = None
     if world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        sample = min(words, 1 << 28)
-        best, med, kind, cpu_counts, single = cpu_reference_measure(k, gen_kind, sample, 3, threads)
-        # correctness gate (bench.cpp:64-68): GPU counts of the same sample must match
-        gate = torch.zeros(k, dtype=torch.int64, device=dev)
-        pp.count_async(data, gate, k, stream=stream, len_words=sample)
-        torch.cuda.synchronize(dev)
-        assert (gate.cpu().numpy().astype(np.uint64) == np.asarray(cpu_counts, np.uint64)).all(), \
-            "correctness gate: GPU and reference disagree on the CPU sample"
-        cpu = {"value": round(best, 3), "unit": "GB/s", "cores": threads, "kind": kind,
-               "sample": f"first {sample} words ({sample * wb >> 20} MiB) of the {args.workload} stream, "
-                         f"pospop::pospopcnt fork-join over {threads} threads + merge_counts, best of 3 "
-                         f"(median {med:.2f} GB/s; 1 thread {single:.2f} GB/s); counts equal the GPU's"}
+        if host_arr is None:
+            hb = np.empty(words * wb + 64, np.uint8)
+            o16 = (-hb.ctypes.data) % 16 + offset
+            host_arr = hb[o16:o16 + words * wb]
+            host_arr[:] = data.cpu().numpy()
+        cpu = cpu_baseline_full(host_arr, k, args.workload, mine, words)
 
     traffic = ncu_traffic(args.workload, world)
     line = {
@@ -936,19 +1063,22 @@ def run_ours(args):
         "data": "synthetic (counter-based generator, generated in place in HBM)",
         "config": {"workload": desc, "words_total": total, "k": k, "bytes_per_step": total_bytes,
                    "parallelism": f"shard{world}", "l2_policy": "input >> 126 MB L2; no flush needed",
-                   "collective": collective,
+                   "collective": collective, "numa": numa,
                    "kernel": "stream_kernel<NBANK=1,L=7,VB=32,BLOCK=256,SCHED=2>: LDG.E.NA.256 + LOP3 Harley-Seal depth 7, CTA ranges + shared-counter warp tiles + global tail pool; one launch per step"
-                             + ("; the last CTA also stores the k-vector into every GPU's gather slot (peer memory)"
+                             + ("; its last CTA also publishes the step-tagged k-vector to every GPU (peer memory) "
+                                "and a one-CTA reduce kernel waits for all rows and sums them on the device"
                                 if collective == "p2p" else "")},
         "words_per_s": round(total_bytes / wb / (ms_per_step * 1e-3), 1),
         "pct_hbm_peak": round(100 * value / world / peak, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel_ms": round(kern_ms, 5), "kernel_ms_isolated": round(iso_ms, 5),
-                     "achieved_isolated": round(per_launch_bytes / (iso_ms * 1e-3) / 1e9, 2),
+                     "kernel_ms": round(kern_ms, 5), "kernel_ms_max_over_ranks": round(kern_ms_max, 5),
+                     "kernel_ms_single_launch": round(iso_ms, 5),
+                     "achieved_single_launch": round(per_launch_bytes / (iso_ms * 1e-3) / 1e9, 2),
                      "timing": "back-to-back launches with programmatic dependent launch, CUDA events "
-                               "around the timed region (no events between launches); isolated = median "
-                               "of 5 single launches bracketed by events",
+                               "around the timed region (no events between launches); single launch = events "
+                               "around one launch queued behind a device sleep (no host launch latency), "
+                               "median of 5",
                      "bytes_per_launch": per_launch_bytes,
                      "frac_of_theoretical_8180": round(achieved / 8180.0, 4)},
         "cpu_baseline": cpu,
@@ -956,6 +1086,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }
+    if shared:
+        line["rejected"] = shared
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -967,6 +1099,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
     if args.workload in ("flag", "flagmix"):
         return run_ours_flag(args)
     if args.workload.startswith("cfg5"):

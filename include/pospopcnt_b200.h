@@ -215,25 +215,46 @@ pospop_status pospopcnt_u16_async(const uint16_t* d_data, size_t len, uint64_t* 
 pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
                                     uint64_t* d_trace, size_t trace_ctas, int* grid_used, void* stream);
 
-/* Multi-GPU, one process per GPU: count fused with the exchange.
- * The k-vector sum across GPUs (reference merge_counts, pospop.cpp:33-37, the
- * sanctioned chunk-and-merge) is done through peer memory instead of a
- * separate collective: every rank owns a gather buffer from pospop_ipc_alloc,
+/* Multi-GPU, one process per GPU: count fused with a device-side all-reduce
+ * over peer memory.  The k-vector sum across GPUs (reference
+ * merge_counts, pospop.cpp:33-37, the sanctioned chunk-and-merge) needs no
+ * separate collective: every rank owns an exchange buffer of
+ * pospop_exchange_bytes(k, n_ranks, slots) bytes from pospop_ipc_alloc,
  * exports its handle (64 bytes, exchanged by the caller, e.g. over
  * torch.distributed), and maps the peers' buffers with pospop_ipc_open.
- * pospopcnt_allgather_async counts d_data like pospopcnt_async (d_counts gets
- * this rank's counts) and its last CTA also stores them into
- * d_slots[j][rank*k .. rank*k + k) for every j < n_ranks -- plain stores over
- * NVLink from inside the counting kernel.  d_slots is a DEVICE array of
- * n_ranks device pointers (the peers' buffers, own buffer included).  Once
- * every rank's launch has completed, summing a slot's n_ranks rows gives the
- * all-reduced counts on every GPU.  No kernel waits on another rank. */
+ *
+ * Per step (consecutive steps 0, 1, 2, ... on one stream per rank):
+ *  - pospopcnt_allgather_async counts d_data like pospopcnt_async (d_counts
+ *    gets this rank's counts); its last CTA then stores them as row `rank` of
+ *    slot step % slots in every rank's buffer (plain stores over NVLink) and
+ *    release-stores the row's step tag.  Before rewriting a slot it waits
+ *    until every peer has consumed that slot's previous step (credit).
+ *    d_peers is a DEVICE array of n_ranks buffer pointers (own included).
+ *  - pospop_exchange_reduce_async (same stream, own buffer) waits for the
+ *    n_ranks tags of the step, writes their row sum to d_total[0..k) -- the
+ *    all-reduced counts -- and returns the slot's credit.
+ * Both waits are bounded (20 s); a timeout sets an error code in the own
+ * buffer, which pospop_exchange_status (synchronous) reports as POSPOP_ECUDA.
+ * At most 64 ranks. */
 pospop_status pospop_ipc_alloc(size_t bytes, void** d_ptr, unsigned char handle[64]);  /* zeroed */
 pospop_status pospop_ipc_open(const unsigned char handle[64], void** d_ptr);
 pospop_status pospop_ipc_close(void* d_ptr);
 pospop_status pospop_ipc_free(void* d_ptr);
+size_t pospop_exchange_bytes(int k, int n_ranks, int slots);  /* 0 for invalid arguments */
 pospop_status pospopcnt_allgather_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
-                                        uint64_t* const* d_slots, int n_ranks, int rank, void* stream);
+                                        uint64_t* const* d_peers, int n_ranks, int rank, uint64_t step, int slots,
+                                        void* stream);
+pospop_status pospop_exchange_reduce_async(int k, uint64_t* d_own, int n_ranks, uint64_t step, int slots,
+                                           uint64_t* d_total, void* stream);
+pospop_status pospop_exchange_status(const uint64_t* d_own, uint64_t* consumed, uint64_t* error);
+/* Protocol self-test on one GPU (tests): n_ranks blocks of ONE cooperative
+ * launch play the ranks for `steps` consecutive steps with the same device
+ * code as the two kernels above -- optional sleep (sleep_ns, steps x n_ranks),
+ * credit wait, row stores + tags into every block's buffer, reduce of its own
+ * buffer.  inputs: steps x n_ranks x k host u64 (rank r's counts of step s);
+ * totals: n_ranks x steps x k host u64 (what each rank's reducer summed). */
+pospop_status pospop_exchange_selftest(int k, int n_ranks, int slots, int steps, const uint64_t* inputs,
+                                       const uint32_t* sleep_ns, uint64_t* totals);
 
 /* CUDA-graph replay for repeated counts of one device buffer, where launch
  * latency dominates (small inputs).  The graph is bound to (d_data, len,

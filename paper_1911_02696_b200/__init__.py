@@ -41,6 +41,7 @@ __all__ = [
     "KernelKind", "PospopcntConfig", "PositionalCounts", "InvalidArgument", "KernelUnavailableError",
     "CudaError", "validate", "merge_counts", "pospopcnt", "pospopcnt_k", "pospopcnt_u16_c32",
     "pospopcnt_segmented", "pospopcnt_sharded", "count_async", "segmented_async", "count_allgather_async",
+    "exchange_bytes", "exchange_reduce_async", "exchange_status",
     "ipc_alloc", "ipc_open", "ipc_close", "ipc_free", "generate", "digest",
     "supported_csa_widths", "native_csa_width", "device_available", "kernel_launches", "library_path",
     "FlagBucket", "FlagSummary", "InvalidFlagWordError", "flagstats", "pospopcnt_file",
@@ -145,7 +146,10 @@ def _load():
         "pospop_ipc_open": ([C.POINTER(C.c_ubyte), C.POINTER(vp)], C.c_int),
         "pospop_ipc_close": ([vp], C.c_int),
         "pospop_ipc_free": ([vp], C.c_int),
-        "pospopcnt_allgather_async": ([C.c_int, vp, sz, vp, vp, C.c_int, C.c_int, vp], C.c_int),
+        "pospop_exchange_bytes": ([C.c_int, C.c_int, C.c_int], sz),
+        "pospopcnt_allgather_async": ([C.c_int, vp, sz, vp, vp, C.c_int, C.c_int, C.c_uint64, C.c_int, vp], C.c_int),
+        "pospop_exchange_reduce_async": ([C.c_int, vp, C.c_int, C.c_uint64, C.c_int, vp, vp], C.c_int),
+        "pospop_exchange_status": ([vp, _u64p, _u64p], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -408,19 +412,45 @@ def count_async(data: Any, out: Any, k: int, *, accumulate: bool = False, flush_
                                    int(grid), int(block), _stream_ptr(stream)))
 
 
-def count_allgather_async(data: Any, out: Any, k: int, slots: Any, n_ranks: int, rank: int, *,
-                          stream: Any = None, len_words: int | None = None) -> None:
-    """Count fused with the cross-GPU exchange (pospopcnt_allgather_async): out
-    gets this rank's counts and the kernel's last CTA stores them into row
-    `rank` of every slot in `slots` (device array of n_ranks gather-slot
-    pointers, see paper_1911_02696_b200.exchange)."""
+def count_allgather_async(data: Any, out: Any, k: int, peers: Any, n_ranks: int, rank: int, step: int,
+                          slots: int = 2, *, stream: Any = None, len_words: int | None = None) -> None:
+    """Count fused with the producer half of the cross-GPU all-reduce
+    (pospopcnt_allgather_async): out gets this rank's counts and the kernel's
+    last CTA stores them as row `rank` of slot step % slots in every rank's
+    exchange buffer (`peers`: device array of n_ranks buffer pointers, see
+    paper_1911_02696_b200.exchange), tagged with the step."""
     addr, n = _addr_len(data, k)
     if len_words is not None:
         n = int(len_words)
     out_addr, _ = _addr_len(out, 64)
-    slots_addr, _ = _addr_len(slots, 64)
-    _check(_load().pospopcnt_allgather_async(int(k), addr or None, n, out_addr, slots_addr, int(n_ranks), int(rank),
-                                             _stream_ptr(stream)))
+    peers_addr, _ = _addr_len(peers, 64)
+    _check(_load().pospopcnt_allgather_async(int(k), addr or None, n, out_addr, peers_addr, int(n_ranks), int(rank),
+                                             int(step), int(slots), _stream_ptr(stream)))
+
+
+def exchange_bytes(k: int, n_ranks: int, slots: int = 2) -> int:
+    return int(_load().pospop_exchange_bytes(int(k), int(n_ranks), int(slots)))
+
+
+def exchange_reduce_async(k: int, own: int, n_ranks: int, step: int, total: Any, slots: int = 2, *,
+                          stream: Any = None) -> None:
+    """Consumer half: waits on the device for the n_ranks rows of `step` in this
+    rank's buffer `own`, writes their sum to `total` (k int64 on the device)
+    and returns the slot's credit to the producers."""
+    total_addr, _ = _addr_len(total, 64)
+    _check(_load().pospop_exchange_reduce_async(int(k), int(own), int(n_ranks), int(step), int(slots), total_addr,
+                                                _stream_ptr(stream)))
+
+
+def exchange_status(own: int) -> tuple[int, int]:
+    """(steps consumed, error code) of an exchange buffer; raises CudaError on a device-reported timeout."""
+    consumed, err = C.c_uint64(0), C.c_uint64(0)
+    st = _load().pospop_exchange_status(int(own), C.byref(consumed), C.byref(err))
+    if st != _OK and err.value == 0:
+        _check(st)
+    if err.value:
+        raise CudaError(f"exchange error {int(err.value)}: {_load().pospop_last_error().decode()}")
+    return int(consumed.value), int(err.value)
 
 
 def ipc_alloc(nbytes: int) -> tuple[int, bytes]:

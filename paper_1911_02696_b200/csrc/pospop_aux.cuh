@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "pospop_device.cuh"
+#include "pospop_stream.cuh"
 
 namespace pospop_b200 {
 namespace dev {
@@ -171,6 +172,40 @@ __global__ void digest_kernel(const uint8_t* data, unsigned long long nbytes, un
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(d, s);
+}
+
+// The reduce kernel: one CTA, launched right after the count on the same
+// stream (programmatic dependent launch: it starts once every CTA of the
+// count is running, so its spin never keeps a count CTA off an SM).
+__global__ void __launch_bounds__(64) exchange_reduce_kernel(unsigned long long* own, int n, int k, int S,
+                                                             unsigned long long step, unsigned long long* out) {
+    pdl_allow_next();
+    xchg_reduce(own, n, k, S, step, out, [] { pdl_wait_prev(); });
+}
+
+// Test harness for the protocol with fewer GPUs than ranks (B200_PROFILING:
+// ranks that wait on one another must not be separate launches on one GPU):
+// one cooperative launch, block r plays rank r for `steps` consecutive steps
+// -- optional device sleep, credit wait, row stores + tags into every block's
+// buffer, reduce of its own buffer -- with the same device functions as the
+// counting and reduce kernels.  inputs: steps x n x k; totals: n x steps x k.
+__global__ void __launch_bounds__(64) exchange_emulate_kernel(unsigned long long* const* bufs, int n, int k, int S,
+                                                              int steps, const unsigned long long* inputs,
+                                                              const unsigned* sleep_ns, unsigned long long* totals) {
+    __shared__ unsigned long long vals[64];
+    const int r = blockIdx.x;
+    for (int step = 0; step < steps; ++step) {
+        if (threadIdx.x == 0 && sleep_ns[step * n + r]) {
+            const unsigned long long t0 = globaltimer();
+            while (globaltimer() - t0 < sleep_ns[step * n + r]) __nanosleep(1000);
+        }
+        for (int p = threadIdx.x; p < k; p += blockDim.x) vals[p] = inputs[((size_t)step * n + r) * k + p];
+        __syncthreads();
+        xchg_wait_credit(bufs, n, r, S, (unsigned long long)step);
+        __syncthreads();
+        xchg_store_rows(bufs, n, r, k, S, (unsigned long long)step, vals, blockDim.x);
+        xchg_reduce(bufs[r], n, k, S, (unsigned long long)step, totals + ((size_t)r * steps + step) * k, [] {});
+    }
 }
 
 }  // namespace dev

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/pospopcnt_b200.h"
+#include "pospop_exchange.h"
 #include "pospop_launch.h"
 
 using namespace pospop_b200;
@@ -1206,11 +1207,19 @@ pospop_status pospop_ipc_free(void* d_ptr) {
     return POSPOP_OK;
 }
 
+size_t pospop_exchange_bytes(int k, int n_ranks, int slots) {
+    if (!valid_k(k) || n_ranks < 1 || n_ranks > kXMaxRanks || slots < 1) return 0;
+    return xbuffer_words(n_ranks, k, slots) * sizeof(uint64_t);
+}
+
 pospop_status pospopcnt_allgather_async(int k, const void* d_data, size_t len, uint64_t* d_counts,
-                                        uint64_t* const* d_slots, int n_ranks, int rank, void* stream) {
+                                        uint64_t* const* d_peers, int n_ranks, int rank, uint64_t step, int slots,
+                                        void* stream) {
     if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
-    if (!d_counts || !d_slots || (!d_data && len)) return fail(POSPOP_EINVAL, "NULL pointer");
-    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return fail(POSPOP_EINVAL, "rank %d of %d", rank, n_ranks);
+    if (!d_counts || !d_peers || (!d_data && len)) return fail(POSPOP_EINVAL, "NULL pointer");
+    if (n_ranks < 1 || n_ranks > kXMaxRanks || rank < 0 || rank >= n_ranks)
+        return fail(POSPOP_EINVAL, "rank %d of %d (at most %d ranks)", rank, n_ranks, kXMaxRanks);
+    if (slots < 1) return fail(POSPOP_EINVAL, "slots must be >= 1, got %d", slots);
     if ((uintptr_t)d_data % ((size_t)k / 8)) return fail(POSPOP_EINVAL, "data is misaligned");
     int dev = 0;
     pospop_status s = current_device(&dev);
@@ -1220,11 +1229,83 @@ pospop_status pospopcnt_allgather_async(int k, const void* d_data, size_t len, u
     LaunchOptions opt;
     if ((s = stream_workspace(dev, st, &ws, d_data, len * ((size_t)k / 8), d_counts, (size_t)k * 8, &opt.no_pdl)))
         return s;
-    opt.peers = reinterpret_cast<unsigned long long* const*>(d_slots);
+    opt.peers = reinterpret_cast<unsigned long long* const*>(d_peers);
     opt.n_peers = n_ranks;
     opt.rank = rank;
+    opt.xstep = step;
+    opt.xslots = slots;
     CU(launch_stream(k, len ? d_data : (const void*)d_counts, len, reinterpret_cast<unsigned long long*>(d_counts),
                      false, opt, ws, st));
+    return POSPOP_OK;
+}
+
+pospop_status pospop_exchange_reduce_async(int k, uint64_t* d_own, int n_ranks, uint64_t step, int slots,
+                                           uint64_t* d_total, void* stream) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (!d_own || !d_total) return fail(POSPOP_EINVAL, "NULL pointer");
+    if (n_ranks < 1 || n_ranks > kXMaxRanks) return fail(POSPOP_EINVAL, "n_ranks %d (at most %d)", n_ranks, kXMaxRanks);
+    if (slots < 1) return fail(POSPOP_EINVAL, "slots must be >= 1, got %d", slots);
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamWorkspace ws;
+    bool no_pdl = false;  // records d_total as a recent output of this stream (PDL hazard tracking)
+    if ((s = stream_workspace(dev, st, &ws, nullptr, 0, d_total, (size_t)k * 8, &no_pdl))) return s;
+    CU(launch_exchange_reduce(k, reinterpret_cast<unsigned long long*>(d_own), n_ranks, step, slots,
+                              reinterpret_cast<unsigned long long*>(d_total), st));
+    return POSPOP_OK;
+}
+
+pospop_status pospop_exchange_status(const uint64_t* d_own, uint64_t* consumed, uint64_t* error) {
+    if (!d_own) return fail(POSPOP_EINVAL, "NULL pointer");
+    uint64_t h[2] = {0, 0};
+    CU(cudaMemcpy(h, d_own, sizeof h, cudaMemcpyDeviceToHost));
+    if (consumed) *consumed = h[0];
+    if (error) *error = h[1];
+    if (h[1]) return fail(POSPOP_ECUDA, "exchange: %s timed out (error %llu)",
+                          h[1] == 1 ? "a producer's credit wait" : "the reducer's row wait", (unsigned long long)h[1]);
+    return POSPOP_OK;
+}
+
+pospop_status pospop_exchange_selftest(int k, int n_ranks, int slots, int steps, const uint64_t* inputs,
+                                       const uint32_t* sleep_ns, uint64_t* totals) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (n_ranks < 1 || n_ranks > kXMaxRanks || slots < 1 || steps < 0 || !inputs || !sleep_ns || !totals)
+        return fail(POSPOP_EINVAL, "bad exchange self-test request");
+    int dev = 0;
+    pospop_status s = current_device(&dev);
+    if (s) return s;
+    const size_t words = xbuffer_words(n_ranks, k, slots);
+    const size_t in_n = (size_t)steps * n_ranks * k, sl_n = (size_t)steps * n_ranks;
+    // one allocation: n buffers, the pointer table, inputs, sleeps, totals
+    const size_t bytes = (n_ranks * words + n_ranks + 2 * in_n) * 8 + sl_n * 4 + 64;
+    unsigned long long* base = nullptr;
+    CU(cudaMalloc(&base, bytes));
+    struct Free {
+        void* p;
+        ~Free() { cudaFree(p); }
+    } guard{base};
+    CU(cudaMemset(base, 0, bytes));
+    std::vector<unsigned long long*> table((size_t)n_ranks);
+    for (int r = 0; r < n_ranks; ++r) table[(size_t)r] = base + (size_t)r * words;
+    unsigned long long* d_table = base + (size_t)n_ranks * words;
+    unsigned long long* d_in = d_table + n_ranks;
+    unsigned long long* d_tot = d_in + in_n;
+    unsigned* d_sleep = reinterpret_cast<unsigned*>(d_tot + in_n);
+    CU(cudaMemcpy(d_table, table.data(), (size_t)n_ranks * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_in, inputs, in_n * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_sleep, sleep_ns, sl_n * 4, cudaMemcpyHostToDevice));
+    CU(launch_exchange_emulate(reinterpret_cast<unsigned long long* const*>(d_table), n_ranks, k, slots, steps, d_in, d_sleep, d_tot, nullptr));
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(totals, d_tot, in_n * 8, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < n_ranks; ++r) {
+        uint64_t h[2];
+        CU(cudaMemcpy(h, table[(size_t)r], sizeof h, cudaMemcpyDeviceToHost));
+        if (h[1] || h[0] != (uint64_t)steps)
+            return fail(POSPOP_ECUDA, "exchange self-test: rank %d consumed %llu of %d steps, error %llu", r,
+                        (unsigned long long)h[0], steps, (unsigned long long)h[1]);
+    }
     return POSPOP_OK;
 }
 

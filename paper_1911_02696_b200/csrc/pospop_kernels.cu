@@ -191,6 +191,8 @@ static void fill_stream_args(StreamArgs& a, int k, const void* data, size_t len_
     a.peers = opt.peers;
     a.n_peers = opt.peers ? opt.n_peers : 0;
     a.rank = opt.rank;
+    a.xstep = opt.xstep;
+    a.xslots = opt.xslots > 0 ? opt.xslots : 1;
 }
 
 // Tree blocks between lane flushes: the caller's threshold, lowered by
@@ -517,6 +519,32 @@ cudaError_t launch_segmented(int k, const void* data, const unsigned long long* 
     const cudaError_t e = cudaLaunchKernelEx(&cfg, var->fn, static_cast<const uint8_t*>(data), d_offsets,
                                              (unsigned long long)n, k, opt.flush_threshold, d_out, ws.next,
                                              ws.ticket, extra);
+    ++g_launches;
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_exchange_reduce(int k, unsigned long long* own, int n_ranks, unsigned long long step, int slots,
+                                   unsigned long long* d_total, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(64);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, exchange_reduce_kernel, own, n_ranks, k, slots, step, d_total);
+    ++g_launches;
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_exchange_emulate(unsigned long long* const* bufs, int n_ranks, int k, int slots, int steps,
+                                    const unsigned long long* inputs, const unsigned* sleep_ns,
+                                    unsigned long long* totals, cudaStream_t stream) {
+    void* args[] = {(void*)&bufs, &n_ranks, &k, &slots, &steps, (void*)&inputs, (void*)&sleep_ns, &totals};
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(exchange_emulate_kernel),
+                                                      dim3((unsigned)n_ranks), dim3(64), args, 0, stream);
     ++g_launches;
     return e != cudaSuccess ? e : cudaGetLastError();
 }

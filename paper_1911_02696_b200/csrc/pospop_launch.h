@@ -40,9 +40,11 @@ struct LaunchOptions {
     int depth = 0;                     // 0 = default tree depth (k=64: per bank)
     unsigned long long* trace = nullptr;  // diagnostics: 5 u64 per CTA (see pospopcnt_trace_async)
     unsigned long long word_base = 0;     // FLAG mode: global index of the first word
-    unsigned long long* const* peers = nullptr;  // fused exchange: device array of n_peers gather slots
+    unsigned long long* const* peers = nullptr;  // fused exchange: device array of n_peers exchange buffers
     int n_peers = 0;
     int rank = 0;
+    unsigned long long xstep = 0;  // fused exchange: step (slot xstep % xslots, tag xstep + 1)
+    int xslots = 2;
     // Launch without programmatic dependent launch: the input may have been
     // written by a preceding launch of this library on the same stream (which
     // lets its dependents start before it finishes; our kernels read their
@@ -69,6 +71,20 @@ cudaError_t launch_flagstats(const uint16_t* flags, size_t len, unsigned long lo
 cudaError_t launch_segmented(int k, const void* data, const unsigned long long* d_offsets,
                              size_t n_arrays, unsigned long long* d_out, const LaunchOptions& opt,
                              const StreamWorkspace& ws, cudaStream_t stream);
+
+// Consumer half of the fused exchange (pospop_exchange.h): waits for the
+// n_ranks rows of `step` in this rank's buffer `own`, sums them into
+// d_total[0..k), then releases the slot.  One single-CTA launch.
+cudaError_t launch_exchange_reduce(int k, unsigned long long* own, int n_ranks, unsigned long long step, int slots,
+                                   unsigned long long* d_total, cudaStream_t stream);
+
+// Protocol self-test: n_ranks co-resident blocks of one cooperative launch
+// play the ranks (exchange_emulate_kernel).  bufs: device array of n_ranks
+// zeroed exchange buffers; inputs steps x n x k, sleep_ns steps x n, totals
+// n x steps x k (all device memory).
+cudaError_t launch_exchange_emulate(unsigned long long* const* bufs, int n_ranks, int k, int slots, int steps,
+                                    const unsigned long long* inputs, const unsigned* sleep_ns,
+                                    unsigned long long* totals, cudaStream_t stream);
 
 // Synthetic inputs (see oracle/pospop_oracle.h orc_generate for the kinds).
 cudaError_t launch_generate(int kind, uint64_t seed, uint64_t index_base, size_t n, void* out,

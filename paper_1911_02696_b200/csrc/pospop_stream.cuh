@@ -10,6 +10,7 @@
 #include <cstdint>
 
 #include "pospop_device.cuh"
+#include "pospop_exchange.h"
 
 namespace pospop_b200 {
 namespace dev {
@@ -41,11 +42,14 @@ struct StreamArgs {
     unsigned long long data_off;  // data start - base, bytes
     unsigned long long word_base; // global index of the first word (host-staged chunks)
     unsigned long long* bad;      // max of ~(index of an invalid FLAG word); 0 = none
-    // Fused exchange (MODE 0): the last CTA also stores out[k] into every
-    // rank's gather slot, peers[j][rank * k + p] (peer memory mapped through
-    // CUDA IPC / peer access; plain stores over NVLink), j < n_peers.
+    // Fused exchange (MODE 0): the last CTA also stores out[k] as row `rank`
+    // of slot xstep % xslots in every rank's exchange buffer peers[j] (peer
+    // memory mapped through CUDA IPC; plain stores over NVLink), j < n_peers,
+    // then release-stores the row's step tag (pospop_exchange.h).
     unsigned long long* const* peers;
     int n_peers, rank;
+    unsigned long long xstep;
+    int xslots;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -67,6 +71,89 @@ __device__ __forceinline__ unsigned smid() {
 // programmatic-serialization attribute.
 __device__ __forceinline__ void pdl_allow_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait_prev() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// System-scope accesses for the cross-GPU exchange (peer memory over NVLink).
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Producer half of the exchange, in two parts, run by the counting kernel's
+// last CTA once out[k] is final.  (1) Credit: before rewriting slot step % S
+// in peer j's buffer, thread j waits (bounded) until j's reducer has consumed
+// the slot's previous step, step - S.  (2) The CTA stores its k counts `vals`
+// (shared memory) as row `rank` in every peer's slot, fences, and each thread
+// j < n release-stores the row's tag step + 1 in peer j.  A timeout sets
+// error 1 in the rank's own buffer and publishes anyway (the host reports it).
+__device__ __forceinline__ void xchg_wait_credit(unsigned long long* const* peers, int n, int rank, int S,
+                                                 unsigned long long step) {
+    if ((int)threadIdx.x < n && step >= (unsigned long long)S) {
+        const unsigned long long need = step - S + 1;
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_sys(peers[threadIdx.x]) < need) {
+            if (globaltimer() - t0 > kXTimeoutNs) {
+                peers[rank][1] = 1ull;
+                break;
+            }
+            __nanosleep(256);
+        }
+    }
+}
+
+__device__ __forceinline__ void xchg_store_rows(unsigned long long* const* peers, int n, int rank, int k, int S,
+                                                unsigned long long step, const unsigned long long* vals,
+                                                unsigned nthreads) {
+    const size_t so = xslot_off((unsigned)(step % (unsigned long long)S), n, k);
+    for (int i = threadIdx.x; i < n * k; i += nthreads) {
+        const int j = i / k, pos = i - j * k;
+        peers[j][so + n + (size_t)rank * k + pos] = vals[pos];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if ((int)threadIdx.x < n) st_release_sys(peers[threadIdx.x] + so + rank, step + 1);
+}
+
+// Consumer half: waits (bounded) for the n tags of `step` in this rank's own
+// buffer, sums the n rows into out[k] (merge_counts, pospop.cpp:33-37), then
+// release-stores "consumed = step + 1" so the producers may reuse the slot.
+// `before_out` runs between the wait and the stores to out (the reduce kernel
+// waits there for the stream's previous kernel).
+template <class BeforeOut>
+__device__ __forceinline__ void xchg_reduce(unsigned long long* own, int n, int k, int S, unsigned long long step,
+                                            unsigned long long* out, BeforeOut before_out) {
+    const size_t so = xslot_off((unsigned)(step % (unsigned long long)S), n, k);
+    if ((int)threadIdx.x < n) {
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_sys(own + so + threadIdx.x) != step + 1) {
+            if (globaltimer() - t0 > kXTimeoutNs) {
+                own[1] = 2ull;
+                break;
+            }
+            __nanosleep(128);
+        }
+    }
+    __syncthreads();
+    before_out();
+    for (int pos = threadIdx.x; pos < k; pos += blockDim.x) {
+        unsigned long long sum = 0;
+        for (int j = 0; j < n; ++j) sum += ld_relaxed_sys(own + so + n + (size_t)j * k + pos);
+        out[pos] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        st_release_sys(own, step + 1);
+    }
+}
 
 // Channel -> position fold: the channels (of 32 * NBANK) that count position
 // p are p + m * k for m = 0 .. 32/k - 1 (k <= 32), or channel p (k = 64).
@@ -233,9 +320,13 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
             }
             if (a.accumulate) sum += a.out[pos];
             a.out[pos] = sum;
-            for (int j = 0; j < a.n_peers; ++j) a.peers[j][a.rank * k + pos] = sum;
+            if (a.n_peers) s_acc[pos] = sum;
         }
-        if (a.n_peers) __threadfence_system();
+        if (a.n_peers) {
+            xchg_wait_credit(a.peers, a.n_peers, a.rank, a.xslots, a.xstep);
+            __syncthreads();
+            xchg_store_rows(a.peers, a.n_peers, a.rank, k, a.xslots, a.xstep, s_acc, block);
+        }
     }
     if (threadIdx.x == 0) {
         *a.ticket = 0u;

@@ -1,26 +1,36 @@
-"""Count fused with the cross-GPU exchange over peer memory.
+"""Count fused with a device-side all-reduce over peer memory.
 
 One process per GPU.  The reference's multi-chunk use is chunk-and-merge
 (``merge_counts``, proj/core/src/pospop.cpp:33-37; proj/tests/test_core.cpp:155-175):
-every shard's k-vector is added element-wise.  Instead of a separate
-collective after the count, every rank's counting kernel delivers its
-k-vector itself: its last CTA stores the k counts into row ``rank`` of a gather
-slot that lives in EVERY rank's memory (mapped through CUDA IPC, so the stores
-travel over NVLink from inside the kernel).  Once all ranks' launches of a step
-have completed, each GPU holds all n k-vectors of that step and the
-all-reduced counts are the slot's row sum -- no NCCL kernel, no extra launch,
-no kernel waiting on another rank.
+every shard's k-vector is added element-wise, and the sum is final only once
+every partial is in.  Instead of a separate collective after the count:
 
-    pg = PeerGather(k=16)                       # after torch.distributed init
-    pg.count(shard, out, step)                  # one kernel: count + deliver
-    ...                                         # (all ranks' launches complete)
-    total = pg.result(step)                     # int64[k] on this GPU
+* the producer is the counting kernel itself: its last CTA stores the rank's
+  k counts as row ``rank`` of slot ``step % slots`` in EVERY rank's exchange
+  buffer (mapped through CUDA IPC, so the stores travel over NVLink from
+  inside the kernel) and release-stores the row's step tag;
+* the consumer is a one-CTA reduce kernel on the same stream: it waits on the
+  device until all n tags of the step have arrived, writes the row sum (the
+  all-reduced counts) and returns the slot's credit;
+* before rewriting a slot, a producer waits until every peer has consumed
+  the slot's previous step, so a rank running ``slots`` steps ahead cannot
+  overwrite rows a slower peer is still reading.
+
+Both waits are bounded (20 s) and report a timeout through the buffer's error
+word (``status()``).  Steps are consecutive integers from 0.
+
+    pg, why = PeerGather.create(k=16)           # after torch.distributed init
+    pg.allreduce(shard, local, total, step)     # count kernel + reduce kernel
+    ...                                         # `total` is final on the device
 """
 from __future__ import annotations
 
 from typing import Any
 
-from . import count_allgather_async, ipc_alloc, ipc_close, ipc_free, ipc_open
+from . import (count_allgather_async, exchange_bytes, exchange_reduce_async, exchange_status, ipc_alloc, ipc_close,
+               ipc_free, ipc_open)
+
+HEADER_WORDS = 8  # pospop_exchange.h kXHeader
 
 
 class _DeviceView:
@@ -32,26 +42,13 @@ class _DeviceView:
 
 
 class PeerGather:
-    """Gather slots in every rank's memory plus the per-slot device tables of
-    peer pointers.  ``slots`` >= 2 lets step i+1 run while step i is read."""
+    """This rank's exchange buffer, the mapped peer buffers and the device
+    table of their pointers.  Build with :meth:`create` (collective-safe)."""
 
-    def __init__(self, k: int, slots: int = 2, group: Any = None):
-        import torch
-        import torch.distributed as dist
-
-        self.k, self.slots = int(k), int(slots)
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        row_bytes = self.k * 8
-        self._slot_bytes = self.world * row_bytes
-        self.ptr, handle = ipc_alloc(self.slots * self._slot_bytes)
-        handles: list = [None] * self.world
-        dist.all_gather_object(handles, handle, group=group)
-        self.peer_ptrs = [self.ptr if j == self.rank else ipc_open(handles[j]) for j in range(self.world)]
-        dev = torch.cuda.current_device()
-        self.tables = [torch.tensor([p + s * self._slot_bytes for p in self.peer_ptrs], dtype=torch.int64,
-                                    device=f"cuda:{dev}") for s in range(self.slots)]
-        self.buffer = torch.as_tensor(_DeviceView(self.ptr, (self.slots, self.world, self.k)), device=f"cuda:{dev}")
+    k: int
+    slots: int
+    world: int
+    rank: int
 
     @classmethod
     def create(cls, k: int, slots: int = 2, group: Any = None) -> "tuple[PeerGather | None, str]":
@@ -64,13 +61,17 @@ class PeerGather:
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         self = cls.__new__(cls)
         self.k, self.slots, self.world, self.rank = int(k), int(slots), world, rank
-        self._slot_bytes = world * self.k * 8
+        self._next_step = 0
         dev = torch.cuda.current_device()
         reason = ""
+        self.ptr, handle = 0, None
         try:
-            self.ptr, handle = ipc_alloc(self.slots * self._slot_bytes)
+            nbytes = exchange_bytes(self.k, world, self.slots)
+            if nbytes == 0:
+                raise ValueError(f"no exchange layout for k={k}, {world} ranks, {slots} slots")
+            self.ptr, handle = ipc_alloc(nbytes)
         except Exception as e:  # noqa: BLE001
-            self.ptr, handle, reason = 0, None, f"ipc_alloc: {e}"
+            reason = f"ipc_alloc: {e}"
         handles: list = [None] * world
         dist.all_gather_object(handles, handle, group=group)  # every rank, always
         opened: list[int] = []
@@ -89,25 +90,50 @@ class PeerGather:
                     ipc_close(p)
             if self.ptr:
                 ipc_free(self.ptr)
-            return None, reason or "a peer could not map the gather buffers"
+            return None, reason or "a peer could not map the exchange buffers"
         self.peer_ptrs = opened
-        self.tables = [torch.tensor([p + s * self._slot_bytes for p in opened], dtype=torch.int64,
-                                    device=f"cuda:{dev}") for s in range(self.slots)]
-        self.buffer = torch.as_tensor(_DeviceView(self.ptr, (self.slots, world, self.k)), device=f"cuda:{dev}")
+        self.table = torch.tensor(opened, dtype=torch.int64, device=f"cuda:{dev}")
+        words = nbytes // 8
+        self.buffer = torch.as_tensor(_DeviceView(self.ptr, (words,)), device=f"cuda:{dev}")
         return self, ""
 
+    def _slot(self, step: int) -> int:
+        return HEADER_WORDS + (step % self.slots) * (self.world + self.world * self.k)
+
     def count(self, data: Any, out: Any, step: int, *, stream: Any = None, len_words: int | None = None) -> None:
-        """One kernel: this rank's counts into `out` and into row `rank` of slot step % slots on every GPU."""
-        count_allgather_async(data, out, self.k, self.tables[step % self.slots], self.world, self.rank,
+        """Producer: one kernel counts into `out` and publishes the row of `step` to every GPU."""
+        if step != self._next_step:
+            raise ValueError(f"exchange steps must be consecutive: expected {self._next_step}, got {step}")
+        count_allgather_async(data, out, self.k, self.table, self.world, self.rank, step, self.slots,
                               stream=stream, len_words=len_words)
+        self._next_step = step + 1
+
+    def reduce(self, step: int, total: Any, *, stream: Any = None) -> None:
+        """Consumer: waits on the device for every rank's row of `step`, total = their sum."""
+        exchange_reduce_async(self.k, self.ptr, self.world, step, total, self.slots, stream=stream)
+
+    def allreduce(self, data: Any, local: Any, total: Any, step: int, *, stream: Any = None,
+                  len_words: int | None = None) -> None:
+        """count + reduce: `local` = this rank's counts, `total` = merge_counts over the ranks."""
+        self.count(data, local, step, stream=stream, len_words=len_words)
+        self.reduce(step, total, stream=stream)
+
+    def tags(self, step: int):
+        o = self._slot(step)
+        return self.buffer[o:o + self.world]
 
     def rows(self, step: int):
-        """The n_ranks k-vectors of a step (valid once every rank's launch completed)."""
-        return self.buffer[step % self.slots]
+        """The n_ranks k-vectors in the slot of `step` (valid once its reduce has run)."""
+        o = self._slot(step) + self.world
+        return self.buffer[o:o + self.world * self.k].view(self.world, self.k)
 
     def result(self, step: int):
-        """merge_counts over the ranks: int64[k] on this GPU."""
+        """merge_counts over the slot's rows: int64[k] on this GPU."""
         return self.rows(step).sum(dim=0)
+
+    def status(self) -> tuple[int, int]:
+        """(steps consumed, error code); raises CudaError if a bounded wait timed out."""
+        return exchange_status(self.ptr)
 
     def close(self) -> None:
         for j, p in enumerate(self.peer_ptrs):
