@@ -179,17 +179,49 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
 
 /* ---- multi-device, one process (the cfg4 shard/reduce driver) ----------- */
 
-/* shards[i] (lens[i] words, device memory on devices[i]) are counted
- * concurrently on their devices, then the k-vectors are summed
- * (merge_counts, pospop.cpp:33-37).  A device may appear more than once.
- * Use torch.distributed / NCCL for the one-process-per-GPU layout
- * (paper_1911_02696_b200.shard). */
+/* shards[i] (lens[i] words) are counted concurrently on devices[i], then the
+ * k-vectors are summed (merge_counts, pospop.cpp:33-37; the fork-join of
+ * proj/tests/test_core.cpp:155-175).  A shard is either device memory that
+ * lives on devices[i] (counted in place) or host memory, pinned or pageable
+ * (streamed to devices[i] by a worker thread bound to that device's local
+ * CPUs, through its own staging ring: N devices use N host links at once).
+ * A device may appear more than once.  Use torch.distributed / NCCL for the
+ * one-process-per-GPU layout (paper_1911_02696_b200.shard). */
 pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* lens,
                                 const int* devices, int n_shards, uint64_t* counts);
+
+/* Host-memory fork-join in one call: the len words at `data` are split into
+ * n_devices contiguous ranges (sizes differ by at most one word), range i is
+ * counted on devices[i] as a host shard of pospopcnt_sharded, and the counts
+ * are summed.  Device-resident `data` is accepted when every listed device
+ * is the one it lives on. */
+pospop_status pospopcnt_split(int k, const void* data, size_t len, const int* devices, int n_devices,
+                              uint64_t* counts);
 
 /* The 16-bit form (BASELINE cfg4): pospopcnt_sharded with k = 16. */
 pospop_status pospopcnt_u16_sharded(const uint16_t* const* shards, const size_t* lens, const int* devices,
                                     int n_devices, uint64_t counts[16]);
+
+/* ---- resources ----------------------------------------------------------- */
+
+/* The library keeps no per-thread state.  A synchronous call leases a
+ * per-device context (streams, result buffers, a 832-byte workspace and,
+ * for host input, a 3 x 64 MiB device staging ring and 4 x 16 MiB pinned
+ * host ring) from a pool of at most 8 per device and returns it when the
+ * call returns; the asynchronous entry points keep one workspace per
+ * (device, stream).  pospop_release_resources() frees every idle context
+ * and every per-stream workspace (it synchronises the devices that own
+ * per-stream workspaces; contexts leased by calls in flight are kept).  The
+ * library stays usable: later calls allocate again. */
+pospop_status pospop_release_resources(void);
+
+/* Synchronises `stream` and frees the library's workspaces for it (call
+ * before destroying a stream used with the asynchronous entry points). */
+pospop_status pospop_release_stream(void* stream);
+
+/* Diagnostics: contexts alive (leased + idle) and idle on `device`, and
+ * per-stream workspaces held for it.  Any pointer may be NULL. */
+pospop_status pospop_resource_stats(int device, int* contexts, int* idle_contexts, int* stream_workspaces);
 
 /* ---- asynchronous device-resident entry points (timing / integration) --- */
 

@@ -40,7 +40,8 @@ import numpy as np
 __all__ = [
     "KernelKind", "PospopcntConfig", "PositionalCounts", "InvalidArgument", "KernelUnavailableError",
     "CudaError", "validate", "merge_counts", "pospopcnt", "pospopcnt_k", "pospopcnt_u16_c32",
-    "pospopcnt_segmented", "pospopcnt_sharded", "count_async", "segmented_async", "count_allgather_async",
+    "pospopcnt_segmented", "pospopcnt_sharded", "pospopcnt_split", "release_resources", "release_stream",
+    "resource_stats", "count_async", "segmented_async", "count_allgather_async",
     "exchange_bytes", "exchange_reduce_async", "exchange_status",
     "ipc_alloc", "ipc_open", "ipc_close", "ipc_free", "generate", "digest",
     "supported_csa_widths", "native_csa_width", "device_available", "kernel_launches", "library_path",
@@ -150,6 +151,10 @@ def _load():
         "pospopcnt_allgather_async": ([C.c_int, vp, sz, vp, vp, C.c_int, C.c_int, C.c_uint64, C.c_int, vp], C.c_int),
         "pospop_exchange_reduce_async": ([C.c_int, vp, C.c_int, C.c_uint64, C.c_int, vp, vp], C.c_int),
         "pospop_exchange_status": ([vp, _u64p, _u64p], C.c_int),
+        "pospopcnt_split": ([C.c_int, vp, sz, C.POINTER(C.c_int), C.c_int, _u64p], C.c_int),
+        "pospop_release_resources": ([], C.c_int),
+        "pospop_release_stream": ([vp], C.c_int),
+        "pospop_resource_stats": ([C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -399,6 +404,34 @@ def pospopcnt_sharded(shards: Sequence[Any], devices: Sequence[int], k: int = 16
     out = np.zeros(k, np.uint64)
     _check(_load().pospopcnt_sharded(int(k), ptrs, lens, devs, n, out.ctypes.data_as(_u64p)))
     return PositionalCounts(out)
+
+
+def pospopcnt_split(data: Any, devices: Sequence[int], k: int = 16) -> PositionalCounts:
+    """Host-memory fork-join in one call (proj/tests/test_core.cpp:155-175): the
+    words are split into len(devices) contiguous ranges, range i is streamed to
+    devices[i] over that device's own host link, and the counts are merged."""
+    addr, n = _addr_len(data, k)
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    out = np.zeros(k, np.uint64)
+    _check(_load().pospopcnt_split(int(k), addr or None, n, devs, len(devices), out.ctypes.data_as(_u64p)))
+    return PositionalCounts(out)
+
+
+def release_resources() -> None:
+    """Frees the library's idle per-device contexts and per-stream workspaces."""
+    _check(_load().pospop_release_resources())
+
+
+def release_stream(stream: Any) -> None:
+    """Synchronises `stream` and frees the library's workspaces for it."""
+    _check(_load().pospop_release_stream(_stream_ptr(stream)))
+
+
+def resource_stats(device: int = 0) -> dict:
+    """{contexts, idle_contexts, stream_workspaces} the library holds for `device`."""
+    a, b, c = C.c_int(), C.c_int(), C.c_int()
+    _check(_load().pospop_resource_stats(int(device), C.byref(a), C.byref(b), C.byref(c)))
+    return {"contexts": a.value, "idle_contexts": b.value, "stream_workspaces": c.value}
 
 
 def count_async(data: Any, out: Any, k: int, *, accumulate: bool = False, flush_threshold_blocks: int = 65535,

@@ -13,7 +13,10 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cerrno>
+#include <pthread.h>
+#include <sched.h>
 #include <condition_variable>
 #include <deque>
 #include <cstdarg>
@@ -24,6 +27,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -95,6 +99,76 @@ pospop_status current_device(int* dev) {
     return check_device(*dev);
 }
 
+pospop_status cuda_set_device(int dev) {
+    CU(cudaSetDevice(dev));
+    return POSPOP_OK;
+}
+
+// Parses a sysfs CPU list ("0-15,32-47") into `set`; false if empty.
+bool parse_cpulist(const char* text, cpu_set_t* set) {
+    CPU_ZERO(set);
+    bool any = false;
+    const char* p = text;
+    while (*p) {
+        char* end = nullptr;
+        const long lo = std::strtol(p, &end, 10);
+        if (end == p) break;
+        long hi = lo;
+        p = end;
+        if (*p == '-') {
+            hi = std::strtol(p + 1, &end, 10);
+            p = end;
+        }
+        for (long c = lo; c <= hi && c < CPU_SETSIZE; ++c) {
+            CPU_SET((int)c, set);
+            any = true;
+        }
+        if (*p == ',') ++p;
+        else break;
+    }
+    return any;
+}
+
+// The CPUs local to device `dev` (sysfs local_cpulist of its PCI function).
+bool device_cpus(int dev, cpu_set_t* set) {
+    char bus[32] = {};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    for (char* q = bus; *q; ++q) *q = (char)std::tolower((unsigned char)*q);
+    const std::string path = std::string("/sys/bus/pci/devices/") + bus + "/local_cpulist";
+    FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) return false;
+    char buf[1024] = {};
+    const bool ok = std::fgets(buf, sizeof buf, f) != nullptr;
+    std::fclose(f);
+    return ok && parse_cpulist(buf, set);
+}
+
+// Binds the calling thread to the CPUs local to device `dev` (host-shard
+// workers: their memcpy / DMA source stays on the device's NUMA node).
+bool bind_to_device_cpus(int dev) {
+    cpu_set_t set;
+    return device_cpus(dev, &set) && pthread_setaffinity_np(pthread_self(), sizeof set, &set) == 0;
+}
+
+// Runs the calling thread on device `dev`'s local CPUs for the lifetime of
+// the scope (pinned host buffers allocated inside are first touched there,
+// so they land on the device's NUMA node), then restores its affinity.
+struct NumaScope {
+    cpu_set_t saved;
+    bool restore = false;
+    explicit NumaScope(int dev) {
+        cpu_set_t set;
+        if (pthread_getaffinity_np(pthread_self(), sizeof saved, &saved) == 0 && device_cpus(dev, &set))
+            restore = pthread_setaffinity_np(pthread_self(), sizeof set, &set) == 0;
+    }
+    ~NumaScope() {
+        if (restore) pthread_setaffinity_np(pthread_self(), sizeof saved, &saved);
+    }
+};
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
@@ -109,13 +183,21 @@ struct DeviceGuard {
 };
 
 // ---------------------------------------------------------------------------
-// Per-thread, per-device context: compute + copy streams, result buffers,
-// the stream workspace, and (lazily) the host-staging ring.
+// Per-call device context: compute + copy streams, result buffers, the
+// stream workspace, and (lazily) the host-staging ring.  Contexts are leased
+// from a per-device pool for the duration of one call (CtxScope), so
+// resources are bounded per device -- at most kMaxCtxPerDevice contexts --
+// whatever the number of calling threads, and nothing is tied to a thread.
+// pospop_release_resources() frees the idle ones.  (The reference keeps all
+// per-call state on the stack, proj/core/src/detail/csa_engine.hpp:107-110;
+// device allocation per call would synchronise the device, so the pool is the
+// closest B200 equivalent.)
 // ---------------------------------------------------------------------------
 constexpr int kRing = 3;
 constexpr size_t kBounceBytes = 1 << 20;  // host inputs up to this size take the single-stream path
 constexpr int kHostRing = 4;              // pinned host slots for pageable / file input
 constexpr size_t kHostChunk = 16 << 20;   // bytes per pinned host slot
+constexpr int kMaxCtxPerDevice = 8;       // concurrent calls per device beyond this wait for a context
 
 // Persistent host worker threads for the CPU side of host-input pipelines
 // (parallel memcpy from pageable memory, parallel pread from files) into the
@@ -217,7 +299,8 @@ struct Ctx {
     // into mapped pinned memory: no D2H copy on the small-call latency path.
     unsigned long long* m_out = nullptr;      // 64 u64, pinned + mapped (host view)
     unsigned long long* m_out_dev = nullptr;  // its device view
-    StreamWorkspace ws;
+    StreamWorkspace ws;      // stream / FLAG launches (kStreamWorkspaceBytes)
+    StreamWorkspace seg_ws;  // segmented launches (kWorkspaceBytes, on first segmented use)
     void* stage[kRing] = {nullptr, nullptr, nullptr};
     void* bounce = nullptr;  // pinned host buffer for small host inputs (kBounceBytes)
     size_t stage_bytes = 0;
@@ -248,28 +331,69 @@ struct Ctx {
     bool host_used[kHostRing] = {};
 };
 
-thread_local std::map<int, Ctx*> t_ctx;
-
-pospop_status alloc_workspace(StreamWorkspace* ws) {
-    CU(cudaMalloc(&ws->acc, kWorkspaceBytes));
+pospop_status alloc_workspace(StreamWorkspace* ws, bool segmented = false) {
+    const size_t bytes = segmented ? kWorkspaceBytes : kStreamWorkspaceBytes;
+    CU(cudaMalloc(&ws->acc, bytes));
     ws->ticket = reinterpret_cast<unsigned int*>(ws->acc + kAccChannels);
     ws->next = ws->acc + kAccChannels + 1;
     ws->bad = ws->acc + kAccChannels + 2;
-    CU(cudaMemset(ws->acc, 0, kWorkspaceBytes));
+    CU(cudaMemset(ws->acc, 0, bytes));
     return POSPOP_OK;
 }
 
-pospop_status get_ctx(int dev, Ctx** out) {
-    auto it = t_ctx.find(dev);
-    if (it != t_ctx.end()) {
-        *out = it->second;
-        return POSPOP_OK;
+void free_workspace(StreamWorkspace* ws) {
+    if (ws->acc) cudaFree(ws->acc);
+    *ws = StreamWorkspace{};
+}
+
+// Frees everything a context owns (its device must be current).  Pending work
+// on its streams is waited for first (a call that failed part-way may have
+// left some).
+void destroy_ctx(Ctx* c) {
+    for (cudaStream_t st : {c->stream, c->copy, c->d2h})
+        if (st) cudaStreamSynchronize(st);
+    for (auto& slot : c->shard_slots) {
+        if (slot.stream) {
+            cudaStreamSynchronize(slot.stream);
+            cudaStreamDestroy(slot.stream);
+        }
+        free_workspace(&slot.ws);
+        if (slot.m_out) cudaFreeHost(slot.m_out);
     }
-    pospop_status s = check_device(dev);
-    if (s) return s;
-    DeviceGuard g(dev);
+    free_workspace(&c->ws);
+    free_workspace(&c->seg_ws);
+    for (int i = 0; i < kRing; ++i) {
+        if (c->stage[i]) cudaFree(c->stage[i]);
+        if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+    }
+    for (int i = 0; i < kHostRing; ++i) {
+        if (c->host_ring[i]) cudaFreeHost(c->host_ring[i]);
+        if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+    }
+    for (void* p : c->scratch)
+        if (p) cudaFree(p);
+    for (cudaEvent_t e : c->seg_ev) cudaEventDestroy(e);
+    if (c->rows_pinned) cudaFreeHost(c->rows_pinned);
+    if (c->bounce) cudaFreeHost(c->bounce);
+    if (c->d_out) cudaFree(c->d_out);
+    if (c->h_out) cudaFreeHost(c->h_out);
+    if (c->m_out) cudaFreeHost(c->m_out);
+    for (cudaStream_t st : {c->stream, c->copy, c->d2h})
+        if (st) cudaStreamDestroy(st);
+    cudaGetLastError();
+    delete c;
+}
+
+pospop_status create_ctx(int dev, Ctx** out) {
     Ctx* c = new Ctx;
     c->dev = dev;
+    struct Undo {  // frees the partial context if a step below fails
+        Ctx*& c;
+        ~Undo() {
+            if (c) destroy_ctx(c);
+        }
+    } undo{c};
     // Blocking streams: synchronous entry points are ordered after prior work
     // on the legacy default stream (where callers typically produced the data).
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault));
@@ -278,10 +402,84 @@ pospop_status get_ctx(int dev, Ctx** out) {
     CU(cudaMallocHost(&c->h_out, 64 * sizeof(unsigned long long)));
     CU(cudaHostAlloc(&c->m_out, 64 * sizeof(unsigned long long), cudaHostAllocMapped));
     CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->m_out_dev), c->m_out, 0));
-    if ((s = alloc_workspace(&c->ws))) return s;
-    t_ctx[dev] = c;
+    pospop_status s = alloc_workspace(&c->ws);
+    if (s) return s;
     *out = c;
+    c = nullptr;  // keep it
     return POSPOP_OK;
+}
+
+struct CtxPool {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::map<int, std::vector<Ctx*>> idle;
+    std::map<int, int> live;  // leased + idle, per device
+    static CtxPool& get() {
+        static CtxPool* pool = new CtxPool;  // never destroyed: no CUDA calls during process exit
+        return *pool;
+    }
+};
+
+// The contexts one call holds, returned to the pool when the call returns.
+// A call that needs several devices acquires them in ascending device order
+// (pospopcnt_sharded), so bounded pools cannot deadlock.
+class CtxScope {
+  public:
+    CtxScope() = default;
+    CtxScope(const CtxScope&) = delete;
+    CtxScope& operator=(const CtxScope&) = delete;
+    ~CtxScope() {
+        if (held_.empty()) return;
+        CtxPool& pool = CtxPool::get();
+        {
+            std::lock_guard<std::mutex> lk(pool.mu);
+            for (auto& h : held_) pool.idle[h.first].push_back(h.second);
+        }
+        pool.cv.notify_all();
+    }
+    pospop_status get(int dev, Ctx** out) {
+        for (auto& h : held_)
+            if (h.first == dev) {
+                *out = h.second;
+                return POSPOP_OK;
+            }
+        pospop_status s = check_device(dev);
+        if (s) return s;
+        CtxPool& pool = CtxPool::get();
+        Ctx* c = nullptr;
+        {
+            std::unique_lock<std::mutex> lk(pool.mu);
+            pool.cv.wait(lk, [&] { return !pool.idle[dev].empty() || pool.live[dev] < kMaxCtxPerDevice; });
+            if (!pool.idle[dev].empty()) {
+                c = pool.idle[dev].back();
+                pool.idle[dev].pop_back();
+            } else {
+                ++pool.live[dev];
+            }
+        }
+        if (!c) {
+            DeviceGuard g(dev);
+            if ((s = create_ctx(dev, &c))) {
+                {
+                    std::lock_guard<std::mutex> lk(pool.mu);
+                    --pool.live[dev];
+                }
+                pool.cv.notify_all();
+                return s;
+            }
+        }
+        held_.emplace_back(dev, c);
+        *out = c;
+        return POSPOP_OK;
+    }
+
+  private:
+    std::vector<std::pair<int, Ctx*>> held_;
+};
+
+pospop_status ensure_seg_ws(Ctx* c) {
+    if (c->seg_ws.acc) return POSPOP_OK;
+    return alloc_workspace(&c->seg_ws, true);
 }
 
 pospop_status ensure_stage(Ctx* c) {
@@ -300,6 +498,7 @@ pospop_status ensure_stage(Ctx* c) {
 
 pospop_status ensure_host_ring(Ctx* c) {
     if (c->host_ring[0]) return POSPOP_OK;
+    NumaScope numa(c->dev);
     for (int i = 0; i < kHostRing; ++i) {
         CU(cudaMallocHost(&c->host_ring[i], kHostChunk));
         CU(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
@@ -400,7 +599,8 @@ pospop_status h2d_on_stream(Ctx* c, void* dst, const void* src, size_t bytes, bo
 // one of them is enqueued without programmatic dependent launch (our kernels
 // let dependents start early and read their own input before waiting).
 struct StreamState {
-    StreamWorkspace ws;
+    StreamWorkspace ws;      // stream / exchange launches
+    StreamWorkspace seg_ws;  // segmented launches (on first use)
     static constexpr int kHist = 8;
     uintptr_t out_lo[kHist] = {}, out_hi[kHist] = {};
     int next = 0;
@@ -410,7 +610,8 @@ std::map<std::pair<int, cudaStream_t>, StreamState> g_ws;
 
 pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out, const void* in = nullptr,
                                size_t in_bytes = 0, const void* dst = nullptr, size_t dst_bytes = 0,
-                               bool* no_pdl = nullptr, const void* in2 = nullptr, size_t in2_bytes = 0) {
+                               bool* no_pdl = nullptr, const void* in2 = nullptr, size_t in2_bytes = 0,
+                               bool segmented = false) {
     std::lock_guard<std::mutex> lock(g_ws_mu);
     auto key = std::make_pair(dev, s);
     auto it = g_ws.find(key);
@@ -421,6 +622,10 @@ pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out, co
         it = g_ws.emplace(key, st).first;
     }
     StreamState& st = it->second;
+    if (segmented && !st.seg_ws.acc) {
+        const pospop_status e = alloc_workspace(&st.seg_ws, true);
+        if (e) return e;
+    }
     if (no_pdl) {
         const uintptr_t lo = reinterpret_cast<uintptr_t>(in), hi = lo + in_bytes;
         *no_pdl = false;
@@ -435,7 +640,7 @@ pospop_status stream_workspace(int dev, cudaStream_t s, StreamWorkspace* out, co
             st.next = (st.next + 1) % StreamState::kHist;
         }
     }
-    *out = st.ws;
+    *out = segmented ? st.seg_ws : st.ws;
     return POSPOP_OK;
 }
 
@@ -484,6 +689,9 @@ Where classify(const void* p, int* dev, bool* pinned = nullptr) {
 // ---------------------------------------------------------------------------
 // The counting core: k in {8,16,32,64}, result in out[0..k).
 // ---------------------------------------------------------------------------
+pospop_status count_on_ctx(Ctx* c, int k, const void* data, size_t len, bool on_device, bool pinned, uint32_t flush,
+                           uint64_t* out);
+
 pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uint64_t* out) {
     if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
     if (!out) return fail(POSPOP_EINVAL, "counts must not be NULL");
@@ -500,15 +708,24 @@ pospop_status count_any(int k, const void* data, size_t len, uint32_t flush, uin
         for (int p = 0; p < k; ++p) out[p] = 0;
         return POSPOP_OK;
     }
-    LaunchOptions opt;
-    opt.flush_threshold = flush;
     bool pinned = false;
     const Where where = classify(data, &dev, &pinned);
     DeviceGuard g(dev);
+    CtxScope scope;
     Ctx* c = nullptr;
-    if ((s = get_ctx(dev, &c))) return s;
+    if ((s = scope.get(dev, &c))) return s;
+    return count_on_ctx(c, k, data, len, where == Where::Device, pinned, flush, out);
+}
 
-    if (where == Where::Device) {
+// Counts len (> 0) k-bit words at data on context c's device (current):
+// device memory in place, host memory through the staging pipelines.
+pospop_status count_on_ctx(Ctx* c, int k, const void* data, size_t len, bool on_device, bool pinned, uint32_t flush,
+                           uint64_t* out) {
+    pospop_status s;
+    const size_t wb = (size_t)k / 8;
+    LaunchOptions opt;
+    opt.flush_threshold = flush;
+    if (on_device) {
         CU(launch_stream(k, data, len, c->m_out_dev, false, opt, c->ws, c->stream));
     } else if (len * wb <= kBounceBytes) {
         // Small host input (the latency path): one DMA (from
@@ -588,6 +805,7 @@ struct SegUnit {
 pospop_status segmented_host_pipeline(Ctx* c, int k, const void* data, const uint64_t* offsets, bool o_dev,
                                       const uint64_t* hoff, size_t n, uint64_t* counts, bool c_dev) {
     pospop_status s;
+    if ((s = ensure_seg_ws(c))) return s;
     const size_t wb = (size_t)k / 8, row_bytes = (size_t)k * sizeof(uint64_t);
     const uint8_t* src = static_cast<const uint8_t*>(data) + hoff[0] * wb;
     bool d_pinned = false, c_pinned = false;
@@ -682,7 +900,7 @@ pospop_status segmented_host_pipeline(Ctx* c, int k, const void* data, const uin
         } else {
             // device pointer whose word hoff[a0] is at dst
             const uint8_t* ddata = dst - u.lo - hoff[0] * wb;
-            CU(launch_segmented(k, ddata, doff + u.a0, u.a1 - u.a0, dout + u.a0 * k, opt, c->ws, c->stream));
+            CU(launch_segmented(k, ddata, doff + u.a0, u.a1 - u.a0, dout + u.a0 * k, opt, c->seg_ws, c->stream));
         }
         CU(cudaEventRecord(c->ev_done[slot], c->stream));
         if (!c_dev && u.last_piece) {
@@ -821,8 +1039,9 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
     const bool c_dev = classify(counts, &cdev) == Where::Device;
     if (d_dev) dev = ddev;
     DeviceGuard g(dev);
+    CtxScope scope;
     Ctx* c = nullptr;
-    if ((s = get_ctx(dev, &c))) return s;
+    if ((s = scope.get(dev, &c))) return s;
 
     // Host offsets are needed on the host for validation and sizing anyway.
     std::vector<uint64_t> h_off;
@@ -869,7 +1088,8 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
         dout = static_cast<unsigned long long*>(buf);
     }
     LaunchOptions opt;
-    CU(launch_segmented(k, ddata ? ddata : (const void*)doff, doff, n, dout, opt, c->ws, c->stream));
+    if ((s = ensure_seg_ws(c))) return s;
+    CU(launch_segmented(k, ddata ? ddata : (const void*)doff, doff, n, dout, opt, c->seg_ws, c->stream));
     if (!c_dev)
         CU(cudaMemcpyAsync(counts, dout, n * (size_t)k * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -902,8 +1122,9 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
     bool pinned = false;
     const Where where = classify(flags, &dev, &pinned);
     DeviceGuard g(dev);
+    CtxScope scope;
     Ctx* c = nullptr;
-    if ((s = get_ctx(dev, &c))) return s;
+    if ((s = scope.get(dev, &c))) return s;
     LaunchOptions opt;
     if (where == Where::Device) {
         CU(launch_flagstats(flags, len, c->m_out_dev, false, opt, c->ws, c->stream));
@@ -1025,8 +1246,9 @@ pospop_status pospopcnt_fd(int fd, int k, uint64_t* counts, uint64_t* n_words) {
     int dev = 0;
     pospop_status s = current_device(&dev);
     if (s) return s;
+    CtxScope scope;
     Ctx* c = nullptr;
-    if ((s = get_ctx(dev, &c))) return s;
+    if ((s = scope.get(dev, &c))) return s;
     if ((s = ensure_stage(c))) return s;
     struct stat st;
     const bool seekable = fstat(fd, &st) == 0 && S_ISREG(st.st_mode);
@@ -1089,51 +1311,183 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
     int dev0 = 0;
     pospop_status s = current_device(&dev0);
     if (s) return s;
+    int n_dev = 0;
+    CU(cudaGetDeviceCount(&n_dev));
     const size_t wb = (size_t)k / 8;
+    std::vector<char> on_device((size_t)n_shards, 0), pinned((size_t)n_shards, 0);
+    std::set<int> device_set;  // devices of the device-resident shards
     for (int i = 0; i < n_shards; ++i) {  // validate everything before launching anything
+        if (devices[i] < 0 || devices[i] >= n_dev)
+            return fail(POSPOP_EINVAL, "shard %d: no device %d (%d visible)", i, devices[i], n_dev);
         if (!shards[i] && lens[i]) return fail(POSPOP_EINVAL, "shard %d is NULL with len %zu", i, lens[i]);
         if ((uintptr_t)shards[i] % wb) return fail(POSPOP_EINVAL, "shard %d is misaligned", i);
+        if ((s = check_device(devices[i]))) return s;
+        if (!lens[i]) continue;
         int pd = devices[i];
-        if (lens[i] && classify(shards[i], &pd) != Where::Device)
-            return fail(POSPOP_EINVAL, "shard %d is not device memory", i);
-        if (lens[i] && pd != devices[i])
-            return fail(POSPOP_EINVAL, "shard %d lives on device %d, not %d", i, pd, devices[i]);
+        bool pin = false;
+        if (classify(shards[i], &pd, &pin) == Where::Device) {
+            if (pd != devices[i]) return fail(POSPOP_EINVAL, "shard %d lives on device %d, not %d", i, pd, devices[i]);
+            on_device[(size_t)i] = 1;
+            device_set.insert(devices[i]);
+        }
+        pinned[(size_t)i] = pin;
     }
-    // Launch every shard before any synchronisation (launch skew).
-    // Shard i is the j-th shard of its device: it uses that device's slot j
-    // (own stream and workspace, so shards on one device may overlap), and
-    // its kernel writes the k counts straight into the slot's mapped buffer.
+    // Device shards: one context per device, acquired in ascending device
+    // order.  Launch every shard before any synchronisation (launch skew,
+    // SURVEY 8e).  Shard i is the j-th device shard of its device: it uses
+    // that context's slot j (own stream and workspace, so shards on one device
+    // may overlap), and its kernel writes the k counts straight into the
+    // slot's mapped buffer.
+    CtxScope scope;
+    std::map<int, Ctx*> ctx;
+    for (int d : device_set) {
+        DeviceGuard g(d);
+        if ((s = scope.get(d, &ctx[d]))) return s;
+    }
     std::vector<Ctx::ShardSlot*> used((size_t)n_shards, nullptr);
     std::map<int, size_t> per_dev;
     LaunchOptions opt;
     for (int i = 0; i < n_shards; ++i) {
+        if (!on_device[(size_t)i]) continue;
         const int d = devices[i];
         DeviceGuard g(d);
-        Ctx* c = nullptr;
-        if ((s = get_ctx(d, &c))) return s;
+        Ctx* c = ctx[d];
         const size_t j = per_dev[d]++;
         if (c->shard_slots.size() <= j) {
-            Ctx::ShardSlot slot;
+            c->shard_slots.emplace_back();
+            Ctx::ShardSlot& slot = c->shard_slots.back();
             CU(cudaStreamCreateWithFlags(&slot.stream, cudaStreamDefault));
             if ((s = alloc_workspace(&slot.ws))) return s;
             CU(cudaHostAlloc(&slot.m_out, 64 * sizeof(unsigned long long), cudaHostAllocMapped));
             CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&slot.m_out_dev), slot.m_out, 0));
-            c->shard_slots.push_back(slot);
         }
         Ctx::ShardSlot* slot = &c->shard_slots[j];
         used[(size_t)i] = slot;
-        if (lens[i]) {
-            CU(launch_stream(k, shards[i], lens[i], slot->m_out_dev, false, opt, slot->ws, slot->stream));
-        } else {
-            for (int p = 0; p < k; ++p) slot->m_out[p] = 0;
+        CU(launch_stream(k, shards[i], lens[i], slot->m_out_dev, false, opt, slot->ws, slot->stream));
+    }
+    // Host shards: one worker thread each, running on the CPUs local to its
+    // device, streams its range through its own context's staging ring over
+    // that device's host link -- N devices' links in parallel.
+    std::vector<std::vector<uint64_t>> host_out;
+    std::vector<pospop_status> host_st;
+    std::vector<std::string> host_err;
+    std::vector<std::thread> workers;
+    host_out.resize((size_t)n_shards);
+    host_st.assign((size_t)n_shards, POSPOP_OK);
+    host_err.resize((size_t)n_shards);
+    for (int i = 0; i < n_shards; ++i) {
+        if (on_device[(size_t)i] || !lens[i]) continue;
+        host_out[(size_t)i].assign((size_t)k, 0);
+        workers.emplace_back([&, i] {
+            const int d = devices[i];
+            pospop_status ws = cuda_set_device(d);
+            if (!ws) {
+                bind_to_device_cpus(d);
+                CtxScope wscope;
+                Ctx* c = nullptr;
+                if (!(ws = wscope.get(d, &c)))
+                    ws = count_on_ctx(c, k, shards[i], lens[i], false, pinned[(size_t)i] != 0, 65535,
+                                      host_out[(size_t)i].data());
+            }
+            host_st[(size_t)i] = ws;
+            if (ws) host_err[(size_t)i] = t_err;
+        });
+    }
+    for (auto& t : workers) t.join();
+    for (int p = 0; p < k; ++p) counts[p] = 0;
+    pospop_status first = POSPOP_OK;
+    int first_i = -1;
+    for (int i = 0; i < n_shards; ++i) {  // merge_counts over shards
+        if (on_device[(size_t)i]) {
+            DeviceGuard g(devices[i]);
+            CU(cudaStreamSynchronize(used[(size_t)i]->stream));
+            for (int p = 0; p < k; ++p) counts[p] += used[(size_t)i]->m_out[p];
+        } else if (lens[i]) {
+            if (host_st[(size_t)i] && !first) {
+                first = host_st[(size_t)i];
+                first_i = i;
+            }
+            for (int p = 0; p < k; ++p) counts[p] += host_out[(size_t)i][(size_t)p];
         }
     }
-    for (int p = 0; p < k; ++p) counts[p] = 0;
-    for (int i = 0; i < n_shards; ++i) {  // merge_counts over shards
-        DeviceGuard g(devices[i]);
-        CU(cudaStreamSynchronize(used[(size_t)i]->stream));
-        for (int p = 0; p < k; ++p) counts[p] += used[(size_t)i]->m_out[p];
+    if (first) return fail(first, "shard %d: %s", first_i, host_err[(size_t)first_i].c_str());
+    return POSPOP_OK;
+}
+
+pospop_status pospopcnt_split(int k, const void* data, size_t len, const int* devices, int n_devices,
+                              uint64_t* counts) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (n_devices < 1 || !devices || !counts) return fail(POSPOP_EINVAL, "need >= 1 device and a counts array");
+    if (!data && len) return fail(POSPOP_EINVAL, "data is NULL but len is %zu", len);
+    const size_t wb = (size_t)k / 8;
+    std::vector<const void*> ptrs((size_t)n_devices);
+    std::vector<size_t> lens((size_t)n_devices);
+    for (int i = 0; i < n_devices; ++i) {  // contiguous word ranges, sizes differing by at most one word
+        const size_t lo = len / n_devices * i + ((size_t)i < len % n_devices ? i : len % n_devices);
+        const size_t n = len / n_devices + ((size_t)i < len % n_devices ? 1 : 0);
+        ptrs[(size_t)i] = static_cast<const uint8_t*>(data) + lo * wb;
+        lens[(size_t)i] = n;
     }
+    return pospopcnt_sharded(k, ptrs.data(), lens.data(), devices, n_devices, counts);
+}
+
+pospop_status pospop_release_resources(void) {
+    std::vector<std::pair<int, Ctx*>> dead;
+    {
+        CtxPool& pool = CtxPool::get();
+        std::lock_guard<std::mutex> lk(pool.mu);
+        for (auto& kv : pool.idle) {
+            for (Ctx* c : kv.second) dead.emplace_back(kv.first, c);
+            pool.live[kv.first] -= (int)kv.second.size();
+            kv.second.clear();
+        }
+    }
+    for (auto& dc : dead) {
+        DeviceGuard g(dc.first);
+        destroy_ctx(dc.second);
+    }
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    std::set<int> synced;
+    for (auto& kv : g_ws) {
+        const int dev = kv.first.first;
+        DeviceGuard g(dev);
+        if (synced.insert(dev).second) cudaDeviceSynchronize();
+        free_workspace(&kv.second.ws);
+        free_workspace(&kv.second.seg_ws);
+    }
+    g_ws.clear();
+    cudaGetLastError();
+    return POSPOP_OK;
+}
+
+pospop_status pospop_release_stream(void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+        if (it->first.second != st) {
+            ++it;
+            continue;
+        }
+        DeviceGuard g(it->first.first);
+        CU(cudaStreamSynchronize(st));
+        free_workspace(&it->second.ws);
+        free_workspace(&it->second.seg_ws);
+        it = g_ws.erase(it);
+    }
+    return POSPOP_OK;
+}
+
+pospop_status pospop_resource_stats(int device, int* contexts, int* idle_contexts, int* stream_workspaces) {
+    {
+        CtxPool& pool = CtxPool::get();
+        std::lock_guard<std::mutex> lk(pool.mu);
+        if (contexts) *contexts = pool.live.count(device) ? pool.live[device] : 0;
+        if (idle_contexts) *idle_contexts = pool.idle.count(device) ? (int)pool.idle[device].size() : 0;
+    }
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    int n = 0;
+    for (auto& kv : g_ws) n += kv.first.first == device;
+    if (stream_workspaces) *stream_workspaces = n;
     return POSPOP_OK;
 }
 
@@ -1428,7 +1782,8 @@ pospop_status pospopcnt_segmented_async(int k, const void* d_data, const uint64_
     const void *dbase = nullptr, *obase = nullptr;
     size_t dbytes = 0, obytes = 0;
     const bool known = (!d_data || alloc_range(d_data, &dbase, &dbytes)) && (!n || alloc_range(d_offsets, &obase, &obytes));
-    if ((s = stream_workspace(dev, st, &ws, dbase, dbytes, d_counts, n * (size_t)k * 8, &opt.no_pdl, obase, obytes)))
+    if ((s = stream_workspace(dev, st, &ws, dbase, dbytes, d_counts, n * (size_t)k * 8, &opt.no_pdl, obase, obytes,
+                              true)))
         return s;
     if (!known) opt.no_pdl = true;
     opt.flush_threshold = flush;
@@ -1457,8 +1812,9 @@ pospop_status pospop_microop(int op, int depth, const uint32_t* in, size_t n_in,
     int dev = 0;
     pospop_status s = current_device(&dev);
     if (s) return s;
+    CtxScope scope;
     Ctx* c = nullptr;
-    if ((s = get_ctx(dev, &c))) return s;
+    if ((s = scope.get(dev, &c))) return s;
     uint32_t *d_in = nullptr, *d_out = nullptr;
     CU(cudaMalloc(&d_in, n_in * 4 + 4));
     CU(cudaMalloc(&d_out, n_out * 4 + 4));
@@ -1480,8 +1836,9 @@ pospop_status pospop_digest(const void* d_data, size_t nbytes, uint64_t* digest)
     if (s) return s;
     classify(d_data, &dev);
     DeviceGuard g(dev);
+    CtxScope scope;
     Ctx* c = nullptr;
-    if ((s = get_ctx(dev, &c))) return s;
+    if ((s = scope.get(dev, &c))) return s;
     CU(cudaMemsetAsync(c->d_out, 0, sizeof(unsigned long long), c->stream));
     CU(launch_digest(d_data, nbytes, c->d_out, c->stream));
     CU(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));

@@ -25,11 +25,14 @@ struct StreamWorkspace {
 // kSegRangeSlots slots (one per array) of 64 partial counts + 1 byte counter
 // (dev::seg_range_slots: `next` + 7), then the segmented giant-array queue
 // (8 + kGiantQ entries of kGiantEntry u64; dev::GiantQueue).  Zero between
-// launches.
+// launches.  Stream and FLAG launches use only the first 104 u64
+// (kStreamWorkspaceBytes); the segmented regions are allocated only for
+// segmented launches.
 constexpr int kAccChannels = 96;
 constexpr int kSegRangeSlotsHost = 16384;
 constexpr int kGiantQHost = 512;
 constexpr int kGiantEntryHost = 72;
+constexpr size_t kStreamWorkspaceBytes = 104 * sizeof(unsigned long long);  // stream / FLAG launches
 constexpr size_t kWorkspaceBytes =
     (104 + (size_t)kSegRangeSlotsHost * 65 + 8 + (size_t)kGiantQHost * kGiantEntryHost) * sizeof(unsigned long long);
 
