@@ -52,10 +52,21 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libpospopcnt_b200.so"
 
 
-def library_path() -> str:
-    """The in-tree library; POSPOP_LIBRARY selects another build of it (tests:
-    the bounds-checked libpospopcnt_b200_debug.so)."""
-    return os.environ.get("POSPOP_LIBRARY") or os.path.join(_HERE, LIB_NAME)
+BUILDS = {
+    "release": "libpospopcnt_b200.so",         # production kernels only; reads no tuning knobs
+    "tuning": "libpospopcnt_b200_tuning.so",   # every measured variant + the POSPOP_* tuning knobs
+    "debug": "libpospopcnt_b200_debug.so",     # the tuning build with bounds-checked vector loads
+}
+
+
+def library_path(build: str | None = None) -> str:
+    """The in-tree library.  `build` (or POSPOP_LIBRARY: a build name or a
+    path) selects another build of it: "tuning" for tools/ sweeps and the
+    tuning tests, "debug" for tests/test_gpu_bounds.py."""
+    sel = build or os.environ.get("POSPOP_LIBRARY") or "release"
+    if sel in BUILDS:
+        return os.path.join(_HERE, BUILDS[sel])
+    return sel
 
 
 # -- errors (status codes of include/pospopcnt_b200.h) -----------------------
@@ -106,11 +117,23 @@ class _Config(C.Structure):
 _lib = None
 
 
+_libs: dict = {}
+
+
 def _load():
     global _lib
-    if _lib is not None:
-        return _lib
-    path = library_path()
+    if _lib is None:
+        _lib = load_library(library_path())
+    return _lib
+
+
+def load_library(path: str):
+    """ctypes handle of one build of the library with every signature set
+    (cached per path).  The package's functions call the handle in
+    `paper_1911_02696_b200._lib` (the release build unless POSPOP_LIBRARY
+    says otherwise; tests/conftest.py's `tuning` fixture swaps it)."""
+    if path in _libs:
+        return _libs[path]
     if not os.path.exists(path):
         raise ImportError(f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "or `make -C paper_1911_02696_b200/csrc` (there is no CPU fallback)")
@@ -160,7 +183,7 @@ def _load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    _lib = lib
+    _libs[path] = lib
     return lib
 
 

@@ -49,7 +49,7 @@ constexpr int kDefaultBlock = 256;
 constexpr int kDefaultDepth1 = 7;  // k = 8/16/32: 128 registers = 512 B per thread per tree block
 constexpr int kDefaultDepth2 = 6;  // k = 64: two banks of 64 registers
 
-// Tuning knobs (POSPOP_*) are read from one snapshot of the environment
+// Tuning knobs (POSPOP_*; tuning build only) are read from one snapshot of the environment
 // taken at the top of each public launcher: a single pass over `environ`
 // instead of a getenv() scan per knob (~0.25 us each with ~130 variables --
 // several microseconds on the small-call latency path otherwise).
@@ -58,6 +58,7 @@ struct EnvSnapshot {
     const char* entry[kMax];
     int n = 0;
 };
+#ifdef POSPOP_TUNING
 thread_local EnvSnapshot t_env;
 
 void env_refresh() {
@@ -73,6 +74,12 @@ const char* env_get(const char* name) {
         if (std::strncmp(t_env.entry[i], name, len) == 0 && t_env.entry[i][len] == '=') return t_env.entry[i] + len + 1;
     return nullptr;
 }
+#else
+// The release library reads no tuning knobs: the kernel, grid and flush
+// threshold depend on the call's arguments only.
+inline void env_refresh() {}
+inline const char* env_get(const char*) { return nullptr; }
+#endif
 
 int env_int(const char* name, int dflt) {
     const char* v = env_get(name);

@@ -4,6 +4,7 @@
 #include "pospop_variants.h"
 
 namespace pospop_b200 {
+#ifdef POSPOP_TUNING  // tuning build only: the release library has no 16-bit-lane FLAG kernel
 namespace {
 using namespace dev;
 #define SV(NB, L, VB, H, B, S) {NB, L, VB, H, B, S, 0, stream_kernel<NB, L, VB, H, B, S, 0>}
@@ -37,5 +38,11 @@ const StreamVariant* stream_variants_flag16(size_t* n) {
     *n = sizeof(kVariants) / sizeof(kVariants[0]);
     return kVariants;
 }
+#else
+const StreamVariant* stream_variants_flag16(size_t* n) {
+    *n = 0;
+    return nullptr;
+}
+#endif
 
 }  // namespace pospop_b200

@@ -12,16 +12,17 @@ using namespace dev;
 #define SVF2(L, VB, B, S) {2, L, VB, 2, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1, 2>}
 #define SVB(L, VB, B, S) {3, L, VB, 0, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2>}
 #define SVB2(L, VB, B, S) {3, L, VB, 2, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2, 2>}
-// Production variants first (the defaults), then tuning variants selectable
-// through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched" (POSPOP_FLAG_VARIANT
-// for MODE 1).
+// The release library holds the production variants only; the tuning build
+// (-DPOSPOP_TUNING) adds the alternatives (POSPOP_FLAG_VARIANT).
 const StreamVariant kVariants[] = {
     // byte-frame FLAG statistics (MODE 2): defaults first
     SVB(5, 32, 512, 2), SVB(5, 32, 0, 2),
+#ifdef POSPOP_TUNING  // the tuning build: measured alternatives (POSPOP_FLAG_VARIANT)
     SVB(5, 32, 256, 2), SVB(4, 32, 512, 2), SVB(4, 32, 256, 2), SVB2(4, 32, 256, 2),
     SVB(4, 16, 512, 2), SVB(6, 32, 256, 2), SVB(5, 16, 512, 2), SVB2(5, 32, 256, 2),
     SVB(4, 32, 512, 4), SVB(4, 16, 512, 4), SVB(3, 32, 512, 4), SVB(4, 32, 256, 4), SVB2(3, 32, 256, 4),
     SVB(5, 32, 256, 4), SVB(5, 32, 512, 5), SVB(5, 16, 512, 5), SVB(6, 32, 256, 5),
+#endif
 };
 
 #undef SV

@@ -32,13 +32,15 @@ using namespace dev;
 // sched 5: grouped, G lanes per array, 2 CTAs/SM
 #define SGG(NB, L, VB, G) {NB, L, VB, 5, segmented_group_kernel<NB, L, VB, G, 2>, G}
 const SegVariant kVariants[] = {
-    SGA(1, 5), SGA(2, 4),
+    SGA(1, 5), SGA(2, 4),                 // the adaptive kernel (default; k <= 32 / k = 64)
+    SGR(1, 7, 32, 1), SGR(2, 6, 32, 1),   // range kernel, one CTA per SM (at most one array per SM)
+#ifdef POSPOP_TUNING  // the tuning build: measured alternatives (POSPOP_SEG_VARIANT)
     SGT(1, 7, 32, 1), SGT(1, 7, 16, 1), SGT(1, 6, 32, 1), SGT(1, 6, 32, 2), SGT(1, 6, 16, 2), SGT(1, 5, 32, 2),
     SGT(2, 6, 32, 1), SGT(2, 5, 32, 1), SGT(2, 5, 32, 2), SGT(2, 5, 16, 2),
     SGTE(1, 7, 32, 1), SGTE(1, 6, 32, 1), SGTE(1, 6, 32, 2), SGTE(2, 6, 32, 1),
     SGTD(1, 7, 32, 1), SGTD(1, 6, 32, 1), SGTD(1, 6, 32, 2), SGTD(2, 6, 32, 1), SGTD(2, 5, 32, 2), SGTD(2, 5, 16, 2),
     SGTD(1, 6, 16, 2), SGTD(1, 5, 16, 2), SGTD(1, 5, 32, 2),
-    SGR(1, 5, 16, 2), SGR(2, 5, 16, 2), SGR(1, 7, 32, 1), SGR(2, 6, 32, 1), SGR(1, 5, 32, 2), SGR(1, 6, 32, 1),
+    SGR(1, 5, 16, 2), SGR(2, 5, 16, 2), SGR(1, 5, 32, 2), SGR(1, 6, 32, 1),
     SGTB(1, 7, 32, 1), SGTB(1, 6, 32, 1), SGTB(1, 6, 32, 2), SGTB(2, 6, 32, 1), SGTB(2, 5, 32, 2), SGPEH(1, 5), SGPEH(1, 4), SGPEH(2, 4),
     SGC(1, 5, 3), SGC(1, 5, 2), SGC(1, 4, 4), SGC(2, 3, 4), SGC(2, 4, 2),
     SGPE(1, 5, 16), SGPE(1, 5, 32), SGPE(1, 4, 16), SGPE(1, 4, 32), SGPE(2, 4, 16), SGPE(2, 4, 32), SGPE(2, 3, 32),
@@ -52,6 +54,7 @@ const SegVariant kVariants[] = {
     SGP(1, 5, 16), SGP(1, 4, 16), SGP(1, 4, 32), SGP(1, 5, 32), SGP(2, 4, 16), SGP(2, 3, 32), SGP(2, 4, 32),
     SGP2(2, 4, 16), SGP2(2, 3, 32), SGP2(2, 3, 16), SGP2(1, 5, 16), SGP2(1, 5, 32),
     SGP3(1, 4, 16), SGP3(1, 4, 32), SGP3(1, 5, 16), SGP3(2, 3, 16), SGP3(2, 3, 32),
+#endif
 };
 #undef SGP2
 #undef SGP3

@@ -15,18 +15,19 @@ using namespace dev;
 #define SVF2(L, VB, B, S) {2, L, VB, 2, B, S, 1, stream_kernel<2, L, VB, 0, B, S, 1, 2>}
 #define SVB(L, VB, B, S) {3, L, VB, 0, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2>}
 #define SVB2(L, VB, B, S) {3, L, VB, 2, B, S, 2, stream_kernel<3, L, VB, 0, B, S, 2, 2>}
-// Production variants first (the defaults), then tuning variants selectable
-// through POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched" (POSPOP_FLAG_VARIANT
-// for MODE 1).
+// The release library holds the production variants only; the tuning build
+// (-DPOSPOP_TUNING) adds the alternatives, selectable through
+// POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched".
 const StreamVariant kVariants[] = {
     SV(1, 7, 32, 0, 256, 2), SV(2, 6, 32, 0, 256, 2),  // defaults (k <= 32 / k = 64)
-    SV(1, 7, 32, 0, 0, 2), SV(2, 6, 32, 0, 0, 2),      // runtime block size (test launches)
+    SV(1, 7, 32, 0, 0, 2), SV(2, 6, 32, 0, 0, 2),      // runtime block size (pospopcnt_async block != 0)
+#ifdef POSPOP_TUNING  // the tuning build (libpospopcnt_b200_tuning.so): measured alternatives
     SV(1, 7, 32, 0, 256, 0), SV(2, 6, 32, 0, 256, 0),  // static CTA partition
     SV(1, 7, 32, 0, 0, 0), SV(2, 6, 32, 0, 0, 0),
     SV(1, 7, 32, 0, 256, 1), SV(2, 6, 32, 0, 256, 1),  // per-warp guided chunks
     SV(1, 7, 32, 0, 0, 1), SV(2, 6, 32, 0, 0, 1), SV(1, 6, 32, 0, 256, 2), SV(1, 7, 16, 0, 256, 2),
     SV2(1, 6, 32, 256, 2), SV2(1, 5, 32, 256, 2), SV2(2, 5, 32, 256, 2), SV2(1, 6, 16, 256, 2),
-
+#endif
 };
 
 #undef SV

@@ -4,6 +4,7 @@
 #include "pospop_variants.h"
 
 namespace pospop_b200 {
+#ifdef POSPOP_TUNING  // tuning build only: the release library has no TMA-staged variants
 namespace {
 using namespace dev;
 #define TV(NB, L, M, NC, ST)                                                                \
@@ -25,5 +26,11 @@ const TmaVariant* tma_variants(size_t* n) {
     *n = sizeof(kVariants) / sizeof(kVariants[0]);
     return kVariants;
 }
+#else
+const TmaVariant* tma_variants(size_t* n) {
+    *n = 0;
+    return nullptr;
+}
+#endif
 
 }  // namespace pospop_b200

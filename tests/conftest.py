@@ -50,3 +50,22 @@ def pp():
         import __graft_entry__
         __graft_entry__.build()
     return pp
+
+
+@pytest.fixture
+def tuning(pp):
+    """Runs the test against the tuning build (libpospopcnt_b200_tuning.so):
+    every measured kernel variant and the POSPOP_* tuning knobs, which the
+    release library does not read.  Same kernel templates, so parity here is
+    parity of the alternatives; the release build's own parity is every other
+    test."""
+    path = pp.library_path("tuning")
+    if not os.path.exists(path):
+        import __graft_entry__
+        __graft_entry__.build()
+    saved = pp._load()
+    pp._lib = pp.load_library(path)
+    try:
+        yield pp._lib
+    finally:
+        pp._lib = saved

@@ -60,6 +60,27 @@ def test_sass_uses_lop3_csa_and_256bit_loads(pp):
     assert "LDG.E.NA.ENL2.256.CONSTANT" in sass, funs
 
 
+def _entries(path):
+    out = subprocess.run(["cuobjdump", "-symbols", path], capture_output=True, text=True).stdout
+    return sorted(set(re.findall(r"STO_ENTRY\s+(\S+)", out)))
+
+
+def test_release_library_holds_only_production_kernels(pp):
+    """The release .so instantiates the production kernels only (<= 20
+    entries) and reads no tuning knob; the tuning build carries the measured
+    alternatives and the POSPOP_* knobs (tools/ sweeps, tuning tests)."""
+    release = _entries(pp.library_path("release"))
+    assert 0 < len(release) <= 20, release
+    strings = subprocess.run(["strings", pp.library_path("release")], capture_output=True, text=True).stdout
+    for knob in ("POSPOP_STREAM_VARIANT", "POSPOP_FLUSH_THRESHOLD", "POSPOP_SEG_VARIANT", "POSPOP_FLAG_VARIANT",
+                 "POSPOP_SMALL_BYTES", "POSPOP_TMA", "POSPOP_PDL"):
+        assert knob not in strings, knob
+    tuning = _entries(pp.library_path("tuning"))
+    assert set(release) < set(tuning) and len(tuning) > 100
+    tstrings = subprocess.run(["strings", pp.library_path("tuning")], capture_output=True, text=True).stdout
+    assert "POSPOP_STREAM_VARIANT" in tstrings and "POSPOP_FLUSH_THRESHOLD" in tstrings
+
+
 def test_validate_like_reference(pp):  # test_core.cpp:184-201
     pp.validate(pp.PospopcntConfig(flush_threshold_blocks=1))
     with pytest.raises(pp.InvalidArgument):

@@ -90,7 +90,7 @@ FLAG_VARIANTS = ["5,32,0,512,2,2", "4,32,0,512,2,2", "4,32,2,256,2,2", "4,16,0,5
 
 @pytest.mark.parametrize("variant", FLAG_VARIANTS)
 @pytest.mark.parametrize("flush", [None, "1", "3"])
-def test_flag_kernel_variants(pp, dev, orc, golden, variant, flush, monkeypatch):
+def test_flag_kernel_variants(pp, tuning, dev, orc, golden, variant, flush, monkeypatch):
     """Every FLAG kernel instantiation (byte-frame MODE 2 and the 16-bit-lane
     MODE 1), with forced lane flushes, on the golden acceptance streams, all
     4096 values at unaligned starts, and the first-invalid-word report."""
@@ -114,7 +114,7 @@ def test_flag_kernel_variants(pp, dev, orc, golden, variant, flush, monkeypatch)
     assert e.value.offset == 77_777
 
 
-def test_flag_byte_frame_full_size_flushes(pp, dev, orc, monkeypatch):
+def test_flag_byte_frame_full_size_flushes(pp, tuning, dev, orc, monkeypatch):
     """8 GiB-class input at the default variant: every thread crosses the
     255-block byte-lane flush several times."""
     n = 1 << 31
@@ -131,7 +131,7 @@ def test_flag_byte_frame_full_size_flushes(pp, dev, orc, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", ["", "5,16,0,512,2,2", "6,32,0,256,2,2"])
-def test_qcfail_fast_path_and_fixup(pp, dev, orc, variant, monkeypatch):
+def test_qcfail_fast_path_and_fixup(pp, tuning, dev, orc, variant, monkeypatch):
     """The byte-frame kernel predicts fail-free tiles and counts only AL/AH
     there; a tile that turns out to hold a QC-fail read is reloaded and its
     fail planes added.  Paired-end-like mix (kind 8: QC-fail 2^-16, so most

@@ -64,7 +64,7 @@ MODES = {"auto": {}, "lane": {"LANE_MEAN_BYTES": 4000, "GROUP_MEAN_BYTES": 4000,
        seed=st.integers(0, 2**32 - 1), empty_frac=st.floats(0, 0.5), flush=st.sampled_from([1, 3, 65535]),
        mode=st.sampled_from(sorted(MODES)), giant_kib=st.sampled_from([1024, 16]), start=st.integers(0, 9),
        huge=st.booleans())
-def test_fuzz_segmented(pp, dev, orc, k, n_arrays, max_len, seed, empty_frac, flush, mode, giant_kib, start, huge):
+def test_fuzz_segmented(pp, tuning, dev, orc, k, n_arrays, max_len, seed, empty_frac, flush, mode, giant_kib, start, huge):
     import os
     rng = np.random.default_rng(seed)
     lens = rng.integers(0, max_len + 1, size=n_arrays)

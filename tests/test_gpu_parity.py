@@ -408,7 +408,7 @@ SEG_VARIANTS = {
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-def test_segmented_every_variant(pp, dev, orc, k, monkeypatch):
+def test_segmented_every_variant(pp, tuning, dev, orc, k, monkeypatch):
     """All segmented schedules (strided, dynamic, software-pipelined) on a ragged
     batch with empty arrays, tiny arrays and misaligned starts."""
     rng = np.random.default_rng(500 + k)
@@ -433,7 +433,7 @@ def test_segmented_every_variant(pp, dev, orc, k, monkeypatch):
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-def test_segmented_grouped_big_arrays_and_flushes(pp, dev, orc, k, monkeypatch):
+def test_segmented_grouped_big_arrays_and_flushes(pp, tuning, dev, orc, k, monkeypatch):
     """Grouped kernel (G lanes per array): batches holding an array above the
     big-array bound are counted one array at a time by the whole warp; forced
     flushes reduce inside each lane group; a few long arrays among many
@@ -533,7 +533,7 @@ def test_segmented_few_huge_arrays(pp, dev, orc, k, monkeypatch):
 
 @pytest.mark.parametrize("k", [8, 32, 64])
 @pytest.mark.parametrize("mode", ["lane", "grouped", "tile"])
-def test_segmented_giant_queue(pp, dev, orc, k, mode, monkeypatch):
+def test_segmented_giant_queue(pp, tuning, dev, orc, k, mode, monkeypatch):
     """Giant arrays among many short ones: the lane / grouped / tile schedules
     publish arrays above the giant bound to the queue and every warp counts
     their chunks at its exit.  A 16 KiB bound makes hundreds of giants (more
@@ -568,7 +568,7 @@ def test_segmented_giant_queue(pp, dev, orc, k, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("var", ["", "7,32,13,1", "7,32,14,1", "6,32,14,2"])
-def test_chained_segmented_launches(pp, dev, orc, var, monkeypatch):
+def test_chained_segmented_launches(pp, tuning, dev, orc, var, monkeypatch):
     """Segmented kernels that read (and count) before waiting for the previous
     launch on the stream: a segmented input produced by the previous launch
     (RAW: programmatic dependent launch dropped), rows overwritten by the next
@@ -657,7 +657,7 @@ def test_sharded_repeated_calls_and_empty_shards(pp, dev, orc):
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
 @pytest.mark.parametrize("mode", ["lane", "grouped", "tile", "range"])
-def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
+def test_segmented_adaptive_modes(pp, tuning, dev, orc, k, mode, monkeypatch):
     """The adaptive kernel (sched 8) in each of its modes -- forced through the
     mean-length thresholds -- on tiny, ragged, empty and large arrays; in lane
     mode a batch with an array above the lane cap takes the full-warp path."""
@@ -687,11 +687,12 @@ def test_segmented_adaptive_modes(pp, dev, orc, k, mode, monkeypatch):
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
 @pytest.mark.parametrize("mode", ["default", "lane"])
-def test_segmented_rows_at_8_byte_aligned_output(pp, dev, orc, k, mode, monkeypatch):
+def test_segmented_rows_at_8_byte_aligned_output(pp, dev, orc, k, mode, monkeypatch, request):
     """Row stores at an output that is only 8-byte aligned: the default path
     (few arrays: the range kernel) and the adaptive kernel's lane mode (staged
     rows copied out with 8-byte stores)."""
-    if mode == "lane":
+    if mode == "lane":  # forced through the tuning build's knobs
+        request.getfixturevalue("tuning")
         monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
         monkeypatch.setenv("POSPOP_SEG_RANGE", "0")
     rng = np.random.default_rng(70 + k)
@@ -748,14 +749,15 @@ def test_typed_entry_points(pp, dev, orc):
 
 @pytest.mark.parametrize("k", [16, 32, 64])
 @pytest.mark.parametrize("mode", ["range_kernel", "adaptive_range"])
-def test_segmented_range_mode_misaligned_data(pp, dev, orc, k, mode, monkeypatch):
+def test_segmented_range_mode_misaligned_data(pp, dev, orc, k, mode, monkeypatch, request):
     """Range mode with data that is word-aligned but not 16-byte aligned
     (+wb, +2wb, +3wb bytes) and offsets[0] = 0, so the first referenced byte
     sits in the first 16-byte block: every range must be counted and no
     workspace slot may be left dirty.  Misaligned and aligned calls alternate
     on one stream (a dirty slot would corrupt the next call's rows); the host
     path (pageable data staged at the caller's 32-byte phase) is checked too."""
-    if mode == "adaptive_range":
+    if mode == "adaptive_range":  # the tuning build (the release library routes this case to the range kernel)
+        request.getfixturevalue("tuning")
         monkeypatch.setenv("POSPOP_SEG_VARIANT", "4,16,8" if k == 64 else "5,16,8")
         monkeypatch.setenv("POSPOP_SEG_RANGE", "63")
     wb = k // 8

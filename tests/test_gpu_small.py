@@ -24,7 +24,7 @@ def guarded(raw, offset, guard=64):
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-def test_small_path_lengths_offsets(pp, dev, orc, k, monkeypatch):
+def test_small_path_lengths_offsets(pp, tuning, dev, orc, k, monkeypatch):
     wb = k // 8
     raw = orc.generate(6, 40 + k, (40 << 10) // 8).view(np.uint8)
     lengths = sorted({0, 1, 2, 3, 31, 32, 33, 255, 256, 1000, 1023, 1024, 4095, 4096, 4097,
@@ -42,7 +42,7 @@ def test_small_path_lengths_offsets(pp, dev, orc, k, monkeypatch):
 
 
 @pytest.mark.parametrize("k", [16, 64])
-def test_small_kernel_multi_tile_and_accumulate(pp, dev, orc, k, monkeypatch):
+def test_small_kernel_multi_tile_and_accumulate(pp, tuning, dev, orc, k, monkeypatch):
     """Raising the switch size makes the one CTA loop over many tiles."""
     monkeypatch.setenv("POSPOP_SMALL_BYTES", str(4 << 20))
     raw = orc.generate(6, 7, (3 << 20) // 8 + 5).view(np.uint8)[: (3 << 20) + 24]
@@ -66,7 +66,7 @@ def test_small_path_launches_one_kernel(pp, dev, orc):
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
 @pytest.mark.parametrize("csize", ["16", "8"])
-def test_cluster_kernel_lengths_offsets_accumulate(pp, dev, orc, k, csize, monkeypatch):
+def test_cluster_kernel_lengths_offsets_accumulate(pp, tuning, dev, orc, k, csize, monkeypatch):
     monkeypatch.setenv("POSPOP_SMALL_BYTES", "0")
     monkeypatch.setenv("POSPOP_CLUSTER_BYTES", str(64 << 20))
     monkeypatch.setenv("POSPOP_CLUSTER", csize)

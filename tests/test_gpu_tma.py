@@ -31,7 +31,7 @@ def dev(pp):
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64])
-def test_tma_stream_lengths_offsets(pp, dev, orc, k, monkeypatch):
+def test_tma_stream_lengths_offsets(pp, tuning, dev, orc, k, monkeypatch):
     wb = k // 8
     raw = orc.generate(6, 17 + k, (5 << 20) // 8).view(np.uint8)
     lengths = [0, 1, 7, 31, 33, 1000, 4097, 65537, 300_001, raw.size // wb - 8]
@@ -45,7 +45,7 @@ def test_tma_stream_lengths_offsets(pp, dev, orc, k, monkeypatch):
                 assert pp.pospopcnt_k(view, k) == orc.pospopcnt(sub, k, threads=4), (var, tma, k, offset, n)
 
 
-def test_tma_forced_flush_and_full_size(pp, dev, orc, monkeypatch):
+def test_tma_forced_flush_and_full_size(pp, tuning, dev, orc, monkeypatch):
     monkeypatch.setenv("POSPOP_STREAM_VARIANT", "5,32,0,256,3")
     monkeypatch.setenv("POSPOP_TMA", "8,6")
     raw = orc.generate(6, 5, 1 << 18).view(np.uint8)
@@ -64,7 +64,7 @@ def test_tma_forced_flush_and_full_size(pp, dev, orc, monkeypatch):
 
 @pytest.mark.parametrize("var,tma", TMA_FLAG)
 @pytest.mark.parametrize("flush", [None, "1"])
-def test_tma_flagstats(pp, dev, orc, golden, var, tma, flush, monkeypatch):
+def test_tma_flagstats(pp, tuning, dev, orc, golden, var, tma, flush, monkeypatch):
     monkeypatch.setenv("POSPOP_FLAG_VARIANT", var)
     monkeypatch.setenv("POSPOP_TMA", tma)
     if flush:

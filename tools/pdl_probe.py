@@ -3,6 +3,7 @@
 (measurement tool, not product).  One JSON line per (size, pdl, events)."""
 import json
 import os
+os.environ.setdefault("POSPOP_LIBRARY", "tuning")  # POSPOP_* knobs: the tuning build
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -9,6 +9,7 @@ with its default thresholds.  1 GiB of u32 (k = 32) per shape.
 import argparse
 import json
 import os
+os.environ.setdefault("POSPOP_LIBRARY", "tuning")  # POSPOP_* knobs: the tuning build
 import statistics
 import sys
 

@@ -1,4 +1,5 @@
 import sys, time, os
+os.environ.setdefault("POSPOP_LIBRARY", "tuning")  # POSPOP_* knobs: the tuning build
 sys.path.insert(0, '/root/repo')
 import numpy as np, torch
 import paper_1911_02696_b200 as pp

@@ -7,6 +7,7 @@ tool): back-to-back launches (PDL) and isolated launches, GB/s of input.
 import argparse
 import json
 import os
+os.environ.setdefault("POSPOP_LIBRARY", "tuning")  # POSPOP_* knobs: the tuning build
 import statistics
 import sys
 

@@ -9,6 +9,7 @@ import argparse
 import ctypes as C
 import json
 import os
+os.environ.setdefault("POSPOP_LIBRARY", "tuning")  # POSPOP_* knobs: the tuning build
 import statistics
 import sys
 
