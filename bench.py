@@ -823,8 +823,8 @@ def run_ours_flag(args):
         "config": {"workload": desc, "words_total": total, "bytes_per_step": total_bytes,
                    "parallelism": f"shard{world}", "l2_policy": "input >> 126 MB L2; no flush needed",
                    "numa": numa,
-                   "kernel": "stream_kernel MODE 2: byte-frame FLAG transform + Harley-Seal trees; one launch + "
-                             "33-counter D2H per step"},
+                   "kernel": "stream_ring_kernel<3,5,MODE=2,16 warps,1 slot>: per-warp cp.async.bulk ring, "
+                             "byte-frame FLAG transform + Harley-Seal trees; one launch + 33-counter D2H per step"},
         "words_per_s": round(total_bytes / 2 / (ms_per_step * 1e-3), 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, world),

@@ -145,6 +145,15 @@ const TmaVariant* pick_tma(int nbank, int depth, int mode, int nc, int stages) {
     return nullptr;
 }
 
+const TmaVariant* pick_ring(int nbank, int depth, int mode, int nw, int stages) {
+    size_t n = 0;
+    const TmaVariant* v = ring_variants(&n);
+    for (size_t i = 0; i < n; ++i)
+        if (v[i].nbank == nbank && v[i].depth == depth && v[i].mode == mode && v[i].nc == nw && v[i].stages == stages)
+            return &v[i];
+    return nullptr;
+}
+
 const SegVariant* pick_segmented(int nbank, int depth, int vb, int sched, int group = 0) {
     size_t n = 0;
     const SegVariant* v = seg_variants(&n);
@@ -262,14 +271,22 @@ static cudaError_t launch_stream_tma(int mode, int nbank, int depth, int k, cons
     return launch_with_pdl(var->fn, grid, 32 * (var->nc + 1), var->smem, stream, a, !opt.no_pdl);
 }
 
+static void set_schedule(StreamArgs& a, int grid, int threads, int vpt);
+static cudaError_t launch_stream_ring(int mode, int nbank, int depth, int k, const void* data, size_t len_words,
+                                      unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
+                                      const StreamWorkspace& ws, cudaStream_t stream, int* grid_used);
+
 static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t len_words,
                                       unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
                                       const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
     // Tuning override: POSPOP_STREAM_VARIANT="depth,vb,hint,block,sched";
     // FLAG statistics: POSPOP_FLAG_VARIANT="depth,vb,hint,block,sched[,mode]"
     // (mode 2 byte-frame kernel, the default; mode 1 the 16-bit-lane kernel).
+    // FLAG statistics default: the per-warp bulk-copy ring kernel, 16 warps
+    // x 1 slot (sched 6; tools/ring_sweep.sh: uniform FLAG words 6276-6380 ->
+    // 6398-6400 GB/s, the paired-end-like mix 6946 -> 7162).
     int depth = mode == 0 ? (k == 64 ? kDefaultDepth2 : kDefaultDepth1) : 5, vb = 32, hint = 0,
-        block = mode == 0 ? kDefaultBlock : 512, sched = 2;
+        block = mode == 0 ? kDefaultBlock : 512, sched = mode == 0 ? 2 : 6;
     if (mode != 0) {
         int fmode = mode;
         if (const char* v = env_get("POSPOP_FLAG_VARIANT")) {
@@ -284,7 +301,9 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     if (opt.depth) depth = opt.depth;
     if (sched == 3 && !opt.block && !opt.grid)
         return launch_stream_tma(mode, nbank, depth, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
-    if (sched == 3) sched = 2;  // explicit test geometry: the LDG kernel
+    if (sched == 6 && !opt.block && !opt.grid)
+        return launch_stream_ring(mode, nbank, depth, k, data, len_words, d_out, accumulate, opt, ws, stream, grid_used);
+    if (sched == 3 || sched == 6) sched = 2;  // explicit test geometry: the LDG kernel
     if (opt.block) block = 0;  // explicit (test) block size: the runtime-block instantiation
     const StreamVariant* var = pick_stream(nbank, depth, vb, hint, block, sched, mode);
     if (!var) var = pick_stream(nbank, depth, vb, 0, 0, sched, mode);
@@ -309,6 +328,15 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
         const unsigned long long cap = (unsigned long long)device_info().sms * per_sm;
         grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
     }
+    set_schedule(a, grid, threads, vpt);
+    if (grid_used) *grid_used = grid;
+    return launch_with_pdl(var->fn, grid, threads, 0, stream, a, !opt.no_pdl);
+}
+
+// Work split shared by the LDG and ring kernels: nwt warp tiles of 32 x vpt
+// vectors; SCHED 1 hands them out in chunks of CA then CB; SCHED 2 / 6 split
+// [0, nwt - pool) into CTA ranges and hand the pool out in chunks of CB.
+static void set_schedule(StreamArgs& a, int grid, int threads, int vpt) {
     // Dynamic schedule: nwt warp tiles; the last ~tail_per_warp warp tiles per
     // warp go out in small chunks of CB, everything before in chunks of CA.
     const unsigned long long wt = 32ull * vpt;
@@ -332,9 +360,48 @@ static cudaError_t launch_stream_mode(int mode, int k, const void* data, size_t 
     if (ppw == 0) ppw = share / 27 < 1 ? 1 : (share / 27 > 16 ? 16 : share / 27);
     a.pool = warps * ppw;
     if (a.pool > a.nwt) a.pool = a.nwt;
+}
 
+// Per-warp bulk-copy ring (SCHED 6, stream_ring_kernel): one CTA of nw warps
+// per SM, each warp staging its next `stages` warp tiles in shared memory.
+static cudaError_t launch_stream_ring(int mode, int nbank, int depth, int k, const void* data, size_t len_words,
+                                      unsigned long long* d_out, bool accumulate, const LaunchOptions& opt,
+                                      const StreamWorkspace& ws, cudaStream_t stream, int* grid_used) {
+    int nw = 16, stages = 1;
+    if (const char* v = env_get("POSPOP_RING")) std::sscanf(v, "%d,%d", &nw, &stages);
+    const TmaVariant* var = pick_ring(nbank, depth, mode, nw, stages);
+    if (!var) return cudaErrorInvalidConfiguration;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, bool> configured;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto key = std::make_pair(dev, reinterpret_cast<const void*>(var->fn));
+        if (!configured[key]) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)var->smem);
+            if (e != cudaSuccess) return e;
+            configured[key] = true;
+        }
+    }
+    StreamArgs a;
+    fill_stream_args(a, k, data, len_words, 32, d_out, accumulate, opt, ws);
+    a.flush_threshold = flush_threshold_for(mode, opt);
+    if (mode != 0) {
+        a.peers = nullptr;
+        a.n_peers = 0;
+    }
+    const int regs = mode == 2 ? (2 << var->depth) : (nbank << var->depth);
+    const int vpt = regs / 8;
+    const int threads = 32 * var->nc;
+    const unsigned long long tile = (unsigned long long)vpt * threads;
+    const unsigned long long want = (a.ng * 32 + tile - 1) / tile;
+    const int cap = device_info().sms;
+    const int grid = (int)(want < 1 ? 1 : (want < (unsigned long long)cap ? want : cap));
+    set_schedule(a, grid, threads, vpt);
     if (grid_used) *grid_used = grid;
-    return launch_with_pdl(var->fn, grid, threads, 0, stream, a, !opt.no_pdl);
+    return launch_with_pdl(var->fn, grid, threads, var->smem, stream, a, !opt.no_pdl);
 }
 
 // Small inputs (<= POSPOP_SMALL_BYTES, default kSmallBytes): one CTA, no

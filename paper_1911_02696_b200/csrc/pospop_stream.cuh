@@ -509,13 +509,30 @@ __device__ __forceinline__ void flag_locate_bad(const StreamArgs& a, const uint3
     atomicMax(a.bad, ~best);
 }
 
+// The rare reserved-bit path.  CANON: r[] holds the tile in the canonical
+// register order (vector v of the lane at r[v * RPV ..]); otherwise (the ring
+// kernel reads its tile from shared memory with swizzled halves) the tile is
+// reloaded from global memory first.
+template <bool CANON, int REGS, int RPV, int VB>
+__device__ __forceinline__ void locate_bad(const StreamArgs& a, const uint32_t (&r)[REGS], unsigned long long first,
+                                           unsigned stride) {
+    if constexpr (CANON) {
+        flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
+    } else {
+        uint32_t rc[REGS];
+        load_tree_block<VB, 0, REGS / RPV>(a, first, stride, false, rc);
+        flag_locate_bad<REGS, RPV, VB>(a, rc, first, stride);
+    }
+}
+
 // Tree-block consumer.  MODE 0: positional counts of the words (NBANK banks).
 // MODE 2: byte-frame FLAG statistics (three banks, see flag_leaf).
 // MODE 1: FLAG statistics -- transform, then bank 0 counts the transformed
 // words of all reads and bank 1 those of QC-fail reads; words with reserved bits 12-15 set are
 // reported through a.bad (the first such index wins, as the reference's
 // check_reserved throws at the first one, flagstats.cpp:34-36).
-template <int MODE, int NBANK, int L, int VB, int REGS, int CD>
+// CANON: see locate_bad.
+template <int MODE, int NBANK, int L, int VB, bool CANON = true, int REGS, int CD>
 __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)[REGS], unsigned long long first,
                                         unsigned stride, uint32_t (&carries)[NBANK][CD],
                                         uint32_t (&counter)[NBANK][16], uint32_t& phase) {
@@ -539,7 +556,7 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
                 FlagByteTree<CD, L, 1>::run(carries, r, top, bad);
                 extract_bytes(counter[0], top[0]);
                 extract_bytes(counter[2], top[1]);
-                if (bad & 0xF0F0F0F0u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);  // r[] dies here
+                if (bad & 0xF0F0F0F0u) locate_bad<CANON, REGS, RPV, VB>(a, r, first, stride);  // r[] dies here
                 if (__any_sync(0xFFFFFFFFu, bad & 0x02020202u)) {
                     uint32_t r2[REGS];
                     load_tree_block<VB, 0, REGS / RPV>(a, first, stride, false, r2);
@@ -556,7 +573,7 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
                 FlagByteTree<CD, L>::run(carries, r, top, bad);
 #pragma unroll
                 for (int b = 0; b < 3; ++b) extract_bytes(counter[b], top[b]);
-                if (bad & 0xF0F0F0F0u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
+                if (bad & 0xF0F0F0F0u) locate_bad<CANON, REGS, RPV, VB>(a, r, first, stride);
                 phase = __any_sync(0xFFFFFFFFu, bad & 0x02020202u) ? 0u : 1u;
             }
             return;
@@ -577,7 +594,7 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
             for (int b = 0; b < 3; ++b) carries[b][L + 1] = top[b];
         }
         phase ^= 1u;
-        if (bad & 0xF0F0F0F0u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
+        if (bad & 0xF0F0F0F0u) locate_bad<CANON, REGS, RPV, VB>(a, r, first, stride);
     } else {
         static_assert(NBANK == 2 && REGS == (1 << L), "FLAG mode: two banks of 2^L registers");
         constexpr int RPV = VB / 4;
@@ -588,10 +605,15 @@ __device__ __forceinline__ void consume(const StreamArgs& a, const uint32_t (&r)
         FlagDualTree<L>::run(carries[0], carries[1], r, top_all, top_fail);
         extract(counter[0], top_all);
         extract(counter[1], top_fail);
-        if (bad & 0xF000F000u) flag_locate_bad<REGS, RPV, VB>(a, r, first, stride);
+        if (bad & 0xF000F000u) locate_bad<CANON, REGS, RPV, VB>(a, r, first, stride);
     }
 }
 
+// consume()'s MODE 2 branch for a tile read in place from shared memory
+// (the ring kernel's direct mode): leaves load their 8 bytes as the tree
+// needs them, so no register tile is live and more warps fit per SM.  The
+// QC-fail fix-up pass re-reads the slot; the reserved-bit report reloads the
+// tile from global memory in canonical order.
 // SCHED 0 (static): CTA b owns a contiguous range of whole 32-vector groups and
 // walks it in CTA tiles of BLOCK x VPT vectors.
 // SCHED 1 (dynamic): warps pull chunks of warp tiles (32 lanes x VPT vectors,
@@ -1112,6 +1134,166 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) stream_tma_kernel(const Stre
                 nb = 0;
             }
         }
+    }
+    cta_finish<NBANK, L, MODE>(a, carries, counter, s_acc, &s_last, block, lane);
+}
+
+
+// ---------------------------------------------------------------------------
+// Per-warp bulk-copy ring (SCHED 6).  The SCHED 2 work split (CTA ranges of
+// warp tiles claimed through a shared counter, then the global tail pool),
+// but each warp stages its own next S warp tiles in shared memory: lane 0
+// issues one cp.async.bulk per tile into the warp's slot, tracked by the
+// slot's mbarrier, so while the warp computes on tile i the loads of tiles
+// i+1 .. i+S are in flight without holding registers.  No slot is shared
+// between warps (the SCHED 3 ring serialised its consumers on a common
+// stage).  The warp copies a ready slot into registers with LDS.128 (16-byte
+// halves swapped on every other quarter-warp: conflict-free, and the
+// counts do not depend on register order; k = 64's lo/hi parity is kept),
+// refills the slot, then runs the same tree/extract as the LDG kernel.
+// Tiles not fully inside [f0, f1) (the stream's first and last vectors) are
+// loaded with the masked LDG path instead.  One CTA of NW warps per SM.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int NBANK, int L, int MODE, int NW, int S>
+__global__ void __launch_bounds__(32 * NW, 1) stream_ring_kernel(const StreamArgs a) {
+    constexpr int VB = 32;
+    constexpr int REGS = MODE == 2 ? (2 << L) : (NBANK << L);  // registers per tree block
+    constexpr int RPV = VB / 4;
+    constexpr int VPT = REGS / RPV;
+    constexpr unsigned long long WT = 32ull * VPT;  // vectors per warp tile
+    constexpr uint32_t TB = (uint32_t)(WT * VB);    // bytes per warp tile
+    constexpr unsigned long long kEnd = ~0ull;
+    extern __shared__ __align__(128) uint8_t ring[];  // NW x S x TB
+    __shared__ __align__(8) unsigned long long bar[NW * S];
+    __shared__ unsigned long long s_acc[32 * NBANK];
+    __shared__ int s_last;
+    __shared__ unsigned s_claim;
+
+    constexpr unsigned block = 32 * NW;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    if (a.trace && threadIdx.x == 0) {
+        a.trace[blockIdx.x * 5 + 0] = globaltimer();
+        a.trace[blockIdx.x * 5 + 4] = smid();
+    }
+    for (int i = threadIdx.x; i < 32 * NBANK; i += block) s_acc[i] = 0;
+    if (threadIdx.x == 0) {
+        s_claim = 0u;
+        for (int i = 0; i < NW * S; ++i) mbar_init(&bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_allow_next();
+    __syncthreads();
+
+    constexpr int CD = pair_tiles<MODE, L>() ? L + 2 : L;
+    uint32_t carries[NBANK][CD];
+    uint32_t counter[NBANK][16];
+    uint32_t phase = 0;
+#pragma unroll
+    for (int b = 0; b < NBANK; ++b)
+#pragma unroll
+        for (int j = 0; j < CD; ++j) carries[b][j] = 0;
+    zero_bank<NBANK>(counter);
+    uint32_t nb = 0;
+
+    const unsigned long long S0 = a.g0 * 32;
+    const unsigned long long P = a.nwt - a.pool;
+    const unsigned long long lo = P * blockIdx.x / gridDim.x;
+    const unsigned long long hi = P * (blockIdx.x + 1) / gridDim.x;
+    bool local = true;
+    unsigned long long pw = 0, pe = 0;  // current pool chunk [pw, pe)
+    unsigned long long pm = 0;          // prefetched pool chunk index (lane 0)
+    // Warp-uniform: the next warp tile of this warp, or kEnd.
+    auto claim = [&]() -> unsigned long long {
+        if (local) {
+            const unsigned m = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
+            const unsigned long long w = lo + __shfl_sync(0xFFFFFFFFu, m, 0);
+            if (w < hi) return w;
+            local = false;
+            if (!a.pool) return kEnd;
+            pdl_wait_prev();  // the pool counter is shared with the previous launch
+            pm = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+        }
+        if (pw >= pe) {
+            const unsigned long long c = __shfl_sync(0xFFFFFFFFu, pm, 0);
+            pm = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+            pw = P + c * a.CB;
+            if (pw >= a.nwt) {
+                pe = pw;
+                return kEnd;
+            }
+            pe = pw + a.CB < a.nwt ? pw + a.CB : a.nwt;
+        }
+        return pw++;
+    };
+
+    uint8_t* mine = ring + (size_t)warp * S * TB;
+    unsigned long long* mbar = bar + warp * S;
+    unsigned long long held[S];  // warp-uniform: the tile slot s holds (kEnd: none)
+    bool bulk[S];                // slot s was filled by a bulk copy (else: masked LDG at consume time)
+    // Fills slot s with tile w: one bulk copy of TB bytes (fully valid tile),
+    // or a bare arrive (no data: the end marker, or an edge tile loaded later).
+    auto fill = [&](int s, unsigned long long w) {
+        const unsigned long long t = S0 + w * WT;
+        const bool full = w != kEnd && t >= a.f0 && t + WT <= a.f1;
+        held[s] = w;
+        bulk[s] = full;
+        if (lane == 0) {
+            if (full) {
+                POSPOP_CHECK(t >= a.v0 && t + WT <= a.v1);
+                fence_proxy_async_smem();  // this warp's earlier LDS reads of the slot precede the copy
+                mbar_arrive_expect_tx(&mbar[s], TB);
+                tma_bulk_g2s(mine + (size_t)s * TB, a.base + t * VB, TB, &mbar[s]);
+            } else {
+                mbar_arrive(&mbar[s]);
+            }
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < S; ++s) fill(s, claim());
+    const uint32_t h = (lane >> 2) & 1u;  // 16-byte half read first
+    for (uint32_t use = 0;; ++use) {
+        bool done = false;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (done) break;
+            mbar_wait(&mbar[s], use & 1u);
+            const unsigned long long w = held[s];
+            if (w == kEnd) {
+                done = true;
+                break;
+            }
+            const unsigned long long first = S0 + w * WT + lane;
+            uint32_t r[REGS];
+            if (bulk[s]) {
+                const uint8_t* base = mine + (size_t)s * TB + (size_t)lane * VB;
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        uint32_t* x = r + v * RPV + 4 * q;
+                        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3])
+                                     : "r"(smem_addr(base + (size_t)v * 32 * VB + 16 * (q ^ h)))
+                                     : "memory");
+                    }
+                }
+            } else {
+                load_tree_block<VB, 0, VPT>(a, first, 32u, false, r);
+            }
+            __syncwarp();
+            fill(s, claim());
+            consume<MODE, NBANK, L, VB, false>(a, r, first, 32u, carries, counter, phase);
+            if (++nb == a.flush_threshold) {  // warp-uniform
+                flush_bank_to_smem<NBANK, L, MODE>(counter, s_acc, lane);
+                nb = 0;
+            }
+        }
+        if (done) break;
     }
     cta_finish<NBANK, L, MODE>(a, carries, counter, s_acc, &s_last, block, lane);
 }

@@ -41,6 +41,7 @@ const StreamVariant* stream_variants_counts(size_t* n);  // MODE 0      (variant
 const StreamVariant* stream_variants_flag16(size_t* n);  // MODE 1      (variants_flag1.cu)
 const StreamVariant* stream_variants_flag8(size_t* n);   // MODE 2      (variants_flag2.cu)
 const TmaVariant* tma_variants(size_t* n);                // SCHED 3     (variants_tma.cu)
+const TmaVariant* ring_variants(size_t* n);               // SCHED 6     (variants_ring.cu; nc = warps per CTA)
 const SegVariant* seg_variants(size_t* n);                // segmented   (variants_seg.cu)
 
 }  // namespace pospop_b200

@@ -16,8 +16,9 @@ using namespace dev;
 // (-DPOSPOP_TUNING) adds the alternatives (POSPOP_FLAG_VARIANT).
 const StreamVariant kVariants[] = {
     // byte-frame FLAG statistics (MODE 2): defaults first
-    SVB(5, 32, 512, 2), SVB(5, 32, 0, 2),
+    SVB(5, 32, 0, 2),  // runtime block size (explicit grid / block; the default is the ring kernel, sched 6)
 #ifdef POSPOP_TUNING  // the tuning build: measured alternatives (POSPOP_FLAG_VARIANT)
+    SVB(5, 32, 512, 2),  // the LDG kernel, default until r02
     SVB(5, 32, 256, 2), SVB(4, 32, 512, 2), SVB(4, 32, 256, 2), SVB2(4, 32, 256, 2),
     SVB(4, 16, 512, 2), SVB(6, 32, 256, 2), SVB(5, 16, 512, 2), SVB2(5, 32, 256, 2),
     SVB(4, 32, 512, 4), SVB(4, 16, 512, 4), SVB(3, 32, 512, 4), SVB(4, 32, 256, 4), SVB2(3, 32, 256, 4),
