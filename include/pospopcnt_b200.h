@@ -241,7 +241,9 @@ pospop_status pospopcnt_u16_async(const uint16_t* d_data, size_t len, uint64_t* 
 
 /* Diagnostics: pospopcnt_async with per-CTA %globaltimer timestamps.
  * d_trace (device, >= 5 * trace_ctas u64, trace_ctas >= 32 * SMs) receives,
- * per CTA: {start, main-loop end, CTA channels flushed, exit, SM id};
+ * per CTA: {start, main-loop end, CTA channels flushed, exit, SM id}, then
+ * (the default multi-CTA kernel) per warp, after grid x 5 u64:
+ * {end of the CTA-range phase, end of the pool phase, pool tiles counted};
  * *grid_used is the grid size.  Used by tools/trace.py to measure the
  * launch/ramp/tail/epilogue overheads of the persistent grid. */
 pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint64_t* d_counts,

@@ -1680,6 +1680,7 @@ pospop_status pospopcnt_trace_async(int k, const void* d_data, size_t len, uint6
     // buffer could be too small for the largest persistent grid.
     int sms = 0;
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // 5 stamps per CTA + 3 per warp (SCHED 2): at most 8 + 3 x 32 u64 per CTA of a persistent grid
     if (trace_ctas < (size_t)sms * 32) return fail(POSPOP_EINVAL, "trace buffer needs >= %d CTAs", sms * 32);
     CU(launch_stream(k, len ? d_data : (const void*)d_counts, len, reinterpret_cast<unsigned long long*>(d_counts),
                      false, opt, ws, st, grid_used));

@@ -280,7 +280,10 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
         // Byte-frame banks: stat j of bank b = sum of channels 8i + j.  Written
         // in MODE 1's layout (flag_transform positions, flagstats.cpp:39-49):
         // out[p] all reads, out[16 + p] QC-fail reads.
-        for (int c = threadIdx.x; c < 96; c += block) s_acc[c] = atomicExch(&a.acc[c], 0ull);
+        for (int c = threadIdx.x; c < 96; c += block) {  // see the MODE 0 branch
+            s_acc[c] = __ldcg(&a.acc[c]);
+            __stcg(&a.acc[c], 0ull);
+        }
         __syncthreads();
         for (int pos = threadIdx.x; pos < 32; pos += block) {
             const int f = pos >> 4, p = pos & 15;
@@ -310,13 +313,22 @@ __device__ __forceinline__ void cta_finish(const StreamArgs& a, uint32_t (&carri
         }
     } else {
         const int k = a.k;
+        // Channel totals: one L2 load per channel, all in parallel (the other
+        // CTAs' atomics were fenced before their tickets), then re-zeroed with
+        // plain stores -- the next launch on the stream touches acc only after
+        // griddepcontrol.wait, i.e. after this launch completed.
+        for (int c = threadIdx.x; c < 32 * NBANK; c += block) {
+            s_acc[c] = __ldcg(&a.acc[c]);
+            __stcg(&a.acc[c], 0ull);
+        }
+        __syncthreads();
         for (int pos = threadIdx.x; pos < k; pos += block) {
             unsigned long long sum = 0;
             if (k == 64) {
-                sum = atomicExch(&a.acc[pos], 0ull);
+                sum = s_acc[pos];
             } else {
                 const int m = channels_per_position(k);
-                for (int j = 0; j < m; ++j) sum += atomicExch(&a.acc[pos + j * k], 0ull);
+                for (int j = 0; j < m; ++j) sum += s_acc[pos + j * k];
             }
             if (a.accumulate) sum += a.out[pos];
             a.out[pos] = sum;
@@ -815,6 +827,11 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
             w = lo + __shfl_sync(0xFFFFFFFFu, mine, 0);
             mine = lane == 0 ? atomicAdd(&s_claim, 1u) : 0u;
         }
+        // diagnostics: per-warp end of the CTA-range phase, then of the pool
+        // phase, after the 5 per-CTA stamps (tools/trace.py)
+        unsigned long long* wtrace = a.trace ? a.trace + gridDim.x * 5ull + (blockIdx.x * (block / 32) + (threadIdx.x >> 5)) * 3 : nullptr;
+        if (wtrace && lane == 0) wtrace[0] = globaltimer();
+        unsigned pool_tiles = 0;
         if (a.pool) {
             pdl_wait_prev();  // the pool counter is shared with the previous launch
             unsigned long long m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
@@ -824,6 +841,7 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                 const unsigned long long w0 = P + c * a.CB;
                 if (w0 >= a.nwt) break;  // warp-uniform
                 const unsigned long long w1 = w0 + a.CB < a.nwt ? w0 + a.CB : a.nwt;
+                pool_tiles += (unsigned)(w1 - w0);
                 for (unsigned long long ww = w0; ww < w1; ++ww) {
                     const unsigned long long t = S0 + ww * WT;
                     uint32_t r[REGS];
@@ -837,6 +855,10 @@ __global__ void __launch_bounds__(BLOCK > 0 ? BLOCK : 256, MINB) stream_kernel(c
                 c = __shfl_sync(0xFFFFFFFFu, m, 0);
                 m = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
             }
+        }
+        if (wtrace && lane == 0) {
+            wtrace[1] = globaltimer();
+            wtrace[2] = pool_tiles;
         }
     } else {
         constexpr unsigned long long WT = 32ull * VPT;  // vectors per warp tile

@@ -34,7 +34,7 @@ def main():
     cap = 148 * 64
     trace = torch.zeros(cap * 5, dtype=torch.int64, device="cuda")
     grid = C.c_int(0)
-    variants = [os.environ.get("POSPOP_STREAM_VARIANT", "")] + sys.argv[1:]
+    variants = [os.environ.get("POSPOP_STREAM_VARIANT", "")] + sys.argv[1:]  # (tuning build for variants)
     for var in variants:
         if var:
             os.environ["POSPOP_STREAM_VARIANT"] = var
@@ -52,6 +52,7 @@ def main():
                     continue  # warm-up
                 g = grid.value
                 t = trace[:g * 5].view(g, 5).cpu().tolist()
+                wt = trace[g * 5:g * 5 + g * 8 * 3].view(g * 8, 3).cpu().tolist()
                 t0 = [r[0] for r in t]
                 t1 = [r[1] for r in t]
                 t2 = [r[2] for r in t]
@@ -67,6 +68,11 @@ def main():
                     "loop_end_spread_us": round((max(t1) - min(t1)) / 1e3, 2),
                     "flush_us_max": round(max(b - a for a, b in zip(t1, t2)) / 1e3, 2),
                     "last_cta_us": round((max(t3) - max(t2)) / 1e3, 2),
+                    "warp_range_end_us_min_med_max": [round((f(x[0] for x in wt) - base) / 1e3, 2)
+                                                      for f in (min, lambda v: statistics.median(list(v)), max)],
+                    "warp_pool_end_us_min_med_max": [round((f(x[1] for x in wt) - base) / 1e3, 2)
+                                                     for f in (min, lambda v: statistics.median(list(v)), max)],
+                    "pool_tiles_min_max_sum": [min(x[2] for x in wt), max(x[2] for x in wt), sum(x[2] for x in wt)],
                     "gbs_event": round(nbytes / (e0.elapsed_time(e1) * 1e6), 1),
                     "gbs_span": round(nbytes / (max(t3) - base), 1),
                 }), flush=True)
