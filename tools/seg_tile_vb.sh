@@ -1,5 +1,6 @@
 #!/bin/bash
 # Adaptive segmented kernel: tile-mode depth / load width (measurement tool; tuning build).
+# (The SGAT variants it names were removed after the measurement, profiles/r02_seg_tile_depth_vb.txt.)
 #   bash tools/seg_tile_vb.sh > gpurun_out/seg_tile_vb.txt
 export POSPOP_LIBRARY=tuning
 run() {
