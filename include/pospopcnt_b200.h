@@ -211,7 +211,9 @@ pospop_status pospopcnt_u16_sharded(const uint16_t* const* shards, const size_t*
  * call returns; the asynchronous entry points keep one workspace per
  * (device, stream).  pospop_release_resources() frees every idle context
  * and every per-stream workspace (it synchronises the devices that own
- * per-stream workspaces; contexts leased by calls in flight are kept).  The
+ * per-stream workspaces; contexts leased by calls in flight are kept).  It
+ * must not run concurrently with an asynchronous entry point (whose
+ * workspace it may free); synchronous calls on other threads are safe.  The
  * library stays usable: later calls allocate again. */
 pospop_status pospop_release_resources(void);
 
