@@ -1,9 +1,14 @@
-"""The fused count + device all-reduce over peer memory (paper_1911_02696_b200.exchange):
-two and three ranks (torchrun, gloo for the handle exchange) on one GPU: a
-different seed every step, no host barrier between steps, ranks pushed out of
-step; every step's on-device total must equal the oracle.  The waits are
-bounded and the ranks' contexts time-slice the one GPU, so a wait on a peer
-cannot deadlock; it can only slow the test down."""
+"""The fused count + device all-reduce over peer memory (paper_1911_02696_b200.exchange).
+
+* Two and three ranks (torchrun, gloo for the handle exchange) on one GPU, a
+  different seed every step and more steps than slots; every step's
+  on-device total must equal the oracle.  The ranks share the GPU, so each
+  phase is separated by a host barrier and no kernel waits on a rank that
+  has not finished (B200_PROFILING.md: kernels of different processes that
+  wait on one another raised Xid 109 on this driver).
+* The unsynchronised protocol -- no host synchronisation at all, ranks
+  pushed steps apart -- runs as n blocks of ONE cooperative launch
+  (pospop_exchange_selftest), the safe way to run waiting ranks on one GPU."""
 import os
 import subprocess
 import sys
