@@ -61,6 +61,19 @@ inline void validate(const pospop::PospopcntConfig& config) {
     throw_on(pospop_validate(&c));
 }
 
+/// The reference's fork-join + merge_counts (proj/tests/test_core.cpp:155-175)
+/// in one call: `words` (host memory) is cut into one contiguous range per
+/// entry of `devices`, each streamed over its own device's host link, and the
+/// counts are merged.  A device may be listed more than once.
+inline pospop::PositionalCounts pospopcnt_split(pospop::Word16Span words, const int* devices, int n_devices) {
+    pospop::PositionalCounts out;
+    throw_on(::pospopcnt_split(16, words.data(), words.size(), devices, n_devices, out.counts.data()));
+    return out;
+}
+
+/// Frees the library's idle per-device contexts and per-stream workspaces.
+inline void release_resources() { throw_on(pospop_release_resources()); }
+
 /// A pospop::KernelRunner (verify.hpp:47) that runs the GPU path, for the
 /// reference's own verify_kernels / bench harnesses.
 struct GpuRunner {

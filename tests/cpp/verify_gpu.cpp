@@ -12,7 +12,9 @@
 //   3. the error conventions match (std::invalid_argument,
 //      pospop::KernelUnavailableError);
 //   4. the harness still catches faults with the GPU underneath (the
-//      reference's own fault-injection self-test, test_verify.cpp:42-76).
+//      reference's own fault-injection self-test, test_verify.cpp:42-76);
+//   5. the fork-join over host memory (pospop_gpu::pospopcnt_split) equals
+//      the reference's single call.
 // Exit code 0 = all passed.
 #include <cstdio>
 #include <cstdlib>
@@ -49,6 +51,21 @@ int main(int argc, char** argv) {
     } else {
         std::printf("FAIL drop-in mismatch on 2^24 words\n");
         ++failures;
+    }
+
+    // (1b) the reference's fork-join over host memory (test_core.cpp:155-175),
+    //      one call over several devices' links (device 0 listed 2 and 3 times
+    //      on a one-GPU box), then every resource handed back
+    {
+        const int devs[3] = {0, 0, 0};
+        const std::vector<std::uint16_t> odd(big.begin(), big.end() - 3);  // a length not divisible by 2 or 3
+        const bool ok = pospop_gpu::pospopcnt_split(big, devs, 2) == pospop::pospopcnt(big) &&
+                        pospop_gpu::pospopcnt_split(odd, devs, 3) == pospop::pospopcnt(odd);
+        pospop_gpu::release_resources();
+        const bool again = pospop_gpu::pospopcnt(big) == pospop::pospopcnt(big);  // usable after a release
+        std::printf("%s pospop_gpu::pospopcnt_split (fork-join over devices) == pospop::pospopcnt; release\n",
+                    ok && again ? "PASS" : "FAIL");
+        failures += ok && again ? 0 : 1;
     }
 
     // (3) error conventions (proj/tests/test_core.cpp:184-201)
