@@ -60,6 +60,15 @@ def test_sass_uses_lop3_csa_and_256bit_loads(pp):
     assert "LDG.E.NA.ENL2.256.CONSTANT" in sass, funs
 
 
+def test_sass_flag_ring_kernel_uses_bulk_copies_and_mbarriers(pp):
+    """The default FLAG kernel, stream_ring_kernel<3,5,2,16,1>:
+    per-warp cp.async.bulk (UBLKCP) into shared memory completing on mbarriers
+    (SYNCS.*), swizzled LDS.128 reads, PRMT byte regrouping and LOP3 CSAs."""
+    funs, sass = _kernel_sass(pp, r"stream_ring_kernelILi3ELi5ELi2ELi16ELi1E")
+    for op in ("UBLKCP", "SYNCS.ARRIVE.TRANS64", "SYNCS.PHASECHK.TRANS64", "LDS.128", "PRMT", "LOP3.LUT"):
+        assert op in sass, (op, funs)
+
+
 def _entries(path):
     out = subprocess.run(["cuobjdump", "-symbols", path], capture_output=True, text=True).stdout
     return sorted(set(re.findall(r"STO_ENTRY\s+(\S+)", out)))
