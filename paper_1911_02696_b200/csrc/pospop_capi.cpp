@@ -1378,11 +1378,11 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
     for (int i = 0; i < n_shards; ++i) {
         if (on_device[(size_t)i] || !lens[i]) continue;
         host_out[(size_t)i].assign((size_t)k, 0);
-        workers.emplace_back([&, i] {
+        auto work = [&, i](bool own_thread) {
             const int d = devices[i];
             pospop_status ws = cuda_set_device(d);
             if (!ws) {
-                bind_to_device_cpus(d);
+                if (own_thread) bind_to_device_cpus(d);
                 CtxScope wscope;
                 Ctx* c = nullptr;
                 if (!(ws = wscope.get(d, &c)))
@@ -1391,7 +1391,13 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
             }
             host_st[(size_t)i] = ws;
             if (ws) host_err[(size_t)i] = t_err;
-        });
+        };
+        try {
+            workers.emplace_back(work, true);
+        } catch (const std::exception&) {  // no thread available: count this shard on the calling thread
+            work(false);
+            cudaSetDevice(dev0);
+        }
     }
     for (auto& t : workers) t.join();
     for (int p = 0; p < k; ++p) counts[p] = 0;
