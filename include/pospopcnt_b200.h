@@ -25,8 +25,9 @@
  *  - data may be DEVICE memory (the fast path: counted in place in HBM) or
  *    HOST memory (pinned or pageable: streamed to the GPU in chunks with
  *    copy/compute overlap).  The classification uses cudaPointerGetAttributes.
- *  - Every call is synchronous, thread-safe and re-entrant (per-thread,
- *    per-device workspaces and streams), like the reference.
+ *  - Every call is synchronous, thread-safe and re-entrant (each call leases
+ *    its own per-device streams and workspace from a bounded pool; see
+ *    "resources" below), like the reference.
  *    Synchronous calls on device memory are ordered after prior work on the
  *    legacy default stream; data produced on another (non-blocking) stream
  *    must be synchronised by the caller, or counted with pospopcnt_async on
