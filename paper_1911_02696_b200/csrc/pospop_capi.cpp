@@ -194,7 +194,8 @@ struct DeviceGuard {
 // closest B200 equivalent.)
 // ---------------------------------------------------------------------------
 constexpr int kRing = 3;
-constexpr size_t kBounceBytes = 1 << 20;  // host inputs up to this size take the single-stream path
+constexpr size_t kBounceBytes = 1 << 20;  // pageable host inputs up to this size: pinned bounce copy, zero-copy kernel
+constexpr size_t kZeroCopyBytes = 2 << 20;  // pinned host inputs up to this size: read in place by the kernel
 constexpr int kHostRing = 4;              // pinned host slots for pageable / file input
 constexpr size_t kHostChunk = 16 << 20;   // bytes per pinned host slot
 constexpr int kMaxCtxPerDevice = 8;       // concurrent calls per device beyond this wait for a context
@@ -670,10 +671,13 @@ bool alloc_range(const void* p, const void** base, size_t* bytes) {
 // ---------------------------------------------------------------------------
 enum class Where { Device, Host };
 
-Where classify(const void* p, int* dev, bool* pinned = nullptr) {
+// mapped: for pinned host memory, its device-accessible address (UVA), or
+// NULL when the allocation is not mapped.
+Where classify(const void* p, int* dev, bool* pinned = nullptr, const void** mapped = nullptr) {
     cudaPointerAttributes a;
     std::memset(&a, 0, sizeof a);
     if (pinned) *pinned = false;
+    if (mapped) *mapped = nullptr;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
         return Where::Host;
@@ -683,6 +687,7 @@ Where classify(const void* p, int* dev, bool* pinned = nullptr) {
         return Where::Device;
     }
     if (pinned) *pinned = a.type == cudaMemoryTypeHost;
+    if (mapped && a.type == cudaMemoryTypeHost) *mapped = a.devicePointer;
     return Where::Host;
 }
 
@@ -727,19 +732,30 @@ pospop_status count_on_ctx(Ctx* c, int k, const void* data, size_t len, bool on_
     opt.flush_threshold = flush;
     if (on_device) {
         CU(launch_stream(k, data, len, c->m_out_dev, false, opt, c->ws, c->stream));
-    } else if (len * wb <= kBounceBytes) {
-        // Small host input (the latency path): one DMA (from
-        // the caller's pinned memory, or via a pinned bounce buffer for
-        // pageable memory) + one launch + one D2H, all on one stream.
-        if ((s = ensure_stage(c))) return s;
+    } else if (len * wb <= (pinned ? kZeroCopyBytes : kBounceBytes)) {
+        // Small host input (the latency path): the kernel
+        // reads the caller's pinned memory -- or a pinned bounce copy of
+        // pageable memory -- in place over the host link (zero-copy through
+        // UVA): no DMA, no device staging, one launch on one stream, the
+        // result written by the last CTA into mapped memory.  Above
+        // kZeroCopyBytes the copy engine's larger transfers win
+        // (tools/zero_copy_probe.py).
         const void* src = data;
+        const void* dsrc = nullptr;
+        int hd = c->dev;
         if (!pinned) {
             if (!c->bounce) CU(cudaMallocHost(&c->bounce, kBounceBytes));
             std::memcpy(c->bounce, data, len * wb);
             src = c->bounce;
         }
-        CU(cudaMemcpyAsync(c->stage[0], src, len * wb, cudaMemcpyHostToDevice, c->stream));
-        CU(launch_stream(k, c->stage[0], len, c->m_out_dev, false, opt, c->ws, c->stream));
+        classify(src, &hd, nullptr, &dsrc);
+        if (dsrc) {
+            CU(launch_stream(k, dsrc, len, c->m_out_dev, false, opt, c->ws, c->stream));
+        } else {  // pinned but not mapped: one DMA into the staging buffer
+            if ((s = ensure_stage(c))) return s;
+            CU(cudaMemcpyAsync(c->stage[0], src, len * wb, cudaMemcpyHostToDevice, c->stream));
+            CU(launch_stream(k, c->stage[0], len, c->m_out_dev, false, opt, c->ws, c->stream));
+        }
     } else if (!pinned) {
         // Pageable host input: parallel memcpy into the pinned host ring
         // overlapping the H2D of the previous slot and the kernel before it.
