@@ -152,3 +152,25 @@ def test_release_stream(pp, dev):
     pp.release_stream(s)
     assert pp.resource_stats(0)["stream_workspaces"] == before
     assert out.cpu()[0].item() == 1 << 20
+
+
+def test_small_host_calls_read_in_place(pp, dev, orc):
+    """Pinned host inputs up to 2 MiB and pageable ones up to 1 MiB are read
+    in place by the kernel (zero-copy): bit-exact, and no device staging ring
+    (3 x 64 MiB) is allocated for them; a larger input still uses it."""
+    rng = np.random.default_rng(11)
+    pageable = rng.integers(0, 1 << 16, size=(1 << 19) - 3, dtype=np.uint16)  # < 1 MiB
+    keep, pinned = pinned_copy(rng.integers(0, 1 << 16, size=(1 << 20) - 5, dtype=np.uint16))  # < 2 MiB
+    pp.release_resources()
+    base = _free_bytes()
+    for k in (8, 16, 32, 64):
+        for words in (pageable, pinned):
+            raw = words.view(np.uint8)
+            n = raw.size // (k // 8) * (k // 8)
+            assert pp.pospopcnt_k(raw[:n], k) == orc.pospopcnt(raw[:n], k, threads=4), k
+    held = base - _free_bytes()
+    assert held < (64 << 20), held  # contexts and workspaces only, no staging ring
+    big = rng.integers(0, 1 << 16, size=(8 << 20) // 2, dtype=np.uint16)  # 8 MiB pageable: staged
+    assert pp.pospopcnt_k(big, 16) == orc.pospopcnt(big, 16, threads=4)
+    assert base - _free_bytes() >= (3 * 64 << 20), base - _free_bytes()
+    pp.release_resources()
