@@ -186,8 +186,10 @@ struct DeviceGuard {
 // Per-call device context: compute + copy streams, result buffers, the
 // stream workspace, and (lazily) the host-staging ring.  Contexts are leased
 // from a per-device pool for the duration of one call (CtxScope), so
-// resources are bounded per device -- at most kMaxCtxPerDevice contexts --
-// whatever the number of calling threads, and nothing is tied to a thread.
+// resources are bounded per device -- at most kMaxCtxPerDevice contexts for
+// the calls in flight (plus one per host shard of a pospopcnt_sharded call
+// in flight) -- whatever the number of calling threads, and nothing is tied
+// to a thread.
 // pospop_release_resources() frees the idle ones.  (The reference keeps all
 // per-call state on the stack, proj/core/src/detail/csa_engine.hpp:107-110;
 // device allocation per call would synchronise the device, so the pool is the
@@ -432,13 +434,28 @@ class CtxScope {
     ~CtxScope() {
         if (held_.empty()) return;
         CtxPool& pool = CtxPool::get();
+        std::vector<std::pair<int, Ctx*>> surplus;  // above the bound (unbounded worker leases): freed
         {
             std::lock_guard<std::mutex> lk(pool.mu);
-            for (auto& h : held_) pool.idle[h.first].push_back(h.second);
+            for (auto& h : held_) {
+                if (pool.live[h.first] > kMaxCtxPerDevice) {
+                    --pool.live[h.first];
+                    surplus.push_back(h);
+                } else {
+                    pool.idle[h.first].push_back(h.second);
+                }
+            }
         }
         pool.cv.notify_all();
+        for (auto& h : surplus) {
+            DeviceGuard g(h.first);
+            destroy_ctx(h.second);
+        }
     }
-    pospop_status get(int dev, Ctx** out) {
+    // bounded = false: never wait for the per-device bound (the host-shard
+    // workers of a call whose caller already holds contexts: waiting there
+    // could deadlock against other callers doing the same).
+    pospop_status get(int dev, Ctx** out, bool bounded = true) {
         for (auto& h : held_)
             if (h.first == dev) {
                 *out = h.second;
@@ -450,7 +467,8 @@ class CtxScope {
         Ctx* c = nullptr;
         {
             std::unique_lock<std::mutex> lk(pool.mu);
-            pool.cv.wait(lk, [&] { return !pool.idle[dev].empty() || pool.live[dev] < kMaxCtxPerDevice; });
+            if (bounded)
+                pool.cv.wait(lk, [&] { return !pool.idle[dev].empty() || pool.live[dev] < kMaxCtxPerDevice; });
             if (!pool.idle[dev].empty()) {
                 c = pool.idle[dev].back();
                 pool.idle[dev].pop_back();
@@ -1401,7 +1419,7 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
                 if (own_thread) bind_to_device_cpus(d);
                 CtxScope wscope;
                 Ctx* c = nullptr;
-                if (!(ws = wscope.get(d, &c)))
+                if (!(ws = wscope.get(d, &c, false)))
                     ws = count_on_ctx(c, k, shards[i], lens[i], false, pinned[(size_t)i] != 0, 65535,
                                       host_out[(size_t)i].data());
             }

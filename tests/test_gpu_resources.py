@@ -174,3 +174,19 @@ def test_small_host_calls_read_in_place(pp, dev, orc):
     assert pp.pospopcnt_k(big, 16) == orc.pospopcnt(big, 16, threads=4)
     assert base - _free_bytes() >= (3 * 64 << 20), base - _free_bytes()
     pp.release_resources()
+
+
+def test_more_host_shards_than_the_context_bound(pp, dev, orc):
+    """12 host shards and a device shard on one device: the host-shard workers
+    may exceed the per-device bound of 8 contexts for the call (waiting there
+    could deadlock against other callers), and the surplus is freed when the
+    call returns."""
+    rng = np.random.default_rng(12)
+    words = rng.integers(0, 1 << 16, size=(12 << 20) + 7, dtype=np.uint16)
+    want = orc.pospopcnt(words, 16, threads=8)
+    cuts = np.linspace(0, words.size, 14).astype(np.int64)
+    shards = [words[cuts[i]:cuts[i + 1]] for i in range(12)]
+    shards.append(torch.from_numpy(words[cuts[12]:].view(np.int16).copy()).cuda())
+    assert pp.pospopcnt_sharded(shards, [0] * 13) == want
+    st = pp.resource_stats(0)
+    assert st["contexts"] <= 8 and st["idle_contexts"] == st["contexts"], st
