@@ -1160,8 +1160,20 @@ pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_su
     Ctx* c = nullptr;
     if ((s = scope.get(dev, &c))) return s;
     LaunchOptions opt;
-    if (where == Where::Device) {
-        CU(launch_flagstats(flags, len, c->m_out_dev, false, opt, c->ws, c->stream));
+    const void* mapped = nullptr;  // small host input read in place (zero-copy), as in count_on_ctx
+    if (where == Where::Host && len * 2 <= (pinned ? kZeroCopyBytes : kBounceBytes)) {
+        const void* src = flags;
+        if (!pinned) {
+            if (!c->bounce) CU(cudaMallocHost(&c->bounce, kBounceBytes));
+            std::memcpy(c->bounce, flags, len * 2);
+            src = c->bounce;
+        }
+        int hd = dev;
+        classify(src, &hd, nullptr, &mapped);
+    }
+    if (where == Where::Device || mapped) {
+        CU(launch_flagstats(mapped ? static_cast<const uint16_t*>(mapped) : flags, len, c->m_out_dev, false, opt,
+                            c->ws, c->stream));
     } else if (!pinned) {  // pageable: parallel copies into the pinned host ring
         const uint8_t* src = reinterpret_cast<const uint8_t*>(flags);
         s = host_ring_pipeline(

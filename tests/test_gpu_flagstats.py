@@ -163,3 +163,26 @@ def test_flagmix_generator_matches_oracle(pp, dev, orc):
     d = torch.empty(n, dtype=torch.int16, device="cuda")
     pp.generate(pp.GEN_FLAGMIX, 11, d, base=12345)
     assert (d.cpu().numpy().view(np.uint16) == orc.generate(8, 11, n, base=12345)).all()
+
+
+def test_small_host_inputs_read_in_place(pp, dev, orc):
+    """Pinned FLAG words up to 2 MiB and pageable ones up to 1 MiB are read
+    in place by the ring kernel (cp.async.bulk from mapped host memory):
+    summaries and the first invalid word's offset as the reference."""
+    w = orc.generate(7, 9, (1 << 20) - 3)  # just under 2 MiB
+    t = torch.empty(w.nbytes + 64, dtype=torch.uint8, pin_memory=True)
+    for off in (0, 2, 6, 34):
+        pv = t.numpy()[off:off + w.nbytes].view(np.uint16)
+        pv[:] = w
+        rc, want, _ = orc.flagstats(w)
+        assert pp.flagstats(pv).as_list() == list(want), off
+        small = w[: (1 << 18) + 1]  # pageable, < 1 MiB
+        rc, want_s, _ = orc.flagstats(small)
+        assert pp.flagstats(small.copy()).as_list() == list(want_s), off
+    pv = t.numpy()[2:2 + w.nbytes].view(np.uint16)
+    pv[:] = w
+    pv[777777] |= 0x4000
+    pv[4099] |= 0x1000
+    with pytest.raises(pp.InvalidFlagWordError) as e:
+        pp.flagstats(pv)
+    assert e.value.offset == 4099 and e.value.word == int(pv[4099])
