@@ -16,6 +16,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+if len(sys.argv) > 1 or os.environ.get("POSPOP_STREAM_VARIANT"):
+    os.environ.setdefault("POSPOP_LIBRARY", "tuning")  # variant strings: the tuning build
 import torch  # noqa: E402
 
 import paper_1911_02696_b200 as pp  # noqa: E402
@@ -34,7 +36,7 @@ def main():
     cap = 148 * 64
     trace = torch.zeros(cap * 5, dtype=torch.int64, device="cuda")
     grid = C.c_int(0)
-    variants = [os.environ.get("POSPOP_STREAM_VARIANT", "")] + sys.argv[1:]  # (tuning build for variants)
+    variants = [os.environ.get("POSPOP_STREAM_VARIANT", "")] + sys.argv[1:]
     for var in variants:
         if var:
             os.environ["POSPOP_STREAM_VARIANT"] = var
