@@ -190,3 +190,16 @@ def test_more_host_shards_than_the_context_bound(pp, dev, orc):
     assert pp.pospopcnt_sharded(shards, [0] * 13) == want
     st = pp.resource_stats(0)
     assert st["contexts"] <= 8 and st["idle_contexts"] == st["contexts"], st
+
+
+def test_split_device_resident_data(pp, dev, orc):
+    """pospopcnt_split on device memory: every range is a device shard on the
+    device holding it, counted in place."""
+    rng = np.random.default_rng(13)
+    host = rng.integers(0, 1 << 16, size=(5 << 20) + 3, dtype=np.uint16)
+    d = torch.from_numpy(host.view(np.int16)).cuda()
+    want = orc.pospopcnt(host, 16, threads=8)
+    for n in (1, 2, 3, 7):
+        assert pp.pospopcnt_split(d, [0] * n, 16) == want, n
+    with pytest.raises(pp.InvalidArgument):
+        pp.pospopcnt_split(d, [torch.cuda.device_count()], 16)
