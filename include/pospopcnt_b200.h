@@ -199,6 +199,17 @@ pospop_status pospopcnt_sharded(int k, const void* const* shards, const size_t* 
 pospop_status pospopcnt_split(int k, const void* data, size_t len, const int* devices, int n_devices,
                               uint64_t* counts);
 
+/* Segmented fork-join over devices in one call (the batched
+ * variant shards by arrays, no exchange): arrays are cut into n_devices
+ * contiguous groups of about equal bytes, group i is counted on devices[i]
+ * -- host data streamed over that device's own link by a worker bound to its
+ * local CPUs -- and its rows land in counts[a * k ...] as with
+ * pospopcnt_segmented.  data, offsets and counts in host memory; operands in
+ * device memory are accepted when every listed device is the one holding
+ * them (then one device counts them all). */
+pospop_status pospopcnt_segmented_split(int k, const void* data, const uint64_t* offsets, size_t n,
+                                        const int* devices, int n_devices, uint64_t* counts);
+
 /* The 16-bit form (BASELINE cfg4): pospopcnt_sharded with k = 16. */
 pospop_status pospopcnt_u16_sharded(const uint16_t* const* shards, const size_t* lens, const int* devices,
                                     int n_devices, uint64_t counts[16]);

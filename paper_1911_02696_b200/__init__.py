@@ -40,7 +40,7 @@ import numpy as np
 __all__ = [
     "KernelKind", "PospopcntConfig", "PositionalCounts", "InvalidArgument", "KernelUnavailableError",
     "CudaError", "validate", "merge_counts", "pospopcnt", "pospopcnt_k", "pospopcnt_u16_c32",
-    "pospopcnt_segmented", "pospopcnt_sharded", "pospopcnt_split", "release_resources", "release_stream",
+    "pospopcnt_segmented", "pospopcnt_segmented_split", "pospopcnt_sharded", "pospopcnt_split", "release_resources", "release_stream",
     "resource_stats", "count_async", "segmented_async", "count_allgather_async",
     "exchange_bytes", "exchange_reduce_async", "exchange_status",
     "ipc_alloc", "ipc_open", "ipc_close", "ipc_free", "generate", "digest",
@@ -175,6 +175,7 @@ def load_library(path: str):
         "pospop_exchange_reduce_async": ([C.c_int, vp, C.c_int, C.c_uint64, C.c_int, vp, vp], C.c_int),
         "pospop_exchange_status": ([vp, _u64p, _u64p], C.c_int),
         "pospopcnt_split": ([C.c_int, vp, sz, C.POINTER(C.c_int), C.c_int, _u64p], C.c_int),
+        "pospopcnt_segmented_split": ([C.c_int, vp, vp, sz, C.POINTER(C.c_int), C.c_int, vp], C.c_int),
         "pospop_release_resources": ([], C.c_int),
         "pospop_release_stream": ([vp], C.c_int),
         "pospop_resource_stats": ([C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
@@ -412,6 +413,22 @@ def pospopcnt_segmented(data: Any, offsets: Any, k: int, out: Any = None) -> Any
     out_addr = _rows_addr(out, n, k)
     if n > 0:
         _check(_load().pospopcnt_segmented(int(k), addr or None, off_addr, n, out_addr))
+    return out
+
+
+def pospopcnt_segmented_split(data: Any, offsets: Any, k: int, devices: Sequence[int], out: Any = None) -> Any:
+    """pospopcnt_segmented with the arrays cut into len(devices) contiguous
+    groups of about equal bytes, group i counted on devices[i] (host data over
+    each device's own link).  Returns (n_arrays, k) uint64."""
+    addr, _ = _addr_len(data, k)
+    if isinstance(offsets, np.ndarray) and offsets.dtype != np.uint64 and offsets.dtype.kind in "iu":
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+    off_addr, n = _offsets_addr(offsets)
+    if out is None:
+        out = np.zeros((n, k), np.uint64)
+    out_addr = _rows_addr(out, n, k)
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    _check(_load().pospopcnt_segmented_split(int(k), addr or None, off_addr, n, devs, len(devices), out_addr))
     return out
 
 

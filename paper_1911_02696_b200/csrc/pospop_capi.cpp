@@ -1057,6 +1057,9 @@ pospop_status pospopcnt_u16_c32(const uint16_t* data, uint32_t len, uint32_t cou
     return POSPOP_OK;
 }
 
+pospop_status segmented_on_ctx(Ctx* c, int k, const void* data, bool d_dev, const uint64_t* offsets, bool o_dev,
+                               size_t n, uint64_t* counts, bool c_dev);
+
 pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offsets, size_t n,
                                   uint64_t* counts) {
     if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
@@ -1076,7 +1079,17 @@ pospop_status pospopcnt_segmented(int k, const void* data, const uint64_t* offse
     CtxScope scope;
     Ctx* c = nullptr;
     if ((s = scope.get(dev, &c))) return s;
+    return segmented_on_ctx(c, k, data, d_dev, offsets, o_dev, n, counts, c_dev);
+}
 
+// The segmented call on context c's device (current): data in device memory
+// on that device (d_dev) or host memory; offsets / counts in device memory
+// (o_dev / c_dev) or host memory.
+pospop_status segmented_on_ctx(Ctx* c, int k, const void* data, bool d_dev, const uint64_t* offsets, bool o_dev,
+                               size_t n, uint64_t* counts, bool c_dev) {
+    pospop_status s;
+    const size_t wb = (size_t)k / 8;
+    const int dev = c->dev;
     // Host offsets are needed on the host for validation and sizing anyway.
     std::vector<uint64_t> h_off;
     const uint64_t* hoff = offsets;
@@ -1141,6 +1154,82 @@ pospop_status pospopcnt_u32_segmented(const uint32_t* data, const uint64_t* offs
 }
 pospop_status pospopcnt_u64_segmented(const uint64_t* data, const uint64_t* offsets, size_t n, uint64_t* counts) {
     return pospopcnt_segmented(64, data, offsets, n, counts);
+}
+
+pospop_status pospopcnt_segmented_split(int k, const void* data, const uint64_t* offsets, size_t n,
+                                        const int* devices, int n_devices, uint64_t* counts) {
+    if (!valid_k(k)) return fail(POSPOP_EINVAL, "k must be 8, 16, 32 or 64, got %d", k);
+    if (n_devices < 1 || !devices) return fail(POSPOP_EINVAL, "need >= 1 device");
+    if (n == 0) return POSPOP_OK;
+    if (!offsets || !counts) return fail(POSPOP_EINVAL, "offsets/counts must not be NULL");
+    const size_t wb = (size_t)k / 8;
+    if ((uintptr_t)data % wb) return fail(POSPOP_EINVAL, "data is not aligned to the %d-bit word size", k);
+    int dev0 = 0;
+    pospop_status s = current_device(&dev0);
+    if (s) return s;
+    int n_dev = 0;
+    CU(cudaGetDeviceCount(&n_dev));
+    for (int i = 0; i < n_devices; ++i) {
+        if (devices[i] < 0 || devices[i] >= n_dev)
+            return fail(POSPOP_EINVAL, "no device %d (%d visible)", devices[i], n_dev);
+        if ((s = check_device(devices[i]))) return s;
+    }
+    int ddev = dev0, odev = dev0, cdev = dev0;
+    const bool d_dev = data && classify(data, &ddev) == Where::Device;
+    const bool o_dev = classify(offsets, &odev) == Where::Device;
+    const bool c_dev = classify(counts, &cdev) == Where::Device;
+    if (d_dev || o_dev || c_dev) {  // device-resident operands: one device holds them all
+        const int home = d_dev ? ddev : o_dev ? odev : cdev;
+        for (int i = 0; i < n_devices; ++i)
+            if (devices[i] != home)
+                return fail(POSPOP_EINVAL, "device-resident operands live on device %d; listed device %d", home,
+                            devices[i]);
+        return pospopcnt_segmented(k, data, offsets, n, counts);
+    }
+    for (size_t a = 0; a < n; ++a)
+        if (offsets[a + 1] < offsets[a]) return fail(POSPOP_EINVAL, "offsets must be non-decreasing (array %zu)", a);
+    // Contiguous groups of arrays with about equal bytes (each at least one
+    // array when there are enough), one per listed device.
+    std::vector<size_t> cut((size_t)n_devices + 1, n);
+    cut[0] = 0;
+    const uint64_t w0 = offsets[0], wn = offsets[n];
+    for (int i = 1; i < n_devices; ++i) {
+        const uint64_t target = w0 + (wn - w0) * (uint64_t)i / (uint64_t)n_devices;
+        size_t a = (size_t)(std::lower_bound(offsets, offsets + n + 1, target) - offsets);
+        a = std::max(a, cut[(size_t)i - 1]);
+        cut[(size_t)i] = std::min(a, n);
+    }
+    std::vector<pospop_status> st((size_t)n_devices, POSPOP_OK);
+    std::vector<std::string> err((size_t)n_devices);
+    std::vector<std::thread> workers;
+    for (int i = 0; i < n_devices; ++i) {
+        const size_t a0 = cut[(size_t)i], a1 = cut[(size_t)i + 1];
+        if (a1 <= a0) continue;
+        auto work = [&, i, a0, a1](bool own_thread) {
+            const int d = devices[i];
+            pospop_status ws = cuda_set_device(d);
+            if (!ws) {
+                if (own_thread) bind_to_device_cpus(d);
+                CtxScope wscope;
+                Ctx* c = nullptr;
+                if (!(ws = wscope.get(d, &c, false)))
+                    ws = segmented_on_ctx(c, k, data, false, offsets + a0, false, a1 - a0, counts + a0 * (size_t)k,
+                                          false);
+            }
+            st[(size_t)i] = ws;
+            if (ws) err[(size_t)i] = t_err;
+        };
+        try {
+            workers.emplace_back(work, true);
+        } catch (const std::exception&) {
+            work(false);
+            cudaSetDevice(dev0);
+        }
+    }
+    for (auto& t : workers) t.join();
+    for (int i = 0; i < n_devices; ++i)
+        if (st[(size_t)i]) return fail(st[(size_t)i], "device group %d: %s", i, err[(size_t)i].c_str());
+    return POSPOP_OK;
 }
 
 pospop_status pospop_flagstats(const uint16_t* flags, size_t len, pospop_flag_summary* out, uint64_t* bad_offset,

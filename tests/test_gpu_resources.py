@@ -203,3 +203,25 @@ def test_split_device_resident_data(pp, dev, orc):
         assert pp.pospopcnt_split(d, [0] * n, 16) == want, n
     with pytest.raises(pp.InvalidArgument):
         pp.pospopcnt_split(d, [torch.cuda.device_count()], 16)
+
+
+@pytest.mark.parametrize("k", [8, 32, 64])
+def test_segmented_split_over_devices(pp, dev, orc, k):
+    """Segmented fork-join over devices [0, 0, 0] from host memory (the
+    batched variant shards by arrays, no exchange): ragged arrays, empty
+    ones, one long array, pageable and pinned data; rows equal the oracle."""
+    rng = np.random.default_rng(20 + k)
+    wb = k // 8
+    lens = rng.integers(0, 5000, size=3000)
+    lens[[7, 1500]] = [0, 3_000_000 // wb]
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    raw = rng.integers(0, 256, size=int(offs[-1]) * wb + 16, dtype=np.uint8)
+    words = raw[: int(offs[-1]) * wb]
+    want = orc.segmented(words, offs, k, threads=8)
+    for devs in ([0], [0, 0], [0, 0, 0], [0] * 5):
+        got = pp.pospopcnt_segmented_split(words, offs, k, devs)
+        assert (np.asarray(got, np.uint64) == want).all(), devs
+    keep, pinned = pinned_copy(words)
+    assert (np.asarray(pp.pospopcnt_segmented_split(pinned, offs, k, [0, 0]), np.uint64) == want).all()
+    d = torch.from_numpy(words.copy()).cuda()  # device-resident: one device counts it all
+    assert (np.asarray(pp.pospopcnt_segmented_split(d, offs, k, [0, 0]), np.uint64) == want).all()
