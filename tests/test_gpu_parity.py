@@ -785,3 +785,23 @@ def test_segmented_range_mode_misaligned_data(pp, dev, orc, k, mode, monkeypatch
             if rep == 0:  # synchronous entry point: device data, host offsets; then pageable host data
                 assert (pp.pospopcnt_segmented(d, offs, k) == want).all(), (k, shift)
                 assert (pp.pospopcnt_segmented(words, offs, k) == want).all(), (k, shift, "host")
+
+
+def test_counts_beyond_2_pow_32_words(pp, dev, orc):
+    """size_t lengths past 2^32 words (16 GiB of u16, 2^31 + u64 words): the
+    reference's uint32_t-length Fig. 6 API could not express these
+    (PAPER.md:316); the stream kernel, the sharded path and the segmented
+    range kernel (one array spanning every range) all agree with the oracle."""
+    n = (1 << 33) + 3
+    d = torch.empty(n, dtype=torch.int16, device="cuda")
+    pp.generate(pp.GEN_CFG4, 5, d)
+    host = d.cpu().numpy().view(np.uint16)
+    want16 = orc.pospopcnt(host, 16, threads=16)
+    assert pp.pospopcnt(d) == want16
+    assert pp.pospopcnt_sharded([d[: n // 3], d[n // 3:]], [0, 0]) == want16
+    want64 = orc.pospopcnt(host.view(np.uint8)[: (n * 2) // 8 * 8], 64, threads=16)
+    assert pp.pospopcnt_k((d.data_ptr(), (n * 2) // 8), 64) == want64
+    offs = torch.tensor([0, 1, n - 1, n], dtype=torch.int64, device="cuda")  # one array over 2^33 words
+    rows = pp.pospopcnt_segmented(d, offs, 16)
+    want_rows = orc.segmented(host, np.array([0, 1, n - 1, n], np.uint64), 16, threads=16)
+    assert (np.asarray(rows, np.uint64) == want_rows).all()
