@@ -14,7 +14,9 @@
 //   4. the harness still catches faults with the GPU underneath (the
 //      reference's own fault-injection self-test, test_verify.cpp:42-76);
 //   5. the fork-join over host memory (pospop_gpu::pospopcnt_split) equals
-//      the reference's single call.
+//      the reference's single call;
+//   6. pospop_gpu::flagstats_pospopcnt (include/pospop_gpu_flagstats.hpp) is
+//      a drop-in for pospop::flagstats_pospopcnt, exception included.
 // Exit code 0 = all passed.
 #include <cstdio>
 #include <cstdlib>
@@ -23,9 +25,11 @@
 #include <vector>
 
 #include "pospop/bench.hpp"
+#include "pospop/flagstats.hpp"
 #include "pospop/pospop.hpp"
 #include "pospop/verify.hpp"
 #include "pospop_gpu.hpp"
+#include "pospop_gpu_flagstats.hpp"
 
 int main(int argc, char** argv) {
     const std::size_t max_len = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 3000;
@@ -66,6 +70,27 @@ int main(int argc, char** argv) {
         std::printf("%s pospop_gpu::pospopcnt_split (fork-join over devices) == pospop::pospopcnt; release\n",
                     ok && again ? "PASS" : "FAIL");
         failures += ok && again ? 0 : 1;
+    }
+
+    // (1c) FLAG statistics: pospop_gpu::flagstats_pospopcnt against the
+    //      reference's flagstats_reference and flagstats_pospopcnt, and the
+    //      first-invalid-word exception (flagstats.cpp:34-36)
+    {
+        std::vector<std::uint16_t> flags(big.size());
+        for (std::size_t i = 0; i < flags.size(); ++i) flags[i] = big[i] & 0x0FFF;  // valid words
+        const pospop::FlagSummary want = pospop::flagstats_reference(flags);
+        bool ok = pospop_gpu::flagstats_pospopcnt(flags) == want && pospop::flagstats_pospopcnt(flags) == want;
+        flags[777] |= 0x2000;
+        flags[123456] |= 0x8000;
+        try {
+            pospop_gpu::flagstats_pospopcnt(flags);
+            ok = false;
+        } catch (const pospop::InvalidFlagWordError& e) {
+            ok = ok && e.offset() == 777 && e.word() == flags[777];
+        }
+        std::printf("%s pospop_gpu::flagstats_pospopcnt == pospop::flagstats_reference; InvalidFlagWordError(777)\n",
+                    ok ? "PASS" : "FAIL");
+        failures += ok ? 0 : 1;
     }
 
     // (3) error conventions (proj/tests/test_core.cpp:184-201)

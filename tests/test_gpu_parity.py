@@ -388,7 +388,7 @@ def test_reference_verify_kernels_with_gpu_runner():
     r = subprocess.run([exe, "3000"], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 7 and "FAIL" not in r.stdout
+    assert r.stdout.count("PASS") == 8 and "FAIL" not in r.stdout
 
 
 _GROUPED = ["6,16,5,8", "6,16,5,4", "5,16,5,8", "6,32,5,8", "5,32,5,8", "5,16,5,4", "6,16,5,16", "5,32,5,4",
