@@ -225,3 +225,39 @@ def test_segmented_split_over_devices(pp, dev, orc, k):
     assert (np.asarray(pp.pospopcnt_segmented_split(pinned, offs, k, [0, 0]), np.uint64) == want).all()
     d = torch.from_numpy(words.copy()).cuda()  # device-resident: one device counts it all
     assert (np.asarray(pp.pospopcnt_segmented_split(d, offs, k, [0, 0]), np.uint64) == want).all()
+
+
+def test_concurrent_splits_and_releases(pp, dev, orc):
+    """Four threads running host-memory splits over [0, 0] while a fifth keeps
+    calling pospop_release_resources (safe against synchronous calls): every
+    result exact, nothing leaked afterwards."""
+    rng = np.random.default_rng(14)
+    inputs = [rng.integers(0, 1 << 16, size=(3 << 20) + i, dtype=np.uint16) for i in range(4)]
+    wants = [orc.pospopcnt(x, 16, threads=4) for x in inputs]
+    errors, stop = [], threading.Event()
+
+    def worker(i):
+        try:
+            torch.cuda.set_device(0)
+            for _ in range(6):
+                assert pp.pospopcnt_split(inputs[i], [0, 0], 16) == wants[i]
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    def releaser():
+        torch.cuda.set_device(0)
+        while not stop.is_set():
+            pp.release_resources()
+
+    r = threading.Thread(target=releaser)
+    r.start()
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    stop.set()
+    r.join()
+    assert not errors, errors[:3]
+    pp.release_resources()
+    assert pp.resource_stats(0)["contexts"] == 0
