@@ -1268,6 +1268,22 @@ struct TileCursor {
 // (Parking the rows finished before the wait in shared memory, so that the
 // warp need not wait at its first store, measured slower: the carve-out it
 // takes shrinks the L1 that stages the in-flight loads.)
+#ifdef POSPOP_TUNING
+// Diagnostics (tuning build only, tools/seg_trace.py): per warp of the tile
+// mode {entry, first array counted, previous launch waited for, exit, SM id}
+// in %globaltimer ns; set with pospop_tuning_seg_trace().
+__device__ unsigned long long* g_seg_trace = nullptr;
+#define POSPOP_SEG_STAMP(i, v)                                                                          \
+    do {                                                                                                \
+        if (g_seg_trace && (threadIdx.x & 31u) == 0)                                                    \
+            g_seg_trace[(((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 5 + (i)] = (v); \
+    } while (0)
+#else
+#define POSPOP_SEG_STAMP(i, v) \
+    do {                       \
+    } while (0)
+#endif
+
 template <int NBANK, int L, int VB, bool EARLY = false>
 __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigned long long* offsets,
                                               unsigned long long n_arrays, int k, unsigned long long* out,
@@ -1282,9 +1298,13 @@ __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigne
     const int wb = k >> 3;
     const PlaneXpose xp(lane);
     bool waited = !EARLY;
+    POSPOP_SEG_STAMP(0, globaltimer());
+    POSPOP_SEG_STAMP(4, smid());
     auto ensure_waited = [&]() {
         if (!waited) {
+            POSPOP_SEG_STAMP(1, globaltimer());
             pdl_wait_prev();
+            POSPOP_SEG_STAMP(2, globaltimer());
             waited = true;
         }
     };
@@ -1306,6 +1326,7 @@ __device__ __forceinline__ void seg_tile_loop(const uint8_t* data, const unsigne
     auto finish_warp = [&]() {
         ensure_waited();
         if (giant_bytes) giant_help<NBANK, NBANK == 1 ? 5 : 4, 16>(q, data, offsets, k, out, lane);
+        POSPOP_SEG_STAMP(3, globaltimer());
     };
     const unsigned long long zero[NBANK] = {};
     if (arr >= cur.static_end) {  // this warp has no static array

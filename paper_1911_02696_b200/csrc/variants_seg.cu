@@ -75,6 +75,16 @@ const SegVariant kVariants[] = {
 
 }  // namespace
 
+#ifdef POSPOP_TUNING
+// Diagnostics entry of the tuning build (not in the public header): the
+// per-warp trace buffer of the segmented tile mode (NULL = off).  Defined in
+// this translation unit because the segmented kernels live in its module.
+extern "C" int pospop_tuning_seg_trace(void* d_buf) {
+    unsigned long long* p = static_cast<unsigned long long*>(d_buf);
+    return (int)cudaMemcpyToSymbol(dev::g_seg_trace, &p, sizeof p);
+}
+#endif
+
 const SegVariant* seg_variants(size_t* n) {
     *n = sizeof(kVariants) / sizeof(kVariants[0]);
     return kVariants;
